@@ -1,0 +1,208 @@
+/*
+ * dicb200 — C-ABI of the B200-native DIC correlation path (integer search +
+ * sub-pixel refinement) of arXiv 1905.06228 / the reference `dicbench` library.
+ *
+ * The reference has no FFI layer; its operator surface is the C++ namespace
+ * `dic`. The drop-in granularity is the batched pipeline entry point
+ * (SURVEY.md §8b):
+ *
+ *   dicb200_analyze_pair      replaces dic::analyze_pair
+ *                             (/root/reference/proj/core/include/dic/pipeline.hpp:76-77,
+ *                              proj/core/src/pipeline.cpp:147-180)
+ *   dicb200_analyze_sequence  replaces dic::analyze_sequence
+ *                             (pipeline.hpp:79-80, pipeline.cpp:182-214)
+ *   dicb200_grid_size /       replaces dic::grid_subsets + RunConfig::effective_margin
+ *   dicb200_grid                (image.hpp:58-61, image.cpp:140-158; pipeline.hpp:43-45)
+ *   dicb200_sequence_pairs    replaces dic::sequence_pairs (pipeline.hpp:71, pipeline.cpp:43-54)
+ *   dicb200_partition_ranges  replaces dic::partition_ranges (pipeline.hpp:74, pipeline.cpp:56-69)
+ *
+ * Every per-subset stage of dic::process_subset (pipeline.cpp:76-135) —
+ * subset_stats, bfs_search / pso_search / mpso_search, refine_nr,
+ * icgn_precompute + refine_icgn — runs inside these calls as sm_100a kernels.
+ *
+ * Plain pointers and sizes only. Images are 8- or 16-bit unsigned gray levels
+ * (the reference stores doubles; integer gray levels map losslessly, which is
+ * what every BASELINE configuration uses). Errors: pair-level failures that the
+ * reference raises as dic::Error return DICB200_ERR_INVALID with the reference's
+ * message in dicb200_last_error_message(); per-POI failures never fail the call
+ * — they are reported in dicb200_poi_record.status with the reference's
+ * partial-fill semantics (pipeline.cpp:82-133).
+ *
+ * Thread safety: every entry point is reentrant (per-call stream, device pools
+ * guarded by a mutex), matching the reference's concurrent analyze_pair calls
+ * from image-parallel workers (pipeline.cpp:201-209).
+ */
+#ifndef DICB200_H
+#define DICB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DICB200_ABI_VERSION 1
+
+typedef enum {
+  DICB200_OK = 0,
+  DICB200_ERR_INVALID = 1,  /* a dic::Error at pair level (message set)      */
+  DICB200_ERR_CUDA = 2,     /* CUDA runtime failure (message set)            */
+  DICB200_ERR_NOMEM = 3,
+  DICB200_ERR_CAPACITY = 4, /* out_cap smaller than the grid                 */
+  DICB200_ERR_NO_DEVICE = 5 /* no CUDA device: the product path never falls back to the CPU */
+} dicb200_status;
+
+/* Pixel storage. */
+enum { DICB200_U8 = 0, DICB200_U16 = 1 };
+
+/* Enum values follow the declaration order of the reference enums. */
+enum { DICB200_INT_BFS = 0, DICB200_INT_PSO = 1, DICB200_INT_MPSO = 2 };   /* IntegerMethod, pipeline.hpp:17 */
+enum { DICB200_SUB_NR = 0, DICB200_SUB_ICGN = 1, DICB200_SUB_NONE = 2 };   /* SubpixelMethod, pipeline.hpp:18 */
+enum { DICB200_MODE_SERIAL = 0, DICB200_MODE_SUBIMAGE = 1, DICB200_MODE_IMAGE = 2 }; /* ExecMode, pipeline.hpp:19 */
+enum { DICB200_POLICY_UPDATE = 0, DICB200_POLICY_FIXED_FIRST = 1 };        /* ReferencePolicy, pipeline.hpp:20 */
+enum { DICB200_BFS_WINDOW = 0, DICB200_BFS_WHOLE_IMAGE = 1 };              /* BfsDomain, integer_search.hpp:12 */
+/* B200 extension (BASELINE.json asks for a constant 0.7 inertia; the reference
+ * hard-codes w(t) = 0.9 - t/(2G), integer_search.cpp:35-37). */
+enum { DICB200_INERTIA_REFERENCE = 0, DICB200_INERTIA_CONSTANT = 1 };
+
+/* Image descriptor: host pointer for the host entry points, device pointer for
+ * the *_device entry points. pitch is in elements (>= width). */
+typedef struct {
+  int32_t width;
+  int32_t height;
+  int32_t pitch;
+  int32_t dtype;  /* DICB200_U8 | DICB200_U16 */
+  int32_t id;     /* GrayImage::id(), copied into field ref_id/tgt_id */
+  int32_t bits;     /* significant bits per pixel (0 = full dtype width); lets u16
+                    * data of <= 12 bits use the exact u32 IMAD path */
+  const void* data;
+} dicb200_image;
+
+/* POD mirror of RunConfig + SearchConfig + RefineConfig + GridParams
+ * (pipeline.hpp:27-49, integer_search.hpp:14-23, subpixel.hpp:41-44).
+ * dicb200_default_config() fills the reference defaults. */
+typedef struct {
+  int32_t integer_method;   /* default mpso */
+  int32_t subpixel_method;  /* default nr */
+  int32_t mode;             /* default serial; controls multi-device use in analyze_sequence */
+  int32_t reference_policy; /* default update_every_pair */
+  int32_t worker_count;     /* default 1; for image mode = number of devices to use (0 = all) */
+  /* SearchConfig */
+  int32_t search_radius;    /* 25 */
+  int32_t bfs_domain;       /* whole_image */
+  int32_t particle_count;   /* 50 */
+  int32_t max_generations;  /* 5 */
+  int32_t pad0;
+  double stop_threshold;    /* 0.995 */
+  double c1;                /* 2.0 */
+  double c2;                /* 2.0 */
+  uint64_t rng_seed;        /* 0 */
+  /* RefineConfig */
+  double tol;               /* 0.01 px on max(|du|,|dv|) */
+  int32_t max_iter;         /* 20 */
+  /* GridParams */
+  int32_t half_width;       /* 15 */
+  int32_t spacing;          /* 10 */
+  int32_t margin;           /* -1: auto = half_width + search_radius */
+  /* B200 extensions */
+  int32_t inertia_mode;     /* DICB200_INERTIA_REFERENCE */
+  int32_t pad1;
+  double inertia_constant;  /* used when inertia_mode == CONSTANT */
+} dicb200_run_config;
+
+/* Per-POI status: 0 = no dic::Error was raised; otherwise which reference
+ * error aborted the chain (the reference swallows the message, pipeline.cpp:131-133,
+ * keeping the fields already filled). */
+enum {
+  DICB200_POI_OK = 0,
+  DICB200_POI_SUBSET_OUT_OF_BOUNDS = 1,   /* "subset out of image bounds"          correlation.cpp:10-11 */
+  DICB200_POI_NO_VALID_POSITION = 2,      /* "no valid search position"            integer_search.cpp:19,31 */
+  DICB200_POI_ALL_DEGENERATE = 3,         /* "all positions degenerate"            integer_search.cpp:77,169 */
+  DICB200_POI_INVALID_SWARM = 4,          /* "invalid swarm configuration"         integer_search.cpp:110-111 */
+  DICB200_POI_DEGENERATE_SUBSET = 5,      /* "degenerate subset"                   subpixel.cpp:227,269,271 */
+  DICB200_POI_DRIFTED = 6,                /* "drifted out of bounds"               subpixel.cpp:140,171 */
+  DICB200_POI_DEGENERATE_TARGET = 7,      /* "degenerate target subset"            subpixel.cpp:239,289,318,349 */
+  DICB200_POI_BORDER_GRADIENTS = 8,       /* "subset too close to border for gradients" subpixel.cpp:193-195 */
+  DICB200_POI_DEGENERATE_TEXTURE = 9,     /* "degenerate texture"                  subpixel.cpp:200,219,335 */
+  DICB200_POI_WARP_NOT_INVERTIBLE = 10,   /* "warp not invertible"                 subpixel.cpp:279,339 */
+  DICB200_POI_INCREMENT_NOT_INVERTIBLE = 11 /* "non-invertible warp increment"     subpixel.cpp:30 */
+};
+
+/* PoiRecord (pipeline.hpp:51-59) + status. */
+typedef struct {
+  int32_t x, y;
+  double u, v;
+  double zncc;              /* NaN when the integer stage failed */
+  int32_t converged;
+  int32_t iterations;
+  int64_t evaluations;
+  int64_t update_evaluations;
+  int32_t status;
+  int32_t integer_dx, integer_dy; /* integer-stage displacement (diagnostic) */
+  int32_t pad;
+} dicb200_poi_record;
+
+/* DisplacementField (pipeline.hpp:61-67); records are caller-owned. */
+typedef struct {
+  int32_t pair_index;
+  int32_t ref_id;
+  int32_t tgt_id;
+  int32_t status;           /* DICB200_OK or the pair-level error */
+  dicb200_poi_record* records;
+  size_t capacity;
+  size_t count;
+  char error[160];          /* reference's dic::Error message when status != OK */
+} dicb200_field;
+
+int dicb200_abi_version(void);
+void dicb200_default_config(dicb200_run_config* cfg);
+const char* dicb200_last_error_message(void);
+int dicb200_device_count(void);
+
+/* Grid (no GPU needed). */
+dicb200_status dicb200_grid_size(int32_t width, int32_t height, const dicb200_run_config* cfg,
+                                 size_t* count);
+dicb200_status dicb200_grid(int32_t width, int32_t height, const dicb200_run_config* cfg,
+                            int32_t* xy_out /* 2*count */, size_t cap, size_t* count);
+dicb200_status dicb200_sequence_pairs(int32_t policy, int32_t image_count, int32_t* pairs_out /* 2*(n-1) */);
+dicb200_status dicb200_partition_ranges(size_t n, int32_t workers, size_t* ranges_out /* 2*workers */);
+
+/* Host-buffer entry points (synchronous). Runs on device `device` (-1 = current). */
+dicb200_status dicb200_analyze_pair(const dicb200_image* reference, const dicb200_image* target,
+                                    const dicb200_run_config* cfg, uint64_t pair_index,
+                                    dicb200_poi_record* out, size_t out_cap, size_t* out_count);
+
+/* Sequence: pairs from dicb200_sequence_pairs(cfg->reference_policy, n).
+ * fields[i] must have records/capacity set. Pair-level failures land in
+ * fields[i].status/error (pipeline.cpp:191-198); the call still returns OK.
+ * mode == IMAGE shards contiguous pair chunks over worker_count devices
+ * (0 = all visible) with partition_ranges semantics. */
+dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_images,
+                                        const dicb200_run_config* cfg, dicb200_field* fields,
+                                        size_t n_fields);
+
+/* Device-resident entry point: images hold device pointers, records are
+ * written to device memory `out_dev`, everything is enqueued on `stream`
+ * (a cudaStream_t; NULL = legacy default) without host synchronisation.
+ * grid rows [row_begin,row_end) only (subset-parallel sharding; -1 = all).
+ * Subset indices (RNG keys) stay global. */
+dicb200_status dicb200_analyze_pair_device(const dicb200_image* reference, const dicb200_image* target,
+                                           const dicb200_run_config* cfg, uint64_t pair_index,
+                                           int32_t row_begin, int32_t row_end,
+                                           dicb200_poi_record* out_dev, size_t out_cap,
+                                           size_t* out_count, void* stream);
+
+/* Kernel launches issued by this thread since the last reset (evidence for
+ * bench.py "gpu_launches"). */
+uint64_t dicb200_launch_count(void);
+void dicb200_reset_launch_count(void);
+
+/* Release pooled device memory on all devices. */
+void dicb200_shutdown(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DICB200_H */

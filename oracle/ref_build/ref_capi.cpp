@@ -1,0 +1,285 @@
+// TEST INFRASTRUCTURE ONLY (oracle/_ref): extern "C" entry points over the
+// UNMODIFIED reference library (/root/reference/proj/core/src/*.cpp, compiled
+// by oracle/Makefile into oracle/_ref/libdicref.so). Used by tests/ to pin the
+// C restatement (oracle/dic_oracle.c) and to generate tests/golden/, and by
+// bench.py --impl reference / cpu_baseline as the reference's own CPU path.
+// Never linked into the product.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "dic/correlation.hpp"
+#include "dic/error.hpp"
+#include "dic/image.hpp"
+#include "dic/integer_search.hpp"
+#include "dic/pipeline.hpp"
+#include "dic/rng.hpp"
+#include "dic/subpixel.hpp"
+#include "dicb200.h"
+
+namespace {
+
+dic::RunConfig to_run_config(const dicb200_run_config& c) {
+  dic::RunConfig r;
+  r.integer_method = static_cast<dic::IntegerMethod>(c.integer_method);
+  r.subpixel_method = static_cast<dic::SubpixelMethod>(c.subpixel_method);
+  r.mode = static_cast<dic::ExecMode>(c.mode);
+  r.reference_policy = static_cast<dic::ReferencePolicy>(c.reference_policy);
+  r.worker_count = c.worker_count;
+  r.search.search_radius = c.search_radius;
+  r.search.bfs_domain = static_cast<dic::BfsDomain>(c.bfs_domain);
+  r.search.particle_count = c.particle_count;
+  r.search.max_generations = c.max_generations;
+  r.search.stop_threshold = c.stop_threshold;
+  r.search.c1 = c.c1;
+  r.search.c2 = c.c2;
+  r.search.rng_seed = c.rng_seed;
+  r.refine.tol = c.tol;
+  r.refine.max_iter = c.max_iter;
+  r.grid.half_width = c.half_width;
+  r.grid.spacing = c.spacing;
+  r.grid.margin = c.margin;
+  return r;
+}
+
+void copy_err(const char* what, char* err, size_t cap) {
+  if (!err || cap == 0) return;
+  std::strncpy(err, what, cap - 1);
+  err[cap - 1] = 0;
+}
+
+void to_record(const dic::PoiRecord& r, dicb200_poi_record& o) {
+  std::memset(&o, 0, sizeof o);
+  o.x = r.x;
+  o.y = r.y;
+  o.u = r.u;
+  o.v = r.v;
+  o.zncc = r.zncc;
+  o.converged = r.converged ? 1 : 0;
+  o.iterations = r.iterations;
+  o.evaluations = r.evaluations;
+  o.update_evaluations = r.update_evaluations;
+  o.status = -1;  // the reference does not expose which error aborted a POI
+}
+
+dic::GrayImage make_image(const double* px, int w, int h, int id = 0) {
+  return dic::GrayImage(w, h, std::vector<double>(px, px + static_cast<size_t>(w) * h), id);
+}
+
+}  // namespace
+
+extern "C" {
+
+int dicref_analyze_pair(const double* ref, const double* tgt, int w, int h,
+                        const dicb200_run_config* cfg, uint64_t pair_index,
+                        dicb200_poi_record* out, size_t cap, size_t* count, char* err,
+                        size_t errcap) {
+  try {
+    const dic::GrayImage a = make_image(ref, w, h, 0), b = make_image(tgt, w, h, 1);
+    const dic::DisplacementField f = dic::analyze_pair(a, b, to_run_config(*cfg), pair_index);
+    *count = f.records.size();
+    if (f.records.size() > cap) return 4;
+    for (size_t i = 0; i < f.records.size(); ++i) to_record(f.records[i], out[i]);
+    return 0;
+  } catch (const std::exception& e) {
+    copy_err(e.what(), err, errcap);
+    return 1;
+  }
+}
+
+// Timed variant for the CPU baseline: images are wrapped once; only
+// analyze_pair runs between the two steady_clock reads (bench.cpp:36-48 style).
+int dicref_analyze_pair_timed(const double* ref, const double* tgt, int w, int h,
+                              const dicb200_run_config* cfg, uint64_t pair_index, int repeats,
+                              double* seconds_out, size_t* count, char* err, size_t errcap) {
+  try {
+    const dic::GrayImage a = make_image(ref, w, h, 0), b = make_image(tgt, w, h, 1);
+    const dic::RunConfig rc = to_run_config(*cfg);
+    double best = 1e300;
+    for (int r = 0; r < repeats; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      const dic::DisplacementField f = dic::analyze_pair(a, b, rc, pair_index);
+      const auto t1 = std::chrono::steady_clock::now();
+      *count = f.records.size();
+      const double s = std::chrono::duration<double>(t1 - t0).count();
+      if (s < best) best = s;
+    }
+    *seconds_out = best;
+    return 0;
+  } catch (const std::exception& e) {
+    copy_err(e.what(), err, errcap);
+    return 1;
+  }
+}
+
+int dicref_analyze_sequence(const double* const* images, size_t n, int w, int h,
+                            const dicb200_run_config* cfg, dicb200_field* fields, size_t n_fields,
+                            double* seconds_out) {
+  std::vector<dic::GrayImage> imgs;
+  imgs.reserve(n);
+  for (size_t i = 0; i < n; ++i) imgs.push_back(make_image(images[i], w, h, static_cast<int>(i)));
+  const auto t0 = std::chrono::steady_clock::now();
+  const auto out = dic::analyze_sequence(imgs, to_run_config(*cfg));
+  const auto t1 = std::chrono::steady_clock::now();
+  if (seconds_out) *seconds_out = std::chrono::duration<double>(t1 - t0).count();
+  if (out.size() != n_fields) return 4;
+  for (size_t i = 0; i < out.size(); ++i) {
+    dicb200_field& f = fields[i];
+    f.pair_index = out[i].pair_index;
+    f.ref_id = out[i].ref_id;
+    f.tgt_id = out[i].tgt_id;
+    f.status = out[i].failed() ? 1 : 0;
+    std::memset(f.error, 0, sizeof f.error);
+    copy_err(out[i].error.c_str(), f.error, sizeof f.error);
+    f.count = out[i].records.size();
+    for (size_t k = 0; k < out[i].records.size() && k < f.capacity; ++k)
+      to_record(out[i].records[k], f.records[k]);
+  }
+  return 0;
+}
+
+// --- per-subset operators (unit-level pins) ------------------------------
+
+// Returns 0 and the coefficient, or 1 with the error message.
+int dicref_zncc(const double* ref, const double* tgt, int w, int h, int cx, int cy, int m,
+                int dx, int dy, double* out, char* err, size_t errcap) {
+  try {
+    const dic::GrayImage a = make_image(ref, w, h), b = make_image(tgt, w, h);
+    const dic::SubsetSpec spec{cx, cy, m};
+    *out = dic::zncc(dic::subset_stats(a, spec), b, spec, dx, dy);
+    return 0;
+  } catch (const std::exception& e) {
+    copy_err(e.what(), err, errcap);
+    return 1;
+  }
+}
+
+// method: 0 bfs, 1 pso, 2 mpso. result: dx, dy, generations_used; zncc; evals.
+int dicref_integer_search(const double* ref, const double* tgt, int w, int h, int cx, int cy,
+                          int m, const dicb200_run_config* cfg, uint64_t stream_seed,
+                          int32_t* ires /*3*/, double* zncc, int64_t* evals /*2*/, char* err,
+                          size_t errcap) {
+  try {
+    const dic::GrayImage a = make_image(ref, w, h), b = make_image(tgt, w, h);
+    const dic::SubsetSpec spec{cx, cy, m};
+    const dic::RunConfig rc = to_run_config(*cfg);
+    const auto stats = dic::subset_stats(a, spec);
+    dic::IntegerResult r;
+    dic::CorrelationMemo memo;
+    dic::StreamRng rng(stream_seed);
+    if (cfg->integer_method == 0)
+      r = dic::bfs_search(stats, b, spec, rc.search);
+    else if (cfg->integer_method == 1)
+      r = dic::pso_search(stats, b, spec, rc.search, memo, rng);
+    else
+      r = dic::mpso_search(stats, b, spec, rc.search, memo, rng);
+    ires[0] = r.dx;
+    ires[1] = r.dy;
+    ires[2] = r.generations_used;
+    *zncc = r.zncc;
+    evals[0] = r.evaluations;
+    evals[1] = r.update_evaluations;
+    return 0;
+  } catch (const std::exception& e) {
+    copy_err(e.what(), err, errcap);
+    return 1;
+  }
+}
+
+// method: 0 nr, 1 icgn. out: u, v, zncc, ux, uy, vx, vy; iters_conv: iterations, converged.
+int dicref_refine(const double* ref, const double* tgt, int w, int h, int cx, int cy, int m,
+                  int init_dx, int init_dy, int method, double tol, int max_iter, double* out,
+                  int32_t* iters_conv, char* err, size_t errcap) {
+  try {
+    const dic::GrayImage a = make_image(ref, w, h), b = make_image(tgt, w, h);
+    const dic::SubsetSpec spec{cx, cy, m};
+    dic::RefineConfig rc;
+    rc.tol = tol;
+    rc.max_iter = max_iter;
+    dic::SubpixelResult r;
+    if (method == 0) {
+      r = dic::refine_nr(dic::subset_stats(a, spec), b, spec, {init_dx, init_dy}, rc);
+    } else {
+      const auto st = dic::icgn_precompute(a, spec);
+      r = dic::refine_icgn(st, b, spec, {init_dx, init_dy}, rc);
+    }
+    out[0] = r.u;
+    out[1] = r.v;
+    out[2] = r.zncc;
+    out[3] = r.warp.ux;
+    out[4] = r.warp.uy;
+    out[5] = r.warp.vx;
+    out[6] = r.warp.vy;
+    iters_conv[0] = r.iterations;
+    iters_conv[1] = r.converged ? 1 : 0;
+    return 0;
+  } catch (const std::exception& e) {
+    copy_err(e.what(), err, errcap);
+    return 1;
+  }
+}
+
+// IC-GN precompute pin: Hessian (36, row-major) and condition number.
+int dicref_icgn_hessian(const double* ref, int w, int h, int cx, int cy, int m, double* hess,
+                        double* condition, char* err, size_t errcap) {
+  try {
+    const dic::GrayImage a = make_image(ref, w, h);
+    const auto st = dic::icgn_precompute(a, dic::SubsetSpec{cx, cy, m});
+    for (int i = 0; i < 6; ++i)
+      for (int j = 0; j < 6; ++j) hess[i * 6 + j] = st.hessian(i, j);
+    *condition = st.condition;
+    return 0;
+  } catch (const std::exception& e) {
+    copy_err(e.what(), err, errcap);
+    return 1;
+  }
+}
+
+double dicref_interp_bilinear(const double* img, int w, int h, double x, double y, int* ok) {
+  try {
+    *ok = 1;
+    return dic::interp_bilinear(make_image(img, w, h), x, y);
+  } catch (const std::exception&) {
+    *ok = 0;
+    return 0.0;
+  }
+}
+
+uint64_t dicref_derive_stream_seed(uint64_t seed, uint64_t pair, uint64_t subset) {
+  return dic::derive_stream_seed(seed, pair, subset);
+}
+
+// n raw mt19937_64 outputs (std::mt19937_64 via StreamRng::next_bits).
+void dicref_mt64(uint64_t seed, size_t n, uint64_t* out) {
+  dic::StreamRng rng(seed);
+  for (size_t i = 0; i < n; ++i) out[i] = rng.next_bits();
+}
+
+void dicref_uniform01(uint64_t seed, size_t n, double* out) {
+  dic::StreamRng rng(seed);
+  for (size_t i = 0; i < n; ++i) out[i] = rng.uniform01();
+}
+
+int dicref_grid(int w, int h, int half_width, int spacing, int margin, int32_t* xy, size_t cap,
+                size_t* count, char* err, size_t errcap) {
+  try {
+    const dic::GrayImage img(w, h, std::vector<double>(static_cast<size_t>(w) * h, 0.0));
+    const auto g = dic::grid_subsets(img, half_width, spacing, margin);
+    *count = g.size();
+    for (size_t i = 0; i < g.size() && i < cap; ++i) {
+      xy[2 * i] = g[i].center_x;
+      xy[2 * i + 1] = g[i].center_y;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    copy_err(e.what(), err, errcap);
+    return 1;
+  }
+}
+
+unsigned dicref_hardware_threads(void) { return std::thread::hardware_concurrency(); }
+
+}  // extern "C"

@@ -1,0 +1,139 @@
+"""ctypes mirror of include/dicb200.h and include/dicb200_synth.h.
+
+Plain C structs only; shared by the product wrapper (dic.py), the oracle
+wrapper (oracle/pyoracle.py) and bench.py.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+U8, U16 = 0, 1
+
+INT_BFS, INT_PSO, INT_MPSO = 0, 1, 2
+SUB_NR, SUB_ICGN, SUB_NONE = 0, 1, 2
+MODE_SERIAL, MODE_SUBIMAGE, MODE_IMAGE = 0, 1, 2
+POLICY_UPDATE, POLICY_FIXED_FIRST = 0, 1
+BFS_WINDOW, BFS_WHOLE_IMAGE = 0, 1
+INERTIA_REFERENCE, INERTIA_CONSTANT = 0, 1
+
+FIELD_NONE, FIELD_AFFINE, FIELD_SINUSOID = 0, 1, 2
+
+POI_STATUS = {
+    0: "ok",
+    1: "subset out of image bounds",
+    2: "no valid search position",
+    3: "all positions degenerate",
+    4: "invalid swarm configuration",
+    5: "degenerate subset",
+    6: "drifted out of bounds",
+    7: "degenerate target subset",
+    8: "subset too close to border for gradients",
+    9: "degenerate texture",
+    10: "warp not invertible",
+    11: "non-invertible warp increment",
+}
+
+
+class Image(C.Structure):
+    _fields_ = [
+        ("width", C.c_int32),
+        ("height", C.c_int32),
+        ("pitch", C.c_int32),
+        ("dtype", C.c_int32),
+        ("id", C.c_int32),
+        ("bits", C.c_int32),
+        ("data", C.c_void_p),
+    ]
+
+
+class RunConfigC(C.Structure):
+    _fields_ = [
+        ("integer_method", C.c_int32),
+        ("subpixel_method", C.c_int32),
+        ("mode", C.c_int32),
+        ("reference_policy", C.c_int32),
+        ("worker_count", C.c_int32),
+        ("search_radius", C.c_int32),
+        ("bfs_domain", C.c_int32),
+        ("particle_count", C.c_int32),
+        ("max_generations", C.c_int32),
+        ("pad0", C.c_int32),
+        ("stop_threshold", C.c_double),
+        ("c1", C.c_double),
+        ("c2", C.c_double),
+        ("rng_seed", C.c_uint64),
+        ("tol", C.c_double),
+        ("max_iter", C.c_int32),
+        ("half_width", C.c_int32),
+        ("spacing", C.c_int32),
+        ("margin", C.c_int32),
+        ("inertia_mode", C.c_int32),
+        ("pad1", C.c_int32),
+        ("inertia_constant", C.c_double),
+    ]
+
+
+class PoiRecordC(C.Structure):
+    _fields_ = [
+        ("x", C.c_int32),
+        ("y", C.c_int32),
+        ("u", C.c_double),
+        ("v", C.c_double),
+        ("zncc", C.c_double),
+        ("converged", C.c_int32),
+        ("iterations", C.c_int32),
+        ("evaluations", C.c_int64),
+        ("update_evaluations", C.c_int64),
+        ("status", C.c_int32),
+        ("integer_dx", C.c_int32),
+        ("integer_dy", C.c_int32),
+        ("pad", C.c_int32),
+    ]
+
+
+class FieldC(C.Structure):
+    _fields_ = [
+        ("pair_index", C.c_int32),
+        ("ref_id", C.c_int32),
+        ("tgt_id", C.c_int32),
+        ("status", C.c_int32),
+        ("records", C.POINTER(PoiRecordC)),
+        ("capacity", C.c_size_t),
+        ("count", C.c_size_t),
+        ("error", C.c_char * 160),
+    ]
+
+
+class SynthSpecC(C.Structure):
+    _fields_ = [
+        ("width", C.c_int32),
+        ("height", C.c_int32),
+        ("dtype", C.c_int32),
+        ("max_value", C.c_int32),
+        ("seed", C.c_uint64),
+        ("blob_count", C.c_int32),
+        ("field", C.c_int32),
+        ("sigma_min", C.c_double),
+        ("sigma_max", C.c_double),
+        ("peak_min", C.c_double),
+        ("peak_max", C.c_double),
+        ("background", C.c_double),
+        ("a", C.c_double * 8),
+    ]
+
+
+# numpy structured dtype with the exact layout of dicb200_poi_record
+def record_dtype():
+    import numpy as np
+
+    return np.dtype(
+        {
+            "names": [f for f, _ in PoiRecordC._fields_],
+            "formats": [
+                np.int32, np.int32, np.float64, np.float64, np.float64, np.int32, np.int32,
+                np.int64, np.int64, np.int32, np.int32, np.int32, np.int32,
+            ],
+            "offsets": [getattr(PoiRecordC, f).offset for f, _ in PoiRecordC._fields_],
+            "itemsize": C.sizeof(PoiRecordC),
+        }
+    )

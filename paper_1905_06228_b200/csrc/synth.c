@@ -1,0 +1,176 @@
+/*
+ * Synthetic speckle frames for the BASELINE configurations (see
+ * include/dicb200_synth.h). Host C, multithreaded over row bands; blobs are
+ * binned into 16x16 px cells so each pixel only visits nearby blobs.
+ */
+#define _GNU_SOURCE
+#include "dicb200_synth.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+#include <unistd.h>
+
+#include "dicb200.h"
+
+#define CELL 16
+
+typedef struct {
+  double cx, cy, inv2s2, peak, reach2;
+} blob_t;
+
+static uint64_t splitmix_next(uint64_t* s) {
+  uint64_t z = (*s += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+static double u01(uint64_t* s) { return (double)(splitmix_next(s) >> 11) * 0x1.0p-53; }
+
+void dicb200_synth_displacement(const dicb200_synth_spec* sp, double yx, double yy, double* dx,
+                                double* dy) {
+  const double* a = sp->a;
+  if (sp->field == DICB200_FIELD_AFFINE) {
+    const double rx = yx - a[6], ry = yy - a[7];
+    *dx = a[0] + a[1] * rx + a[2] * ry;
+    *dy = a[3] + a[4] * rx + a[5] * ry;
+  } else if (sp->field == DICB200_FIELD_SINUSOID) {
+    *dx = a[0] * sin(2.0 * M_PI * yy / a[1]);
+    *dy = a[2] * cos(2.0 * M_PI * yx / a[3]);
+  } else {
+    *dx = 0.0;
+    *dy = 0.0;
+  }
+}
+
+/* Preimage y of pixel x under x = y + d(y). */
+static void preimage(const dicb200_synth_spec* sp, double x, double y, double* px, double* py) {
+  const double* a = sp->a;
+  if (sp->field == DICB200_FIELD_AFFINE) {
+    /* x - o = (I + A)(y - o) + t  =>  y = o + (I + A)^-1 (x - o - t) */
+    const double m00 = 1.0 + a[1], m01 = a[2], m10 = a[4], m11 = 1.0 + a[5];
+    const double det = m00 * m11 - m01 * m10;
+    const double bx = x - a[6] - a[0], by = y - a[7] - a[3];
+    *px = a[6] + (m11 * bx - m01 * by) / det;
+    *py = a[7] + (-m10 * bx + m00 * by) / det;
+  } else if (sp->field == DICB200_FIELD_SINUSOID) {
+    double yx = x, yy = y;
+    for (int it = 0; it < 60; ++it) {
+      double dx, dy;
+      dicb200_synth_displacement(sp, yx, yy, &dx, &dy);
+      const double nx = x - dx, ny = y - dy;
+      const double ch = fabs(nx - yx) + fabs(ny - yy);
+      yx = nx;
+      yy = ny;
+      if (ch < 1e-13) break;
+    }
+    *px = yx;
+    *py = yy;
+  } else {
+    *px = x;
+    *py = y;
+  }
+}
+
+typedef struct {
+  const dicb200_synth_spec* sp;
+  const blob_t* blobs;
+  const int* cell_start;
+  const int* cell_items;
+  int gx, gy;
+  void* out;
+  int pitch;
+  int y0, y1;
+} job_t;
+
+static void* render_rows(void* arg) {
+  const job_t* j = (const job_t*)arg;
+  const dicb200_synth_spec* sp = j->sp;
+  const double maxv = (double)sp->max_value;
+  const int reach_cells = (int)ceil(5.0 * sp->sigma_max / CELL) + 1;
+  for (int y = j->y0; y < j->y1; ++y)
+    for (int x = 0; x < sp->width; ++x) {
+      double qx, qy;
+      preimage(sp, x, y, &qx, &qy);
+      double v = sp->background;
+      const int cx = (int)floor(qx / CELL), cy = (int)floor(qy / CELL);
+      for (int by = cy - reach_cells; by <= cy + reach_cells; ++by) {
+        if (by < 0 || by >= j->gy) continue;
+        for (int bx = cx - reach_cells; bx <= cx + reach_cells; ++bx) {
+          if (bx < 0 || bx >= j->gx) continue;
+          const int c = by * j->gx + bx;
+          for (int i = j->cell_start[c]; i < j->cell_start[c + 1]; ++i) {
+            const blob_t* b = &j->blobs[j->cell_items[i]];
+            const double ddx = qx - b->cx, ddy = qy - b->cy;
+            const double r2 = ddx * ddx + ddy * ddy;
+            if (r2 <= b->reach2) v += b->peak * exp(-r2 * b->inv2s2);
+          }
+        }
+      }
+      if (v < 0.0) v = 0.0;
+      if (v > maxv) v = maxv;
+      const double q = floor(v + 0.5);
+      if (sp->dtype == DICB200_U8)
+        ((uint8_t*)j->out)[(size_t)y * j->pitch + x] = (uint8_t)q;
+      else
+        ((uint16_t*)j->out)[(size_t)y * j->pitch + x] = (uint16_t)q;
+    }
+  return NULL;
+}
+
+int dicb200_synth_render(const dicb200_synth_spec* sp, void* out, int32_t pitch, int32_t threads) {
+  if (sp->width < 1 || sp->height < 1 || sp->blob_count < 0 || pitch < sp->width) return 1;
+  const int n = sp->blob_count;
+  blob_t* blobs = (blob_t*)malloc((size_t)(n > 0 ? n : 1) * sizeof(blob_t));
+  uint64_t s = sp->seed;
+  for (int i = 0; i < n; ++i) {
+    blob_t* b = &blobs[i];
+    b->cx = u01(&s) * sp->width;
+    b->cy = u01(&s) * sp->height;
+    const double sigma = sp->sigma_min + (sp->sigma_max - sp->sigma_min) * u01(&s);
+    b->peak = sp->peak_min + (sp->peak_max - sp->peak_min) * u01(&s);
+    b->inv2s2 = 1.0 / (2.0 * sigma * sigma);
+    b->reach2 = 25.0 * sigma * sigma; /* 5 sigma cut-off */
+  }
+  /* bin blob centres into CELL x CELL cells over the padded frame */
+  const int gx = (sp->width + CELL - 1) / CELL, gy = (sp->height + CELL - 1) / CELL;
+  int* cnt = (int*)calloc((size_t)gx * gy + 1, sizeof(int));
+  int* cell_of = (int*)malloc((size_t)(n > 0 ? n : 1) * sizeof(int));
+  for (int i = 0; i < n; ++i) {
+    int cxx = (int)(blobs[i].cx / CELL), cyy = (int)(blobs[i].cy / CELL);
+    if (cxx >= gx) cxx = gx - 1;
+    if (cyy >= gy) cyy = gy - 1;
+    cell_of[i] = cyy * gx + cxx;
+    cnt[cell_of[i] + 1]++;
+  }
+  for (int c = 0; c < gx * gy; ++c) cnt[c + 1] += cnt[c];
+  int* items = (int*)malloc((size_t)(n > 0 ? n : 1) * sizeof(int));
+  int* fill = (int*)malloc((size_t)gx * gy * sizeof(int));
+  memcpy(fill, cnt, (size_t)gx * gy * sizeof(int));
+  for (int i = 0; i < n; ++i) items[fill[cell_of[i]]++] = i; /* ascending blob order per cell */
+
+  if (threads <= 0) threads = (int)sysconf(_SC_NPROCESSORS_ONLN);
+  if (threads < 1) threads = 1;
+  if (threads > sp->height) threads = sp->height;
+  job_t* jobs = (job_t*)calloc((size_t)threads, sizeof(job_t));
+  pthread_t* tid = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = (job_t){sp, blobs, cnt, items, gx, gy, out, pitch,
+                      (int)((long)sp->height * t / threads), (int)((long)sp->height * (t + 1) / threads)};
+    if (threads == 1)
+      render_rows(&jobs[t]);
+    else
+      pthread_create(&tid[t], NULL, render_rows, &jobs[t]);
+  }
+  if (threads > 1)
+    for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+  free(jobs);
+  free(tid);
+  free(fill);
+  free(items);
+  free(cell_of);
+  free(cnt);
+  free(blobs);
+  return 0;
+}

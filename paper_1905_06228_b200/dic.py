@@ -1,0 +1,329 @@
+"""Host-side mirror of the reference's `namespace dic` pipeline interface.
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/core/include/dic/{pipeline,integer_search,subpixel,image}.hpp,
+so parity tests read like the reference's own tests. Every call goes through
+the C-ABI library libdicb200.so (include/dicb200.h) onto the sm_100a kernels;
+there is no CPU fallback: a missing library or a missing GPU raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from enum import IntEnum
+from typing import List, Sequence, Tuple
+
+import numpy as np
+
+from . import _abi
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdicb200.so")
+
+
+class DicError(RuntimeError):
+    """Mirror of dic::Error (error.hpp:10-13): recoverable engine failures."""
+
+
+class IntegerMethod(IntEnum):  # pipeline.hpp:17
+    bfs = 0
+    pso = 1
+    mpso = 2
+
+
+class SubpixelMethod(IntEnum):  # pipeline.hpp:18
+    nr = 0
+    icgn = 1
+    none = 2
+
+
+class ExecMode(IntEnum):  # pipeline.hpp:19
+    serial = 0
+    subimage_parallel = 1
+    image_parallel = 2
+
+
+class ReferencePolicy(IntEnum):  # pipeline.hpp:20
+    update_every_pair = 0
+    fixed_first = 1
+
+
+class BfsDomain(IntEnum):  # integer_search.hpp:12
+    window = 0
+    whole_image = 1
+
+
+class InertiaMode(IntEnum):  # B200 extension (BASELINE asks for constant 0.7)
+    reference_schedule = 0
+    constant = 1
+
+
+@dataclass
+class SearchConfig:  # integer_search.hpp:14-23
+    search_radius: int = 25
+    bfs_domain: BfsDomain = BfsDomain.whole_image
+    particle_count: int = 50
+    max_generations: int = 5
+    stop_threshold: float = 0.995
+    c1: float = 2.0
+    c2: float = 2.0
+    rng_seed: int = 0
+
+
+@dataclass
+class RefineConfig:  # subpixel.hpp:41-44
+    tol: float = 0.01
+    max_iter: int = 20
+
+
+@dataclass
+class GridParams:  # pipeline.hpp:27-31
+    half_width: int = 15
+    spacing: int = 10
+    margin: int = -1
+
+
+@dataclass
+class RunConfig:  # pipeline.hpp:33-49
+    integer_method: IntegerMethod = IntegerMethod.mpso
+    subpixel_method: SubpixelMethod = SubpixelMethod.nr
+    mode: ExecMode = ExecMode.serial
+    reference_policy: ReferencePolicy = ReferencePolicy.update_every_pair
+    worker_count: int = 1
+    search: SearchConfig = field(default_factory=SearchConfig)
+    refine: RefineConfig = field(default_factory=RefineConfig)
+    grid: GridParams = field(default_factory=GridParams)
+    inertia_mode: InertiaMode = InertiaMode.reference_schedule
+    inertia_constant: float = 0.7
+
+    def effective_margin(self) -> int:
+        return self.grid.margin if self.grid.margin >= 0 else self.grid.half_width + self.search.search_radius
+
+    def effective_workers(self) -> int:
+        return 1 if self.mode == ExecMode.serial else max(1, self.worker_count)
+
+    def to_c(self) -> _abi.RunConfigC:
+        c = _abi.RunConfigC()
+        c.integer_method = int(self.integer_method)
+        c.subpixel_method = int(self.subpixel_method)
+        c.mode = int(self.mode)
+        c.reference_policy = int(self.reference_policy)
+        c.worker_count = int(self.worker_count)
+        c.search_radius = int(self.search.search_radius)
+        c.bfs_domain = int(self.search.bfs_domain)
+        c.particle_count = int(self.search.particle_count)
+        c.max_generations = int(self.search.max_generations)
+        c.stop_threshold = float(self.search.stop_threshold)
+        c.c1 = float(self.search.c1)
+        c.c2 = float(self.search.c2)
+        c.rng_seed = int(self.search.rng_seed) & 0xFFFFFFFFFFFFFFFF
+        c.tol = float(self.refine.tol)
+        c.max_iter = int(self.refine.max_iter)
+        c.half_width = int(self.grid.half_width)
+        c.spacing = int(self.grid.spacing)
+        c.margin = int(self.grid.margin)
+        c.inertia_mode = int(self.inertia_mode)
+        c.inertia_constant = float(self.inertia_constant)
+        return c
+
+
+class GrayImage:
+    """Immutable single-channel image (image.hpp:14-31).
+
+    The reference stores doubles; the device path stores the integer gray
+    levels losslessly as uint8 / uint16. A float array is accepted only when
+    every value is an integer in [0, 65535] (raises DicError otherwise).
+    """
+
+    def __init__(self, pixels: np.ndarray, id: int = 0):
+        a = np.asarray(pixels)
+        if a.ndim != 2 or a.shape[0] < 1 or a.shape[1] < 1:
+            raise DicError("zero-dimension image")
+        if a.dtype == np.uint8 or a.dtype == np.uint16:
+            px = np.ascontiguousarray(a)
+        else:
+            f = a.astype(np.float64)
+            if not np.all(np.isfinite(f)):
+                raise DicError("non-finite gray level")
+            if np.any(f != np.round(f)) or f.min() < 0 or f.max() > 65535:
+                raise DicError("device path requires integer gray levels in [0, 65535]")
+            px = np.ascontiguousarray(f.astype(np.uint8 if f.max() <= 255 else np.uint16))
+        px.setflags(write=False)
+        self._px = px
+        self._id = int(id)
+
+    def width(self) -> int:
+        return self._px.shape[1]
+
+    def height(self) -> int:
+        return self._px.shape[0]
+
+    def id(self) -> int:
+        return self._id
+
+    def pixels(self) -> np.ndarray:
+        return self._px
+
+    def at(self, x: int, y: int) -> float:
+        return float(self._px[y, x])
+
+    def as_c(self) -> _abi.Image:
+        im = _abi.Image()
+        im.width = self.width()
+        im.height = self.height()
+        im.pitch = self.width()
+        im.dtype = _abi.U8 if self._px.dtype == np.uint8 else _abi.U16
+        im.id = self._id
+        im.data = self._px.ctypes.data
+        return im
+
+
+@dataclass
+class DisplacementField:  # pipeline.hpp:61-67
+    pair_index: int = 0
+    ref_id: int = 0
+    tgt_id: int = 0
+    records: np.ndarray = None  # structured array, dtype = _abi.record_dtype()
+    error: str = ""
+
+    def failed(self) -> bool:
+        return bool(self.error)
+
+
+_lib_handle = None
+
+
+def lib() -> C.CDLL:
+    """The product library. Raises (never falls back) when it is missing."""
+    global _lib_handle
+    if _lib_handle is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        L = C.CDLL(LIB_PATH)
+        L.dicb200_last_error_message.restype = C.c_char_p
+        L.dicb200_launch_count.restype = C.c_uint64
+        L.dicb200_analyze_pair.argtypes = [
+            C.POINTER(_abi.Image), C.POINTER(_abi.Image), C.POINTER(_abi.RunConfigC), C.c_uint64,
+            C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t),
+        ]
+        L.dicb200_analyze_pair_device.argtypes = [
+            C.POINTER(_abi.Image), C.POINTER(_abi.Image), C.POINTER(_abi.RunConfigC), C.c_uint64,
+            C.c_int32, C.c_int32, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t), C.c_void_p,
+        ]
+        L.dicb200_analyze_sequence.argtypes = [
+            C.POINTER(_abi.Image), C.c_size_t, C.POINTER(_abi.RunConfigC), C.POINTER(_abi.FieldC), C.c_size_t,
+        ]
+        L.dicb200_grid_size.argtypes = [C.c_int32, C.c_int32, C.POINTER(_abi.RunConfigC), C.POINTER(C.c_size_t)]
+        L.dicb200_grid.argtypes = [
+            C.c_int32, C.c_int32, C.POINTER(_abi.RunConfigC), C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t),
+        ]
+        L.dicb200_sequence_pairs.argtypes = [C.c_int32, C.c_int32, C.c_void_p]
+        L.dicb200_partition_ranges.argtypes = [C.c_size_t, C.c_int32, C.c_void_p]
+        L.dicb200_synth_render.argtypes = [C.POINTER(_abi.SynthSpecC), C.c_void_p, C.c_int32, C.c_int32]
+        L.dicb200_synth_displacement.argtypes = [
+            C.POINTER(_abi.SynthSpecC), C.c_double, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double),
+        ]
+        _lib_handle = L
+    return _lib_handle
+
+
+def _raise(status: int) -> None:
+    msg = lib().dicb200_last_error_message().decode()
+    if status == 1:
+        raise DicError(msg)
+    raise RuntimeError(f"dicb200 status {status}: {msg}")
+
+
+def grid_subsets(width: int, height: int, half_width: int, spacing: int, margin: int) -> List[Tuple[int, int]]:
+    """image.cpp:140-158 (through the C-ABI, no GPU needed)."""
+    cfg = RunConfig()
+    cfg.grid = GridParams(half_width, spacing, margin)
+    c = cfg.to_c()
+    n = C.c_size_t(0)
+    st = lib().dicb200_grid_size(width, height, C.byref(c), C.byref(n))
+    if st:
+        _raise(st)
+    xy = np.zeros(2 * n.value, np.int32)
+    st = lib().dicb200_grid(width, height, C.byref(c), xy.ctypes.data, n.value, C.byref(n))
+    if st:
+        _raise(st)
+    return [(int(xy[2 * i]), int(xy[2 * i + 1])) for i in range(n.value)]
+
+
+def sequence_pairs(policy: ReferencePolicy, image_count: int) -> List[Tuple[int, int]]:
+    """pipeline.cpp:43-54."""
+    if image_count < 2:
+        raise DicError("insufficient images")
+    out = np.zeros(2 * (image_count - 1), np.int32)
+    st = lib().dicb200_sequence_pairs(int(policy), image_count, out.ctypes.data)
+    if st:
+        _raise(st)
+    return [(int(out[2 * i]), int(out[2 * i + 1])) for i in range(image_count - 1)]
+
+
+def partition_ranges(n: int, workers: int) -> List[Tuple[int, int]]:
+    """pipeline.cpp:56-69."""
+    if workers < 1:
+        raise DicError("worker count must be >= 1")
+    out = np.zeros(2 * workers, np.uint64)
+    st = lib().dicb200_partition_ranges(n, workers, out.ctypes.data)
+    if st:
+        _raise(st)
+    return [(int(out[2 * i]), int(out[2 * i + 1])) for i in range(workers)]
+
+
+def analyze_pair(reference: GrayImage, target: GrayImage, cfg: RunConfig, pair_index: int = 0) -> DisplacementField:
+    """pipeline.hpp:76-77 / pipeline.cpp:147-180, on the GPU."""
+    if reference.width() != target.width() or reference.height() != target.height():
+        raise DicError("dimension mismatch")
+    c = cfg.to_c()
+    n = C.c_size_t(0)
+    st = lib().dicb200_grid_size(reference.width(), reference.height(), C.byref(c), C.byref(n))
+    if st:
+        _raise(st)
+    recs = np.zeros(n.value, dtype=_abi.record_dtype())
+    a, b = reference.as_c(), target.as_c()
+    cnt = C.c_size_t(0)
+    st = lib().dicb200_analyze_pair(C.byref(a), C.byref(b), C.byref(c), pair_index, recs.ctypes.data, n.value, C.byref(cnt))
+    if st:
+        _raise(st)
+    return DisplacementField(pair_index, reference.id(), target.id(), recs[: cnt.value], "")
+
+
+def analyze_sequence(images: Sequence[GrayImage], cfg: RunConfig) -> List[DisplacementField]:
+    """pipeline.hpp:79-80 / pipeline.cpp:182-214, on the GPU(s)."""
+    pairs = sequence_pairs(cfg.reference_policy, len(images))
+    c = cfg.to_c()
+    imgs = (_abi.Image * len(images))(*[im.as_c() for im in images])
+    fields = (_abi.FieldC * len(pairs))()
+    bufs = []
+    for i, (ra, tb) in enumerate(pairs):
+        n = C.c_size_t(0)
+        st = lib().dicb200_grid_size(images[ra].width(), images[ra].height(), C.byref(c), C.byref(n))
+        cap = n.value if st == 0 else 0
+        buf = np.zeros(max(cap, 1), dtype=_abi.record_dtype())
+        bufs.append(buf)
+        fields[i].records = C.cast(buf.ctypes.data, C.POINTER(_abi.PoiRecordC))
+        fields[i].capacity = cap
+    st = lib().dicb200_analyze_sequence(imgs, len(images), C.byref(c), fields, len(pairs))
+    if st:
+        _raise(st)
+    out = []
+    for i in range(len(pairs)):
+        f = fields[i]
+        out.append(DisplacementField(f.pair_index, f.ref_id, f.tgt_id, bufs[i][: f.count], f.error.decode()))
+    return out
+
+
+def field_csv_string(field_: DisplacementField) -> str:
+    """pipeline.cpp:216-231 (same printf formats)."""
+    lines = ["x,y,u,v,zncc,converged,iterations,evaluations\n"]
+    for r in field_.records:
+        lines.append(
+            "%d,%d,%.17g,%.17g,%.17g,%d,%d,%d\n"
+            % (r["x"], r["y"], r["u"], r["v"], r["zncc"], 1 if r["converged"] else 0, r["iterations"], r["evaluations"])
+        )
+    return "".join(lines)
