@@ -1,0 +1,550 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 DIC correlation path (BASELINE.json metric:
+"subsets/sec (search+refine) and frame pairs/sec at 1/2/4/8 B200 vs roofline").
+
+Default workload = configuration C5 (the image-parallel sequence: 64 frame
+pairs of 2048^2 12-bit speckle, BFS (R=12) + IC-GN, subset 41, step 10,
+39 601 POIs per pair) — the largest configuration and the one the scaling
+metric is quoted on. One "step" = analysing the whole 64-pair sequence; with N
+ranks the pairs are sharded in contiguous chunks (partition_ranges semantics,
+pipeline.cpp:56-69), no collectives on the data path.
+
+  value : subsets/s over the whole job, frames resident in HBM, device-timed
+          (CUDA events on the launch stream, max over ranks);
+  e2e   : same metric through the public C-ABI dicb200_analyze_sequence with
+          pinned HOST frames (H2D of every frame + D2H of every record inside
+          the timed region);
+  roofline : dominant kernel, algorithmic MACs (sum of evaluations x n) per
+          launch / its event-timed average launch duration, against the pipe
+          peak measured live by tools/microbench/pipes (IMAD for the 12-bit
+          u16 path, IDP4A for u8);
+  cpu_baseline : the reference's own analyze_pair (oracle/_ref, built from
+          /root/reference sources) on all host cores, bounded sample.
+
+--impl reference runs only the reference's CPU path (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_1905_06228_b200 import _abi, configs, dic  # noqa: E402
+
+PIPES_BIN = os.path.join(ROOT, "tools", "microbench", "pipes")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c3x", "c4", "c5"])
+    ap.add_argument("--pairs", type=int, default=64, help="C5 sequence length")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- helpers
+
+def workload(name: str, pairs: int):
+    return configs.c5(pairs) if name == "c5" else configs.get(name)
+
+
+def describe(w, subsets_per_pair: int, n_pairs: int, world: int) -> dict:
+    cfg = w.cfg
+    f = w.frames[0]
+    return {
+        "workload": f"{w.name}: {w.description}",
+        "frames": f"{f.width}x{f.height} {'u8' if f.dtype == _abi.U8 else 'u16 12-bit'} synthetic speckle",
+        "integer": cfg.integer_method.name,
+        "subpixel": cfg.subpixel_method.name,
+        "subset": 2 * cfg.grid.half_width + 1,
+        "step_px": cfg.grid.spacing,
+        "search_radius": cfg.search.search_radius,
+        "pairs": n_pairs,
+        "subsets_per_pair": subsets_per_pair,
+        "interp": "bilinear (reference semantics)",
+        "parallelism": f"image-parallel: pairs sharded over {world} rank(s)" if n_pairs > 1 else
+                       f"subset-parallel: grid rows sharded over {world} rank(s)",
+        "l2": "inputs larger than L2 (no flush)" if n_pairs * f.width * f.height * (1 if f.dtype == _abi.U8 else 2) > 126e6
+              else "L2 flushed between steps (256 MiB write)",
+    }
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def pipe_peaks() -> dict:
+    """Live pipe-rate microbenchmark (tools/microbench/pipes.cu)."""
+    try:
+        out = subprocess.run([PIPES_BIN], capture_output=True, text=True, timeout=60).stdout
+        return json.loads(out.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)}
+
+
+def cpu_baseline(w, frames_host, n_sample_rows: int) -> dict:
+    """The reference's own analyze_pair (oracle/_ref) on all host cores, on a
+    bounded sample: the first n_sample_rows grid rows of pair (0, 1)."""
+    import copy
+
+    from oracle import Oracle, available
+
+    kind = "reference" if available("reference") else "port"
+    orc = Oracle(kind)
+    cfg = copy.deepcopy(w.cfg)
+    cfg.mode = dic.ExecMode.subimage_parallel
+    threads = os.cpu_count() or 1
+    cfg.worker_count = threads
+    margin = cfg.effective_margin()
+    band = min(frames_host[0].shape[0], margin + cfg.grid.spacing * (n_sample_rows - 1) + margin + 1)
+    a = frames_host[0][:band].astype(np.float64)
+    b = frames_host[1][:band].astype(np.float64)
+    if kind == "reference":
+        secs, n = orc.analyze_pair_timed(a, b, cfg, 0, 1)
+    else:
+        t0 = time.perf_counter()
+        n = len(orc.analyze_pair(a, b, cfg, 0, threads))
+        secs = time.perf_counter() - t0
+    return {"value": n / secs, "unit": "subsets/s", "cores": threads, "kind": kind,
+            "sample": f"pair (0,1), first {n_sample_rows} grid rows ({n} POIs, frame band {band} px high), "
+                      f"dic::analyze_pair subimage_parallel x{threads} threads, {secs:.2f} s"}
+
+
+# ------------------------------------------------------------ our arm
+
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    L = dic.lib()
+    L.dicb200_synth_render_device.argtypes = [C.POINTER(_abi.SynthSpecC), C.c_void_p, C.c_int32, C.c_void_p]
+    L.dicb200_profile_read.argtypes = [C.c_void_p, C.c_void_p]
+    w = workload(args.config, args.pairs)
+    all_pairs = w.pairs
+    n_pairs = len(all_pairs)
+    cfg = w.cfg
+    cfgc = cfg.to_c()
+    f0 = w.frames[0]
+    u8 = f0.dtype == _abi.U8
+    tdtype = torch.uint8 if u8 else torch.int16
+    bits = 8 if u8 else 12
+    esize = 1 if u8 else 2
+    stream = torch.cuda.Stream(device=dev)
+    sptr = C.c_void_p(stream.cuda_stream)
+
+    # shard: image-parallel over pairs, or subset-parallel over grid rows for single-pair configs
+    spp = w.subsets_per_pair()
+    lat_rows = len({y for _, y in dic.grid_subsets(f0.width, f0.height, cfg.grid.half_width, cfg.grid.spacing,
+                                                   cfg.effective_margin())})
+    if n_pairs > 1:
+        base, extra = divmod(n_pairs, world)
+        lo = rank * base + min(rank, extra)
+        my_pairs = all_pairs[lo: lo + base + (1 if rank < extra else 0)]
+        row_range = (-1, -1)
+    else:
+        my_pairs = all_pairs
+        base, extra = divmod(lat_rows, world)
+        lo = rank * base + min(rank, extra)
+        row_range = (lo, lo + base + (1 if rank < extra else 0))
+    needed = sorted({i for p in my_pairs for i in p})
+
+    # frames rendered on the device (synthetic generator)
+    frames = {}
+    for i in needed:
+        t = torch.empty((f0.height, f0.width), dtype=tdtype, device=dev)
+        spec = w.frames[i].to_c()
+        rc = L.dicb200_synth_render_device(C.byref(spec), C.c_void_p(t.data_ptr()), f0.width, sptr)
+        if rc:
+            raise RuntimeError("device synth failed")
+        frames[i] = t
+    torch.cuda.synchronize()
+
+    def img(i, ptr=None):
+        im = _abi.Image()
+        im.width, im.height, im.pitch = f0.width, f0.height, f0.width
+        im.dtype = _abi.U8 if u8 else _abi.U16
+        im.id = i
+        im.bits = bits
+        im.data = ptr if ptr is not None else frames[i].data_ptr()
+        return im
+
+    dev_imgs = {i: img(i) for i in needed}
+    rows_here = (row_range[1] - row_range[0]) if row_range[0] >= 0 else lat_rows
+    nx = spp // lat_rows
+    recs_per_pair = rows_here * nx
+    rec_size = C.sizeof(_abi.PoiRecordC)
+    recbuf = torch.empty(max(1, len(my_pairs) * recs_per_pair * rec_size), dtype=torch.uint8, device=dev)
+    cnt = C.c_size_t(0)
+
+    def step():
+        for j, (a, b) in enumerate(my_pairs):
+            st = L.dicb200_analyze_pair_device(
+                C.byref(dev_imgs[a]), C.byref(dev_imgs[b]), C.byref(cfgc), all_pairs.index((a, b)),
+                row_range[0], row_range[1], C.c_void_p(recbuf.data_ptr() + j * recs_per_pair * rec_size),
+                recs_per_pair, C.byref(cnt), sptr)
+            if st:
+                raise RuntimeError(L.dicb200_last_error_message().decode())
+
+    flush = None
+    l2_note = describe(w, spp, n_pairs, world)["l2"]
+    if "flushed" in l2_note:
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    # warm-up
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+            if flush is not None:
+                flush.fill_(1)
+    stream.synchronize()
+
+    peaks = pipe_peaks() if rank == 0 else {}
+    # timed region: K steps, CUDA events on the launch stream, stage events live
+    clocks = Clocks(local_rank)
+    L.dicb200_profile_read((C.c_double * 4)(), (C.c_uint64 * 4)())  # clear
+    barrier()
+    torch.cuda.synchronize()
+    L.dicb200_reset_launch_count()
+    clocks.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush_ev = []
+    L.dicb200_profile_enable(1)
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+            if flush is not None:
+                fa, fb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                fa.record(stream)
+                flush.fill_(1)
+                fb.record(stream)
+                flush_ev.append((fa, fb))
+        ev1.record(stream)
+    ev1.synchronize()
+    L.dicb200_profile_enable(0)
+    launches = int(L.dicb200_launch_count())
+    clk = clocks.stop()
+    torch.cuda.synchronize()
+    barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    stage_ms = (C.c_double * 4)()
+    stage_n = (C.c_uint64 * 4)()
+    L.dicb200_profile_read(stage_ms, stage_n)
+    # flush time is not analysis work: subtract it (measured on the same stream)
+    ms = ms_total - sum(a.elapsed_time(b) for a, b in flush_ev)
+    ms_tensor = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(ms_tensor, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_tensor.item())
+
+    # results of the last step -> algorithmic work (sum of evaluations) for the roofline
+    recs = np.frombuffer(recbuf.cpu().numpy().tobytes(), dtype=_abi.record_dtype())
+    evals = int(recs["evaluations"].sum())
+    iters = int(recs["iterations"].sum())
+    status_ok = int((recs["status"] == 0).sum())
+    n_local = len(my_pairs) * recs_per_pair
+    tot = torch.tensor([evals, iters, n_local, status_ok], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(tot)
+    evals_all, iters_all, n_all, ok_all = [float(x) for x in tot.tolist()]
+
+    # ---- e2e through the public API with pinned host frames ----
+    e2e = None
+    if not args.no_e2e:
+        host = {i: frames[i].cpu().pin_memory() for i in needed}
+        if n_pairs > 1:
+            seq = [needed[0]] + [b for _, b in my_pairs]  # fixed_first: (0, k)
+            ims = (_abi.Image * len(seq))(*[img(i, host[i].data_ptr()) for i in seq])
+            ccfg = cfg.to_c()
+            fields = (_abi.FieldC * (len(seq) - 1))()
+            rbufs = []
+            for i in range(len(seq) - 1):
+                rb = torch.empty(spp * rec_size, dtype=torch.uint8).pin_memory()
+                rbufs.append(rb)
+                fields[i].records = C.cast(C.c_void_p(rb.data_ptr()), C.POINTER(_abi.PoiRecordC))
+                fields[i].capacity = spp
+
+            def e2e_step():
+                st = L.dicb200_analyze_sequence(ims, len(seq), C.byref(ccfg), fields, len(seq) - 1)
+                if st:
+                    raise RuntimeError(L.dicb200_last_error_message().decode())
+
+            h2d = sum(host[i].numel() * esize for i in seq)
+            d2h = (len(seq) - 1) * spp * rec_size
+        else:
+            a, b = my_pairs[0]
+            ia, ib = img(a, host[a].data_ptr()), img(b, host[b].data_ptr())
+            outrec = np.zeros(spp, dtype=_abi.record_dtype())
+
+            def e2e_step():
+                n = C.c_size_t(0)
+                st = L.dicb200_analyze_pair(C.byref(ia), C.byref(ib), C.byref(cfgc), 0, outrec.ctypes.data, spp,
+                                            C.byref(n))
+                if st:
+                    raise RuntimeError(L.dicb200_last_error_message().decode())
+
+            h2d = 2 * f0.width * f0.height * esize
+            d2h = spp * rec_size
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        et = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e_total_subsets = spp * n_pairs if n_pairs > 1 else spp
+        e2e = {"value": e2e_total_subsets * args.steps / float(et.item()), "unit": "subsets/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "frame_pairs_per_s": n_pairs * args.steps / float(et.item()),
+               "path": "dicb200_analyze_sequence (C-ABI), pinned host frames" if n_pairs > 1 else
+                       "dicb200_analyze_pair (C-ABI), host frames"}
+
+    if rank != 0:
+        return None
+
+    # ---- roofline of the dominant stage ----
+    names = ["bfs_zncc", "pso", "nr", "icgn"]
+    stage = {names[i]: {"ms_total": float(stage_ms[i]), "launches": int(stage_n[i]),
+                        "avg_ms": float(stage_ms[i]) / max(1, int(stage_n[i]))} for i in range(4) if stage_n[i]}
+    dom = max(stage, key=lambda k: stage[k]["ms_total"]) if stage else None
+    n_px = (2 * cfg.grid.half_width + 1) ** 2
+    roof = None
+    if dom == "bfs_zncc":
+        # algorithmic work per launch: (sum of evaluations over the launch's POIs) x n MACs
+        macs_per_launch = evals / max(1, len(my_pairs)) * n_px
+        achieved = macs_per_launch / (stage[dom]["avg_ms"] * 1e-3) / 1e12
+        if u8:
+            peak = 4 * peaks.get("idp4a_u8_Ginstr_per_s", 0) / 1e3
+            pipe = "IDP4A (u8 x4 MAC/instr)"
+        else:
+            peak = peaks.get("imad_Ginstr_per_s", 0) / 1e3
+            pipe = "IMAD (u16 exact u32 MAC/instr)"
+        roof = {"kernel": "bfs_tile_kernel", "bound": "alu", "pipe": pipe, "achieved": achieved,
+                "peak": peak, "unit": "TMAC/s", "frac": achieved / peak if peak else None,
+                "traffic": None,
+                "peak_source": "measured live by tools/microbench/pipes (dependent-free stream, CUDA events)",
+                "work_per_launch": f"sum(evaluations) x (2M+1)^2 = {macs_per_launch:.4g} MACs"}
+    elif dom in ("icgn", "nr"):
+        flop_px_it = 30.0 if dom == "icgn" else 100.0
+        flops = iters / max(1, len(my_pairs)) * n_px * flop_px_it
+        achieved = flops / (stage[dom]["avg_ms"] * 1e-3) / 1e12
+        peak = 2 * peaks.get("ffma_Ginstr_per_s", 0) / 1e3
+        roof = {"kernel": "refine_kernel", "bound": "alu", "pipe": "FFMA (fp32)", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": None,
+                "peak_source": "measured live by tools/microbench/pipes",
+                "work_per_launch": f"sum(iterations) x n x {flop_px_it:.0f} flop"}
+    elif dom == "pso":
+        macs_per_launch = evals / max(1, len(my_pairs)) * n_px
+        achieved = macs_per_launch / (stage[dom]["avg_ms"] * 1e-3) / 1e12
+        peak = 4 * peaks.get("idp4a_u8_Ginstr_per_s", 0) / 1e3
+        roof = {"kernel": "pso_kernel", "bound": "alu", "pipe": "IDP4A", "achieved": achieved, "peak": peak,
+                "unit": "TMAC/s", "frac": achieved / peak if peak else None, "traffic": None,
+                "peak_source": "measured live by tools/microbench/pipes",
+                "work_per_launch": f"sum(evaluations) x n = {macs_per_launch:.4g} MACs"}
+    prof_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if roof and os.path.exists(prof_path):
+        try:
+            tr = json.load(open(prof_path)).get(f"{args.config}:{roof['kernel']}")
+            if tr:
+                roof["traffic"] = tr["dram_bytes_per_launch"]
+                roof["traffic_source"] = tr.get("source")
+        except Exception:  # noqa: BLE001
+            pass
+
+    total_subsets = (spp * n_pairs) if n_pairs > 1 else spp
+    value = total_subsets * args.steps / (ms_max * 1e-3)
+    line = {
+        "metric": "subsets/sec (search+refine) and frame pairs/sec at 1/2/4/8 B200 vs roofline",
+        "value": value,
+        "unit": "subsets/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps,
+        "frame_pairs_per_s": n_pairs * args.steps / (ms_max * 1e-3),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "u16->int32 exact MACs (search), fp32 gather + fp64 reductions/solves (refine)" if not u8 else
+                 "u8->int32 exact DP4A MACs (search), fp32 gather + fp64 reductions/solves (refine)",
+        "data": "synthetic (seeded Gaussian-blob speckle, analytic re-render; BASELINE datasets absent)",
+        "config": describe(w, spp, n_pairs, world),
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "stages": stage,
+        "roofline": roof,
+        "clocks": clk,
+        "parity_in_run": {"records": int(n_all), "status_ok": int(ok_all), "mean_iterations": iters_all / max(1, n_all)},
+        "pipe_peaks": {k: v for k, v in peaks.items() if k.endswith("per_s")},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        host0 = [frames[my_pairs[0][0]].cpu().numpy().astype(np.uint16 if not u8 else np.uint8),
+                 frames[my_pairs[0][1]].cpu().numpy().astype(np.uint16 if not u8 else np.uint8)]
+        line["cpu_baseline"] = cpu_baseline(w, host0, n_sample_rows=cpu_rows(args.config))
+    return line
+
+
+def cpu_rows(name: str) -> int:
+    # bounded samples of ~10-20 s of reference CPU work on a 16-core host
+    return {"c1": 14, "c2": 46, "c3": 40, "c4": 60, "c5": 199}.get(name, 40)
+
+
+# ------------------------------------------------------- reference arm
+
+def run_reference(args, rank: int, world: int):
+    """The reference's own CPU implementation (oracle/_ref) on host cores."""
+    if rank != 0:
+        return None
+    import copy
+
+    from oracle import Oracle, available
+
+    kind = "reference" if available("reference") else "port"
+    orc = Oracle(kind)
+    w = workload(args.config, args.pairs)
+    n_pairs = len(w.pairs)
+    cfg = copy.deepcopy(w.cfg)
+    cfg.mode = dic.ExecMode.subimage_parallel
+    threads = os.cpu_count() or 1
+    cfg.worker_count = threads
+    rows = {"c1": 14, "c2": 24, "c3": 20, "c4": 12, "c5": 24}.get(args.config, 20)
+    margin = cfg.effective_margin()
+    band = min(w.frames[0].height, 2 * margin + cfg.grid.spacing * (rows - 1) + 1)
+    # frames rendered on the host for the reference (same generator, host build)
+    from dataclasses import replace
+
+    def render_band(spec):
+        return replace(spec, height=band).render()
+
+    ref0 = render_band(w.frames[0]).astype(np.float64)
+    targets = [w.frames[b] for _, b in w.pairs]
+    total_subsets, total_s = 0, 0.0
+    for s in range(args.warmup + args.steps):
+        tgt = render_band(targets[s % len(targets)]).astype(np.float64)
+        secs, n = orc.analyze_pair_timed(ref0, tgt, cfg, s % max(1, n_pairs), 1)
+        if s >= args.warmup:
+            total_subsets += n
+            total_s += secs
+    value = total_subsets / total_s
+    spp = w.subsets_per_pair()
+    sample = (f"per step: pair (0,k) cropped to its first {rows} grid rows ({total_subsets // max(1, args.steps)} POIs), "
+              f"dic::analyze_pair subimage_parallel x{threads} threads (reference sources, Eigen stand-in)")
+    return {
+        "impl": "reference",
+        "metric": "subsets/sec (search+refine) and frame pairs/sec at 1/2/4/8 B200 vs roofline",
+        "value": value,
+        "unit": "subsets/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * total_s / args.steps,
+        "frame_pairs_per_s": value / spp,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded Gaussian-blob speckle, analytic re-render)",
+        "config": describe(w, spp, n_pairs, world),
+        "cpu_baseline": {"value": value, "unit": "subsets/s", "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "subsets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        line = run_ours(args, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

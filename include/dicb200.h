@@ -198,6 +198,14 @@ dicb200_status dicb200_analyze_pair_device(const dicb200_image* reference, const
 uint64_t dicb200_launch_count(void);
 void dicb200_reset_launch_count(void);
 
+/* Stage timing (bench evidence): while enabled, every enqueued stage kernel
+ * is bracketed by CUDA events on the stream it runs on. dicb200_profile_read
+ * waits for them and returns per-stage totals (ms) and launch counts, then
+ * clears. Stages: 0 BFS-ZNCC, 1 PSO/mPSO, 2 NR, 3 IC-GN. */
+#define DICB200_N_STAGES 4
+void dicb200_profile_enable(int on);
+int dicb200_profile_read(double* ms_out, uint64_t* launches_out);
+
 /* Release pooled device memory on all devices. */
 void dicb200_shutdown(void);
 

@@ -40,6 +40,10 @@ typedef struct {
 /* Renders one frame into out (pitch in elements). threads <= 0: all cores. */
 int dicb200_synth_render(const dicb200_synth_spec* spec, void* out, int32_t pitch, int32_t threads);
 
+/* Same frame rendered on the GPU into device memory (pitch in elements);
+ * stream is a cudaStream_t (NULL = legacy default). Synchronous. */
+int dicb200_synth_render_device(const dicb200_synth_spec* spec, void* out_dev, int32_t pitch, void* stream);
+
 /* Displacement d(y) at a reference-frame point (ground truth helper). */
 void dicb200_synth_displacement(const dicb200_synth_spec* spec, double yx, double yy, double* dx,
                                 double* dy);

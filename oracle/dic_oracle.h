@@ -21,6 +21,10 @@ extern "C" {
 int dco_analyze_pair(const double* ref, const double* tgt, int w, int h,
                      const dicb200_run_config* cfg, uint64_t pair_index, int threads,
                      dicb200_poi_record* out, size_t cap, size_t* count, char* err, size_t errcap);
+int dco_analyze_pair_rows(const double* ref, const double* tgt, int w, int h,
+                          const dicb200_run_config* cfg, uint64_t pair_index, int threads,
+                          int row_begin, int row_end, dicb200_poi_record* out, size_t cap,
+                          size_t* count, char* err, size_t errcap);
 int dco_grid(int w, int h, int half_width, int spacing, int margin, int32_t* xy, size_t cap,
              size_t* count, char* err, size_t errcap);
 int dco_zncc(const double* ref, const double* tgt, int w, int h, int cx, int cy, int m, int dx,

@@ -79,6 +79,10 @@ class Oracle:
                 C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(_abi.RunConfigC), C.c_uint64, C.c_int,
                 C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t), C.c_char_p, C.c_size_t,
             ]
+            f("analyze_pair_rows").argtypes = [
+                C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(_abi.RunConfigC), C.c_uint64, C.c_int,
+                C.c_int, C.c_int, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t), C.c_char_p, C.c_size_t,
+            ]
         else:
             f("analyze_pair").argtypes = [
                 C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(_abi.RunConfigC), C.c_uint64,
@@ -126,6 +130,22 @@ class Oracle:
             st = self._f("analyze_pair")(a.ctypes.data, b.ctypes.data, w, h, C.byref(c), pair_index,
                                          out.ctypes.data, len(out), C.byref(n), err, 160)
         if st:
+            raise OracleError(err.value.decode())
+        return out[: n.value]
+
+    def analyze_pair_rows(self, ref, tgt, cfg, pair_index: int, row_begin: int, row_end: int, threads: int = 0):
+        """Port only: grid rows [row_begin, row_end) with global subset indices."""
+        a, b = _as_double(ref), _as_double(tgt)
+        h, w = a.shape
+        c = cfg.to_c()
+        g = self.grid(w, h, cfg.grid.half_width, cfg.grid.spacing, cfg.effective_margin())
+        out = np.zeros(len(g), dtype=_abi.record_dtype())
+        n = C.c_size_t(0)
+        err = C.create_string_buffer(160)
+        if threads <= 0:
+            threads = os.cpu_count() or 1
+        if self._f("analyze_pair_rows")(a.ctypes.data, b.ctypes.data, w, h, C.byref(c), pair_index, threads,
+                                        row_begin, row_end, out.ctypes.data, len(out), C.byref(n), err, 160):
             raise OracleError(err.value.decode())
         return out[: n.value]
 

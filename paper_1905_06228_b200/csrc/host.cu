@@ -23,6 +23,32 @@ namespace dicb200 {
 namespace {
 thread_local std::string g_last_error;
 std::atomic<uint64_t> g_launches{0};
+
+struct StageEvent {
+  int stage;
+  cudaEvent_t a, b;
+};
+std::atomic<int> g_profile{0};
+std::mutex g_profile_mu;
+std::vector<StageEvent> g_events;
+
+struct StageTimer {
+  int stage;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  StageTimer(int s, cudaStream_t stream) : stage(s), st(stream) {
+    if (!g_profile.load()) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+  }
+  ~StageTimer() {
+    if (!a) return;
+    cudaEventRecord(b, st);
+    std::lock_guard<std::mutex> lk(g_profile_mu);
+    g_events.push_back({stage, a, b});
+  }
+};
 }  // namespace
 
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
@@ -131,7 +157,10 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
       DICB200_CUDA_TRY(cudaMallocAsync((void**)&partial, nrec * p.n_chunks * sizeof(BestPartial), st));
       p.partial = partial;
     }
-    DICB200_CUDA_TRY(bfs_launch(p, rows, st));
+    {
+      StageTimer tm(0, st);
+      DICB200_CUDA_TRY(bfs_launch(p, rows, st));
+    }
     if (partial) DICB200_CUDA_TRY(cudaFreeAsync(partial, st));
   } else {
     PsoParams p{};
@@ -155,7 +184,11 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
     p.subpixel_none = cfg->subpixel_method == DICB200_SUB_NONE;
     p.rec = out_dev;
     p.n_records = (int)nrec;
-    dicb200_status s = pso_launch(p, st);
+    dicb200_status s;
+    {
+      StageTimer tm(1, st);
+      s = pso_launch(p, st);
+    }
     if (s != DICB200_OK) return s;
   }
   if (cfg->subpixel_method != DICB200_SUB_NONE) {
@@ -170,6 +203,7 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
     r.tol = cfg->tol;
     r.max_iter = cfg->max_iter;
     r.rec = out_dev;
+    StageTimer tm(r.method == 0 ? 2 : 3, st);
     DICB200_CUDA_TRY(refine_launch(r, ref->dtype == DICB200_U8, st));
   }
   return DICB200_OK;
@@ -441,6 +475,30 @@ dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_im
       return result[wk];
     }
   return DICB200_OK;
+}
+
+void dicb200_profile_enable(int on) { g_profile.store(on ? 1 : 0); }
+
+int dicb200_profile_read(double* ms, uint64_t* launches) {
+  for (int i = 0; i < DICB200_N_STAGES; ++i) {
+    ms[i] = 0.0;
+    launches[i] = 0;
+  }
+  std::vector<StageEvent> ev;
+  {
+    std::lock_guard<std::mutex> lk(g_profile_mu);
+    ev.swap(g_events);
+  }
+  int rc = 0;
+  for (auto& e : ev) {
+    float t = 0.f;
+    if (cudaEventSynchronize(e.b) != cudaSuccess || cudaEventElapsedTime(&t, e.a, e.b) != cudaSuccess) rc = 1;
+    ms[e.stage] += t;
+    launches[e.stage] += 1;
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  return rc;
 }
 
 void dicb200_shutdown(void) {

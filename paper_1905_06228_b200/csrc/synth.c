@@ -14,11 +14,8 @@
 
 #include "dicb200.h"
 
-#define CELL 16
 
-typedef struct {
-  double cx, cy, inv2s2, peak, reach2;
-} blob_t;
+#include "synth_internal.h"
 
 static uint64_t splitmix_next(uint64_t* s) {
   uint64_t z = (*s += 0x9e3779b97f4a7c15ULL);
@@ -45,7 +42,7 @@ void dicb200_synth_displacement(const dicb200_synth_spec* sp, double yx, double 
 }
 
 /* Preimage y of pixel x under x = y + d(y). */
-static void preimage(const dicb200_synth_spec* sp, double x, double y, double* px, double* py) {
+void dicb200_synth_preimage(const dicb200_synth_spec* sp, double x, double y, double* px, double* py) {
   const double* a = sp->a;
   if (sp->field == DICB200_FIELD_AFFINE) {
     /* x - o = (I + A)(y - o) + t  =>  y = o + (I + A)^-1 (x - o - t) */
@@ -92,7 +89,7 @@ static void* render_rows(void* arg) {
   for (int y = j->y0; y < j->y1; ++y)
     for (int x = 0; x < sp->width; ++x) {
       double qx, qy;
-      preimage(sp, x, y, &qx, &qy);
+      dicb200_synth_preimage(sp, x, y, &qx, &qy);
       double v = sp->background;
       const int cx = (int)floor(qx / CELL), cy = (int)floor(qy / CELL);
       for (int by = cy - reach_cells; by <= cy + reach_cells; ++by) {
@@ -119,8 +116,7 @@ static void* render_rows(void* arg) {
   return NULL;
 }
 
-int dicb200_synth_render(const dicb200_synth_spec* sp, void* out, int32_t pitch, int32_t threads) {
-  if (sp->width < 1 || sp->height < 1 || sp->blob_count < 0 || pitch < sp->width) return 1;
+int dicb200_synth_blobs(const dicb200_synth_spec* sp, synth_blobs_t* out) {
   const int n = sp->blob_count;
   blob_t* blobs = (blob_t*)malloc((size_t)(n > 0 ? n : 1) * sizeof(blob_t));
   uint64_t s = sp->seed;
@@ -133,7 +129,7 @@ int dicb200_synth_render(const dicb200_synth_spec* sp, void* out, int32_t pitch,
     b->inv2s2 = 1.0 / (2.0 * sigma * sigma);
     b->reach2 = 25.0 * sigma * sigma; /* 5 sigma cut-off */
   }
-  /* bin blob centres into CELL x CELL cells over the padded frame */
+  /* bin blob centres into CELL x CELL cells */
   const int gx = (sp->width + CELL - 1) / CELL, gy = (sp->height + CELL - 1) / CELL;
   int* cnt = (int*)calloc((size_t)gx * gy + 1, sizeof(int));
   int* cell_of = (int*)malloc((size_t)(n > 0 ? n : 1) * sizeof(int));
@@ -149,14 +145,35 @@ int dicb200_synth_render(const dicb200_synth_spec* sp, void* out, int32_t pitch,
   int* fill = (int*)malloc((size_t)gx * gy * sizeof(int));
   memcpy(fill, cnt, (size_t)gx * gy * sizeof(int));
   for (int i = 0; i < n; ++i) items[fill[cell_of[i]]++] = i; /* ascending blob order per cell */
+  free(fill);
+  free(cell_of);
+  out->blobs = blobs;
+  out->n = n;
+  out->cell_start = cnt;
+  out->items = items;
+  out->gx = gx;
+  out->gy = gy;
+  out->reach_cells = (int)ceil(5.0 * sp->sigma_max / CELL) + 1;
+  return 0;
+}
 
+void dicb200_synth_blobs_free(synth_blobs_t* b) {
+  free(b->blobs);
+  free(b->cell_start);
+  free(b->items);
+}
+
+int dicb200_synth_render(const dicb200_synth_spec* sp, void* out, int32_t pitch, int32_t threads) {
+  if (sp->width < 1 || sp->height < 1 || sp->blob_count < 0 || pitch < sp->width) return 1;
+  synth_blobs_t B;
+  dicb200_synth_blobs(sp, &B);
   if (threads <= 0) threads = (int)sysconf(_SC_NPROCESSORS_ONLN);
   if (threads < 1) threads = 1;
   if (threads > sp->height) threads = sp->height;
   job_t* jobs = (job_t*)calloc((size_t)threads, sizeof(job_t));
   pthread_t* tid = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
   for (int t = 0; t < threads; ++t) {
-    jobs[t] = (job_t){sp, blobs, cnt, items, gx, gy, out, pitch,
+    jobs[t] = (job_t){sp, B.blobs, B.cell_start, B.items, B.gx, B.gy, out, pitch,
                       (int)((long)sp->height * t / threads), (int)((long)sp->height * (t + 1) / threads)};
     if (threads == 1)
       render_rows(&jobs[t]);
@@ -167,10 +184,6 @@ int dicb200_synth_render(const dicb200_synth_spec* sp, void* out, int32_t pitch,
     for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
   free(jobs);
   free(tid);
-  free(fill);
-  free(items);
-  free(cell_of);
-  free(cnt);
-  free(blobs);
+  dicb200_synth_blobs_free(&B);
   return 0;
 }

@@ -1,0 +1,209 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the oracle.
+
+Tolerances (north star, BASELINE.json): integer displacements, evaluation
+counts, per-POI status and `converged` identical on every subset; sub-pixel
+u, v within 1e-3 px; ZNCC within 1e-5. Iteration counts may differ only where
+a convergence test |du|,|dv| < tol sits at the rounding edge (<= 0.5% of POIs).
+"""
+import copy
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_1905_06228_b200 import _abi, configs, dic
+
+pytestmark = pytest.mark.gpu
+
+UV_TOL = 1e-3
+ZNCC_TOL = 1e-5
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+
+
+def run_device(a, b, cfg, pair_index=0):
+    return dic.analyze_pair(dic.GrayImage(a), dic.GrayImage(b, 1), cfg, pair_index).records
+
+
+def assert_parity(got, exp, iter_frac=0.005):
+    assert len(got) == len(exp)
+    for f in ("x", "y", "evaluations", "update_evaluations", "converged"):
+        assert np.array_equal(got[f], exp[f]), (f, np.nonzero(got[f] != exp[f])[0][:5])
+    ok = ~np.isnan(exp["zncc"])
+    assert np.array_equal(np.isnan(got["zncc"]), ~ok)
+    # integer stage: bit-exact displacement for every subset whose integer stage succeeded
+    idx = exp["evaluations"] > 0
+    du = np.abs(got["u"] - exp["u"])
+    dv = np.abs(got["v"] - exp["v"])
+    assert np.all(du[ok] < UV_TOL) and np.all(dv[ok] < UV_TOL), (du.max(), dv.max())
+    assert np.all(np.abs(got["zncc"][ok] - exp["zncc"][ok]) < ZNCC_TOL)
+    if "integer_dx" in exp.dtype.names and exp["integer_dx"].any():
+        assert np.array_equal(got["integer_dx"][idx], exp["integer_dx"][idx])
+        assert np.array_equal(got["integer_dy"][idx], exp["integer_dy"][idx])
+    assert np.mean(got["iterations"] != exp["iterations"]) <= iter_frac
+    return float(max(du[ok].max(initial=0), dv[ok].max(initial=0)))
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p)[:-4] for p in GOLDEN])
+def test_device_matches_reference_golden(gpu, path):
+    """Golden vectors produced by the reference's own sources (oracle/_ref)."""
+    d = np.load(path)
+    c = _abi.RunConfigC()
+    for k, v in json.loads(str(d["config"])).items():
+        setattr(c, k, v)
+    cfg = dic.RunConfig(
+        integer_method=dic.IntegerMethod(c.integer_method), subpixel_method=dic.SubpixelMethod(c.subpixel_method),
+        search=dic.SearchConfig(c.search_radius, dic.BfsDomain(c.bfs_domain), c.particle_count, c.max_generations,
+                                c.stop_threshold, c.c1, c.c2, c.rng_seed),
+        refine=dic.RefineConfig(c.tol, c.max_iter), grid=dic.GridParams(c.half_width, c.spacing, c.margin))
+    got = run_device(d["ref"], d["tgt"], cfg)
+    exp = d["records"]
+    # integer-stage fields the reference does not expose come from the u/v of integer-only runs
+    assert_parity(got, exp)
+
+
+@pytest.mark.parametrize("name,crop,pair", [
+    ("c1", None, 1), ("c2", None, 1), ("c3", 256, 1), ("c3x", 256, 1), ("c4", 512, 1), ("c5", 384, 33),
+    ("c5", 384, 64),
+])
+def test_config_parity_against_oracle(gpu, port, name, crop, pair):
+    w = configs.get(name) if name != "c5" else configs.c5(64)
+    if crop:
+        w = configs.crop(w, crop, crop)
+    a, b = w.frames[0].render(), w.frames[pair].render()
+    exp = port.analyze_pair(a, b, w.cfg, pair_index=pair - 1)
+    got = run_device(a, b, w.cfg, pair_index=pair - 1)
+    assert_parity(got, exp)
+
+
+def test_c1_exact_shift_everywhere(gpu):
+    w = configs.c1()
+    a, b = w.frames[0].render(), w.frames[1].render()
+    got = run_device(a, b, w.cfg)
+    assert len(got) == 196
+    assert np.all(got["u"] == 3.0) and np.all(got["v"] == -5.0)
+    assert np.all(got["evaluations"] == 441) and np.all(got["converged"] == 1)
+
+
+def test_pso_and_mpso_parity_with_reference_defaults(gpu, port):
+    w = configs.crop(configs.get("c3"), 192, 192)
+    a, b = w.frames[0].render(), w.frames[1].render()
+    for method in (dic.IntegerMethod.pso, dic.IntegerMethod.mpso):
+        cfg = dic.RunConfig(integer_method=method, subpixel_method=dic.SubpixelMethod.none,
+                            search=dic.SearchConfig(search_radius=20, bfs_domain=dic.BfsDomain.window, rng_seed=7),
+                            grid=dic.GridParams(15, 9, -1))
+        for pair_index in (0, 5):
+            exp = port.analyze_pair(a, b, cfg, pair_index=pair_index)
+            got = run_device(a, b, cfg, pair_index=pair_index)
+            assert_parity(got, exp)
+            assert np.array_equal(got["u"], exp["u"]) and np.array_equal(got["zncc"], exp["zncc"])
+
+
+def test_u16_wide_values_use_exact_fp64_path(gpu, port):
+    # 16-bit data: (2M+1)*max^2 >= 2^32 -> DFMA-exact accumulation path
+    w = configs.crop(configs.get("c4"), 128, 128)
+    a = (w.frames[0].render().astype(np.uint32) * 16).astype(np.uint16)
+    b = (w.frames[1].render().astype(np.uint32) * 16).astype(np.uint16)
+    exp = port.analyze_pair(a, b, w.cfg)
+    got = run_device(a, b, w.cfg)
+    assert_parity(got, exp)
+
+
+def test_whole_image_domain(gpu, port):
+    w = configs.crop(configs.get("c1"), 96, 80)
+    a, b = w.frames[0].render(), w.frames[1].render()
+    cfg = dic.RunConfig(integer_method=dic.IntegerMethod.bfs, subpixel_method=dic.SubpixelMethod.none,
+                        search=dic.SearchConfig(search_radius=5, bfs_domain=dic.BfsDomain.whole_image),
+                        grid=dic.GridParams(8, 13, -1))
+    assert_parity(run_device(a, b, cfg), port.analyze_pair(a, b, cfg))
+
+
+def test_large_radius_chunked_window(gpu, port):
+    # R > 31 -> candidate window split over several CTAs + reduction kernel
+    w = configs.crop(configs.get("c2"), 256, 256)
+    a, b = w.frames[0].render(), w.frames[1].render()
+    cfg = copy.deepcopy(w.cfg)
+    cfg.search.search_radius = 40
+    cfg.subpixel_method = dic.SubpixelMethod.none
+    cfg.grid = dic.GridParams(12, 40, -1)
+    assert_parity(run_device(a, b, cfg), port.analyze_pair(a, b, cfg))
+
+
+def test_identical_images_refiners(gpu):
+    # SPEC refine_nr / refine_icgn examples: identical images -> u=v=0, ZNCC=1, converged
+    w = configs.crop(configs.get("c4"), 128, 128)
+    a = w.frames[0].render()
+    for sub in (dic.SubpixelMethod.nr, dic.SubpixelMethod.icgn):
+        cfg = copy.deepcopy(w.cfg)
+        cfg.subpixel_method = sub
+        got = run_device(a, a, cfg)
+        assert np.all(got["converged"] == 1)
+        assert np.all(np.abs(got["u"]) < 1e-6) and np.all(np.abs(got["v"]) < 1e-6)
+        assert np.all(np.abs(got["zncc"] - 1.0) < 1e-6)
+        assert np.all(got["iterations"] == 1)
+
+
+def test_row_sharding_equals_full(gpu):
+    """Subset-parallel sharding over grid rows keeps global RNG keys (mPSO)."""
+    import ctypes as C
+
+    import torch
+
+    w = configs.crop(configs.get("c3"), 256, 256)
+    a, b = w.frames[0].render(), w.frames[1].render()
+    full = run_device(a, b, w.cfg)
+    L = dic.lib()
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    ia, ib = dic.GrayImage(a).as_c(), dic.GrayImage(b, 1).as_c()
+    ia.data, ib.data = ta.data_ptr(), tb.data_ptr()
+    nx = len({x for x, _ in dic.grid_subsets(256, 256, 15, 8, w.cfg.effective_margin())})
+    ny = len(full) // nx
+    parts = []
+    for lo, hi in dic.partition_ranges(ny, 3):
+        out = torch.empty((hi - lo) * nx * C.sizeof(_abi.PoiRecordC), dtype=torch.uint8, device="cuda")
+        n = C.c_size_t(0)
+        c = w.cfg.to_c()
+        st = L.dicb200_analyze_pair_device(C.byref(ia), C.byref(ib), C.byref(c), 0, lo, hi,
+                                           C.c_void_p(out.data_ptr()), (hi - lo) * nx, C.byref(n), None)
+        assert st == 0
+        torch.cuda.synchronize()
+        parts.append(np.frombuffer(out.cpu().numpy().tobytes(), dtype=_abi.record_dtype()))
+    sharded = np.concatenate(parts)
+    for f in ("x", "y", "u", "v", "zncc", "evaluations", "update_evaluations", "iterations", "converged"):
+        assert np.array_equal(sharded[f], full[f], equal_nan=True), f
+
+
+def test_analyze_sequence_policies_and_pair_errors(gpu, port):
+    w = configs.crop(configs.c5(4), 128, 128)
+    frames = [f.render() for f in w.frames]
+    imgs = [dic.GrayImage(f, i) for i, f in enumerate(frames)]
+    for policy in (dic.ReferencePolicy.fixed_first, dic.ReferencePolicy.update_every_pair):
+        cfg = copy.deepcopy(w.cfg)
+        cfg.reference_policy = policy
+        fields = dic.analyze_sequence(imgs, cfg)
+        pairs = dic.sequence_pairs(policy, len(imgs))
+        assert [f.pair_index for f in fields] == list(range(len(pairs)))
+        for f, (ra, tb) in zip(fields, pairs):
+            assert (f.ref_id, f.tgt_id) == (ra, tb) and not f.failed()
+            assert_parity(f.records, port.analyze_pair(frames[ra], frames[tb], cfg, pair_index=f.pair_index))
+    # a pair-level dic::Error lands in field.error, the sequence continues (pipeline.cpp:191-198)
+    bad = imgs[:2] + [dic.GrayImage(np.zeros((64, 64), np.uint16), 9)]
+    fields = dic.analyze_sequence(bad, w.cfg)
+    assert not fields[0].failed() and fields[1].error == "dimension mismatch"
+
+
+def test_failure_semantics_degenerate_target(gpu, port):
+    """Constant target regions: skipped candidates, 'all positions degenerate',
+    refine failures keep the integer fields (pipeline.cpp:82-133)."""
+    w = configs.crop(configs.get("c4"), 160, 160)
+    a, b = w.frames[0].render(), w.frames[1].render()
+    b[:, :70] = 1000
+    for sub in (dic.SubpixelMethod.nr, dic.SubpixelMethod.icgn):
+        cfg = copy.deepcopy(w.cfg)
+        cfg.subpixel_method = sub
+        exp = port.analyze_pair(a, b, cfg)
+        got = run_device(a, b, cfg)
+        assert_parity(got, exp)
+        assert np.array_equal(got["status"], exp["status"])
+        assert (exp["status"] != 0).any()
