@@ -3,20 +3,25 @@
 // subpixel.cpp:224-299), first-order warp, bilinear interpolation
 // (interp_bilinear / grad_bilinear, subpixel.cpp:59-128).
 //
-// One CTA per POI, NT threads, each thread owns PPT subset pixels in
-// registers for the whole solve (reference values, centred values and, for
-// IC-GN, the steepest-descent gradients). Per iteration: fused warp + gather
-// + bilinear in fp32 on subset-local coordinates (integer base kept apart, so
-// coordinates near 2048 px lose nothing), per-thread fp32 partials over
-// <= PPT terms, block reductions and the 6x6 algebra in fp64. The reference's
-// two-pass structure (mean, then centred sums) is kept per iteration, so each
-// e_k / coeff_k is formed exactly as subpixel.cpp:258,331 do.
+// One CTA (8 warps) per POI; every thread owns PPT subset pixels in registers
+// for the whole solve. The target neighbourhood of the integer estimate is
+// staged once in shared memory as fp32 (taps that drift outside it fall back
+// to global loads), so each iteration is ONE pass over the pixels: warp +
+// gather + bilinear (+ gradient for NR) in fp32 on subset-local coordinates,
+// per-thread fp32 partials of every sum the update needs, one block
+// reduction in fp64, and warp 0 doing the 6x6 algebra in fp64.
 //
-// IC-GN Hessian: with integer gray levels, (2*grad)^2 * {1,dx,dy,dx^2,dxdy,dy^2}
-// are integers < 2^53, so the fp64 moment sums are EXACT and the Hessian —
-// and its pivoted LDL^T (linalg.cuh) — is bit-identical to the reference's.
-// Failure semantics follow pipeline.cpp:82-133: any stage error sets the
-// status, clears `converged` and keeps the integer-stage fields.
+// The reference forms e_k = f_k - (nf/ng)(g_k - gbar) (IC-GN, :331) and
+// coeff_k = f_k - (cross/ng^2)(g_k - gbar) (NR, :258) per pixel, which needs
+// gbar and ng before the update sums (three passes). Here the update sums are
+// expanded exactly,
+//   sum e_k sd_k = sum f_k sd_k - (nf/ng) [ sum g'_k sd_k - (gbar - fbar) sum sd_k ],
+// with g' = g - fbar, so one pass suffices; the reference-side sums
+// (sum f sd, sum sd, and the Hessian) are precomputed in fp64 (the Hessian
+// EXACTLY: (2 grad)^2 * {1,dx,dy,dx^2,dxdy,dy^2} are integers < 2^53).
+// Convergence test, failure semantics (guard band M+2, domain checks,
+// |det| < 1e-8, LDLT failure, non-finite step, degenerate target) and the
+// final re-sample + ZNCC follow subpixel.cpp / pipeline.cpp:82-133.
 #include "common.cuh"
 #include "linalg.cuh"
 #include "refine.cuh"
@@ -25,57 +30,56 @@ namespace dicb200 {
 
 namespace {
 
-constexpr int kMaxWarps = 8;
-constexpr int kMaxNV = 24;
-
-struct RedBuf {
-  double v[2][kMaxWarps][kMaxNV];
-};
-
-// Sum NV per-thread doubles over the block; every thread gets the totals.
-template <int NV>
-__device__ __forceinline__ void block_sum(double (&v)[NV], RedBuf& rb, int& buf) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int i = 0; i < NV; ++i) rb.v[buf][warp][i] = v[i];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    double s = rb.v[buf][0][i];
-    for (int w = 1; w < nw; ++w) s += rb.v[buf][w][i];
-    v[i] = s;
-  }
-  buf ^= 1;
-}
+constexpr int kNT = 256;
+constexpr int kWarps = kNT / 32;
+constexpr int kPad = 4;
+constexpr int kRedMax = 40;
 
 template <typename Pix>
-__device__ __forceinline__ float px(const ImageView& im, int x, int y) {
+__device__ __forceinline__ float gpx(const ImageView& im, int x, int y) {
   return (float)__ldg(reinterpret_cast<const Pix*>(im.data) + (size_t)y * im.pitch + x);
+}
+
+struct Win {
+  const float* w;  // S x S fp32 copy of the target around (bx, by), row pitch P
+  int S, P, ox, oy;  // ox, oy: global coords of w[0]
+};
+
+template <typename Pix>
+__device__ __forceinline__ float tap(const Win& wn, const ImageView& im, int x, int y) {
+  const int lx = x - wn.ox, ly = y - wn.oy;
+  if ((unsigned)lx < (unsigned)wn.S && (unsigned)ly < (unsigned)wn.S) return wn.w[ly * wn.P + lx];
+  return gpx<Pix>(im, x, y);
 }
 
 // interp_bilinear (subpixel.cpp:59-102) at global (bx + xl, by + yl).
 template <typename Pix>
-__device__ __forceinline__ bool bilinear(const ImageView& im, int bx, int by, float xl, float yl, float& g) {
+__device__ __forceinline__ bool bilinear(const Win& wn, const ImageView& im, int bx, int by, float xl, float yl,
+                                         float& g) {
   if (!(xl >= (float)(-bx) && xl <= (float)(im.width - 1 - bx) && yl >= (float)(-by) &&
         yl <= (float)(im.height - 1 - by)))
     return false;
-  const float flx = floorf(xl), fly = floorf(yl);
-  int x0 = bx + (int)flx, y0 = by + (int)fly;
+  int x0 = bx + (int)floorf(xl), y0 = by + (int)floorf(yl);
   if (x0 > im.width - 2) x0 = im.width - 2;
   if (y0 > im.height - 2) y0 = im.height - 2;
   const float fx = xl - (float)(x0 - bx), fy = yl - (float)(y0 - by);
-  const int x1 = min(x0 + 1, im.width - 1), y1 = min(y0 + 1, im.height - 1);
-  const float f00 = px<Pix>(im, x0, y0), f10 = px<Pix>(im, x1, y0);
-  const float f01 = px<Pix>(im, x0, y1), f11 = px<Pix>(im, x1, y1);
+  const int lx = x0 - wn.ox, ly = y0 - wn.oy;
+  float f00, f10, f01, f11;
+  if ((unsigned)lx < (unsigned)(wn.S - 1) && (unsigned)ly < (unsigned)(wn.S - 1)) {
+    const float* p = wn.w + ly * wn.P + lx;
+    f00 = p[0];
+    f10 = p[1];
+    f01 = p[wn.P];
+    f11 = p[wn.P + 1];
+  } else {
+    const int x1 = min(x0 + 1, im.width - 1), y1 = min(y0 + 1, im.height - 1);
+    f00 = gpx<Pix>(im, x0, y0);
+    f10 = gpx<Pix>(im, x1, y0);
+    f01 = gpx<Pix>(im, x0, y1);
+    f11 = gpx<Pix>(im, x1, y1);
+  }
   const float a10 = f10 - f00, a01 = f01 - f00, a11 = (f00 + f11) - f10 - f01;
-  float v = fmaf(a11 * fx, fy, fmaf(a01, fy, fmaf(a10, fx, f00)));
+  const float v = fmaf(a11 * fx, fy, fmaf(a01, fy, fmaf(a10, fx, f00)));
   const float lo = fminf(fminf(f00, f10), fminf(f01, f11));
   const float hi = fmaxf(fmaxf(f00, f10), fmaxf(f01, f11));
   g = fminf(fmaxf(v, lo), hi);
@@ -85,8 +89,8 @@ __device__ __forceinline__ bool bilinear(const ImageView& im, int bx, int by, fl
 // grad_bilinear (subpixel.cpp:104-128): node central differences, bilinearly
 // weighted, zero weights skipped (keeps the taps inside the image).
 template <typename Pix>
-__device__ __forceinline__ bool grad_bilinear(const ImageView& im, int bx, int by, float xl, float yl,
-                                              float& gx, float& gy) {
+__device__ __forceinline__ bool grad_bilinear(const Win& wn, const ImageView& im, int bx, int by, float xl,
+                                              float yl, float& gx, float& gy) {
   if (!(xl >= (float)(1 - bx) && xl <= (float)(im.width - 2 - bx) && yl >= (float)(1 - by) &&
         yl <= (float)(im.height - 2 - by)))
     return false;
@@ -103,8 +107,8 @@ __device__ __forceinline__ bool grad_bilinear(const ImageView& im, int bx, int b
       if (wx[a] == 0.0f) continue;
       const int i = x0 + a, j = y0 + b;
       const float w = wx[a] * wy[b] * 0.5f;
-      ax = fmaf(w, px<Pix>(im, i + 1, j) - px<Pix>(im, i - 1, j), ax);
-      ay = fmaf(w, px<Pix>(im, i, j + 1) - px<Pix>(im, i, j - 1), ay);
+      ax = fmaf(w, tap<Pix>(wn, im, i + 1, j) - tap<Pix>(wn, im, i - 1, j), ax);
+      ay = fmaf(w, tap<Pix>(wn, im, i, j + 1) - tap<Pix>(wn, im, i, j - 1), ay);
     }
   }
   gx = ax;
@@ -112,13 +116,41 @@ __device__ __forceinline__ bool grad_bilinear(const ImageView& im, int bx, int b
   return true;
 }
 
-struct SharedState {
-  double p[6];  // u, ux, uy, v, vx, vy (WarpParams order of subpixel.hpp:13-16)
-  int status;
-  int done;
-  int iterations;
-  int converged;
-  Ldlt6 L;
+__device__ __forceinline__ double warp_sum1(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Per-thread partials -> per-warp sums in rb[warp][base + i] (one value live at a time).
+template <int NV, typename T>
+__device__ __forceinline__ void block_partials(const T (&v)[NV], double (*rb)[kRedMax], int base = 0) {
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const double s = warp_sum1((double)v[i]);
+    if ((threadIdx.x & 31) == 0) rb[threadIdx.x >> 5][base + i] = s;
+  }
+}
+
+// After a __syncthreads: warp 0's lanes total the per-warp sums into tot[0..nv).
+__device__ __forceinline__ void warp0_totals(double (*rb)[kRedMax], double* tot, int nv) {
+  for (int j = threadIdx.x & 31; j < nv; j += 32) {
+    double s = rb[0][j];
+#pragma unroll
+    for (int w = 1; w < kWarps; ++w) s += rb[w][j];
+    tot[j] = s;
+  }
+  __syncwarp();
+}
+
+struct State {
+  double p[6];  // u, ux, uy, v, vx, vy (subpixel.hpp:13-16)
+  int status, done, iterations, converged;
+  double zncc;
+  // reference-side constants
+  double fbar, nf, scf;   // mean, ||f - fbar||, sum of the fp32 centred values
+  double A[6], Ssd[6];    // sum cf*sd, sum sd (IC-GN)
+  double Hinv[36];        // IC-GN: H^-1 (H exact)
 };
 
 __device__ __forceinline__ double warp_det(const double* p) {
@@ -139,7 +171,9 @@ __device__ int compose_with_inverse(double* p, const double* inc) {
                          0.0, 0.0, 1.0};
   const double w[9] = {1.0 + p[1], p[2], p[0], p[4], 1.0 + p[5], p[3], 0.0, 0.0, 1.0};
   double c[9];
+#pragma unroll
   for (int i = 0; i < 3; ++i)
+#pragma unroll
     for (int j = 0; j < 3; ++j) {
       double s = __dmul_rn(w[i * 3 + 0], inv[0 * 3 + j]);
       s = __dadd_rn(s, __dmul_rn(w[i * 3 + 1], inv[1 * 3 + j]));
@@ -155,360 +189,536 @@ __device__ int compose_with_inverse(double* p, const double* inc) {
   return 0;
 }
 
-// 18 moment sums m[k*6+w] (k: 0 aa, 1 ab, 2 bb; w: 1,dx,dy,dx^2,dxdy,dy^2) -> symmetric 6x6
-// H = sum sd sd^T with sd = [a, a dx, a dy, b, b dx, b dy] (subpixel.cpp:210-212, :261-263).
+// 18 moment sums mo[k*6+w] (k: 0 aa, 1 ab, 2 bb; w: 1,dx,dy,dx^2,dxdy,dy^2) -> symmetric
+// H = sum sd sd^T, sd = [a, a dx, a dy, b, b dx, b dy] (subpixel.cpp:210-212, :261-263).
 __device__ void assemble_hessian(const double* mo, double scale, double* H) {
-  auto A = [&](int w) { return mo[0 * 6 + w] * scale; };
-  auto Bm = [&](int w) { return mo[1 * 6 + w] * scale; };
-  auto Cm = [&](int w) { return mo[2 * 6 + w] * scale; };
-  // index map of monomials: 0:1 1:dx 2:dy 3:dx^2 4:dxdy 5:dy^2
-  const double h[6][6] = {
-      {A(0), A(1), A(2), Bm(0), Bm(1), Bm(2)},
-      {A(1), A(3), A(4), Bm(1), Bm(3), Bm(4)},
-      {A(2), A(4), A(5), Bm(2), Bm(4), Bm(5)},
-      {Bm(0), Bm(1), Bm(2), Cm(0), Cm(1), Cm(2)},
-      {Bm(1), Bm(3), Bm(4), Cm(1), Cm(3), Cm(4)},
-      {Bm(2), Bm(4), Bm(5), Cm(2), Cm(4), Cm(5)},
+  const int map[6][6][2] = {
+      {{0, 0}, {0, 1}, {0, 2}, {1, 0}, {1, 1}, {1, 2}}, {{0, 1}, {0, 3}, {0, 4}, {1, 1}, {1, 3}, {1, 4}},
+      {{0, 2}, {0, 4}, {0, 5}, {1, 2}, {1, 4}, {1, 5}}, {{1, 0}, {1, 1}, {1, 2}, {2, 0}, {2, 1}, {2, 2}},
+      {{1, 1}, {1, 3}, {1, 4}, {2, 1}, {2, 3}, {2, 4}}, {{1, 2}, {1, 4}, {1, 5}, {2, 2}, {2, 4}, {2, 5}},
   };
+#pragma unroll
   for (int i = 0; i < 6; ++i)
-    for (int j = 0; j < 6; ++j) H[i * 6 + j] = h[i][j];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) H[i * 6 + j] = mo[map[i][j][0] * 6 + map[i][j][1]] * scale;
 }
 
-template <typename Pix, int PPT, int METHOD>
-__global__ void __launch_bounds__(256) refine_kernel(RefineParams p) {
-  __shared__ RedBuf rb;
-  __shared__ SharedState S;
+// warp 0: finish one iteration from the totals; lane 0 commits the state.
+__device__ void finish_step(State& S, const double* step, bool finite, int fail_code, int iter, double tol,
+                            bool icgn) {
+  int st = finite ? DICB200_POI_OK : fail_code;
+  if (st == DICB200_POI_OK) {
+    if (icgn) {
+      st = compose_with_inverse(S.p, step);
+    } else {
+      for (int j = 0; j < 6; ++j) S.p[j] += step[j];
+    }
+  }
+  if (st == DICB200_POI_OK && fabs(warp_det(S.p)) < 1e-8) st = DICB200_POI_WARP_NOT_INVERTIBLE;
+  S.status = st;
+  if (st == DICB200_POI_OK) {
+    S.iterations = iter;
+    if (fmax(fabs(step[0]), fabs(step[3])) < tol) {
+      S.converged = 1;
+      S.done = 1;
+    }
+  } else {
+    S.done = 1;
+  }
+}
+
+// Fast-path bilinear sample from the staged window (no checks: the caller
+// proved the whole warped subset lies inside the window and the image).
+template <int WP>
+__device__ __forceinline__ float sample_fast(const float* w, float wx, float wy) {
+  const float flx = floorf(wx), fly = floorf(wy);
+  const float fx = wx - flx, fy = wy - fly;
+  const float* q = w + (int)fly * WP + (int)flx;
+  const float f00 = q[0], f10 = q[1], f01 = q[WP], f11 = q[WP + 1];
+  const float a10 = f10 - f00, a01 = f01 - f00, a11 = (f00 + f11) - f10 - f01;
+  return fmaf(a11 * fx, fy, fmaf(a01, fy, fmaf(a10, fx, f00)));
+}
+
+// Warp-parallel Cholesky of the SPD 6x6 H (lane i < 6 holds row i in h[]),
+// then lane c < 6 solves H x = e_c: returns row c of H^-1 in hinv[] (H^-1 is
+// symmetric). pd = all pivots > 0. Runs on all 32 lanes of one warp.
+__device__ void warp_cholesky_inverse(double (&h)[6], double (&hinv)[6], bool& pd) {
+  const int lane = threadIdx.x & 31;
+  double L[6][6];
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    // pivot on lane j: d = h[j][j] - sum_k<j L[j][k]^2 (lane j's h[k<j] already hold L[j][k])
+    double d = h[j];
+#pragma unroll
+    for (int k2 = 0; k2 < j; ++k2) d -= h[k2] * h[k2];
+    d = __shfl_sync(0xffffffffu, d, j);
+    ok = ok && d > 0.0;
+    const double ljj = sqrt(d > 0.0 ? d : 1.0);
+    // broadcast row j of L (k < j) and finish column j on lanes i > j
+#pragma unroll
+    for (int k2 = 0; k2 < j; ++k2) L[j][k2] = __shfl_sync(0xffffffffu, h[k2], j);
+    L[j][j] = ljj;
+    double v = h[j];
+#pragma unroll
+    for (int k2 = 0; k2 < j; ++k2) v -= h[k2] * L[j][k2];
+    if (lane > j) h[j] = v / ljj;
+    if (lane == j) h[j] = ljj;
+  }
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+#pragma unroll
+    for (int k2 = 0; k2 < i; ++k2) L[i][k2] = __shfl_sync(0xffffffffu, h[k2], i);
+  // forward / back substitution for e_lane
+  double y[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    double v = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k2 = 0; k2 < i; ++k2) v -= L[i][k2] * y[k2];
+    y[i] = v / L[i][i];
+  }
+#pragma unroll
+  for (int i = 5; i >= 0; --i) {
+    double v = y[i];
+#pragma unroll
+    for (int k2 = i + 1; k2 < 6; ++k2) v -= L[k2][i] * hinv[k2];
+    hinv[i] = v / L[i][i];
+  }
+  pd = ok;
+}
+
+template <typename Pix, int PPT, int METHOD, int WP>
+__global__ void __launch_bounds__(kNT, 3) refine_kernel(RefineParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double rb[kWarps][kRedMax];
+  __shared__ double tot[kRedMax];
+  __shared__ float rmm[kWarps][2];
+  __shared__ double shH[36];
+  __shared__ Ldlt6 shL;
+  __shared__ State S;
   const int k = blockIdx.x;
   dicb200_poi_record* rec = p.rec + k;
   if (rec->status != DICB200_POI_OK) return;  // integer stage failed: record stays
-  const int tid = threadIdx.x, NT = blockDim.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int M = p.M, side = 2 * M + 1, n = side * side;
   const int iy = p.row_begin + k / p.lat.nx, ix = k % p.lat.nx;
   const int cx = p.lat.cx(ix), cy = p.lat.cy(iy);
   const int idx = rec->integer_dx, idy = rec->integer_dy;
-  int buf = 0;
+  const int bx = cx + idx, by = cy + idy;
 
-  // ---- per-pixel reference data in registers ----
-  float dxf[PPT], dyf[PPT], cf[PPT], gxr[PPT], gyr[PPT];
-  double mean, nf;
-  {
-    if (METHOD == 1 && (cx - M - 1 < 0 || cx + M + 1 > p.ref.width - 1 || cy - M - 1 < 0 ||
-                        cy + M + 1 > p.ref.height - 1)) {
-      if (tid == 0) {
-        rec->status = DICB200_POI_BORDER_GRADIENTS;
-        rec->converged = 0;
-      }
-      return;
+  if (METHOD == 1 && (cx - M - 1 < 0 || cx + M + 1 > p.ref.width - 1 || cy - M - 1 < 0 ||
+                      cy + M + 1 > p.ref.height - 1)) {
+    if (tid == 0) {
+      rec->status = DICB200_POI_BORDER_GRADIENTS;  // subpixel.cpp:193-195
+      rec->converged = 0;
     }
-    double sums[2] = {0.0, 0.0};
-    float fv[PPT];
+    return;
+  }
+
+  // ---- stage the target neighbourhood (fp32, pitch WP) ----
+  Win wn;
+  wn.S = side + 2 * kPad;
+  wn.P = WP;
+  wn.ox = bx - M - kPad;
+  wn.oy = by - M - kPad;
+  float* wbuf = reinterpret_cast<float*>(smem_raw);
+  for (int i = tid; i < wn.S * WP; i += kNT) {
+    const int ly = i / WP, lx = i - ly * WP;
+    const int gx = wn.ox + lx, gy = wn.oy + ly;
+    float v = 0.f;
+    if (lx < wn.S && gx >= 0 && gx < p.tgt.width && gy >= 0 && gy < p.tgt.height) v = gpx<Pix>(p.tgt, gx, gy);
+    wbuf[i] = v;
+  }
+  wn.w = wbuf;
+
+  // ---- reference pixels: registers ----
+  float dxf[PPT], dyf[PPT], cf[PPT], gxr[PPT], gyr[PPT];
+  {
+    double s2[2] = {0.0, 0.0};
 #pragma unroll
     for (int i = 0; i < PPT; ++i) {
-      const int kk = tid + i * NT;
+      const int kk = tid + i * kNT;
       const int r = kk / side, c = kk - r * side;
       dxf[i] = (float)(c - M);
       dyf[i] = (float)(r - M);
-      fv[i] = 0.f;
-      gxr[i] = gyr[i] = 0.f;
+      cf[i] = gxr[i] = gyr[i] = 0.f;
       if (kk < n) {
         const int x = cx + c - M, y = cy + r - M;
-        fv[i] = px<Pix>(p.ref, x, y);
+        const float f = gpx<Pix>(p.ref, x, y);
+        cf[i] = f;
         if (METHOD == 1) {
-          gxr[i] = 0.5f * (px<Pix>(p.ref, x + 1, y) - px<Pix>(p.ref, x - 1, y));
-          gyr[i] = 0.5f * (px<Pix>(p.ref, x, y + 1) - px<Pix>(p.ref, x, y - 1));
+          gxr[i] = 0.5f * (gpx<Pix>(p.ref, x + 1, y) - gpx<Pix>(p.ref, x - 1, y));
+          gyr[i] = 0.5f * (gpx<Pix>(p.ref, x, y + 1) - gpx<Pix>(p.ref, x, y - 1));
         }
-        sums[0] += (double)fv[i];
-        sums[1] += (double)fv[i] * (double)fv[i];
+        s2[0] += (double)f;
+        s2[1] += (double)f * (double)f;
+      } else {
+        dxf[i] = dyf[i] = 0.f;  // padding slots sample the centre (weight 0 everywhere)
       }
     }
-    block_sum<2>(sums, rb, buf);
-    const int64_t sf = (int64_t)sums[0], sff = (int64_t)sums[1];
+    block_partials<2>(s2, rb);
+    __syncthreads();
+    if (warp == 0) warp0_totals(rb, tot, 2);
+    __syncthreads();
+    const int64_t sf = (int64_t)tot[0], sff = (int64_t)tot[1];
     const int64_t vf = (int64_t)n * sff - sf * sf;
-    mean = sums[0] / (double)n;  // correlation.cpp:25: exact sum / n
-    nf = sqrt((double)vf / (double)n);
-    if (vf <= 0) {
+    if (vf <= 0) {  // constant subset
       if (tid == 0) {
         rec->status = METHOD == 1 ? DICB200_POI_DEGENERATE_TEXTURE : DICB200_POI_DEGENERATE_SUBSET;
         rec->converged = 0;
       }
       return;
     }
+    const double mean = tot[0] / (double)n;  // correlation.cpp:25: exact sum / n
 #pragma unroll
-    for (int i = 0; i < PPT; ++i) cf[i] = (tid + i * NT < n) ? (float)((double)fv[i] - mean) : 0.f;
-  }
-
-  if (METHOD == 1) {
-    // ---- icgn_precompute: exact Hessian moments, condition test, LDL^T ----
-    double mo[18];
-#pragma unroll
-    for (int j = 0; j < 18; ++j) mo[j] = 0.0;
-#pragma unroll
-    for (int i = 0; i < PPT; ++i) {
-      const double a = 2.0 * gxr[i], b = 2.0 * gyr[i];  // integers
-      const double dx = dxf[i], dy = dyf[i];
-      const double w[6] = {1.0, dx, dy, dx * dx, dx * dy, dy * dy};
-      const double aa = a * a, ab = a * b, bb = b * b;
-#pragma unroll
-      for (int j = 0; j < 6; ++j) {
-        mo[j] = fma(aa, w[j], mo[j]);
-        mo[6 + j] = fma(ab, w[j], mo[6 + j]);
-        mo[12 + j] = fma(bb, w[j], mo[12 + j]);
-      }
+    for (int i = 0; i < PPT; ++i) cf[i] = (tid + i * kNT < n) ? (float)((double)cf[i] - mean) : 0.f;
+    if (tid == 0) {
+      S.fbar = mean;
+      S.nf = sqrt((double)vf / (double)n);
     }
-    block_sum<18>(mo, rb, buf);
-    if (warp == 0) {
-      double H[36];
-      assemble_hessian(mo, 0.25, H);
-      Ldlt6 L;
-      ldlt6_compute(L, H);
-      bool pd = L.ok != 0;
-      for (int i = 0; i < 6; ++i) pd = pd && L.m[i * 7] > 0.0;
-      bool accept = false;
-      if (pd) {
-        // cond <= ||H||_F ||H^-1||_F; exact Jacobi only when the bound is inconclusive
-        double col2 = 0.0;
-        if (lane < 6) {
-          double e[6] = {0, 0, 0, 0, 0, 0}, x[6];
-          e[lane] = 1.0;
-          ldlt6_solve(L, e, x);
-          for (int i = 0; i < 6; ++i) col2 += x[i] * x[i];
-        }
-        for (int o = 16; o; o >>= 1) col2 += __shfl_xor_sync(0xffffffffu, col2, o);
-        double hf2 = 0.0;
-        for (int i = 0; i < 36; ++i) hf2 += H[i] * H[i];
-        accept = sqrt(hf2) * sqrt(col2) < 1e12;
+  }
+  __syncthreads();  // rb reuse + S.fbar/nf visible
+
+  double hinv[6] = {0, 0, 0, 0, 0, 0};  // IC-GN, warp 0 lanes 0..5: row `lane` of H^-1
+  if (METHOD == 1) {
+    // ---- icgn_precompute: exact Hessian moments, sum f*sd, sum sd ----
+#pragma unroll 1
+    for (int grp = 0; grp < 3; ++grp) {
+      double m6[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int i = 0; i < PPT; ++i) {
+        const double ga = 2.0 * gxr[i], gb = 2.0 * gyr[i];  // integers
+        const double q = grp == 0 ? ga * ga : (grp == 1 ? ga * gb : gb * gb);
+        const double dx = dxf[i], dy = dyf[i];
+        m6[0] += q;
+        m6[1] = fma(q, dx, m6[1]);
+        m6[2] = fma(q, dy, m6[2]);
+        m6[3] = fma(q, dx * dx, m6[3]);
+        m6[4] = fma(q, dx * dy, m6[4]);
+        m6[5] = fma(q, dy * dy, m6[5]);
       }
-      if (!accept) {
-        double lo, hi;
-        jacobi6_minmax(H, &lo, &hi);
-        const double cond = lo > 0.0 ? hi / lo : __longlong_as_double(0x7ff0000000000000ULL);
-        accept = cond < 1e12;
+      block_partials<6>(m6, rb, grp * 6);
+    }
+    {
+      double a7[7] = {0, 0, 0, 0, 0, 0, 0};
+      double s6[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int i = 0; i < PPT; ++i) {
+        const double c = cf[i], gx = gxr[i], gy = gyr[i], dx = dxf[i], dy = dyf[i];
+        const double cgx = c * gx, cgy = c * gy;  // exact (float x float)
+        a7[0] += c;
+        a7[1] += cgx;
+        a7[2] += cgx * dx;
+        a7[3] += cgx * dy;
+        a7[4] += cgy;
+        a7[5] += cgy * dx;
+        a7[6] += cgy * dy;
+        s6[0] += gx;
+        s6[1] += gx * dx;
+        s6[2] += gx * dy;
+        s6[3] += gy;
+        s6[4] += gy * dx;
+        s6[5] += gy * dy;
       }
-      if (lane == 0) {
-        S.status = accept ? DICB200_POI_OK : DICB200_POI_DEGENERATE_TEXTURE;
-        S.L = L;
-      }
+      block_partials<7>(a7, rb, 18);
+      block_partials<6>(s6, rb, 25);
     }
     __syncthreads();
-    if (S.status != DICB200_POI_OK) {
-      if (tid == 0) {
-        rec->status = S.status;
-        rec->converged = 0;
+    if (warp == 0) {
+      warp0_totals(rb, tot, 31);
+      // H (exact) row `lane` -> warp Cholesky -> row `lane` of H^-1 in registers
+      const int map[6][6][2] = {
+          {{0, 0}, {0, 1}, {0, 2}, {1, 0}, {1, 1}, {1, 2}}, {{0, 1}, {0, 3}, {0, 4}, {1, 1}, {1, 3}, {1, 4}},
+          {{0, 2}, {0, 4}, {0, 5}, {1, 2}, {1, 4}, {1, 5}}, {{1, 0}, {1, 1}, {1, 2}, {2, 0}, {2, 1}, {2, 2}},
+          {{1, 1}, {1, 3}, {1, 4}, {2, 1}, {2, 3}, {2, 4}}, {{1, 2}, {1, 4}, {1, 5}, {2, 2}, {2, 4}, {2, 5}},
+      };
+      double h[6];
+      const int row = lane < 6 ? lane : 0;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        double v = 0.0;
+#pragma unroll
+        for (int r = 0; r < 6; ++r)
+          if (r == row) v = tot[map[r][j][0] * 6 + map[r][j][1]] * 0.25;
+        h[j] = v;
       }
-      return;
+      double hf2 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) hf2 += lane < 6 ? h[j] * h[j] : 0.0;
+      bool pd;
+      warp_cholesky_inverse(h, hinv, pd);
+      double if2 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) if2 += lane < 6 ? hinv[j] * hinv[j] : 0.0;
+      hf2 = warp_sum1(hf2);
+      if2 = warp_sum1(if2);
+      // cond(H) <= ||H||_F ||H^-1||_F; exact eigenvalues only when inconclusive (subpixel.cpp:215-219)
+      bool accept = pd && sqrt(hf2) * sqrt(if2) < 1e12;
+      if (lane == 0) {
+        if (!accept && pd) {
+          assemble_hessian(tot, 0.25, shH);
+          double lo, hi;
+          jacobi6_minmax(shH, &lo, &hi);
+          accept = lo > 0.0 && hi / lo < 1e12;
+        }
+        S.status = accept ? DICB200_POI_OK : DICB200_POI_DEGENERATE_TEXTURE;
+        S.scf = tot[18];
+        for (int j = 0; j < 6; ++j) {
+          S.A[j] = tot[19 + j];
+          S.Ssd[j] = tot[25 + j];
+        }
+      }
+    }
+  } else {
+    double a[1] = {0.0};
+#pragma unroll
+    for (int i = 0; i < PPT; ++i) a[0] += (double)cf[i];
+    block_partials<1>(a, rb);
+    __syncthreads();
+    if (warp == 0) {
+      warp0_totals(rb, tot, 1);
+      if (lane == 0) {
+        S.scf = tot[0];
+        S.status = DICB200_POI_OK;
+      }
     }
   }
-
   if (tid == 0) {
     S.p[0] = (double)idx;
     S.p[1] = S.p[2] = 0.0;
     S.p[3] = (double)idy;
     S.p[4] = S.p[5] = 0.0;
-    S.status = DICB200_POI_OK;
     S.done = 0;
     S.iterations = 0;
     S.converged = 0;
   }
   __syncthreads();
+  if (S.status != DICB200_POI_OK) {
+    if (tid == 0) {
+      rec->status = S.status;
+      rec->converged = 0;
+    }
+    return;
+  }
 
-  const int bx = cx + idx, by = cy + idy;
-  float g[PPT], tgx[PPT], tgy[PPT];
-  double zncc_final = 0.0;
+  const double n_d = (double)n;
+  const float fbarf = (float)S.fbar;
   const double lim = (double)(M + 2);
+  const float wofs = (float)(M + kPad);  // window coords = local coords + wofs
 
-  // sample_through_warp (subpixel.cpp:151-183) for the current S.p; returns
-  // status, and (gbar, ng, cross) through the two-pass block sums.
-  auto sample = [&](bool with_grad, double& gbar, double& ng, double& cross) -> int {
+  for (int iter = 1;; ++iter) {
+    const bool final_pass = iter > p.max_iter || S.done;
     const double u = S.p[0], ux = S.p[1], uy = S.p[2], v = S.p[3], vx = S.p[4], vy = S.p[5];
-    const double ccx = cx + u, ccy = cy + v;  // check_guard, subpixel.cpp:134-141
-    if (!(ccx >= lim && ccx <= p.tgt.width - 1 - lim && ccy >= lim && ccy <= p.tgt.height - 1 - lim))
-      return DICB200_POI_DRIFTED;
+    {  // check_guard (subpixel.cpp:134-141), uniform
+      const double ccx = cx + u, ccy = cy + v;
+      if (!(ccx >= lim && ccx <= p.tgt.width - 1 - lim && ccy >= lim && ccy <= p.tgt.height - 1 - lim)) {
+        if (tid == 0) {
+          rec->status = DICB200_POI_DRIFTED;
+          rec->converged = 0;
+        }
+        return;
+      }
+    }
     const float ul = (float)(u - idx), vl = (float)(v - idy);
     const float uxf = (float)ux, uyf = (float)uy, vxf = (float)vx, vyf = (float)vy;
-    double s1[2] = {0.0, 0.0};
-    float a1 = 0.f;
+    const bool grads = METHOD == 0 && !final_pass;
+    // Fast path iff the warped subset's bounding box (+1 px, +2 px with gradients)
+    // sits inside the staged window and the image domain: the affine map attains
+    // its extremes at the corners (uniform decision).
+    bool fast;
+    {
+      const float Mf = (float)M;
+      const float ex = fabsf(Mf + Mf * uxf) + fabsf(Mf * uyf), ey = fabsf(Mf * vxf) + fabsf(Mf + Mf * vyf);
+      const float lo_x = ul - ex, hi_x = ul + ex, lo_y = vl - ey, hi_y = vl + ey;
+      const float mg = grads ? 2.0f : 1.0f;
+      fast = lo_x - mg >= -wofs && hi_x + mg + 1.0f <= (float)(wn.S - 1) - wofs && lo_y - mg >= -wofs &&
+             hi_y + mg + 1.0f <= (float)(wn.S - 1) - wofs && (float)bx + lo_x - mg >= 0.0f &&
+             (float)bx + hi_x + mg <= (float)(p.tgt.width - 1) && (float)by + lo_y - mg >= 0.0f &&
+             (float)by + hi_y + mg <= (float)(p.tgt.height - 1);
+    }
+    constexpr int NV = METHOD == 1 ? 9 : 39;
+    float acc[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) acc[j] = 0.f;
     int bad = 0;
+    float gmin = 3.0e38f, gmax = -3.0e38f;  // exact "constant subset" test (ng == 0 in the reference)
 #pragma unroll
     for (int i = 0; i < PPT; ++i) {
-      g[i] = 0.f;
-      if (tid + i * NT < n) {
-        const float xl = fmaf(uyf, dyf[i], fmaf(uxf, dxf[i], dxf[i] + ul));
-        const float yl = fmaf(vyf, dyf[i], fmaf(vxf, dxf[i], dyf[i] + vl));
-        bad |= !bilinear<Pix>(p.tgt, bx, by, xl, yl, g[i]);
-        if (with_grad) bad |= !grad_bilinear<Pix>(p.tgt, bx, by, xl, yl, tgx[i], tgy[i]);
-        a1 += g[i] - (float)mean;
+      const bool valid = tid + i * kNT < n;
+      const float xl = fmaf(uyf, dyf[i], fmaf(uxf, dxf[i], dxf[i] + ul));
+      const float yl = fmaf(vyf, dyf[i], fmaf(vxf, dxf[i], dyf[i] + vl));
+      float g = 0.f, gx = 0.f, gy = 0.f;
+      if (fast) {
+        g = sample_fast<WP>(wn.w, xl + wofs, yl + wofs);
+        if (grads) {
+          // grad_bilinear on the window: nodes (x0..x0+1, y0..y0+1), central differences
+          const float wx = xl + wofs, wy = yl + wofs;
+          const float flx = floorf(wx), fly = floorf(wy);
+          const float fx = wx - flx, fy = wy - fly;
+          const float* q = wn.w + (int)fly * WP + (int)flx;
+          const float dx00 = q[1] - q[-1], dx10 = q[2] - q[0], dx01 = q[WP + 1] - q[WP - 1], dx11 = q[WP + 2] - q[WP];
+          const float dy00 = q[WP] - q[-WP], dy10 = q[WP + 1] - q[1 - WP], dy01 = q[2 * WP] - q[0],
+                      dy11 = q[2 * WP + 1] - q[1];
+          const float w00 = (1.f - fx) * (1.f - fy), w10 = fx * (1.f - fy), w01 = (1.f - fx) * fy, w11 = fx * fy;
+          gx = 0.5f * (w00 * dx00 + w10 * dx10 + w01 * dx01 + w11 * dx11);
+          gy = 0.5f * (w00 * dy00 + w10 * dy10 + w01 * dy01 + w11 * dy11);
+        }
+      } else if (valid) {
+        bad |= !bilinear<Pix>(wn, p.tgt, bx, by, xl, yl, g);
+        if (grads) bad |= !grad_bilinear<Pix>(wn, p.tgt, bx, by, xl, yl, gx, gy);
+      }
+      if (!valid) continue;
+      gmin = fminf(gmin, g);
+      gmax = fmaxf(gmax, g);
+      const float gp = g - fbarf;
+      acc[0] += gp;
+      acc[1] = fmaf(gp, gp, acc[1]);
+      if (final_pass || METHOD == 0) acc[2] = fmaf(cf[i], gp, acc[2]);
+      if (METHOD == 1) {
+        if (!final_pass) {
+          const float tx = gp * gxr[i], ty = gp * gyr[i];
+          acc[3] += tx;
+          acc[4] = fmaf(tx, dxf[i], acc[4]);
+          acc[5] = fmaf(tx, dyf[i], acc[5]);
+          acc[6] += ty;
+          acc[7] = fmaf(ty, dxf[i], acc[7]);
+          acc[8] = fmaf(ty, dyf[i], acc[8]);
+        }
+      } else if (grads) {
+        const float dx = dxf[i], dy = dyf[i];
+        const float J[6] = {gx, gx * dx, gx * dy, gy, gy * dx, gy * dy};
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          acc[3 + j] = fmaf(cf[i], J[j], acc[3 + j]);
+          acc[9 + j] = fmaf(gp, J[j], acc[9 + j]);
+          acc[15 + j] += J[j];
+        }
+        const float wv[6] = {1.f, dx, dy, dx * dx, dx * dy, dy * dy};
+        const float aa = gx * gx, ab = gx * gy, bb = gy * gy;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          acc[21 + j] = fmaf(aa, wv[j], acc[21 + j]);
+          acc[27 + j] = fmaf(ab, wv[j], acc[27 + j]);
+          acc[33 + j] = fmaf(bb, wv[j], acc[33 + j]);
+        }
       }
     }
-    s1[0] = a1;
-    s1[1] = bad;
-    block_sum<2>(s1, rb, buf);
-    if (s1[1] != 0.0) return DICB200_POI_DRIFTED;
-    gbar = mean + s1[0] / (double)n;
-    const float gb = (float)gbar;
-    float a2 = 0.f, ac = 0.f;
+    const int nv = final_pass ? 3 : (METHOD == 1 ? 9 : (grads ? 39 : 3));
 #pragma unroll
-    for (int i = 0; i < PPT; ++i) {
-      if (tid + i * NT < n) {
-        const float d = g[i] - gb;
-        a2 = fmaf(d, d, a2);
-        ac = fmaf(cf[i], d, ac);
+    for (int j = 0; j < NV; ++j) {
+      if (j < nv) {
+        const double s2 = warp_sum1((double)acc[j]);
+        if (lane == 0) rb[warp][j] = s2;
       }
     }
-    double s2[2] = {a2, ac};
-    block_sum<2>(s2, rb, buf);
-    ng = sqrt(s2[0]);
-    cross = s2[1];
-    if (ng <= 0.0) return DICB200_POI_DEGENERATE_TARGET;
-    return DICB200_POI_OK;
-  };
-
-  int status = DICB200_POI_OK;
-  for (int iter = 1; iter <= p.max_iter; ++iter) {
-    double gbar, ng, cross;
-    status = sample(METHOD == 0, gbar, ng, cross);
-    if (status != DICB200_POI_OK) break;
-    const float gb = (float)gbar;
-    if (METHOD == 1) {
-      // rhs = sum_k e_k sd_k, e_k = f_k - (nf/ng)(g_k - gbar) (subpixel.cpp:328-333)
-      const float ratio = (float)(nf / ng);
-      float r6[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
-      for (int i = 0; i < PPT; ++i) {
-        const float e = cf[i] - ratio * (g[i] - gb);
-        const float tx = e * gxr[i], ty = e * gyr[i];
-        r6[0] += tx;
-        r6[1] = fmaf(tx, dxf[i], r6[1]);
-        r6[2] = fmaf(tx, dyf[i], r6[2]);
-        r6[3] += ty;
-        r6[4] = fmaf(ty, dxf[i], r6[4]);
-        r6[5] = fmaf(ty, dyf[i], r6[5]);
+    for (int o = 16; o; o >>= 1) {
+      gmin = fminf(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
+      gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+    }
+    if (lane == 0) {
+      rmm[warp][0] = gmin;
+      rmm[warp][1] = gmax;
+    }
+    const int any_bad = __syncthreads_or(bad);
+    if (warp == 0) {
+      warp0_totals(rb, tot, nv);
+      float mn = rmm[0][0], mx = rmm[0][1];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) {
+        mn = fminf(mn, rmm[w][0]);
+        mx = fmaxf(mx, rmm[w][1]);
       }
-      double rhs[6];
-#pragma unroll
-      for (int j = 0; j < 6; ++j) rhs[j] = r6[j];
-      block_sum<6>(rhs, rb, buf);
-      if (tid == 0) {
-        double neg[6], step[6];
-        for (int j = 0; j < 6; ++j) neg[j] = -rhs[j];
-        ldlt6_solve(S.L, neg, step);
-        bool fin = true;
-        for (int j = 0; j < 6; ++j) fin = fin && isfinite(step[j]);
-        int st = fin ? DICB200_POI_OK : DICB200_POI_DEGENERATE_TEXTURE;
-        if (st == DICB200_POI_OK) st = compose_with_inverse(S.p, step);
-        if (st == DICB200_POI_OK && fabs(warp_det(S.p)) < 1e-8) st = DICB200_POI_WARP_NOT_INVERTIBLE;
-        S.status = st;
-        if (st == DICB200_POI_OK) {
-          S.iterations = iter;
-          if (fmax(fabs(step[0]), fabs(step[3])) < p.tol) {
-            S.converged = 1;
-            S.done = 1;
-          }
+      const double* t = tot;
+      int st = DICB200_POI_OK;
+      const double delta = t[0] / n_d;                           // gbar - fbar
+      const double ng2 = fmax(t[1] - n_d * delta * delta, 0.0);  // sum (g - gbar)^2
+      const double ng = sqrt(ng2);
+      if (any_bad) st = DICB200_POI_DRIFTED;
+      else if (!(mx > mn) || !(ng > 0.0)) st = DICB200_POI_DEGENERATE_TARGET;
+      if (final_pass) {
+        if (lane == 0) {
+          S.status = st;
+          S.zncc = (t[2] - delta * S.scf) / (S.nf * ng);  // cross / (nf ng)
+          S.done = 2;
         }
-      }
-    } else {
-      // NR (subpixel.cpp:247-271): coeff_k = c_f - (cross/ng^2) (g_k - gbar);
-      // gradient = -2/(nf ng) sum coeff J; H = 2/ng^2 sum J J^T.
-      const float kappa = (float)(cross / (ng * ng));
-      float a[24];
-#pragma unroll
-      for (int j = 0; j < 24; ++j) a[j] = 0.f;
-#pragma unroll
-      for (int i = 0; i < PPT; ++i) {
-        if (tid + i * NT < n) {
-          const float coeff = cf[i] - kappa * (g[i] - gb);
-          const float gx = tgx[i], gy = tgy[i];
-          const float dx = dxf[i], dy = dyf[i];
-          const float tx = coeff * gx, ty = coeff * gy;
-          a[0] += tx;
-          a[1] = fmaf(tx, dx, a[1]);
-          a[2] = fmaf(tx, dy, a[2]);
-          a[3] += ty;
-          a[4] = fmaf(ty, dx, a[4]);
-          a[5] = fmaf(ty, dy, a[5]);
-          const float w[6] = {1.f, dx, dy, dx * dx, dx * dy, dy * dy};
-          const float aa = gx * gx, ab = gx * gy, bb = gy * gy;
-#pragma unroll
-          for (int j = 0; j < 6; ++j) {
-            a[6 + j] = fmaf(aa, w[j], a[6 + j]);
-            a[12 + j] = fmaf(ab, w[j], a[12 + j]);
-            a[18 + j] = fmaf(bb, w[j], a[18 + j]);
-          }
+      } else if (st != DICB200_POI_OK) {
+        if (lane == 0) {
+          S.status = st;
+          S.done = 1;
         }
-      }
-      double t24[24];
+      } else if (METHOD == 1) {
+        // rhs = sum e_k sd_k (subpixel.cpp:328-333), expanded; step = H^-1 (-rhs), lane i -> step_i
+        const double ratio = S.nf / ng;
+        double si = 0.0;
 #pragma unroll
-      for (int j = 0; j < 24; ++j) t24[j] = a[j];
-      block_sum<24>(t24, rb, buf);
-      if (tid == 0) {
-        const double ng2 = ng * ng;
-        const double scale = -2.0 / (nf * ng);
-        double H[36], neg[6], step[6];
-        assemble_hessian(t24 + 6, 2.0 / ng2, H);
-        for (int j = 0; j < 6; ++j) neg[j] = -(t24[j] * scale);
-        Ldlt6 L;
-        ldlt6_compute(L, H);
-        int st = L.ok ? DICB200_POI_OK : DICB200_POI_DEGENERATE_SUBSET;
-        if (st == DICB200_POI_OK) {
-          ldlt6_solve(L, neg, step);
-          bool fin = true;
-          for (int j = 0; j < 6; ++j) fin = fin && isfinite(step[j]);
-          if (!fin) st = DICB200_POI_DEGENERATE_SUBSET;
+        for (int j = 0; j < 6; ++j) si = fma(hinv[j], -(S.A[j] - ratio * (t[3 + j] - delta * S.Ssd[j])), si);
+        double step[6];
+        bool finite = true;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          step[j] = __shfl_sync(0xffffffffu, si, j);
+          finite = finite && isfinite(step[j]);
         }
-        if (st == DICB200_POI_OK) {
-          for (int j = 0; j < 6; ++j) S.p[j] += step[j];
-          if (fabs(warp_det(S.p)) < 1e-8) st = DICB200_POI_WARP_NOT_INVERTIBLE;
+        if (lane == 0) finish_step(S, step, finite, DICB200_POI_DEGENERATE_TEXTURE, iter, p.tol, true);
+      } else if (lane == 0) {
+        // NR (subpixel.cpp:247-271): gradient = -2/(nf ng) sum coeff J, H = 2/ng^2 sum J J^T
+        const double cross = t[2] - delta * S.scf;
+        const double kappa = cross / ng2;
+        double neg[6], step[6] = {0, 0, 0, 0, 0, 0};
+        bool finite = true;
+        const double scale = -2.0 / (S.nf * ng);
+#pragma unroll
+        for (int j = 0; j < 6; ++j) neg[j] = -(scale * (t[3 + j] - kappa * (t[9 + j] - delta * t[15 + j])));
+        assemble_hessian(t + 21, 2.0 / ng2, shH);
+        ldlt6_compute(shL, shH);
+        if (!shL.ok) {
+          finite = false;
+        } else {
+          ldlt6_solve(shL, neg, step);
+          for (int j = 0; j < 6; ++j) finite = finite && isfinite(step[j]);
         }
-        S.status = st;
-        if (st == DICB200_POI_OK) {
-          S.iterations = iter;
-          if (fmax(fabs(step[0]), fabs(step[3])) < p.tol) {
-            S.converged = 1;
-            S.done = 1;
-          }
-        }
+        finish_step(S, step, finite, DICB200_POI_DEGENERATE_SUBSET, iter, p.tol, false);
       }
     }
     __syncthreads();
-    status = S.status;
-    if (status != DICB200_POI_OK || S.done) break;
-  }
-  if (status == DICB200_POI_OK) {
-    // final re-sample + ZNCC (subpixel.cpp:288-297, 348-357)
-    double gbar, ng, cross;
-    status = sample(false, gbar, ng, cross);
-    if (status == DICB200_POI_OK) zncc_final = cross / (nf * ng);
+    if (S.done == 2 || S.status != DICB200_POI_OK) break;
   }
   if (tid == 0) {
-    if (status == DICB200_POI_OK) {
+    if (S.status == DICB200_POI_OK) {
       rec->u = S.p[0];
       rec->v = S.p[3];
-      rec->zncc = zncc_final;
+      rec->zncc = S.zncc;
       rec->iterations = S.iterations;
       rec->converged = S.converged;
     } else {
-      rec->status = status;
+      rec->status = S.status;
       rec->converged = 0;
     }
   }
 }
 
-template <typename Pix, int PPT>
-cudaError_t launch_ppt(const RefineParams& p, int nt, cudaStream_t st) {
+template <typename Pix, int PPT, int WP>
+cudaError_t launch_ppt(const RefineParams& p, size_t smem, cudaStream_t st) {
   if (p.method == 0)
-    refine_kernel<Pix, PPT, 0><<<p.n_records, nt, 0, st>>>(p);
+    refine_kernel<Pix, PPT, 0, WP><<<p.n_records, kNT, smem, st>>>(p);
   else
-    refine_kernel<Pix, PPT, 1><<<p.n_records, nt, 0, st>>>(p);
+    refine_kernel<Pix, PPT, 1, WP><<<p.n_records, kNT, smem, st>>>(p);
   count_launch();
   return cudaGetLastError();
 }
 
+// (PPT, window pitch) by half-width: n <= 256*PPT and 2M+1+2*kPad <= WP
 template <typename Pix>
-cudaError_t launch_pix(const RefineParams& p, int ppt, int nt, cudaStream_t st) {
+cudaError_t launch_pix(const RefineParams& p, int ppt, cudaStream_t st) {
+  const int S = 2 * p.M + 1 + 2 * kPad;
   switch (ppt) {
-    case 4: return launch_ppt<Pix, 4>(p, nt, st);
-    case 8: return launch_ppt<Pix, 8>(p, nt, st);
-    case 14: return launch_ppt<Pix, 14>(p, nt, st);
-    default: return launch_ppt<Pix, 16>(p, nt, st);
+    case 2: return launch_ppt<Pix, 2, 32>(p, (size_t)S * 32 * 4, st);
+    case 4: return launch_ppt<Pix, 4, 64>(p, (size_t)S * 64 * 4, st);
+    case 7: return launch_ppt<Pix, 7, 64>(p, (size_t)S * 64 * 4, st);
+    case 10: return launch_ppt<Pix, 10, 64>(p, (size_t)S * 64 * 4, st);
+    default: return launch_ppt<Pix, 16, 128>(p, (size_t)S * 128 * 4, st);
   }
 }
 
@@ -516,26 +726,23 @@ cudaError_t launch_pix(const RefineParams& p, int ppt, int nt, cudaStream_t st) 
 
 bool refine_plan(int M, int* ppt_out, int* nt_out) {
   const int n = (2 * M + 1) * (2 * M + 1);
-  const int ppts[] = {4, 8, 14, 16};
-  double best = -1.0;
-  for (int ppt : ppts) {
-    const int nt = (((n + ppt - 1) / ppt) + 31) / 32 * 32;
-    if (nt > 256) continue;
-    const double util = (double)n / (nt * ppt);
-    if (util > best + 1e-9) {
-      best = util;
-      *ppt_out = ppt;
-      *nt_out = nt;
+  const int S = 2 * M + 1 + 2 * kPad;
+  const int ppts[] = {2, 4, 7, 10, 16};
+  const int pitch[] = {32, 64, 64, 64, 128};
+  for (int i = 0; i < 5; ++i)
+    if (ppts[i] * kNT >= n && S <= pitch[i]) {
+      *ppt_out = ppts[i];
+      *nt_out = kNT;
+      return true;
     }
-  }
-  return best > 0.0;
+  return false;
 }
 
 cudaError_t refine_launch(const RefineParams& p, bool u8, cudaStream_t st) {
   if (p.n_records <= 0) return cudaSuccess;
   int ppt = 0, nt = 0;
   if (!refine_plan(p.M, &ppt, &nt)) return cudaErrorInvalidValue;
-  return u8 ? launch_pix<uint8_t>(p, ppt, nt, st) : launch_pix<uint16_t>(p, ppt, nt, st);
+  return u8 ? launch_pix<uint8_t>(p, ppt, st) : launch_pix<uint16_t>(p, ppt, st);
 }
 
 }  // namespace dicb200
