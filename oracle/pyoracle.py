@@ -24,6 +24,8 @@ def build(verbose: bool = False) -> None:
     targets = ["oracle"]
     if os.path.isdir(REFERENCE_SRC):
         targets.append("ref")
+        if os.path.exists(os.path.join(HERE, "..", "paper_1905_06228_b200", "libdicb200.so")):
+            targets.append("shim")
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True,
                    stdout=None if verbose else subprocess.DEVNULL)
 

@@ -1,0 +1,67 @@
+// TEST INFRASTRUCTURE ONLY: builds the C++ drop-in shim (include/dic_b200/pipeline.hpp)
+// INSIDE the reference build and compares dic::b200::analyze_pair with the
+// reference's own dic::analyze_pair on a synthetic pair (run on the GPU box by
+// tests/test_gpu_shim.py). Output: one line per check, exit code 0 on parity.
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "dic/pipeline.hpp"
+#include "dic_b200/pipeline.hpp"
+#include "dicb200_synth.h"
+
+int main() {
+  const int W = 192, H = 160;
+  dicb200_synth_spec sp{};
+  sp.width = W;
+  sp.height = H;
+  sp.dtype = DICB200_U8;
+  sp.max_value = 255;
+  sp.seed = 11;
+  sp.blob_count = W * H / 60;
+  sp.field = DICB200_FIELD_NONE;
+  sp.sigma_min = 2.0;
+  sp.sigma_max = 4.0;
+  sp.peak_min = 60.0;
+  sp.peak_max = 200.0;
+  std::vector<uint8_t> a(W * H), b(W * H);
+  dicb200_synth_render(&sp, a.data(), W, 1);
+  sp.field = DICB200_FIELD_AFFINE;
+  sp.a[0] = 2.3;
+  sp.a[3] = -1.4;
+  dicb200_synth_render(&sp, b.data(), W, 1);
+  dic::GrayImage ga(W, H, std::vector<double>(a.begin(), a.end()), 0);
+  dic::GrayImage gb(W, H, std::vector<double>(b.begin(), b.end()), 1);
+  int bad = 0;
+  for (int method = 0; method < 3; ++method) {
+    dic::RunConfig cfg;
+    cfg.integer_method = static_cast<dic::IntegerMethod>(method);
+    cfg.subpixel_method = method == 1 ? dic::SubpixelMethod::icgn : dic::SubpixelMethod::nr;
+    cfg.search.bfs_domain = dic::BfsDomain::window;
+    cfg.search.search_radius = 8;
+    cfg.grid.half_width = 10;
+    cfg.grid.spacing = 12;
+    cfg.refine.tol = 1e-4;
+    const auto ref = dic::analyze_pair(ga, gb, cfg, 3);
+    const auto got = dic::b200::analyze_pair(ga, gb, cfg, 3);
+    int mism = 0;
+    double du = 0.0;
+    for (size_t i = 0; i < ref.records.size(); ++i) {
+      const auto &r = ref.records[i], &g = got.records[i];
+      if (r.x != g.x || r.y != g.y || r.evaluations != g.evaluations || r.converged != g.converged) ++mism;
+      if (r.converged) du = std::fmax(du, std::fmax(std::fabs(r.u - g.u), std::fabs(r.v - g.v)));
+    }
+    const bool ok = ref.records.size() == got.records.size() && mism == 0 && du < 1e-3;
+    std::printf("method %d: %zu POIs, integer mismatches %d, max |du|,|dv| %.3g -> %s\n", method,
+                ref.records.size(), mism, du, ok ? "ok" : "FAIL");
+    bad += !ok;
+  }
+  try {
+    dic::GrayImage small(W, H - 1, std::vector<double>(W * (H - 1), 0.0));
+    dic::b200::analyze_pair(ga, small, dic::RunConfig{});
+    ++bad;
+  } catch (const dic::Error& e) {
+    std::printf("pair error rethrown as dic::Error: %s\n", e.what());
+  }
+  return bad;
+}
