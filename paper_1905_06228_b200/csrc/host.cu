@@ -121,7 +121,7 @@ static dicb200_status validate_pair(const dicb200_image* a, const dicb200_image*
   if (cfg->subpixel_method != DICB200_SUB_NONE) {
     int ppt, nt;
     if (!refine_plan(cfg->half_width, &ppt, &nt))
-      return invalid("half_width too large for the device refiners (M <= 31)");
+      return invalid("half_width too large for the device refiners (M <= 64)");
   }
   return DICB200_OK;
 }

@@ -3,25 +3,28 @@
 // subpixel.cpp:224-299), first-order warp, bilinear interpolation
 // (interp_bilinear / grad_bilinear, subpixel.cpp:59-128).
 //
-// One CTA (8 warps) per POI; every thread owns PPT subset pixels in registers
-// for the whole solve. The target neighbourhood of the integer estimate is
-// staged once in shared memory as fp32 (taps that drift outside it fall back
-// to global loads), so each iteration is ONE pass over the pixels: warp +
-// gather + bilinear (+ gradient for NR) in fp32 on subset-local coordinates,
-// per-thread fp32 partials of every sum the update needs, one block
-// reduction in fp64, and warp 0 doing the 6x6 algebra in fp64.
+// One WARP per POI; a CTA (8 warps) takes a strip of 8 neighbouring POIs of
+// one grid row, which share one staged fp32 reference region (subsets + 1 px
+// gradient border) and one staged fp32 target region (union of the 8
+// neighbourhoods of the integer estimates + kPad). After staging there are no
+// block barriers: every reduction is a warp shuffle and the 6x6 algebra runs
+// lane-parallel in fp64 on the same warp. Samples whose warped subset leaves
+// the staged region (or needs domain checks near the image border) take the
+// checked slow path with global loads, so any drift is handled exactly.
 //
-// The reference forms e_k = f_k - (nf/ng)(g_k - gbar) (IC-GN, :331) and
-// coeff_k = f_k - (cross/ng^2)(g_k - gbar) (NR, :258) per pixel, which needs
-// gbar and ng before the update sums (three passes). Here the update sums are
-// expanded exactly,
+// Each iteration is ONE pass over the pixels: warp + gather + bilinear
+// (+ gradient for NR) in fp32 on subset-local coordinates, per-lane fp32
+// partials, fp64 warp reductions. The reference forms e_k (:331) / coeff_k
+// (:258) after gbar and ng are known; the update sums are expanded exactly,
 //   sum e_k sd_k = sum f_k sd_k - (nf/ng) [ sum g'_k sd_k - (gbar - fbar) sum sd_k ],
-// with g' = g - fbar, so one pass suffices; the reference-side sums
-// (sum f sd, sum sd, and the Hessian) are precomputed in fp64 (the Hessian
-// EXACTLY: (2 grad)^2 * {1,dx,dy,dx^2,dxdy,dy^2} are integers < 2^53).
-// Convergence test, failure semantics (guard band M+2, domain checks,
-// |det| < 1e-8, LDLT failure, non-finite step, degenerate target) and the
-// final re-sample + ZNCC follow subpixel.cpp / pipeline.cpp:82-133.
+// g' = g - fbar, with the reference-side sums precomputed in fp64 (the IC-GN
+// Hessian EXACTLY: (2 grad)^2 * {1,dx,dy,dx^2,dxdy,dy^2} are integers < 2^53).
+// 6x6 solves: warp-parallel Cholesky H^-1 (H is SPD: J^T J); IC-GN keeps H^-1
+// in registers for all iterations. "Degenerate target" (ng == 0 in the
+// reference) is detected exactly as "all samples equal" (min == max).
+// Convergence test, guard band M+2, domain checks, |det| < 1e-8, non-finite
+// steps and the final re-sample + ZNCC follow subpixel.cpp; failure semantics
+// follow pipeline.cpp:82-133 (status set, converged = 0, integer fields kept).
 #include "common.cuh"
 #include "linalg.cuh"
 #include "refine.cuh"
@@ -30,10 +33,10 @@ namespace dicb200 {
 
 namespace {
 
-constexpr int kNT = 256;
-constexpr int kWarps = kNT / 32;
-constexpr int kPad = 4;
-constexpr int kRedMax = 40;
+constexpr int kWarps = 8;        // POIs per CTA
+constexpr int kNT = 32 * kWarps;
+constexpr int kPad = 4;          // staged target margin around each neighbourhood (px)
+constexpr int kSpread = 12;      // max spread of integer estimates folded into one region
 
 template <typename Pix>
 __device__ __forceinline__ float gpx(const ImageView& im, int x, int y) {
@@ -123,36 +126,6 @@ __device__ __forceinline__ double warp_sum1(double v) {
 }
 
 // Per-thread partials -> per-warp sums in rb[warp][base + i] (one value live at a time).
-template <int NV, typename T>
-__device__ __forceinline__ void block_partials(const T (&v)[NV], double (*rb)[kRedMax], int base = 0) {
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const double s = warp_sum1((double)v[i]);
-    if ((threadIdx.x & 31) == 0) rb[threadIdx.x >> 5][base + i] = s;
-  }
-}
-
-// After a __syncthreads: warp 0's lanes total the per-warp sums into tot[0..nv).
-__device__ __forceinline__ void warp0_totals(double (*rb)[kRedMax], double* tot, int nv) {
-  for (int j = threadIdx.x & 31; j < nv; j += 32) {
-    double s = rb[0][j];
-#pragma unroll
-    for (int w = 1; w < kWarps; ++w) s += rb[w][j];
-    tot[j] = s;
-  }
-  __syncwarp();
-}
-
-struct State {
-  double p[6];  // u, ux, uy, v, vx, vy (subpixel.hpp:13-16)
-  int status, done, iterations, converged;
-  double zncc;
-  // reference-side constants
-  double fbar, nf, scf;   // mean, ||f - fbar||, sum of the fp32 centred values
-  double A[6], Ssd[6];    // sum cf*sd, sum sd (IC-GN)
-  double Hinv[36];        // IC-GN: H^-1 (H exact)
-};
-
 __device__ __forceinline__ double warp_det(const double* p) {
   return __dsub_rn(__dmul_rn(1.0 + p[1], 1.0 + p[5]), __dmul_rn(p[2], p[4]));
 }
@@ -201,42 +174,6 @@ __device__ void assemble_hessian(const double* mo, double scale, double* H) {
   for (int i = 0; i < 6; ++i)
 #pragma unroll
     for (int j = 0; j < 6; ++j) H[i * 6 + j] = mo[map[i][j][0] * 6 + map[i][j][1]] * scale;
-}
-
-// warp 0: finish one iteration from the totals; lane 0 commits the state.
-__device__ void finish_step(State& S, const double* step, bool finite, int fail_code, int iter, double tol,
-                            bool icgn) {
-  int st = finite ? DICB200_POI_OK : fail_code;
-  if (st == DICB200_POI_OK) {
-    if (icgn) {
-      st = compose_with_inverse(S.p, step);
-    } else {
-      for (int j = 0; j < 6; ++j) S.p[j] += step[j];
-    }
-  }
-  if (st == DICB200_POI_OK && fabs(warp_det(S.p)) < 1e-8) st = DICB200_POI_WARP_NOT_INVERTIBLE;
-  S.status = st;
-  if (st == DICB200_POI_OK) {
-    S.iterations = iter;
-    if (fmax(fabs(step[0]), fabs(step[3])) < tol) {
-      S.converged = 1;
-      S.done = 1;
-    }
-  } else {
-    S.done = 1;
-  }
-}
-
-// Fast-path bilinear sample from the staged window (no checks: the caller
-// proved the whole warped subset lies inside the window and the image).
-template <int WP>
-__device__ __forceinline__ float sample_fast(const float* w, float wx, float wy) {
-  const float flx = floorf(wx), fly = floorf(wy);
-  const float fx = wx - flx, fy = wy - fly;
-  const float* q = w + (int)fly * WP + (int)flx;
-  const float f00 = q[0], f10 = q[1], f01 = q[WP], f11 = q[WP + 1];
-  const float a10 = f10 - f00, a01 = f01 - f00, a11 = (f00 + f11) - f10 - f01;
-  return fmaf(a11 * fx, fy, fmaf(a01, fy, fmaf(a10, fx, f00)));
 }
 
 // Warp-parallel Cholesky of the SPD 6x6 H (lane i < 6 holds row i in h[]),
@@ -288,164 +225,239 @@ __device__ void warp_cholesky_inverse(double (&h)[6], double (&hinv)[6], bool& p
   pd = ok;
 }
 
-template <typename Pix, int PPT, int METHOD, int WP>
-__global__ void __launch_bounds__(kNT, 3) refine_kernel(RefineParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ double rb[kWarps][kRedMax];
-  __shared__ double tot[kRedMax];
-  __shared__ float rmm[kWarps][2];
-  __shared__ double shH[36];
-  __shared__ Ldlt6 shL;
-  __shared__ State S;
-  const int k = blockIdx.x;
-  dicb200_poi_record* rec = p.rec + k;
-  if (rec->status != DICB200_POI_OK) return;  // integer stage failed: record stays
+
+struct StripGeom {
+  int rX0, rY0, rP, rH;   // reference region: global origin, pitch (floats), rows
+  int tX0, tY0, tP, tH;   // target region
+};
+
+template <typename Pix>
+__device__ __forceinline__ bool sample_slow(const Win& wn, const ImageView& im, int bx, int by, float xl, float yl,
+                                            bool grads, float& g, float& gx, float& gy) {
+  bool ok = bilinear<Pix>(wn, im, bx, by, xl, yl, g);
+  if (grads) ok = ok && grad_bilinear<Pix>(wn, im, bx, by, xl, yl, gx, gy);
+  return ok;
+}
+
+// Lane-parallel step from H^-1 rows (lane i < 6 holds row i) and the rhs;
+// returns the 6-vector on every lane.
+__device__ __forceinline__ void hinv_step(const double (&hinv)[6], const double (&rhs)[6], double (&step)[6],
+                                          bool& finite) {
+  double si = 0.0;
+#pragma unroll
+  for (int j = 0; j < 6; ++j) si = fma(hinv[j], -rhs[j], si);
+  finite = true;
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    step[j] = __shfl_sync(0xffffffffu, si, j);
+    finite = finite && isfinite(step[j]);
+  }
+}
+
+template <typename Pix, int METHOD>
+__global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
+  extern __shared__ __align__(16) float smem_f[];
+  __shared__ int s_idx[kWarps], s_idy[kWarps], s_ok[kWarps];
+  __shared__ StripGeom G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int M = p.M, side = 2 * M + 1, n = side * side;
-  const int iy = p.row_begin + k / p.lat.nx, ix = k % p.lat.nx;
-  const int cx = p.lat.cx(ix), cy = p.lat.cy(iy);
-  const int idx = rec->integer_dx, idy = rec->integer_dy;
+  const int iy = p.row_begin + blockIdx.y;
+  const int ix0 = blockIdx.x * p.spc;
+  const int ts = min(p.spc, p.lat.nx - ix0);
+  const int cy = p.lat.cy(iy);
+  const size_t rec0 = (size_t)(iy - p.row_begin) * p.lat.nx + ix0;
+
+  // ---- strip geometry from the integer estimates ----
+  if (tid < kWarps) {
+    int ok = 0, dx = 0, dy = 0;
+    if (tid < ts) {
+      const dicb200_poi_record& r = p.rec[rec0 + tid];
+      ok = r.status == DICB200_POI_OK;
+      dx = r.integer_dx;
+      dy = r.integer_dy;
+    }
+    s_ok[tid] = ok;
+    s_idx[tid] = dx;
+    s_idy[tid] = dy;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int first = -1;
+    for (int s = 0; s < ts; ++s)
+      if (s_ok[s]) {
+        first = s;
+        break;
+      }
+    int dxlo = 0, dxhi = 0, dylo = 0, dyhi = 0;
+    if (first >= 0) {
+      dxlo = dxhi = s_idx[first];
+      dylo = dyhi = s_idy[first];
+      for (int s = 0; s < ts; ++s)
+        if (s_ok[s]) {
+          dxlo = min(dxlo, s_idx[s]);
+          dxhi = max(dxhi, s_idx[s]);
+          dylo = min(dylo, s_idy[s]);
+          dyhi = max(dyhi, s_idy[s]);
+        }
+      // bound the region: outliers beyond kSpread fall back to the slow path
+      dxlo = max(dxlo, s_idx[first] - kSpread);
+      dxhi = min(dxhi, s_idx[first] + kSpread);
+      dylo = max(dylo, s_idy[first] - kSpread);
+      dyhi = min(dyhi, s_idy[first] + kSpread);
+    }
+    const int cx0 = p.lat.cx(ix0), cx1 = p.lat.cx(ix0 + ts - 1);
+    G.rX0 = cx0 - M - 1;
+    G.rY0 = cy - M - 1;
+    G.rP = (cx1 - cx0) + side + 2;
+    G.rH = side + 2;
+    G.tX0 = cx0 + dxlo - M - kPad;
+    G.tY0 = cy + dylo - M - kPad;
+    G.tP = (cx1 - cx0) + (dxhi - dxlo) + side + 2 * kPad;
+    G.tH = (dyhi - dylo) + side + 2 * kPad;
+  }
+  __syncthreads();
+  const StripGeom g = G;
+  float* R = smem_f;                    // reference region [rH][rP]
+  float* T = smem_f + g.rH * g.rP;      // target region [tH][tP]
+  // ---- stage both regions (fp32), zero outside the images ----
+  for (int i = tid; i < g.rH * g.rP; i += kNT) {
+    const int y = i / g.rP, x = i - y * g.rP;
+    const int gx = g.rX0 + x, gy = g.rY0 + y;
+    R[i] = (gx >= 0 && gx < p.ref.width && gy >= 0 && gy < p.ref.height) ? gpx<Pix>(p.ref, gx, gy) : 0.f;
+  }
+  for (int i = tid; i < g.tH * g.tP; i += kNT) {
+    const int y = i / g.tP, x = i - y * g.tP;
+    const int gx = g.tX0 + x, gy = g.tY0 + y;
+    T[i] = (gx >= 0 && gx < p.tgt.width && gy >= 0 && gy < p.tgt.height) ? gpx<Pix>(p.tgt, gx, gy) : 0.f;
+  }
+  __syncthreads();
+  // ==== from here on every warp is independent (no block barriers) ====
+  if (warp >= ts || !s_ok[warp]) return;
+  dicb200_poi_record* rec = p.rec + rec0 + warp;
+  const int cx = p.lat.cx(ix0 + warp);
+  const int idx = s_idx[warp], idy = s_idy[warp];
   const int bx = cx + idx, by = cy + idy;
 
-  if (METHOD == 1 && (cx - M - 1 < 0 || cx + M + 1 > p.ref.width - 1 || cy - M - 1 < 0 ||
-                      cy + M + 1 > p.ref.height - 1)) {
-    if (tid == 0) {
-      rec->status = DICB200_POI_BORDER_GRADIENTS;  // subpixel.cpp:193-195
+  auto fail = [&](int code) {
+    if (lane == 0) {
+      rec->status = code;
       rec->converged = 0;
     }
+  };
+  if (METHOD == 1 && (cx - M - 1 < 0 || cx + M + 1 > p.ref.width - 1 || cy - M - 1 < 0 ||
+                      cy + M + 1 > p.ref.height - 1)) {
+    fail(DICB200_POI_BORDER_GRADIENTS);  // subpixel.cpp:193-195
     return;
   }
+  // pixel walk: lane handles k = lane + 32 i; (rr, cc) advanced incrementally
+  const int npl = (n + 31) / 32;
+  const int q32 = 32 / side, r32 = 32 - q32 * side;
+  const int rr0 = lane / side, cc0 = lane - (lane / side) * side;
+  // reference region pointer of the pixel (rr, cc): R + (rr + 1) * rP + (cx - cx0) + cc + 1
+  const float* Rs = R + g.rP + (cx - p.lat.cx(ix0)) + 1;
 
-  // ---- stage the target neighbourhood (fp32, pitch WP) ----
-  Win wn;
-  wn.S = side + 2 * kPad;
-  wn.P = WP;
-  wn.ox = bx - M - kPad;
-  wn.oy = by - M - kPad;
-  float* wbuf = reinterpret_cast<float*>(smem_raw);
-  for (int i = tid; i < wn.S * WP; i += kNT) {
-    const int ly = i / WP, lx = i - ly * WP;
-    const int gx = wn.ox + lx, gy = wn.oy + ly;
-    float v = 0.f;
-    if (lx < wn.S && gx >= 0 && gx < p.tgt.width && gy >= 0 && gy < p.tgt.height) v = gpx<Pix>(p.tgt, gx, gy);
-    wbuf[i] = v;
-  }
-  wn.w = wbuf;
-
-  // ---- reference pixels: registers ----
-  float dxf[PPT], dyf[PPT], cf[PPT], gxr[PPT], gyr[PPT];
+  // ---- subset_stats: exact sums ----
+  double sf = 0.0, sff = 0.0;
   {
-    double s2[2] = {0.0, 0.0};
-#pragma unroll
-    for (int i = 0; i < PPT; ++i) {
-      const int kk = tid + i * kNT;
-      const int r = kk / side, c = kk - r * side;
-      dxf[i] = (float)(c - M);
-      dyf[i] = (float)(r - M);
-      cf[i] = gxr[i] = gyr[i] = 0.f;
-      if (kk < n) {
-        const int x = cx + c - M, y = cy + r - M;
-        const float f = gpx<Pix>(p.ref, x, y);
-        cf[i] = f;
-        if (METHOD == 1) {
-          gxr[i] = 0.5f * (gpx<Pix>(p.ref, x + 1, y) - gpx<Pix>(p.ref, x - 1, y));
-          gyr[i] = 0.5f * (gpx<Pix>(p.ref, x, y + 1) - gpx<Pix>(p.ref, x, y - 1));
-        }
-        s2[0] += (double)f;
-        s2[1] += (double)f * (double)f;
-      } else {
-        dxf[i] = dyf[i] = 0.f;  // padding slots sample the centre (weight 0 everywhere)
+    int rr = rr0, cc = cc0;
+    for (int i = 0; i < npl; ++i) {
+      if (rr < side) {
+        const double f = Rs[rr * g.rP + cc];
+        sf += f;
+        sff += f * f;
       }
-    }
-    block_partials<2>(s2, rb);
-    __syncthreads();
-    if (warp == 0) warp0_totals(rb, tot, 2);
-    __syncthreads();
-    const int64_t sf = (int64_t)tot[0], sff = (int64_t)tot[1];
-    const int64_t vf = (int64_t)n * sff - sf * sf;
-    if (vf <= 0) {  // constant subset
-      if (tid == 0) {
-        rec->status = METHOD == 1 ? DICB200_POI_DEGENERATE_TEXTURE : DICB200_POI_DEGENERATE_SUBSET;
-        rec->converged = 0;
+      cc += r32;
+      rr += q32;
+      if (cc >= side) {
+        cc -= side;
+        ++rr;
       }
-      return;
-    }
-    const double mean = tot[0] / (double)n;  // correlation.cpp:25: exact sum / n
-#pragma unroll
-    for (int i = 0; i < PPT; ++i) cf[i] = (tid + i * kNT < n) ? (float)((double)cf[i] - mean) : 0.f;
-    if (tid == 0) {
-      S.fbar = mean;
-      S.nf = sqrt((double)vf / (double)n);
     }
   }
-  __syncthreads();  // rb reuse + S.fbar/nf visible
+  sf = warp_sum1(sf);
+  sff = warp_sum1(sff);
+  const int64_t vf = (int64_t)n * (int64_t)sff - (int64_t)sf * (int64_t)sf;
+  if (vf <= 0) {  // constant subset
+    fail(METHOD == 1 ? DICB200_POI_DEGENERATE_TEXTURE : DICB200_POI_DEGENERATE_SUBSET);
+    return;
+  }
+  const double fbar = sf / (double)n;  // correlation.cpp:25: exact sum / n
+  const double nf = sqrt((double)vf / (double)n);
+  const float fbarf = (float)fbar;
 
-  double hinv[6] = {0, 0, 0, 0, 0, 0};  // IC-GN, warp 0 lanes 0..5: row `lane` of H^-1
-  if (METHOD == 1) {
-    // ---- icgn_precompute: exact Hessian moments, sum f*sd, sum sd ----
-#pragma unroll 1
-    for (int grp = 0; grp < 3; ++grp) {
-      double m6[6] = {0, 0, 0, 0, 0, 0};
+  // ---- precompute: sum cf; IC-GN: exact Hessian -> H^-1, sum cf*sd, sum sd ----
+  double scf = 0.0, A[6] = {0, 0, 0, 0, 0, 0}, Ssd[6] = {0, 0, 0, 0, 0, 0};
+  double hinv[6] = {0, 0, 0, 0, 0, 0};
+  {
+    double mo[18];
 #pragma unroll
-      for (int i = 0; i < PPT; ++i) {
-        const double ga = 2.0 * gxr[i], gb = 2.0 * gyr[i];  // integers
-        const double q = grp == 0 ? ga * ga : (grp == 1 ? ga * gb : gb * gb);
-        const double dx = dxf[i], dy = dyf[i];
-        m6[0] += q;
-        m6[1] = fma(q, dx, m6[1]);
-        m6[2] = fma(q, dy, m6[2]);
-        m6[3] = fma(q, dx * dx, m6[3]);
-        m6[4] = fma(q, dx * dy, m6[4]);
-        m6[5] = fma(q, dy * dy, m6[5]);
-      }
-      block_partials<6>(m6, rb, grp * 6);
-    }
-    {
-      double a7[7] = {0, 0, 0, 0, 0, 0, 0};
-      double s6[6] = {0, 0, 0, 0, 0, 0};
+    for (int j = 0; j < 18; ++j) mo[j] = 0.0;
+    int rr = rr0, cc = cc0;
+    for (int i = 0; i < npl; ++i) {
+      if (rr < side) {
+        const float* q = Rs + rr * g.rP + cc;
+        const float cfv = (float)((double)q[0] - fbar);
+        scf += (double)cfv;
+        if (METHOD == 1) {
+          const float gxv = 0.5f * (q[1] - q[-1]), gyv = 0.5f * (q[g.rP] - q[-g.rP]);
+          const double dx = cc - M, dy = rr - M;
+          const double ga = 2.0 * gxv, gb = 2.0 * gyv;  // integers
+          const double w6[6] = {1.0, dx, dy, dx * dx, dx * dy, dy * dy};
+          const double aa = ga * ga, ab = ga * gb, bb = gb * gb;
 #pragma unroll
-      for (int i = 0; i < PPT; ++i) {
-        const double c = cf[i], gx = gxr[i], gy = gyr[i], dx = dxf[i], dy = dyf[i];
-        const double cgx = c * gx, cgy = c * gy;  // exact (float x float)
-        a7[0] += c;
-        a7[1] += cgx;
-        a7[2] += cgx * dx;
-        a7[3] += cgx * dy;
-        a7[4] += cgy;
-        a7[5] += cgy * dx;
-        a7[6] += cgy * dy;
-        s6[0] += gx;
-        s6[1] += gx * dx;
-        s6[2] += gx * dy;
-        s6[3] += gy;
-        s6[4] += gy * dx;
-        s6[5] += gy * dy;
+          for (int j = 0; j < 6; ++j) {
+            mo[j] = fma(aa, w6[j], mo[j]);
+            mo[6 + j] = fma(ab, w6[j], mo[6 + j]);
+            mo[12 + j] = fma(bb, w6[j], mo[12 + j]);
+          }
+          const double cgx = (double)cfv * gxv, cgy = (double)cfv * gyv;  // exact (float x float)
+          A[0] += cgx;
+          A[1] += cgx * dx;
+          A[2] += cgx * dy;
+          A[3] += cgy;
+          A[4] += cgy * dx;
+          A[5] += cgy * dy;
+          Ssd[0] += gxv;
+          Ssd[1] += gxv * dx;
+          Ssd[2] += gxv * dy;
+          Ssd[3] += gyv;
+          Ssd[4] += gyv * dx;
+          Ssd[5] += gyv * dy;
+        }
       }
-      block_partials<7>(a7, rb, 18);
-      block_partials<6>(s6, rb, 25);
+      cc += r32;
+      rr += q32;
+      if (cc >= side) {
+        cc -= side;
+        ++rr;
+      }
     }
-    __syncthreads();
-    if (warp == 0) {
-      warp0_totals(rb, tot, 31);
-      // H (exact) row `lane` -> warp Cholesky -> row `lane` of H^-1 in registers
+    scf = warp_sum1(scf);
+    if (METHOD == 1) {
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        A[j] = warp_sum1(A[j]);
+        Ssd[j] = warp_sum1(Ssd[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 18; ++j) mo[j] = warp_sum1(mo[j]);
       const int map[6][6][2] = {
           {{0, 0}, {0, 1}, {0, 2}, {1, 0}, {1, 1}, {1, 2}}, {{0, 1}, {0, 3}, {0, 4}, {1, 1}, {1, 3}, {1, 4}},
           {{0, 2}, {0, 4}, {0, 5}, {1, 2}, {1, 4}, {1, 5}}, {{1, 0}, {1, 1}, {1, 2}, {2, 0}, {2, 1}, {2, 2}},
           {{1, 1}, {1, 3}, {1, 4}, {2, 1}, {2, 3}, {2, 4}}, {{1, 2}, {1, 4}, {1, 5}, {2, 2}, {2, 4}, {2, 5}},
       };
       double h[6];
-      const int row = lane < 6 ? lane : 0;
 #pragma unroll
       for (int j = 0; j < 6; ++j) {
         double v = 0.0;
 #pragma unroll
         for (int r = 0; r < 6; ++r)
-          if (r == row) v = tot[map[r][j][0] * 6 + map[r][j][1]] * 0.25;
+          if (r == lane) v = mo[map[r][j][0] * 6 + map[r][j][1]] * 0.25;
         h[j] = v;
       }
       double hf2 = 0.0;
 #pragma unroll
-      for (int j = 0; j < 6; ++j) hf2 += lane < 6 ? h[j] * h[j] : 0.0;
+      for (int j = 0; j < 6; ++j) hf2 += h[j] * h[j];
       bool pd;
       warp_cholesky_inverse(h, hinv, pd);
       double if2 = 0.0;
@@ -454,86 +466,58 @@ __global__ void __launch_bounds__(kNT, 3) refine_kernel(RefineParams p) {
       hf2 = warp_sum1(hf2);
       if2 = warp_sum1(if2);
       // cond(H) <= ||H||_F ||H^-1||_F; exact eigenvalues only when inconclusive (subpixel.cpp:215-219)
-      bool accept = pd && sqrt(hf2) * sqrt(if2) < 1e12;
-      if (lane == 0) {
-        if (!accept && pd) {
-          assemble_hessian(tot, 0.25, shH);
+      int accept = pd && sqrt(hf2) * sqrt(if2) < 1e12;
+      if (!accept && pd) {
+        if (lane == 0) {
+          double H[36];
+          assemble_hessian(mo, 0.25, H);
           double lo, hi;
-          jacobi6_minmax(shH, &lo, &hi);
+          jacobi6_minmax(H, &lo, &hi);
           accept = lo > 0.0 && hi / lo < 1e12;
         }
-        S.status = accept ? DICB200_POI_OK : DICB200_POI_DEGENERATE_TEXTURE;
-        S.scf = tot[18];
-        for (int j = 0; j < 6; ++j) {
-          S.A[j] = tot[19 + j];
-          S.Ssd[j] = tot[25 + j];
-        }
+        accept = __shfl_sync(0xffffffffu, accept, 0);
       }
-    }
-  } else {
-    double a[1] = {0.0};
-#pragma unroll
-    for (int i = 0; i < PPT; ++i) a[0] += (double)cf[i];
-    block_partials<1>(a, rb);
-    __syncthreads();
-    if (warp == 0) {
-      warp0_totals(rb, tot, 1);
-      if (lane == 0) {
-        S.scf = tot[0];
-        S.status = DICB200_POI_OK;
-      }
-    }
-  }
-  if (tid == 0) {
-    S.p[0] = (double)idx;
-    S.p[1] = S.p[2] = 0.0;
-    S.p[3] = (double)idy;
-    S.p[4] = S.p[5] = 0.0;
-    S.done = 0;
-    S.iterations = 0;
-    S.converged = 0;
-  }
-  __syncthreads();
-  if (S.status != DICB200_POI_OK) {
-    if (tid == 0) {
-      rec->status = S.status;
-      rec->converged = 0;
-    }
-    return;
-  }
-
-  const double n_d = (double)n;
-  const float fbarf = (float)S.fbar;
-  const double lim = (double)(M + 2);
-  const float wofs = (float)(M + kPad);  // window coords = local coords + wofs
-
-  for (int iter = 1;; ++iter) {
-    const bool final_pass = iter > p.max_iter || S.done;
-    const double u = S.p[0], ux = S.p[1], uy = S.p[2], v = S.p[3], vx = S.p[4], vy = S.p[5];
-    {  // check_guard (subpixel.cpp:134-141), uniform
-      const double ccx = cx + u, ccy = cy + v;
-      if (!(ccx >= lim && ccx <= p.tgt.width - 1 - lim && ccy >= lim && ccy <= p.tgt.height - 1 - lim)) {
-        if (tid == 0) {
-          rec->status = DICB200_POI_DRIFTED;
-          rec->converged = 0;
-        }
+      if (!accept) {
+        fail(DICB200_POI_DEGENERATE_TEXTURE);
         return;
       }
     }
-    const float ul = (float)(u - idx), vl = (float)(v - idy);
-    const float uxf = (float)ux, uyf = (float)uy, vxf = (float)vx, vyf = (float)vy;
+  }
+
+  // ---- iterations (all lanes hold the same warp parameters) ----
+  double P[6] = {(double)idx, 0.0, 0.0, (double)idy, 0.0, 0.0};  // u, ux, uy, v, vx, vy
+  int iterations = 0, converged = 0, done = 0;
+  const double n_d = (double)n;
+  const double lim = (double)(M + 2);
+  const float offx = (float)(bx - g.tX0), offy = (float)(by - g.tY0);  // local -> region coords
+  Win wn;  // slow path: region as a window (global coords of T[0]), global fallback outside
+  wn.w = T;
+  wn.S = min(g.tP, g.tH);
+  wn.P = g.tP;
+  wn.ox = g.tX0;
+  wn.oy = g.tY0;
+  double zncc = 0.0;
+  int status = DICB200_POI_OK;
+  for (int iter = 1;; ++iter) {
+    const bool final_pass = iter > p.max_iter || done;
+    {  // check_guard (subpixel.cpp:134-141)
+      const double ccx = cx + P[0], ccy = cy + P[3];
+      if (!(ccx >= lim && ccx <= p.tgt.width - 1 - lim && ccy >= lim && ccy <= p.tgt.height - 1 - lim)) {
+        status = DICB200_POI_DRIFTED;
+        break;
+      }
+    }
+    const float ul = (float)(P[0] - idx), vl = (float)(P[3] - idy);
+    const float uxf = (float)P[1], uyf = (float)P[2], vxf = (float)P[4], vyf = (float)P[5];
     const bool grads = METHOD == 0 && !final_pass;
-    // Fast path iff the warped subset's bounding box (+1 px, +2 px with gradients)
-    // sits inside the staged window and the image domain: the affine map attains
-    // its extremes at the corners (uniform decision).
     bool fast;
     {
       const float Mf = (float)M;
       const float ex = fabsf(Mf + Mf * uxf) + fabsf(Mf * uyf), ey = fabsf(Mf * vxf) + fabsf(Mf + Mf * vyf);
       const float lo_x = ul - ex, hi_x = ul + ex, lo_y = vl - ey, hi_y = vl + ey;
       const float mg = grads ? 2.0f : 1.0f;
-      fast = lo_x - mg >= -wofs && hi_x + mg + 1.0f <= (float)(wn.S - 1) - wofs && lo_y - mg >= -wofs &&
-             hi_y + mg + 1.0f <= (float)(wn.S - 1) - wofs && (float)bx + lo_x - mg >= 0.0f &&
+      fast = offx + lo_x - mg >= 0.0f && offx + hi_x + mg + 1.0f <= (float)(g.tP - 1) && offy + lo_y - mg >= 0.0f &&
+             offy + hi_y + mg + 1.0f <= (float)(g.tH - 1) && (float)bx + lo_x - mg >= 0.0f &&
              (float)bx + hi_x + mg <= (float)(p.tgt.width - 1) && (float)by + lo_y - mg >= 0.0f &&
              (float)by + hi_y + mg <= (float)(p.tgt.height - 1);
     }
@@ -542,207 +526,221 @@ __global__ void __launch_bounds__(kNT, 3) refine_kernel(RefineParams p) {
 #pragma unroll
     for (int j = 0; j < NV; ++j) acc[j] = 0.f;
     int bad = 0;
-    float gmin = 3.0e38f, gmax = -3.0e38f;  // exact "constant subset" test (ng == 0 in the reference)
-#pragma unroll
-    for (int i = 0; i < PPT; ++i) {
-      const bool valid = tid + i * kNT < n;
-      const float xl = fmaf(uyf, dyf[i], fmaf(uxf, dxf[i], dxf[i] + ul));
-      const float yl = fmaf(vyf, dyf[i], fmaf(vxf, dxf[i], dyf[i] + vl));
-      float g = 0.f, gx = 0.f, gy = 0.f;
-      if (fast) {
-        g = sample_fast<WP>(wn.w, xl + wofs, yl + wofs);
-        if (grads) {
-          // grad_bilinear on the window: nodes (x0..x0+1, y0..y0+1), central differences
-          const float wx = xl + wofs, wy = yl + wofs;
+    float gmin = 3.0e38f, gmax = -3.0e38f;
+    int rr = rr0, cc = cc0;
+    for (int i = 0; i < npl; ++i) {
+      if (rr < side) {
+        const float dx = (float)(cc - M), dy = (float)(rr - M);
+        const float xl = fmaf(uyf, dy, fmaf(uxf, dx, dx + ul));
+        const float yl = fmaf(vyf, dy, fmaf(vxf, dx, dy + vl));
+        float gv = 0.f, gx = 0.f, gy = 0.f;
+        if (fast) {
+          const float wx = xl + offx, wy = yl + offy;
           const float flx = floorf(wx), fly = floorf(wy);
           const float fx = wx - flx, fy = wy - fly;
-          const float* q = wn.w + (int)fly * WP + (int)flx;
-          const float dx00 = q[1] - q[-1], dx10 = q[2] - q[0], dx01 = q[WP + 1] - q[WP - 1], dx11 = q[WP + 2] - q[WP];
-          const float dy00 = q[WP] - q[-WP], dy10 = q[WP + 1] - q[1 - WP], dy01 = q[2 * WP] - q[0],
-                      dy11 = q[2 * WP + 1] - q[1];
-          const float w00 = (1.f - fx) * (1.f - fy), w10 = fx * (1.f - fy), w01 = (1.f - fx) * fy, w11 = fx * fy;
-          gx = 0.5f * (w00 * dx00 + w10 * dx10 + w01 * dx01 + w11 * dx11);
-          gy = 0.5f * (w00 * dy00 + w10 * dy10 + w01 * dy01 + w11 * dy11);
+          const float* t = T + (int)fly * g.tP + (int)flx;
+          const float f00 = t[0], f10 = t[1], f01 = t[g.tP], f11 = t[g.tP + 1];
+          const float a10 = f10 - f00, a01 = f01 - f00, a11 = (f00 + f11) - f10 - f01;
+          gv = fmaf(a11 * fx, fy, fmaf(a01, fy, fmaf(a10, fx, f00)));
+          if (grads) {
+            const int P2 = 2 * g.tP;
+            const float dx00 = f10 - t[-1], dx10 = t[2] - f00, dx01 = f11 - t[g.tP - 1], dx11 = t[g.tP + 2] - f01;
+            const float dy00 = f01 - t[-g.tP], dy10 = f11 - t[1 - g.tP], dy01 = t[P2] - f00, dy11 = t[P2 + 1] - f10;
+            const float w00 = (1.f - fx) * (1.f - fy), w10 = fx * (1.f - fy), w01 = (1.f - fx) * fy, w11 = fx * fy;
+            gx = 0.5f * (w00 * dx00 + w10 * dx10 + w01 * dx01 + w11 * dx11);
+            gy = 0.5f * (w00 * dy00 + w10 * dy10 + w01 * dy01 + w11 * dy11);
+          }
+        } else {
+          bad |= !sample_slow<Pix>(wn, p.tgt, bx, by, xl, yl, grads, gv, gx, gy);
         }
-      } else if (valid) {
-        bad |= !bilinear<Pix>(wn, p.tgt, bx, by, xl, yl, g);
-        if (grads) bad |= !grad_bilinear<Pix>(wn, p.tgt, bx, by, xl, yl, gx, gy);
+        gmin = fminf(gmin, gv);
+        gmax = fmaxf(gmax, gv);
+        const float* q = Rs + rr * g.rP + cc;
+        const float cfv = q[0] - fbarf;
+        const float gp = gv - fbarf;
+        acc[0] += gp;
+        acc[1] = fmaf(gp, gp, acc[1]);
+        if (final_pass || METHOD == 0) acc[2] = fmaf(cfv, gp, acc[2]);
+        if (METHOD == 1) {
+          if (!final_pass) {
+            const float gxr = 0.5f * (q[1] - q[-1]), gyr = 0.5f * (q[g.rP] - q[-g.rP]);
+            const float tx = gp * gxr, ty = gp * gyr;
+            acc[3] += tx;
+            acc[4] = fmaf(tx, dx, acc[4]);
+            acc[5] = fmaf(tx, dy, acc[5]);
+            acc[6] += ty;
+            acc[7] = fmaf(ty, dx, acc[7]);
+            acc[8] = fmaf(ty, dy, acc[8]);
+          }
+        } else if (grads) {
+          const float J[6] = {gx, gx * dx, gx * dy, gy, gy * dx, gy * dy};
+#pragma unroll
+          for (int j = 0; j < 6; ++j) {
+            acc[3 + j] = fmaf(cfv, J[j], acc[3 + j]);
+            acc[9 + j] = fmaf(gp, J[j], acc[9 + j]);
+            acc[15 + j] += J[j];
+          }
+          const float wv[6] = {1.f, dx, dy, dx * dx, dx * dy, dy * dy};
+          const float aa = gx * gx, ab = gx * gy, bb = gy * gy;
+#pragma unroll
+          for (int j = 0; j < 6; ++j) {
+            acc[21 + j] = fmaf(aa, wv[j], acc[21 + j]);
+            acc[27 + j] = fmaf(ab, wv[j], acc[27 + j]);
+            acc[33 + j] = fmaf(bb, wv[j], acc[33 + j]);
+          }
+        }
       }
-      if (!valid) continue;
-      gmin = fminf(gmin, g);
-      gmax = fmaxf(gmax, g);
-      const float gp = g - fbarf;
-      acc[0] += gp;
-      acc[1] = fmaf(gp, gp, acc[1]);
-      if (final_pass || METHOD == 0) acc[2] = fmaf(cf[i], gp, acc[2]);
-      if (METHOD == 1) {
-        if (!final_pass) {
-          const float tx = gp * gxr[i], ty = gp * gyr[i];
-          acc[3] += tx;
-          acc[4] = fmaf(tx, dxf[i], acc[4]);
-          acc[5] = fmaf(tx, dyf[i], acc[5]);
-          acc[6] += ty;
-          acc[7] = fmaf(ty, dxf[i], acc[7]);
-          acc[8] = fmaf(ty, dyf[i], acc[8]);
-        }
-      } else if (grads) {
-        const float dx = dxf[i], dy = dyf[i];
-        const float J[6] = {gx, gx * dx, gx * dy, gy, gy * dx, gy * dy};
-#pragma unroll
-        for (int j = 0; j < 6; ++j) {
-          acc[3 + j] = fmaf(cf[i], J[j], acc[3 + j]);
-          acc[9 + j] = fmaf(gp, J[j], acc[9 + j]);
-          acc[15 + j] += J[j];
-        }
-        const float wv[6] = {1.f, dx, dy, dx * dx, dx * dy, dy * dy};
-        const float aa = gx * gx, ab = gx * gy, bb = gy * gy;
-#pragma unroll
-        for (int j = 0; j < 6; ++j) {
-          acc[21 + j] = fmaf(aa, wv[j], acc[21 + j]);
-          acc[27 + j] = fmaf(ab, wv[j], acc[27 + j]);
-          acc[33 + j] = fmaf(bb, wv[j], acc[33 + j]);
-        }
+      cc += r32;
+      rr += q32;
+      if (cc >= side) {
+        cc -= side;
+        ++rr;
       }
     }
-    const int nv = final_pass ? 3 : (METHOD == 1 ? 9 : (grads ? 39 : 3));
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      if (j < nv) {
-        const double s2 = warp_sum1((double)acc[j]);
-        if (lane == 0) rb[warp][j] = s2;
-      }
-    }
+    // ---- warp reductions ----
+    bad = __any_sync(0xffffffffu, bad);
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       gmin = fminf(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
       gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
     }
-    if (lane == 0) {
-      rmm[warp][0] = gmin;
-      rmm[warp][1] = gmax;
+    const double t0 = warp_sum1((double)acc[0]), t1 = warp_sum1((double)acc[1]);
+    const double t2 = (final_pass || METHOD == 0) ? warp_sum1((double)acc[2]) : 0.0;
+    const double delta = t0 / n_d;                           // gbar - fbar
+    const double ng2 = fmax(t1 - n_d * delta * delta, 0.0);  // sum (g - gbar)^2
+    const double ng = sqrt(ng2);
+    if (bad) {
+      status = DICB200_POI_DRIFTED;
+      break;
     }
-    const int any_bad = __syncthreads_or(bad);
-    if (warp == 0) {
-      warp0_totals(rb, tot, nv);
-      float mn = rmm[0][0], mx = rmm[0][1];
-#pragma unroll
-      for (int w = 1; w < kWarps; ++w) {
-        mn = fminf(mn, rmm[w][0]);
-        mx = fmaxf(mx, rmm[w][1]);
-      }
-      const double* t = tot;
-      int st = DICB200_POI_OK;
-      const double delta = t[0] / n_d;                           // gbar - fbar
-      const double ng2 = fmax(t[1] - n_d * delta * delta, 0.0);  // sum (g - gbar)^2
-      const double ng = sqrt(ng2);
-      if (any_bad) st = DICB200_POI_DRIFTED;
-      else if (!(mx > mn) || !(ng > 0.0)) st = DICB200_POI_DEGENERATE_TARGET;
-      if (final_pass) {
-        if (lane == 0) {
-          S.status = st;
-          S.zncc = (t[2] - delta * S.scf) / (S.nf * ng);  // cross / (nf ng)
-          S.done = 2;
-        }
-      } else if (st != DICB200_POI_OK) {
-        if (lane == 0) {
-          S.status = st;
-          S.done = 1;
-        }
-      } else if (METHOD == 1) {
-        // rhs = sum e_k sd_k (subpixel.cpp:328-333), expanded; step = H^-1 (-rhs), lane i -> step_i
-        const double ratio = S.nf / ng;
-        double si = 0.0;
-#pragma unroll
-        for (int j = 0; j < 6; ++j) si = fma(hinv[j], -(S.A[j] - ratio * (t[3 + j] - delta * S.Ssd[j])), si);
-        double step[6];
-        bool finite = true;
-#pragma unroll
-        for (int j = 0; j < 6; ++j) {
-          step[j] = __shfl_sync(0xffffffffu, si, j);
-          finite = finite && isfinite(step[j]);
-        }
-        if (lane == 0) finish_step(S, step, finite, DICB200_POI_DEGENERATE_TEXTURE, iter, p.tol, true);
-      } else if (lane == 0) {
-        // NR (subpixel.cpp:247-271): gradient = -2/(nf ng) sum coeff J, H = 2/ng^2 sum J J^T
-        const double cross = t[2] - delta * S.scf;
-        const double kappa = cross / ng2;
-        double neg[6], step[6] = {0, 0, 0, 0, 0, 0};
-        bool finite = true;
-        const double scale = -2.0 / (S.nf * ng);
-#pragma unroll
-        for (int j = 0; j < 6; ++j) neg[j] = -(scale * (t[3 + j] - kappa * (t[9 + j] - delta * t[15 + j])));
-        assemble_hessian(t + 21, 2.0 / ng2, shH);
-        ldlt6_compute(shL, shH);
-        if (!shL.ok) {
-          finite = false;
-        } else {
-          ldlt6_solve(shL, neg, step);
-          for (int j = 0; j < 6; ++j) finite = finite && isfinite(step[j]);
-        }
-        finish_step(S, step, finite, DICB200_POI_DEGENERATE_SUBSET, iter, p.tol, false);
-      }
+    if (!(gmax > gmin) || !(ng > 0.0)) {
+      status = DICB200_POI_DEGENERATE_TARGET;
+      break;
     }
-    __syncthreads();
-    if (S.done == 2 || S.status != DICB200_POI_OK) break;
-  }
-  if (tid == 0) {
-    if (S.status == DICB200_POI_OK) {
-      rec->u = S.p[0];
-      rec->v = S.p[3];
-      rec->zncc = S.zncc;
-      rec->iterations = S.iterations;
-      rec->converged = S.converged;
+    if (final_pass) {
+      zncc = (t2 - delta * scf) / (nf * ng);  // cross / (nf ng)
+      break;
+    }
+    double step[6];
+    bool finite;
+    if (METHOD == 1) {
+      // rhs = sum e_k sd_k (subpixel.cpp:328-333), expanded; step = H^-1 (-rhs)
+      const double ratio = nf / ng;
+      double rhs[6];
+#pragma unroll
+      for (int j = 0; j < 6; ++j) rhs[j] = A[j] - ratio * (warp_sum1((double)acc[3 + j]) - delta * Ssd[j]);
+      hinv_step(hinv, rhs, step, finite);
+      if (!finite) {
+        status = DICB200_POI_DEGENERATE_TEXTURE;
+        break;
+      }
+      const int st = compose_with_inverse(P, step);
+      if (st != DICB200_POI_OK) {
+        status = st;
+        break;
+      }
     } else {
-      rec->status = S.status;
+      // NR (subpixel.cpp:247-279): gradient = -2/(nf ng) sum coeff J, H = 2/ng^2 sum J J^T,
+      // additive update
+      const double kappa = t2 - delta * scf;  // cross
+      const double kap = kappa / ng2;
+      const double scale = -2.0 / (nf * ng);
+      double grad[6];
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        const double cj = warp_sum1((double)acc[3 + j]), gj = warp_sum1((double)acc[9 + j]),
+                     sj = warp_sum1((double)acc[15 + j]);
+        grad[j] = scale * (cj - kap * (gj - delta * sj));
+      }
+      double mo[18];
+#pragma unroll
+      for (int j = 0; j < 18; ++j) mo[j] = warp_sum1((double)acc[21 + j]);
+      const int map[6][6][2] = {
+          {{0, 0}, {0, 1}, {0, 2}, {1, 0}, {1, 1}, {1, 2}}, {{0, 1}, {0, 3}, {0, 4}, {1, 1}, {1, 3}, {1, 4}},
+          {{0, 2}, {0, 4}, {0, 5}, {1, 2}, {1, 4}, {1, 5}}, {{1, 0}, {1, 1}, {1, 2}, {2, 0}, {2, 1}, {2, 2}},
+          {{1, 1}, {1, 3}, {1, 4}, {2, 1}, {2, 3}, {2, 4}}, {{1, 2}, {1, 4}, {1, 5}, {2, 2}, {2, 4}, {2, 5}},
+      };
+      const double hs = 2.0 / ng2;
+      double h[6], hi6[6];
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        double v = 0.0;
+#pragma unroll
+        for (int r = 0; r < 6; ++r)
+          if (r == lane) v = mo[map[r][j][0] * 6 + map[r][j][1]] * hs;
+        h[j] = v;
+      }
+      bool pd;
+      warp_cholesky_inverse(h, hi6, pd);
+      hinv_step(hi6, grad, step, finite);  // step = H^-1 (-gradient)
+      if (!pd || !finite) {
+        status = DICB200_POI_DEGENERATE_SUBSET;
+        break;
+      }
+#pragma unroll
+      for (int j = 0; j < 6; ++j) P[j] += step[j];
+    }
+    if (fabs(warp_det(P)) < 1e-8) {
+      status = DICB200_POI_WARP_NOT_INVERTIBLE;
+      break;
+    }
+    iterations = iter;
+    if (fmax(fabs(step[0]), fabs(step[3])) < p.tol) {
+      converged = 1;
+      done = 1;
+    }
+  }
+  if (lane == 0) {
+    if (status == DICB200_POI_OK) {
+      rec->u = P[0];
+      rec->v = P[3];
+      rec->zncc = zncc;
+      rec->iterations = iterations;
+      rec->converged = converged;
+    } else {
+      rec->status = status;
       rec->converged = 0;
     }
   }
 }
 
-template <typename Pix, int PPT, int WP>
-cudaError_t launch_ppt(const RefineParams& p, size_t smem, cudaStream_t st) {
-  if (p.method == 0)
-    refine_kernel<Pix, PPT, 0, WP><<<p.n_records, kNT, smem, st>>>(p);
-  else
-    refine_kernel<Pix, PPT, 1, WP><<<p.n_records, kNT, smem, st>>>(p);
-  count_launch();
-  return cudaGetLastError();
-}
-
-// (PPT, window pitch) by half-width: n <= 256*PPT and 2M+1+2*kPad <= WP
-template <typename Pix>
-cudaError_t launch_pix(const RefineParams& p, int ppt, cudaStream_t st) {
-  const int S = 2 * p.M + 1 + 2 * kPad;
-  switch (ppt) {
-    case 2: return launch_ppt<Pix, 2, 32>(p, (size_t)S * 32 * 4, st);
-    case 4: return launch_ppt<Pix, 4, 64>(p, (size_t)S * 64 * 4, st);
-    case 7: return launch_ppt<Pix, 7, 64>(p, (size_t)S * 64 * 4, st);
-    case 10: return launch_ppt<Pix, 10, 64>(p, (size_t)S * 64 * 4, st);
-    default: return launch_ppt<Pix, 16, 128>(p, (size_t)S * 128 * 4, st);
-  }
-}
-
 }  // namespace
 
-bool refine_plan(int M, int* ppt_out, int* nt_out) {
-  const int n = (2 * M + 1) * (2 * M + 1);
-  const int S = 2 * M + 1 + 2 * kPad;
-  const int ppts[] = {2, 4, 7, 10, 16};
-  const int pitch[] = {32, 64, 64, 64, 128};
-  for (int i = 0; i < 5; ++i)
-    if (ppts[i] * kNT >= n && S <= pitch[i]) {
-      *ppt_out = ppts[i];
-      *nt_out = kNT;
-      return true;
-    }
-  return false;
+static size_t strip_smem(int M, int step, int spc) {
+  const int side = 2 * M + 1;
+  const int span = step * (spc - 1);
+  return (size_t)4 * ((size_t)(side + 2) * (span + side + 2) +
+                      (size_t)(side + 2 * kPad + 2 * kSpread) * (span + 2 * kSpread + side + 2 * kPad));
 }
 
-cudaError_t refine_launch(const RefineParams& p, bool u8, cudaStream_t st) {
-  if (p.n_records <= 0) return cudaSuccess;
-  int ppt = 0, nt = 0;
-  if (!refine_plan(p.M, &ppt, &nt)) return cudaErrorInvalidValue;
-  return u8 ? launch_pix<uint8_t>(p, ppt, st) : launch_pix<uint16_t>(p, ppt, st);
+bool refine_plan(int M, int* ppt_out, int* nt_out) {
+  *ppt_out = ((2 * M + 1) * (2 * M + 1) + 31) / 32;
+  *nt_out = kNT;
+  return M >= 1 && strip_smem(M, 1, 1) <= 100 * 1024;
+}
+
+cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st) {
+  if (p0.n_records <= 0) return cudaSuccess;
+  RefineParams p = p0;
+  p.spc = kWarps;
+  while (p.spc > 1 && strip_smem(p.M, p.lat.step, p.spc) > 100 * 1024) --p.spc;
+  const size_t smem = strip_smem(p.M, p.lat.step, p.spc);
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  const int rows = p.n_records / p.lat.nx;
+  dim3 grid((p.lat.nx + p.spc - 1) / p.spc, rows);
+  cudaError_t e;
+  if (p.method == 0) {
+    auto k = u8 ? refine_strip_kernel<uint8_t, 0> : refine_strip_kernel<uint16_t, 0>;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) k<<<grid, kNT, smem, st>>>(p);
+  } else {
+    auto k = u8 ? refine_strip_kernel<uint8_t, 1> : refine_strip_kernel<uint16_t, 1>;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) k<<<grid, kNT, smem, st>>>(p);
+  }
+  count_launch();
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
 }
 
 }  // namespace dicb200

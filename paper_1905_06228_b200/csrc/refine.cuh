@@ -14,6 +14,7 @@ struct RefineParams {
   double tol;
   int max_iter;
   dicb200_poi_record* rec;
+  int spc;  // POIs per CTA strip (<= 8), chosen by refine_launch to fit shared memory
 };
 
 bool refine_plan(int M, int* ppt, int* nt);
