@@ -254,10 +254,161 @@ __device__ __forceinline__ void hinv_step(const double (&hinv)[6], const double 
   }
 }
 
+
+// Strided pixel walk of one warp over a (2M+1)^2 subset: lane handles pixels
+// k = lane + 32 i (consecutive lanes -> consecutive pixels: conflict-free smem).
+struct Walk {
+  int npl, last_valid;     // trips; whether the last trip is a real pixel for this lane
+  float dxf, dyf;          // subset-local coordinates of the current pixel
+  float r32f, q32f, sidef, Mf;
+  int roff, roff_step, roff_wrap;  // reference-region offset (rr * rP + cc)
+  __device__ __forceinline__ void init(int M, int lane, int rP) {
+    const int side = 2 * M + 1, n = side * side;
+    npl = (n + 31) / 32;
+    last_valid = lane + 32 * (npl - 1) < n;
+    const int rr = lane / side, cc = lane - rr * side;
+    const int q = 32 / side, r = 32 - q * side;
+    dxf = (float)(cc - M);
+    dyf = (float)(rr - M);
+    r32f = (float)r;
+    q32f = (float)q;
+    sidef = (float)side;
+    Mf = (float)M;
+    roff = rr * rP + cc;
+    roff_step = q * rP + r;
+    roff_wrap = rP - side;
+  }
+  __device__ __forceinline__ void advance() {
+    dxf += r32f;
+    dyf += q32f;
+    roff += roff_step;
+    if (dxf > Mf) {
+      dxf -= sidef;
+      dyf += 1.0f;
+      roff += roff_wrap;
+    }
+  }
+};
+
+struct WarpConst {
+  double scf, nf;
+  double A[6], S[6];
+};
+
+struct PassCtx {
+  const float* T;   // target region
+  const float* Rs;  // reference pixel (0,0) of the subset in the reference region
+  int tP, rP;
+  float offx, offy;  // subset-local -> target-region coordinates
+  float fbar;
+  float ul, vl, ux, uy, vx, vy;
+  Win wn;
+  int bx, by;
+};
+
+enum { kIcgn = 0, kNr = 1, kFinal = 2 };
+
+// One pass over the subset pixels for the current warp parameters.
+// kIcgn : acc = {sum g', sum g'^2, -, sum g' 2gx {1,dx,dy}, sum g' 2gy {1,dx,dy}}
+// kNr   : acc = {sum g', sum g'^2, sum cf g', sum cf J[6], sum g' J[6], sum J[6], moments[18]}
+// kFinal: acc = {sum g', sum g'^2, sum cf g'}
+template <bool FAST, int KIND, typename Pix>
+__device__ __forceinline__ void pixel_pass(const PassCtx& c, const ImageView& tgt, const Walk& w0,
+                                           float* acc, int& bad, float& gmin, float& gmax) {
+  constexpr int NV = KIND == kNr ? 39 : 9;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) acc[j] = 0.f;
+  gmin = 3.0e38f;
+  gmax = -3.0e38f;
+  bad = 0;
+  Walk w = w0;
+  for (int i = 0; i < w.npl; ++i) {
+    if (i == w.npl - 1 && !w.last_valid) break;
+    const float dx = w.dxf, dy = w.dyf;
+    const float xl = fmaf(c.uy, dy, fmaf(c.ux, dx, dx + c.ul));
+    const float yl = fmaf(c.vy, dy, fmaf(c.vx, dx, dy + c.vl));
+    float gv, gx = 0.f, gy = 0.f;
+    if (FAST) {
+      const float wx = xl + c.offx, wy = yl + c.offy;
+      const float flx = floorf(wx), fly = floorf(wy);
+      const float fx = wx - flx, fy = wy - fly;
+      const float* t = c.T + (int)fly * c.tP + (int)flx;
+      const float f00 = t[0], f10 = t[1], f01 = t[c.tP], f11 = t[c.tP + 1];
+      const float a10 = f10 - f00, a01 = f01 - f00, a11 = (f00 + f11) - f10 - f01;
+      gv = fmaf(a11 * fx, fy, fmaf(a01, fy, fmaf(a10, fx, f00)));
+      if (KIND == kNr) {
+        const int P2 = 2 * c.tP;
+        const float dx00 = f10 - t[-1], dx10 = t[2] - f00, dx01 = f11 - t[c.tP - 1], dx11 = t[c.tP + 2] - f01;
+        const float dy00 = f01 - t[-c.tP], dy10 = f11 - t[1 - c.tP], dy01 = t[P2] - f00, dy11 = t[P2 + 1] - f10;
+        const float w00 = (1.f - fx) * (1.f - fy), w10 = fx * (1.f - fy), w01 = (1.f - fx) * fy, w11 = fx * fy;
+        gx = 0.5f * (w00 * dx00 + w10 * dx10 + w01 * dx01 + w11 * dx11);
+        gy = 0.5f * (w00 * dy00 + w10 * dy10 + w01 * dy01 + w11 * dy11);
+      }
+    } else {
+      gv = 0.f;
+      bool ok = bilinear<Pix>(c.wn, tgt, c.bx, c.by, xl, yl, gv);
+      if (KIND == kNr) ok = ok && grad_bilinear<Pix>(c.wn, tgt, c.bx, c.by, xl, yl, gx, gy);
+      bad |= !ok;
+    }
+    gmin = fminf(gmin, gv);
+    gmax = fmaxf(gmax, gv);
+    const float* q = c.Rs + w.roff;
+    const float gp = gv - c.fbar;
+    acc[0] += gp;
+    acc[1] = fmaf(gp, gp, acc[1]);
+    if (KIND != kIcgn) acc[2] = fmaf(q[0] - c.fbar, gp, acc[2]);
+    if (KIND == kIcgn) {
+      const float tx = gp * (q[1] - q[-1]), ty = gp * (q[c.rP] - q[-c.rP]);  // g' * 2 grad f
+      acc[3] += tx;
+      acc[4] = fmaf(tx, dx, acc[4]);
+      acc[5] = fmaf(tx, dy, acc[5]);
+      acc[6] += ty;
+      acc[7] = fmaf(ty, dx, acc[7]);
+      acc[8] = fmaf(ty, dy, acc[8]);
+    } else if (KIND == kNr) {
+      const float cfv = q[0] - c.fbar;
+      const float J[6] = {gx, gx * dx, gx * dy, gy, gy * dx, gy * dy};
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        acc[3 + j] = fmaf(cfv, J[j], acc[3 + j]);
+        acc[9 + j] = fmaf(gp, J[j], acc[9 + j]);
+        acc[15 + j] += J[j];
+      }
+      const float wv[6] = {1.f, dx, dy, dx * dx, dx * dy, dy * dy};
+      const float aa = gx * gx, ab = gx * gy, bb = gy * gy;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        acc[21 + j] = fmaf(aa, wv[j], acc[21 + j]);
+        acc[27 + j] = fmaf(ab, wv[j], acc[27 + j]);
+        acc[33 + j] = fmaf(bb, wv[j], acc[33 + j]);
+      }
+    }
+    w.advance();
+  }
+}
+
+// Row `lane` (< 6) of H = scale * assemble(mo); other lanes get row 0.
+__device__ __forceinline__ void hessian_row(const double* mo, double scale, int lane, double (&h)[6]) {
+  const int map[6][6][2] = {
+      {{0, 0}, {0, 1}, {0, 2}, {1, 0}, {1, 1}, {1, 2}}, {{0, 1}, {0, 3}, {0, 4}, {1, 1}, {1, 3}, {1, 4}},
+      {{0, 2}, {0, 4}, {0, 5}, {1, 2}, {1, 4}, {1, 5}}, {{1, 0}, {1, 1}, {1, 2}, {2, 0}, {2, 1}, {2, 2}},
+      {{1, 1}, {1, 3}, {1, 4}, {2, 1}, {2, 3}, {2, 4}}, {{1, 2}, {1, 4}, {1, 5}, {2, 2}, {2, 4}, {2, 5}},
+  };
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    double v = mo[map[0][j][0] * 6 + map[0][j][1]];
+#pragma unroll
+    for (int r = 1; r < 6; ++r)
+      if (r == lane) v = mo[map[r][j][0] * 6 + map[r][j][1]];
+    h[j] = v * scale;
+  }
+}
+
 template <typename Pix, int METHOD>
 __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
   extern __shared__ __align__(16) float smem_f[];
   __shared__ int s_idx[kWarps], s_idy[kWarps], s_ok[kWarps];
+  __shared__ WarpConst s_const[kWarps];
   __shared__ StripGeom G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int M = p.M, side = 2 * M + 1, n = side * side;
@@ -349,29 +500,21 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
     fail(DICB200_POI_BORDER_GRADIENTS);  // subpixel.cpp:193-195
     return;
   }
-  // pixel walk: lane handles k = lane + 32 i; (rr, cc) advanced incrementally
-  const int npl = (n + 31) / 32;
-  const int q32 = 32 / side, r32 = 32 - q32 * side;
-  const int rr0 = lane / side, cc0 = lane - (lane / side) * side;
-  // reference region pointer of the pixel (rr, cc): R + (rr + 1) * rP + (cx - cx0) + cc + 1
-  const float* Rs = R + g.rP + (cx - p.lat.cx(ix0)) + 1;
+  Walk wk;
+  wk.init(M, lane, g.rP);
+  const float* Rs = R + g.rP + (cx - p.lat.cx(ix0)) + 1;  // reference pixel (0,0) of this subset
 
   // ---- subset_stats: exact sums ----
   double sf = 0.0, sff = 0.0;
   {
-    int rr = rr0, cc = cc0;
-    for (int i = 0; i < npl; ++i) {
-      if (rr < side) {
-        const double f = Rs[rr * g.rP + cc];
+    Walk w = wk;
+    for (int i = 0; i < w.npl; ++i) {
+      if (i < w.npl - 1 || w.last_valid) {
+        const double f = Rs[w.roff];
         sf += f;
         sff += f * f;
       }
-      cc += r32;
-      rr += q32;
-      if (cc >= side) {
-        cc -= side;
-        ++rr;
-      }
+      w.advance();
     }
   }
   sf = warp_sum1(sf);
@@ -384,77 +527,70 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
   const double fbar = sf / (double)n;  // correlation.cpp:25: exact sum / n
   const double nf = sqrt((double)vf / (double)n);
   const float fbarf = (float)fbar;
+  WarpConst& C = s_const[warp];
 
   // ---- precompute: sum cf; IC-GN: exact Hessian -> H^-1, sum cf*sd, sum sd ----
-  double scf = 0.0, A[6] = {0, 0, 0, 0, 0, 0}, Ssd[6] = {0, 0, 0, 0, 0, 0};
   double hinv[6] = {0, 0, 0, 0, 0, 0};
   {
     double mo[18];
 #pragma unroll
     for (int j = 0; j < 18; ++j) mo[j] = 0.0;
-    int rr = rr0, cc = cc0;
-    for (int i = 0; i < npl; ++i) {
-      if (rr < side) {
-        const float* q = Rs + rr * g.rP + cc;
+    double scf = 0.0, A[6] = {0, 0, 0, 0, 0, 0}, Ssd[6] = {0, 0, 0, 0, 0, 0};
+    Walk w = wk;
+    for (int i = 0; i < w.npl; ++i) {
+      if (i < w.npl - 1 || w.last_valid) {
+        const float* q = Rs + w.roff;
         const float cfv = (float)((double)q[0] - fbar);
         scf += (double)cfv;
         if (METHOD == 1) {
-          const float gxv = 0.5f * (q[1] - q[-1]), gyv = 0.5f * (q[g.rP] - q[-g.rP]);
-          const double dx = cc - M, dy = rr - M;
-          const double ga = 2.0 * gxv, gb = 2.0 * gyv;  // integers
+          const float ga = q[1] - q[-1], gb = q[g.rP] - q[-g.rP];  // 2 * gradient: integers
+          const double dx = w.dxf, dy = w.dyf;
           const double w6[6] = {1.0, dx, dy, dx * dx, dx * dy, dy * dy};
-          const double aa = ga * ga, ab = ga * gb, bb = gb * gb;
+          const double aa = (double)ga * ga, ab = (double)ga * gb, bb = (double)gb * gb;
 #pragma unroll
           for (int j = 0; j < 6; ++j) {
             mo[j] = fma(aa, w6[j], mo[j]);
             mo[6 + j] = fma(ab, w6[j], mo[6 + j]);
             mo[12 + j] = fma(bb, w6[j], mo[12 + j]);
           }
-          const double cgx = (double)cfv * gxv, cgy = (double)cfv * gyv;  // exact (float x float)
+          const double cgx = (double)cfv * ga, cgy = (double)cfv * gb;  // exact (float x float)
           A[0] += cgx;
           A[1] += cgx * dx;
           A[2] += cgx * dy;
           A[3] += cgy;
           A[4] += cgy * dx;
           A[5] += cgy * dy;
-          Ssd[0] += gxv;
-          Ssd[1] += gxv * dx;
-          Ssd[2] += gxv * dy;
-          Ssd[3] += gyv;
-          Ssd[4] += gyv * dx;
-          Ssd[5] += gyv * dy;
+          Ssd[0] += ga;
+          Ssd[1] += ga * dx;
+          Ssd[2] += ga * dy;
+          Ssd[3] += gb;
+          Ssd[4] += gb * dx;
+          Ssd[5] += gb * dy;
         }
       }
-      cc += r32;
-      rr += q32;
-      if (cc >= side) {
-        cc -= side;
-        ++rr;
-      }
+      w.advance();
     }
     scf = warp_sum1(scf);
+    if (lane == 0) {
+      C.scf = scf;
+      C.nf = nf;
+    }
     if (METHOD == 1) {
 #pragma unroll
       for (int j = 0; j < 6; ++j) {
-        A[j] = warp_sum1(A[j]);
-        Ssd[j] = warp_sum1(Ssd[j]);
+        A[j] = warp_sum1(A[j]) * 0.5;    // sum cf * sd   (sd uses 0.5 * (2 grad))
+        Ssd[j] = warp_sum1(Ssd[j]) * 0.5;  // sum sd
       }
+      if (lane == 0)
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          C.A[j] = A[j];
+          C.S[j] = Ssd[j];
+        }
 #pragma unroll
       for (int j = 0; j < 18; ++j) mo[j] = warp_sum1(mo[j]);
-      const int map[6][6][2] = {
-          {{0, 0}, {0, 1}, {0, 2}, {1, 0}, {1, 1}, {1, 2}}, {{0, 1}, {0, 3}, {0, 4}, {1, 1}, {1, 3}, {1, 4}},
-          {{0, 2}, {0, 4}, {0, 5}, {1, 2}, {1, 4}, {1, 5}}, {{1, 0}, {1, 1}, {1, 2}, {2, 0}, {2, 1}, {2, 2}},
-          {{1, 1}, {1, 3}, {1, 4}, {2, 1}, {2, 3}, {2, 4}}, {{1, 2}, {1, 4}, {1, 5}, {2, 2}, {2, 4}, {2, 5}},
-      };
       double h[6];
-#pragma unroll
-      for (int j = 0; j < 6; ++j) {
-        double v = 0.0;
-#pragma unroll
-        for (int r = 0; r < 6; ++r)
-          if (r == lane) v = mo[map[r][j][0] * 6 + map[r][j][1]] * 0.25;
-        h[j] = v;
-      }
+      hessian_row(mo, 0.25, lane, h);
       double hf2 = 0.0;
 #pragma unroll
       for (int j = 0; j < 6; ++j) hf2 += h[j] * h[j];
@@ -463,7 +599,7 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
       double if2 = 0.0;
 #pragma unroll
       for (int j = 0; j < 6; ++j) if2 += lane < 6 ? hinv[j] * hinv[j] : 0.0;
-      hf2 = warp_sum1(hf2);
+      hf2 = warp_sum1(lane < 6 ? hf2 : 0.0);
       if2 = warp_sum1(if2);
       // cond(H) <= ||H||_F ||H^-1||_F; exact eigenvalues only when inconclusive (subpixel.cpp:215-219)
       int accept = pd && sqrt(hf2) * sqrt(if2) < 1e12;
@@ -483,19 +619,28 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
       }
     }
   }
+  __syncwarp();
 
   // ---- iterations (all lanes hold the same warp parameters) ----
   double P[6] = {(double)idx, 0.0, 0.0, (double)idy, 0.0, 0.0};  // u, ux, uy, v, vx, vy
   int iterations = 0, converged = 0, done = 0;
   const double n_d = (double)n;
   const double lim = (double)(M + 2);
-  const float offx = (float)(bx - g.tX0), offy = (float)(by - g.tY0);  // local -> region coords
-  Win wn;  // slow path: region as a window (global coords of T[0]), global fallback outside
-  wn.w = T;
-  wn.S = min(g.tP, g.tH);
-  wn.P = g.tP;
-  wn.ox = g.tX0;
-  wn.oy = g.tY0;
+  PassCtx pc;
+  pc.T = T;
+  pc.Rs = Rs;
+  pc.tP = g.tP;
+  pc.rP = g.rP;
+  pc.offx = (float)(bx - g.tX0);
+  pc.offy = (float)(by - g.tY0);
+  pc.fbar = fbarf;
+  pc.wn.w = T;
+  pc.wn.S = min(g.tP, g.tH);
+  pc.wn.P = g.tP;
+  pc.wn.ox = g.tX0;
+  pc.wn.oy = g.tY0;
+  pc.bx = bx;
+  pc.by = by;
   double zncc = 0.0;
   int status = DICB200_POI_OK;
   for (int iter = 1;; ++iter) {
@@ -507,95 +652,43 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
         break;
       }
     }
-    const float ul = (float)(P[0] - idx), vl = (float)(P[3] - idy);
-    const float uxf = (float)P[1], uyf = (float)P[2], vxf = (float)P[4], vyf = (float)P[5];
+    pc.ul = (float)(P[0] - idx);
+    pc.vl = (float)(P[3] - idy);
+    pc.ux = (float)P[1];
+    pc.uy = (float)P[2];
+    pc.vx = (float)P[4];
+    pc.vy = (float)P[5];
     const bool grads = METHOD == 0 && !final_pass;
     bool fast;
     {
       const float Mf = (float)M;
-      const float ex = fabsf(Mf + Mf * uxf) + fabsf(Mf * uyf), ey = fabsf(Mf * vxf) + fabsf(Mf + Mf * vyf);
-      const float lo_x = ul - ex, hi_x = ul + ex, lo_y = vl - ey, hi_y = vl + ey;
+      const float ex = fabsf(Mf + Mf * pc.ux) + fabsf(Mf * pc.uy), ey = fabsf(Mf * pc.vx) + fabsf(Mf + Mf * pc.vy);
+      const float lo_x = pc.ul - ex, hi_x = pc.ul + ex, lo_y = pc.vl - ey, hi_y = pc.vl + ey;
       const float mg = grads ? 2.0f : 1.0f;
-      fast = offx + lo_x - mg >= 0.0f && offx + hi_x + mg + 1.0f <= (float)(g.tP - 1) && offy + lo_y - mg >= 0.0f &&
-             offy + hi_y + mg + 1.0f <= (float)(g.tH - 1) && (float)bx + lo_x - mg >= 0.0f &&
-             (float)bx + hi_x + mg <= (float)(p.tgt.width - 1) && (float)by + lo_y - mg >= 0.0f &&
-             (float)by + hi_y + mg <= (float)(p.tgt.height - 1);
+      fast = pc.offx + lo_x - mg >= 0.0f && pc.offx + hi_x + mg + 1.0f <= (float)(g.tP - 1) &&
+             pc.offy + lo_y - mg >= 0.0f && pc.offy + hi_y + mg + 1.0f <= (float)(g.tH - 1) &&
+             (float)bx + lo_x - mg >= 0.0f && (float)bx + hi_x + mg <= (float)(p.tgt.width - 1) &&
+             (float)by + lo_y - mg >= 0.0f && (float)by + hi_y + mg <= (float)(p.tgt.height - 1);
     }
     constexpr int NV = METHOD == 1 ? 9 : 39;
     float acc[NV];
-#pragma unroll
-    for (int j = 0; j < NV; ++j) acc[j] = 0.f;
     int bad = 0;
-    float gmin = 3.0e38f, gmax = -3.0e38f;
-    int rr = rr0, cc = cc0;
-    for (int i = 0; i < npl; ++i) {
-      if (rr < side) {
-        const float dx = (float)(cc - M), dy = (float)(rr - M);
-        const float xl = fmaf(uyf, dy, fmaf(uxf, dx, dx + ul));
-        const float yl = fmaf(vyf, dy, fmaf(vxf, dx, dy + vl));
-        float gv = 0.f, gx = 0.f, gy = 0.f;
-        if (fast) {
-          const float wx = xl + offx, wy = yl + offy;
-          const float flx = floorf(wx), fly = floorf(wy);
-          const float fx = wx - flx, fy = wy - fly;
-          const float* t = T + (int)fly * g.tP + (int)flx;
-          const float f00 = t[0], f10 = t[1], f01 = t[g.tP], f11 = t[g.tP + 1];
-          const float a10 = f10 - f00, a01 = f01 - f00, a11 = (f00 + f11) - f10 - f01;
-          gv = fmaf(a11 * fx, fy, fmaf(a01, fy, fmaf(a10, fx, f00)));
-          if (grads) {
-            const int P2 = 2 * g.tP;
-            const float dx00 = f10 - t[-1], dx10 = t[2] - f00, dx01 = f11 - t[g.tP - 1], dx11 = t[g.tP + 2] - f01;
-            const float dy00 = f01 - t[-g.tP], dy10 = f11 - t[1 - g.tP], dy01 = t[P2] - f00, dy11 = t[P2 + 1] - f10;
-            const float w00 = (1.f - fx) * (1.f - fy), w10 = fx * (1.f - fy), w01 = (1.f - fx) * fy, w11 = fx * fy;
-            gx = 0.5f * (w00 * dx00 + w10 * dx10 + w01 * dx01 + w11 * dx11);
-            gy = 0.5f * (w00 * dy00 + w10 * dy10 + w01 * dy01 + w11 * dy11);
-          }
-        } else {
-          bad |= !sample_slow<Pix>(wn, p.tgt, bx, by, xl, yl, grads, gv, gx, gy);
-        }
-        gmin = fminf(gmin, gv);
-        gmax = fmaxf(gmax, gv);
-        const float* q = Rs + rr * g.rP + cc;
-        const float cfv = q[0] - fbarf;
-        const float gp = gv - fbarf;
-        acc[0] += gp;
-        acc[1] = fmaf(gp, gp, acc[1]);
-        if (final_pass || METHOD == 0) acc[2] = fmaf(cfv, gp, acc[2]);
-        if (METHOD == 1) {
-          if (!final_pass) {
-            const float gxr = 0.5f * (q[1] - q[-1]), gyr = 0.5f * (q[g.rP] - q[-g.rP]);
-            const float tx = gp * gxr, ty = gp * gyr;
-            acc[3] += tx;
-            acc[4] = fmaf(tx, dx, acc[4]);
-            acc[5] = fmaf(tx, dy, acc[5]);
-            acc[6] += ty;
-            acc[7] = fmaf(ty, dx, acc[7]);
-            acc[8] = fmaf(ty, dy, acc[8]);
-          }
-        } else if (grads) {
-          const float J[6] = {gx, gx * dx, gx * dy, gy, gy * dx, gy * dy};
-#pragma unroll
-          for (int j = 0; j < 6; ++j) {
-            acc[3 + j] = fmaf(cfv, J[j], acc[3 + j]);
-            acc[9 + j] = fmaf(gp, J[j], acc[9 + j]);
-            acc[15 + j] += J[j];
-          }
-          const float wv[6] = {1.f, dx, dy, dx * dx, dx * dy, dy * dy};
-          const float aa = gx * gx, ab = gx * gy, bb = gy * gy;
-#pragma unroll
-          for (int j = 0; j < 6; ++j) {
-            acc[21 + j] = fmaf(aa, wv[j], acc[21 + j]);
-            acc[27 + j] = fmaf(ab, wv[j], acc[27 + j]);
-            acc[33 + j] = fmaf(bb, wv[j], acc[33 + j]);
-          }
-        }
-      }
-      cc += r32;
-      rr += q32;
-      if (cc >= side) {
-        cc -= side;
-        ++rr;
-      }
+    float gmin, gmax;
+    if (final_pass) {
+      if (fast)
+        pixel_pass<true, kFinal, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
+      else
+        pixel_pass<false, kFinal, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
+    } else if (METHOD == 1) {
+      if (fast)
+        pixel_pass<true, kIcgn, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
+      else
+        pixel_pass<false, kIcgn, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
+    } else {
+      if (fast)
+        pixel_pass<true, kNr, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
+      else
+        pixel_pass<false, kNr, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
     }
     // ---- warp reductions ----
     bad = __any_sync(0xffffffffu, bad);
@@ -618,17 +711,17 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
       break;
     }
     if (final_pass) {
-      zncc = (t2 - delta * scf) / (nf * ng);  // cross / (nf ng)
+      zncc = (t2 - delta * C.scf) / (C.nf * ng);  // cross / (nf ng)
       break;
     }
     double step[6];
     bool finite;
     if (METHOD == 1) {
       // rhs = sum e_k sd_k (subpixel.cpp:328-333), expanded; step = H^-1 (-rhs)
-      const double ratio = nf / ng;
+      const double ratio = C.nf / ng;
       double rhs[6];
 #pragma unroll
-      for (int j = 0; j < 6; ++j) rhs[j] = A[j] - ratio * (warp_sum1((double)acc[3 + j]) - delta * Ssd[j]);
+      for (int j = 0; j < 6; ++j) rhs[j] = C.A[j] - ratio * (0.5 * warp_sum1((double)acc[3 + j]) - delta * C.S[j]);
       hinv_step(hinv, rhs, step, finite);
       if (!finite) {
         status = DICB200_POI_DEGENERATE_TEXTURE;
@@ -642,9 +735,8 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
     } else {
       // NR (subpixel.cpp:247-279): gradient = -2/(nf ng) sum coeff J, H = 2/ng^2 sum J J^T,
       // additive update
-      const double kappa = t2 - delta * scf;  // cross
-      const double kap = kappa / ng2;
-      const double scale = -2.0 / (nf * ng);
+      const double kap = (t2 - delta * C.scf) / ng2;  // cross / ng^2
+      const double scale = -2.0 / (C.nf * ng);
       double grad[6];
 #pragma unroll
       for (int j = 0; j < 6; ++j) {
@@ -655,21 +747,8 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
       double mo[18];
 #pragma unroll
       for (int j = 0; j < 18; ++j) mo[j] = warp_sum1((double)acc[21 + j]);
-      const int map[6][6][2] = {
-          {{0, 0}, {0, 1}, {0, 2}, {1, 0}, {1, 1}, {1, 2}}, {{0, 1}, {0, 3}, {0, 4}, {1, 1}, {1, 3}, {1, 4}},
-          {{0, 2}, {0, 4}, {0, 5}, {1, 2}, {1, 4}, {1, 5}}, {{1, 0}, {1, 1}, {1, 2}, {2, 0}, {2, 1}, {2, 2}},
-          {{1, 1}, {1, 3}, {1, 4}, {2, 1}, {2, 3}, {2, 4}}, {{1, 2}, {1, 4}, {1, 5}, {2, 2}, {2, 4}, {2, 5}},
-      };
-      const double hs = 2.0 / ng2;
       double h[6], hi6[6];
-#pragma unroll
-      for (int j = 0; j < 6; ++j) {
-        double v = 0.0;
-#pragma unroll
-        for (int r = 0; r < 6; ++r)
-          if (r == lane) v = mo[map[r][j][0] * 6 + map[r][j][1]] * hs;
-        h[j] = v;
-      }
+      hessian_row(mo, 2.0 / ng2, lane, h);
       bool pd;
       warp_cholesky_inverse(h, hi6, pd);
       hinv_step(hi6, grad, step, finite);  // step = H^-1 (-gradient)
