@@ -17,6 +17,7 @@
 // identical to the reference's sequential double loop except for ties closer
 // than ~1e-15 relative (SURVEY.md Appendix C.4 measured 0 mismatches).
 #include <cstdio>
+#include <type_traits>
 
 #include "bfs.cuh"
 #include "common.cuh"
@@ -71,7 +72,7 @@ __host__ __device__ BfsSmem bfs_smem_layout(const BfsParams& p) {
   else
     s.ref = take((size_t)(2 * p.M + 1) * p.ref_pitch * 2);
   s.v1 = take((size_t)p.DYC * p.RW * 4);
-  s.v2 = take((size_t)p.DYC * p.RW * 8);
+  s.v2 = take((size_t)p.DYC * p.RW * (p.f64 ? 8 : 4));  // u32 whenever (2M+1) max^2 < 2^32
   s.stats = take((size_t)p.TS * 16);
   s.items = take((size_t)p.items_max * sizeof(BestPartial));
   s.total = (off + 15) & ~size_t(15);
@@ -183,8 +184,9 @@ __global__ void __launch_bounds__(512) bfs_tile_kernel(BfsParams p) {
   }
   // ---- column sums of the region: V1[t][x] = sum_r T[t+r][x], V2 of squares ----
   {
+    using V2T = typename std::conditional<kF64, uint64_t, uint32_t>::type;
     uint32_t* V1 = reinterpret_cast<uint32_t*>(smem + L.v1);
-    uint64_t* V2 = reinterpret_cast<uint64_t*>(smem + L.v2);
+    V2T* V2 = reinterpret_cast<V2T*>(smem + L.v2);
     for (int x = tid; x < p.RW; x += nthr) {
       uint32_t s1 = 0;
       uint64_t s2 = 0;
@@ -194,13 +196,13 @@ __global__ void __launch_bounds__(512) bfs_tile_kernel(BfsParams p) {
         s2 += (uint64_t)v * v;
       }
       V1[x] = s1;
-      V2[x] = s2;
+      V2[x] = (V2T)s2;
       for (int t = 1; t < g.dyn; ++t) {
         const uint32_t a = T[(t + side - 1) * p.region_pitch + x], b = T[(t - 1) * p.region_pitch + x];
         s1 += a - b;
         s2 += (uint64_t)a * a - (uint64_t)b * b;
         V1[t * p.RW + x] = s1;
-        V2[t * p.RW + x] = s2;
+        V2[t * p.RW + x] = (V2T)s2;
       }
     }
   }
@@ -211,7 +213,8 @@ __global__ void __launch_bounds__(512) bfs_tile_kernel(BfsParams p) {
   const int n_items = g.ts * g.dyn * p.B;
   const uint64_t* st = reinterpret_cast<const uint64_t*>(smem + L.stats);
   const uint32_t* V1 = reinterpret_cast<const uint32_t*>(smem + L.v1);
-  const uint64_t* V2 = reinterpret_cast<const uint64_t*>(smem + L.v2);
+  using V2R = typename std::conditional<kF64, uint64_t, uint32_t>::type;
+  const V2R* V2 = reinterpret_cast<const V2R*>(smem + L.v2);
   for (int item = tid; item < n_items; item += nthr) {
     const int b = item % p.B, st_ = item / p.B, t = st_ % g.dyn, s = st_ / g.dyn;
     const int cx = p.lat.cx(g.ix0 + s);
@@ -295,6 +298,7 @@ __global__ void __launch_bounds__(512) bfs_tile_kernel(BfsParams p) {
 #pragma unroll
         for (int j = 0; j < J; ++j) sfg[j] = (uint64_t)accd[j];
       } else {
+        const int full = (side / J) * J;  // mask-free blocks, then one uniform tail block
         for (int r = 0; r < side; ++r) {
           const uint16_t* frow = F + r * p.ref_pitch + s * p.lat.step;
           const uint16_t* grow = T16 + (t + r) * p.region_pitch + cs;
@@ -304,14 +308,24 @@ __global__ void __launch_bounds__(512) bfs_tile_kernel(BfsParams p) {
           for (int j = 0; j < J; ++j) acc[j] = 0;
 #pragma unroll
           for (int i = 0; i < J - 1; ++i) gw[i] = grow[i];
-          for (int c0 = 0; c0 < p.CP; c0 += J) {
+          for (int c0 = 0; c0 < full; c0 += J) {
 #pragma unroll
             for (int k = 0; k < J; ++k) {
-              const int c = c0 + k;
-              const uint32_t f = c < side ? (uint32_t)frow[c] : 0u;
-              gw[(k + J - 1) % J] = grow[c + J - 1];
+              const uint32_t f = frow[c0 + k];
+              gw[(k + J - 1) % J] = grow[c0 + k + J - 1];
 #pragma unroll
               for (int j = 0; j < J; ++j) acc[j] += f * gw[(k + j) % J];
+            }
+          }
+          if (full < side) {
+#pragma unroll
+            for (int k = 0; k < J; ++k) {
+              if (full + k < side) {  // uniform across the warp
+                const uint32_t f = frow[full + k];
+                gw[(k + J - 1) % J] = grow[full + k + J - 1];
+#pragma unroll
+                for (int j = 0; j < J; ++j) acc[j] += f * gw[(k + j) % J];
+              }
             }
           }
 #pragma unroll
@@ -335,7 +349,7 @@ __global__ void __launch_bounds__(512) bfs_tile_kernel(BfsParams p) {
     best.count = 0;
     best.found = 0;
     const uint32_t* v1 = V1 + t * p.RW + cs;
-    const uint64_t* v2 = V2 + t * p.RW + cs;
+    const V2R* v2 = V2 + t * p.RW + cs;
     uint64_t s1 = 0, s2 = 0;
     for (int c = 0; c < side; ++c) {
       s1 += v1[c];
@@ -345,7 +359,7 @@ __global__ void __launch_bounds__(512) bfs_tile_kernel(BfsParams p) {
     for (int j = 0; j < J; ++j) {
       if (j > 0) {
         s1 += (uint64_t)v1[j + side - 1] - v1[j - 1];
-        s2 += v2[j + side - 1] - v2[j - 1];
+        s2 += (uint64_t)v2[j + side - 1] - (uint64_t)v2[j - 1];
       }
       const int dxp = dxs + j;
       const int dx = dx_lo_nom + dxp;
@@ -473,7 +487,7 @@ bool bfs_plan(BfsParams& p, size_t smem_limit) {
   p.QP = ((Q + U - 1) / U) * U;
   p.CP = ((side + p.J - 1) / p.J) * p.J;
   // subsets per tile: aim for <= 512 items and fit shared memory
-  int TS = p.whole ? 1 : max(1, 512 / (p.DYC * p.B));
+  int TS = p.whole ? 1 : max(1, 384 / (p.DYC * p.B));
   TS = min(TS, p.lat.nx);
   for (;; --TS) {
     p.TS = TS;

@@ -151,7 +151,7 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
     p.subpixel_none = cfg->subpixel_method == DICB200_SUB_NONE;
     p.rec = out_dev;
     if (!p.whole && p.R < 0) return invalid("search radius must be >= 0");
-    if (!bfs_plan(p, 110 * 1024)) return invalid("subset too large for the BFS tile (shared memory)");
+    if (!bfs_plan(p, 72 * 1024) && !bfs_plan(p, 200 * 1024)) return invalid("subset too large for the BFS tile (shared memory)");
     BestPartial* partial = nullptr;
     if (p.n_chunks > 1) {
       DICB200_CUDA_TRY(cudaMallocAsync((void**)&partial, nrec * p.n_chunks * sizeof(BestPartial), st));
