@@ -80,7 +80,7 @@ __host__ __device__ BfsSmem bfs_smem_layout(const BfsParams& p) {
 }
 
 template <typename Pix, int J, bool kF64>
-__global__ void __launch_bounds__(512) bfs_tile_kernel(BfsParams p) {
+__global__ void __launch_bounds__(256, 3) bfs_tile_kernel(BfsParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const BfsSmem L = bfs_smem_layout(p);
   constexpr bool kU8 = PixTraits<Pix>::kU8;
@@ -441,13 +441,15 @@ cudaError_t launch_t(const BfsParams& p, dim3 grid, int threads, size_t smem, cu
   auto kern = bfs_tile_kernel<Pix, J, kF64>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) return e;
   kern<<<grid, threads, smem, st>>>(p);
   count_launch();
   return cudaGetLastError();
 }
 
-const int kJu8[] = {4, 8, 12, 16, 20, 24, 28, 32, 36};
-const int kJu16[] = {4, 6, 8, 11, 12, 13, 16};
+const int kJu8[] = {4, 8, 12, 16};
+const int kJu16[] = {4, 6, 8, 11, 12, 13};
 
 }  // namespace
 
@@ -487,7 +489,7 @@ bool bfs_plan(BfsParams& p, size_t smem_limit) {
   p.QP = ((Q + U - 1) / U) * U;
   p.CP = ((side + p.J - 1) / p.J) * p.J;
   // subsets per tile: aim for <= 512 items and fit shared memory
-  int TS = p.whole ? 1 : max(1, 384 / (p.DYC * p.B));
+  int TS = p.whole ? 1 : max(1, 256 / (p.DYC * p.B));
   TS = min(TS, p.lat.nx);
   for (;; --TS) {
     p.TS = TS;
@@ -512,7 +514,7 @@ bool bfs_plan(BfsParams& p, size_t smem_limit) {
 
 cudaError_t bfs_launch(BfsParams& p, int rows, cudaStream_t st) {
   const BfsSmem s = bfs_smem_layout(p);
-  const int threads = min(512, ((p.items_max + 31) / 32) * 32);
+  const int threads = min(256, ((p.items_max + 31) / 32) * 32);
   dim3 grid(p.tiles_x * p.n_chunks, rows);
   cudaError_t e = cudaErrorInvalidValue;
 #define DICB200_BFS_CASE(PIX, JJ, F64) \
@@ -522,11 +524,6 @@ cudaError_t bfs_launch(BfsParams& p, int rows, cudaStream_t st) {
     DICB200_BFS_CASE(uint8_t, 8, false)
     DICB200_BFS_CASE(uint8_t, 12, false)
     DICB200_BFS_CASE(uint8_t, 16, false)
-    DICB200_BFS_CASE(uint8_t, 20, false)
-    DICB200_BFS_CASE(uint8_t, 24, false)
-    DICB200_BFS_CASE(uint8_t, 28, false)
-    DICB200_BFS_CASE(uint8_t, 32, false)
-    DICB200_BFS_CASE(uint8_t, 36, false)
   } else if (!p.f64) {
     DICB200_BFS_CASE(uint16_t, 4, false)
     DICB200_BFS_CASE(uint16_t, 6, false)
@@ -534,7 +531,6 @@ cudaError_t bfs_launch(BfsParams& p, int rows, cudaStream_t st) {
     DICB200_BFS_CASE(uint16_t, 11, false)
     DICB200_BFS_CASE(uint16_t, 12, false)
     DICB200_BFS_CASE(uint16_t, 13, false)
-    DICB200_BFS_CASE(uint16_t, 16, false)
   } else {
     DICB200_BFS_CASE(uint16_t, 4, true)
     DICB200_BFS_CASE(uint16_t, 6, true)
@@ -542,7 +538,6 @@ cudaError_t bfs_launch(BfsParams& p, int rows, cudaStream_t st) {
     DICB200_BFS_CASE(uint16_t, 11, true)
     DICB200_BFS_CASE(uint16_t, 12, true)
     DICB200_BFS_CASE(uint16_t, 13, true)
-    DICB200_BFS_CASE(uint16_t, 16, true)
   }
 #undef DICB200_BFS_CASE
   if (e != cudaSuccess) return e;

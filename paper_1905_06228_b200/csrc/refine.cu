@@ -811,10 +811,14 @@ cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st) {
   if (p.method == 0) {
     auto k = u8 ? refine_strip_kernel<uint8_t, 0> : refine_strip_kernel<uint16_t, 0>;
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     if (e == cudaSuccess) k<<<grid, kNT, smem, st>>>(p);
   } else {
     auto k = u8 ? refine_strip_kernel<uint8_t, 1> : refine_strip_kernel<uint16_t, 1>;
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     if (e == cudaSuccess) k<<<grid, kNT, smem, st>>>(p);
   }
   count_launch();
