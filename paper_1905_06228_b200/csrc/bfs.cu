@@ -274,30 +274,44 @@ __global__ void __launch_bounds__(256, 3) bfs_tile_kernel(BfsParams p) {
     } else {
       const uint16_t* F = reinterpret_cast<const uint16_t*>(smem + L.ref);
       const uint16_t* T16 = reinterpret_cast<const uint16_t*>(T);
-      if constexpr (kF64) {
+      // Exact fp64 accumulation on the DFMA pipe: used for every warp when the data
+      // is too wide for u32 row sums (kF64), and for the odd warps of a 12-bit
+      // tile (p.mix) so that IMAD and DFMA pipes run concurrently.
+      if (kF64 || (p.mix && ((tid >> 5) & 1))) {
         double accd[J];
 #pragma unroll
         for (int j = 0; j < J; ++j) accd[j] = 0.0;
+        const int full = (side / J) * J;
         for (int r = 0; r < side; ++r) {
           const uint16_t* frow = F + r * p.ref_pitch + s * p.lat.step;
           const uint16_t* grow = T16 + (t + r) * p.region_pitch + cs;
           double gw[J];
 #pragma unroll
           for (int i = 0; i < J - 1; ++i) gw[i] = (double)grow[i];
-          for (int c0 = 0; c0 < p.CP; c0 += J) {
+          for (int c0 = 0; c0 < full; c0 += J) {
 #pragma unroll
             for (int k = 0; k < J; ++k) {
-              const int c = c0 + k;
-              const double f = c < side ? (double)frow[c] : 0.0;
-              gw[(k + J - 1) % J] = (double)grow[c + J - 1];
+              const double f = (double)frow[c0 + k];
+              gw[(k + J - 1) % J] = (double)grow[c0 + k + J - 1];
 #pragma unroll
               for (int j = 0; j < J; ++j) accd[j] = fma(f, gw[(k + j) % J], accd[j]);
+            }
+          }
+          if (full < side) {
+#pragma unroll
+            for (int k = 0; k < J; ++k) {
+              if (full + k < side) {
+                const double f = (double)frow[full + k];
+                gw[(k + J - 1) % J] = (double)grow[full + k + J - 1];
+#pragma unroll
+                for (int j = 0; j < J; ++j) accd[j] = fma(f, gw[(k + j) % J], accd[j]);
+              }
             }
           }
         }
 #pragma unroll
         for (int j = 0; j < J; ++j) sfg[j] = (uint64_t)accd[j];
-      } else {
+        } else {
         const int full = (side / J) * J;  // mask-free blocks, then one uniform tail block
         for (int r = 0; r < side; ++r) {
           const uint16_t* frow = F + r * p.ref_pitch + s * p.lat.step;

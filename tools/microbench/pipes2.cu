@@ -1,0 +1,61 @@
+// Pipe concurrency probe: IMAD alone, DFMA alone, IMAD+DFMA interleaved,
+// IMAD+FFMA interleaved, I2F.F64 conversion rate.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#define ILP 8
+template <int OP>
+__global__ void kern(uint32_t* out, int iters, uint32_t seed) {
+  uint32_t a[ILP], b = seed * 3u + threadIdx.x, c = seed ^ 0x9e37u;
+  double d[ILP], db = (double)b * 1e-12, dc = 1.0000000001;
+  float f[ILP], fb = 1e-7f, fc = 1.0000001f;
+  #pragma unroll
+  for (int i = 0; i < ILP; ++i) { a[i] = threadIdx.x + i; d[i] = (double)(threadIdx.x + i); f[i] = (float)i; }
+  for (int it = 0; it < iters; ++it) {
+    #pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      #pragma unroll
+      for (int i = 0; i < ILP; ++i) {
+        if (OP == 0) a[i] = a[i] * b + c;
+        if (OP == 1) d[i] = fma(d[i], dc, db);
+        if (OP == 2) { a[i] = a[i] * b + c; d[i] = fma(d[i], dc, db); }
+        if (OP == 3) { a[i] = a[i] * b + c; f[i] = fmaf(f[i], fc, fb); }
+        if (OP == 4) { d[i] += (double)(uint16_t)(a[i] + u); }
+        if (OP == 5) { a[i] = a[i] * b + c; f[i] = fmaf(f[i], fc, fb); d[i] = fma(d[i], dc, db); }
+      }
+    }
+  }
+  uint32_t s = 0;
+  #pragma unroll
+  for (int i = 0; i < ILP; ++i) s += a[i] + (uint32_t)__double_as_longlong(d[i]) + __float_as_uint(f[i]);
+  if (s == 0x12345678u) out[0] = s;
+}
+int main() {
+  cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
+  uint32_t* out; cudaMalloc(&out, 4);
+  const char* names[] = {"imad", "dfma", "imad+dfma(pairs)", "imad+ffma(pairs)", "i2f64+dadd", "imad+ffma+dfma(triples)"};
+  printf("{");
+  for (int op = 0; op < 6; ++op) {
+    int grid = p.multiProcessorCount * 8, block = 256, iters = 2048;
+    auto launch = [&]() {
+      switch (op) {
+        case 0: kern<0><<<grid, block>>>(out, iters, 1); break;
+        case 1: kern<1><<<grid, block>>>(out, iters, 1); break;
+        case 2: kern<2><<<grid, block>>>(out, iters, 1); break;
+        case 3: kern<3><<<grid, block>>>(out, iters, 1); break;
+        case 4: kern<4><<<grid, block>>>(out, iters, 1); break;
+        case 5: kern<5><<<grid, block>>>(out, iters, 1); break;
+      }
+    };
+    launch(); cudaDeviceSynchronize();
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    for (int r = 0; r < 5; ++r) launch();
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    double groups = 5.0 * grid * block * (double)iters * 8 * ILP;  // per "group" of ops
+    printf("%s\"%s_Ggroups_per_s\": %.1f", op ? ", " : "", names[op], groups / (ms * 1e-3) / 1e9);
+  }
+  printf("}\n");
+  return 0;
+}
