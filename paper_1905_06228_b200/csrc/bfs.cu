@@ -379,10 +379,16 @@ __global__ void __launch_bounds__(256, 3) bfs_tile_kernel(BfsParams p) {
       const int dx = dx_lo_nom + dxp;
       const bool in_chunk = dxp >= g.dx0 && dxp < g.dx0 + g.dxn;
       const bool ok = in_chunk && row_ok && (p.whole || (dx >= fx_lo && dx <= fx_hi));
-      if (!ok || sqrt_vf <= 0.0) continue;
       const int64_t vg = n * (int64_t)s2 - (int64_t)s1 * (int64_t)s1;
-      if (vg <= 0) continue;  // constant target window: skipped, not counted
-      const double c = zncc_from_moments(n, (int64_t)sfg[j], sf, (int64_t)s1, (int64_t)s2, sqrt_vf);
+      const bool valid = ok && sqrt_vf > 0.0 && vg > 0;  // constant target window: skipped, not counted
+      const double c = valid ? zncc_from_moments(n, (int64_t)sfg[j], sf, (int64_t)s1, (int64_t)s2, sqrt_vf)
+                             : __longlong_as_double(0x7ff8000000000000ULL);
+      if (p.surface && in_chunk) {
+        // full correlation surface for the swarm walk (K2): NaN = no result
+        const size_t k = (size_t)(g.iy - p.row_begin) * p.lat.nx + (g.ix0 + s);
+        p.surface[k * p.EX * p.EY + (size_t)(g.dy0 + t) * p.EX + dxp] = c;
+      }
+      if (!valid) continue;
       best.count++;
       if (!best.found || improves(c, dx, dy, best.c, best.dx, best.dy)) {
         best.found = 1;

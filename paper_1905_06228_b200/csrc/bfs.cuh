@@ -17,6 +17,7 @@ struct BfsParams {
   int RW, RH, region_pitch, ref_pitch, items_max;
   dicb200_poi_record* rec;  // records of the launched rows: index (iy-row_begin)*nx + ix
   BestPartial* partial;     // [subset][n_chunks] when n_chunks > 1
+  double* surface;          // optional [subset][EY][EX] ZNCC surface (NaN = no result) for K2
 };
 
 struct BfsSmem {

@@ -168,32 +168,80 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
     }
     if (partial) DICB200_CUDA_TRY(cudaFreeAsync(partial, st));
   } else {
-    PsoParams p{};
-    p.ref = view(ref);
-    p.tgt = view(tgt);
-    p.lat = lat;
-    p.row_begin = rb;
-    p.M = cfg->half_width;
-    p.R = cfg->search_radius;
-    p.u8 = ref->dtype == DICB200_U8;
-    p.star = cfg->integer_method == DICB200_INT_MPSO;
-    p.P = cfg->particle_count;
-    p.G = cfg->max_generations;
-    p.stop = cfg->stop_threshold;
-    p.c1 = cfg->c1;
-    p.c2 = cfg->c2;
-    p.seed = cfg->rng_seed;
-    p.pair_index = pair_index;
-    p.inertia_constant = cfg->inertia_mode == DICB200_INERTIA_CONSTANT;
-    p.w_const = cfg->inertia_constant;
-    p.subpixel_none = cfg->subpixel_method == DICB200_SUB_NONE;
-    p.rec = out_dev;
-    p.n_records = (int)nrec;
-    dicb200_status s;
-    {
-      StageTimer tm(1, st);
-      s = pso_launch(p, st);
+    // K2: exact ZNCC surface of every POI's +-R window (K1 kernel), then the
+    // warp-per-POI swarm walk over it. Rows are processed in chunks so the
+    // surface buffer stays bounded.
+    const int W = 2 * cfg->search_radius + 1;
+    if (cfg->search_radius < 0) return invalid("search radius must be >= 0");
+    const size_t per_row = (size_t)lat.nx * W * W * sizeof(double);
+    const int rows_per_chunk = std::max<int>(1, (int)std::min<size_t>((size_t)rows, ((size_t)1 << 30) / per_row));
+    double* surface = nullptr;
+    DICB200_CUDA_TRY(cudaMallocAsync((void**)&surface, per_row * rows_per_chunk, st));
+    dicb200_status s = DICB200_OK;
+    for (int r0 = rb; r0 < re && s == DICB200_OK; r0 += rows_per_chunk) {
+      const int r1 = std::min(re, r0 + rows_per_chunk);
+      dicb200_poi_record* out_chunk = out_dev + (size_t)(r0 - rb) * lat.nx;
+      BfsParams b{};
+      b.ref = view(ref);
+      b.tgt = view(tgt);
+      b.lat = lat;
+      b.row_begin = r0;
+      b.M = cfg->half_width;
+      b.R = cfg->search_radius;
+      b.whole = 0;  // the swarm always searches the feasible +-R window (integer_search.cpp:113-114)
+      b.u8 = ref->dtype == DICB200_U8;
+      {
+        const int bits = std::max(ref->bits, tgt->bits);
+        const double maxv = (bits > 0 && bits < 16) ? (double)((1 << bits) - 1) : 65535.0;
+        b.f64 = !b.u8 && (double)(2 * b.M + 1) * maxv * maxv >= 4294967296.0;
+      }
+      b.subpixel_none = 1;
+      b.rec = out_chunk;
+      b.surface = surface;
+      if (!bfs_plan(b, 72 * 1024) && !bfs_plan(b, 200 * 1024)) {
+        s = invalid("subset too large for the BFS tile (shared memory)");
+        break;
+      }
+      BestPartial* partial = nullptr;
+      if (b.n_chunks > 1) {
+        cudaError_t e = cudaMallocAsync((void**)&partial, (size_t)(r1 - r0) * lat.nx * b.n_chunks * sizeof(BestPartial), st);
+        if (e != cudaSuccess) {
+          s = cuda_fail(e, "cudaMallocAsync(partial)", __FILE__, __LINE__);
+          break;
+        }
+        b.partial = partial;
+      }
+      PsoParams p{};
+      p.ref = view(ref);
+      p.tgt = view(tgt);
+      p.lat = lat;
+      p.row_begin = r0;
+      p.M = cfg->half_width;
+      p.R = cfg->search_radius;
+      p.u8 = ref->dtype == DICB200_U8;
+      p.star = cfg->integer_method == DICB200_INT_MPSO;
+      p.P = cfg->particle_count;
+      p.G = cfg->max_generations;
+      p.stop = cfg->stop_threshold;
+      p.c1 = cfg->c1;
+      p.c2 = cfg->c2;
+      p.seed = cfg->rng_seed;
+      p.pair_index = pair_index;
+      p.inertia_constant = cfg->inertia_mode == DICB200_INERTIA_CONSTANT;
+      p.w_const = cfg->inertia_constant;
+      p.subpixel_none = cfg->subpixel_method == DICB200_SUB_NONE;
+      p.rec = out_chunk;
+      p.n_records = (r1 - r0) * lat.nx;
+      p.surface = surface;
+      {
+        StageTimer tm(1, st);
+        cudaError_t e = bfs_launch(b, r1 - r0, st);
+        if (e != cudaSuccess) s = cuda_fail(e, "bfs_launch(surface)", __FILE__, __LINE__);
+        if (s == DICB200_OK) s = pso_walk_launch(p, st);
+      }
+      if (partial) cudaFreeAsync(partial, st);
     }
+    cudaFreeAsync(surface, st);
     if (s != DICB200_OK) return s;
   }
   if (cfg->subpixel_method != DICB200_SUB_NONE) {

@@ -17,13 +17,10 @@ struct PsoParams {
   int subpixel_none;
   dicb200_poi_record* rec;
   int n_records;
-  // plan
-  int wmax;          // window side bound (2R+1)
-  int region_pitch;  // bytes (u8) or elements (u16), multiple of 4 bytes
-  int QP;            // u8 words per subset row
-  size_t smem;
+  const double* surface;  // [n_records][2R+1][2R+1] ZNCC surface from the BFS kernel (NaN = no result)
 };
 
-dicb200_status pso_launch(PsoParams& p, cudaStream_t st);
+size_t pso_walk_smem(const PsoParams& p);
+dicb200_status pso_walk_launch(PsoParams& p, cudaStream_t st);
 
 }  // namespace dicb200
