@@ -492,12 +492,15 @@ bool bfs_plan(BfsParams& p, size_t smem_limit) {
   int bestJ = 0, bestB = 0, bestSlots = 1 << 30;
   const int* Js = p.u8 ? kJu8 : kJu16;
   const int nJ = p.u8 ? (int)(sizeof(kJu8) / sizeof(int)) : (int)(sizeof(kJu16) / sizeof(int));
+  // cost ~ candidate slots + per-block overhead (u8: f/word loads + 3 PRMT per
+  // step amortised over J; u16: 2 loads per step)
+  const int ovh = p.u8 ? 5 : 2;
   for (int i = 0; i < nJ; ++i) {
     const int J = Js[i];
     const int B = (need + J - 1) / J;
-    const int slots = B * J;
-    if (slots < bestSlots || (slots == bestSlots && B < bestB)) {
-      bestSlots = slots;
+    const int cost = B * J + ovh * B;
+    if (cost < bestSlots || (cost == bestSlots && B < bestB)) {
+      bestSlots = cost;
       bestJ = J;
       bestB = B;
     }

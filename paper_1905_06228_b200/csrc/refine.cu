@@ -126,6 +126,39 @@ __device__ __forceinline__ double warp_sum1(double v) {
 }
 
 // Per-thread partials -> per-warp sums in rb[warp][base + i] (one value live at a time).
+// Transposed warp reduction by recursive halving: N (power of two <= 32)
+// per-lane partials in, lane l gets the warp total of value (l >> (5 - log2 N)).
+// (N-1) x (4 SEL + 2 SHFL + DADD) instead of N x 5 x (2 SHFL + DADD).
+template <int N>
+__device__ __forceinline__ double warp_transpose_sum(double (&v)[N]) {
+  const int lane = threadIdx.x & 31;
+  constexpr int L = N == 1 ? 0 : N == 2 ? 1 : N == 4 ? 2 : N == 8 ? 3 : N == 16 ? 4 : 5;
+  static_assert((1 << L) == N, "N must be a power of two <= 32");
+#pragma unroll
+  for (int st = 0; st < L; ++st) {
+    const int m = 16 >> st;
+    const int half = N >> (st + 1);
+    const bool upper = (lane & m) != 0;
+#pragma unroll
+    for (int j = 0; j < half; ++j) {
+      const double send = upper ? v[j] : v[j + half];
+      const double keep = upper ? v[j + half] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+  }
+  double r = v[0];
+#pragma unroll
+  for (int m = 16 >> L; m; m >>= 1) r += __shfl_xor_sync(0xffffffffu, r, m);
+  return r;
+}
+
+// Broadcast value j (held by lanes j << (5 - L)) of a transposed reduction.
+template <int N>
+__device__ __forceinline__ double tget(double r, int j) {
+  constexpr int L = N == 1 ? 0 : N == 2 ? 1 : N == 4 ? 2 : N == 8 ? 3 : N == 16 ? 4 : 5;
+  return __shfl_sync(0xffffffffu, r, j << (5 - L));
+}
+
 __device__ __forceinline__ double warp_det(const double* p) {
   return __dsub_rn(__dmul_rn(1.0 + p[1], 1.0 + p[5]), __dmul_rn(p[2], p[4]));
 }
@@ -697,8 +730,21 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
       gmin = fminf(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
       gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
     }
-    const double t0 = warp_sum1((double)acc[0]), t1 = warp_sum1((double)acc[1]);
-    const double t2 = (final_pass || METHOD == 0) ? warp_sum1((double)acc[2]) : 0.0;
+    double t0, t1, t2 = 0.0, G6[6] = {0, 0, 0, 0, 0, 0};
+    if (METHOD == 1 && !final_pass) {
+      double v8[8] = {acc[0], acc[1], acc[3], acc[4], acc[5], acc[6], acc[7], acc[8]};
+      const double r = warp_transpose_sum<8>(v8);
+      t0 = tget<8>(r, 0);
+      t1 = tget<8>(r, 1);
+#pragma unroll
+      for (int j = 0; j < 6; ++j) G6[j] = tget<8>(r, 2 + j);
+    } else {
+      double v4[4] = {acc[0], acc[1], acc[2], 0.0};
+      const double r = warp_transpose_sum<4>(v4);
+      t0 = tget<4>(r, 0);
+      t1 = tget<4>(r, 1);
+      t2 = tget<4>(r, 2);
+    }
     const double delta = t0 / n_d;                           // gbar - fbar
     const double ng2 = fmax(t1 - n_d * delta * delta, 0.0);  // sum (g - gbar)^2
     const double ng = sqrt(ng2);
@@ -721,7 +767,7 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
       const double ratio = C.nf / ng;
       double rhs[6];
 #pragma unroll
-      for (int j = 0; j < 6; ++j) rhs[j] = C.A[j] - ratio * (0.5 * warp_sum1((double)acc[3 + j]) - delta * C.S[j]);
+      for (int j = 0; j < 6; ++j) rhs[j] = C.A[j] - ratio * (0.5 * G6[j] - delta * C.S[j]);
       hinv_step(hinv, rhs, step, finite);
       if (!finite) {
         status = DICB200_POI_DEGENERATE_TEXTURE;
@@ -737,16 +783,23 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
       // additive update
       const double kap = (t2 - delta * C.scf) / ng2;  // cross / ng^2
       const double scale = -2.0 / (C.nf * ng);
+      double v32[32], v4[4];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v32[j] = acc[3 + j];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v4[j] = acc[35 + j];
+      const double ra = warp_transpose_sum<32>(v32), rb2 = warp_transpose_sum<4>(v4);
       double grad[6];
 #pragma unroll
       for (int j = 0; j < 6; ++j) {
-        const double cj = warp_sum1((double)acc[3 + j]), gj = warp_sum1((double)acc[9 + j]),
-                     sj = warp_sum1((double)acc[15 + j]);
+        const double cj = tget<32>(ra, j), gj = tget<32>(ra, 6 + j), sj = tget<32>(ra, 12 + j);
         grad[j] = scale * (cj - kap * (gj - delta * sj));
       }
       double mo[18];
 #pragma unroll
-      for (int j = 0; j < 18; ++j) mo[j] = warp_sum1((double)acc[21 + j]);
+      for (int j = 0; j < 14; ++j) mo[j] = tget<32>(ra, 18 + j);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) mo[14 + j] = tget<4>(rb2, j);
       double h[6], hi6[6];
       hessian_row(mo, 2.0 / ng2, lane, h);
       bool pd;
