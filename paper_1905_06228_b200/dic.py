@@ -19,7 +19,7 @@ import numpy as np
 from . import _abi
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdicb200.so")
+LIB_PATH = os.environ.get("DICB200_LIB") or os.path.join(_HERE, "libdicb200.so")  # override: A/B builds
 
 
 class DicError(RuntimeError):
