@@ -93,12 +93,31 @@ static dicb200_status make_lattice(int w, int h, const dicb200_run_config* cfg, 
   return DICB200_OK;
 }
 
+// Keep stream-ordered allocations (PSO surfaces, per-call images/records) in
+// the device pool across calls instead of returning them at every sync.
+static void retain_pool_memory() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lk(mu);
+  for (int d : done)
+    if (d == dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.push_back(dev);
+}
+
 static bool has_device() {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
+  if (n > 0) retain_pool_memory();
   return n > 0;
 }
 
