@@ -79,6 +79,32 @@ __host__ __device__ BfsSmem bfs_smem_layout(const BfsParams& p) {
   return s;
 }
 
+// Remainder of a subset row after the J-unrolled blocks: R (< J) steps,
+// straight-line (no per-step predicate), selected by a runtime switch.
+template <int J, int R>
+__device__ __forceinline__ void imad_tail(const uint16_t* frow, const uint16_t* grow, uint32_t (&acc)[J],
+                                          uint32_t (&gw)[J]) {
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const uint32_t f = frow[k];
+    gw[(k + J - 1) % J] = grow[k + J - 1];
+#pragma unroll
+    for (int j = 0; j < J; ++j) acc[j] += f * gw[(k + j) % J];
+  }
+}
+
+template <int J, int R = 1>
+__device__ __forceinline__ void imad_tail_dispatch(int rem, const uint16_t* frow, const uint16_t* grow,
+                                                   uint32_t (&acc)[J], uint32_t (&gw)[J]) {
+  if constexpr (R < J) {
+    if (rem == R) {
+      imad_tail<J, R>(frow, grow, acc, gw);
+      return;
+    }
+    imad_tail_dispatch<J, R + 1>(rem, frow, grow, acc, gw);
+  }
+}
+
 template <typename Pix, int J, bool kF64>
 __global__ void __launch_bounds__(256, 3) bfs_tile_kernel(BfsParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -331,17 +357,7 @@ __global__ void __launch_bounds__(256, 3) bfs_tile_kernel(BfsParams p) {
               for (int j = 0; j < J; ++j) acc[j] += f * gw[(k + j) % J];
             }
           }
-          if (full < side) {
-#pragma unroll
-            for (int k = 0; k < J; ++k) {
-              if (full + k < side) {  // uniform across the warp
-                const uint32_t f = frow[full + k];
-                gw[(k + J - 1) % J] = grow[full + k + J - 1];
-#pragma unroll
-                for (int j = 0; j < J; ++j) acc[j] += f * gw[(k + j) % J];
-              }
-            }
-          }
+          if (full < side) imad_tail_dispatch<J>(side - full, frow + full, grow + full, acc, gw);
 #pragma unroll
           for (int j = 0; j < J; ++j) sfg[j] += acc[j];
         }
