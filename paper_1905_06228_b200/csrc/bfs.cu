@@ -300,10 +300,10 @@ __global__ void __launch_bounds__(256, 3) bfs_tile_kernel(BfsParams p) {
     } else {
       const uint16_t* F = reinterpret_cast<const uint16_t*>(smem + L.ref);
       const uint16_t* T16 = reinterpret_cast<const uint16_t*>(T);
-      // Exact fp64 accumulation on the DFMA pipe: used for every warp when the data
-      // is too wide for u32 row sums (kF64), and for the odd warps of a 12-bit
-      // tile (p.mix) so that IMAD and DFMA pipes run concurrently.
-      if (kF64 || (p.mix && ((tid >> 5) & 1))) {
+      // Exact fp64 accumulation on the DFMA pipe when the data is too wide for
+      // u32 row sums (kF64). (Splitting 12-bit work between the IMAD and DFMA
+      // pipes — per warp or per thread — was measured slower: DESIGN.md §7.)
+      if constexpr (kF64) {
         double accd[J];
 #pragma unroll
         for (int j = 0; j < J; ++j) accd[j] = 0.0;

@@ -9,7 +9,6 @@ struct BfsParams {
   Lattice lat;
   int row_begin;   // first grid row of this launch (global row index)
   int M, R, whole, u8, f64;
-  int mix;  // u16 <= 13-bit: odd warps accumulate on the DFMA pipe, even warps on IMAD
   int subpixel_none;
   // plan (bfs_plan)
   int EX, EY, DXC, DYC, n_dx_chunks, n_dy_chunks, n_chunks;

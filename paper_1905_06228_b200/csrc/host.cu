@@ -167,10 +167,7 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
       const int bits = std::max(ref->bits, tgt->bits);
       const double maxv = (bits > 0 && bits < 16) ? (double)((1 << bits) - 1) : 65535.0;
       p.f64 = !p.u8 && (double)(2 * p.M + 1) * maxv * maxv >= 4294967296.0;
-      if (std::getenv("DICB200_FORCE_F64")) p.f64 = !p.u8;  // experiment switch: all-DFMA
-      // IMAD/DFMA warp interleave (pipes run concurrently, but the kernel is
-      // latency-bound, measured slower): opt-in only.
-      p.mix = !p.u8 && !p.f64 && std::getenv("DICB200_MIX") != nullptr;
+      if (std::getenv("DICB200_FORCE_F64")) p.f64 = !p.u8;  // experiment switch: all-DFMA path
     }
     p.subpixel_none = cfg->subpixel_method == DICB200_SUB_NONE;
     p.rec = out_dev;

@@ -537,91 +537,79 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
   wk.init(M, lane, g.rP);
   const float* Rs = R + g.rP + (cx - p.lat.cx(ix0)) + 1;  // reference pixel (0,0) of this subset
 
-  // ---- subset_stats: exact sums ----
-  double sf = 0.0, sff = 0.0;
-  {
-    Walk w = wk;
-    for (int i = 0; i < w.npl; ++i) {
-      if (i < w.npl - 1 || w.last_valid) {
-        const double f = Rs[w.roff];
-        sf += f;
-        sff += f * f;
-      }
-      w.advance();
-    }
-  }
-  sf = warp_sum1(sf);
-  sff = warp_sum1(sff);
-  const int64_t vf = (int64_t)n * (int64_t)sff - (int64_t)sf * (int64_t)sf;
-  if (vf <= 0) {  // constant subset
-    fail(METHOD == 1 ? DICB200_POI_DEGENERATE_TEXTURE : DICB200_POI_DEGENERATE_SUBSET);
-    return;
-  }
-  const double fbar = sf / (double)n;  // correlation.cpp:25: exact sum / n
-  const double nf = sqrt((double)vf / (double)n);
-  const float fbarf = (float)fbar;
+  // ---- one precompute pass: exact subset_stats sums (fp64) and, for IC-GN,
+  // the reference-side update constants in fp32 per lane (<= npl terms):
+  // sum f*sd, sum sd, and the Hessian moments of sd = (2 grad) x {1,dx,dy}.
+  // A = sum (f - fbar) sd = sum f sd - fbar sum sd needs no second pass.
   WarpConst& C = s_const[warp];
-
-  // ---- precompute: sum cf; IC-GN: exact Hessian -> H^-1, sum cf*sd, sum sd ----
+  double fbar, nf;
   double hinv[6] = {0, 0, 0, 0, 0, 0};
   {
-    double mo[18];
+    double sf = 0.0, sff = 0.0;
+    float a[30];
 #pragma unroll
-    for (int j = 0; j < 18; ++j) mo[j] = 0.0;
-    double scf = 0.0, A[6] = {0, 0, 0, 0, 0, 0}, Ssd[6] = {0, 0, 0, 0, 0, 0};
+    for (int j = 0; j < 30; ++j) a[j] = 0.f;
     Walk w = wk;
     for (int i = 0; i < w.npl; ++i) {
       if (i < w.npl - 1 || w.last_valid) {
         const float* q = Rs + w.roff;
-        const float cfv = (float)((double)q[0] - fbar);
-        scf += (double)cfv;
+        const float f = q[0];
+        sf += (double)f;
+        sff = fma((double)f, (double)f, sff);
         if (METHOD == 1) {
-          const float ga = q[1] - q[-1], gb = q[g.rP] - q[-g.rP];  // 2 * gradient: integers
-          const double dx = w.dxf, dy = w.dyf;
-          const double w6[6] = {1.0, dx, dy, dx * dx, dx * dy, dy * dy};
-          const double aa = (double)ga * ga, ab = (double)ga * gb, bb = (double)gb * gb;
+          const float ga = q[1] - q[-1], gb = q[g.rP] - q[-g.rP];  // 2 * gradient (exact)
+          const float dx = w.dxf, dy = w.dyf;
+          const float w6[6] = {1.f, dx, dy, dx * dx, dx * dy, dy * dy};
+          const float aa = ga * ga, ab = ga * gb, bb = gb * gb;
 #pragma unroll
           for (int j = 0; j < 6; ++j) {
-            mo[j] = fma(aa, w6[j], mo[j]);
-            mo[6 + j] = fma(ab, w6[j], mo[6 + j]);
-            mo[12 + j] = fma(bb, w6[j], mo[12 + j]);
+            a[j] = fmaf(aa, w6[j], a[j]);
+            a[6 + j] = fmaf(ab, w6[j], a[6 + j]);
+            a[12 + j] = fmaf(bb, w6[j], a[12 + j]);
           }
-          const double cgx = (double)cfv * ga, cgy = (double)cfv * gb;  // exact (float x float)
-          A[0] += cgx;
-          A[1] += cgx * dx;
-          A[2] += cgx * dy;
-          A[3] += cgy;
-          A[4] += cgy * dx;
-          A[5] += cgy * dy;
-          Ssd[0] += ga;
-          Ssd[1] += ga * dx;
-          Ssd[2] += ga * dy;
-          Ssd[3] += gb;
-          Ssd[4] += gb * dx;
-          Ssd[5] += gb * dy;
+          const float fga = f * ga, fgb = f * gb;
+          a[18] += fga;
+          a[19] = fmaf(fga, dx, a[19]);
+          a[20] = fmaf(fga, dy, a[20]);
+          a[21] += fgb;
+          a[22] = fmaf(fgb, dx, a[22]);
+          a[23] = fmaf(fgb, dy, a[23]);
+          a[24] += ga;
+          a[25] = fmaf(ga, dx, a[25]);
+          a[26] = fmaf(ga, dy, a[26]);
+          a[27] += gb;
+          a[28] = fmaf(gb, dx, a[28]);
+          a[29] = fmaf(gb, dy, a[29]);
         }
       }
       w.advance();
     }
-    scf = warp_sum1(scf);
+    sf = warp_sum1(sf);
+    sff = warp_sum1(sff);
+    const int64_t vf = (int64_t)n * (int64_t)sff - (int64_t)sf * (int64_t)sf;
+    if (vf <= 0) {  // constant subset (exact test)
+      fail(METHOD == 1 ? DICB200_POI_DEGENERATE_TEXTURE : DICB200_POI_DEGENERATE_SUBSET);
+      return;
+    }
+    fbar = sf / (double)n;  // correlation.cpp:25: exact sum / n
+    nf = sqrt((double)vf / (double)n);
     if (lane == 0) {
-      C.scf = scf;
+      C.scf = sf - (double)n * fbar;  // sum of centred values
       C.nf = nf;
     }
     if (METHOD == 1) {
+      double v32[32];
 #pragma unroll
-      for (int j = 0; j < 6; ++j) {
-        A[j] = warp_sum1(A[j]) * 0.5;    // sum cf * sd   (sd uses 0.5 * (2 grad))
-        Ssd[j] = warp_sum1(Ssd[j]) * 0.5;  // sum sd
-      }
-      if (lane == 0)
+      for (int j = 0; j < 30; ++j) v32[j] = a[j];
+      v32[30] = v32[31] = 0.0;
+      const double r = warp_transpose_sum<32>(v32);  // lane l holds total l
+      // lanes 18..23: sum f sd (x2), 24..29: sum sd (x2)
+      if (lane >= 24 && lane < 30) C.S[lane - 24] = 0.5 * r;
+      __syncwarp();
+      if (lane >= 18 && lane < 24) C.A[lane - 18] = 0.5 * r - fbar * C.S[lane - 18];
+      double mo[18];
 #pragma unroll
-        for (int j = 0; j < 6; ++j) {
-          C.A[j] = A[j];
-          C.S[j] = Ssd[j];
-        }
-#pragma unroll
-      for (int j = 0; j < 18; ++j) mo[j] = warp_sum1(mo[j]);
+      for (int j = 0; j < 18; ++j) mo[j] = __shfl_sync(0xffffffffu, r, j);
       double h[6];
       hessian_row(mo, 0.25, lane, h);
       double hf2 = 0.0;
@@ -652,6 +640,7 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
       }
     }
   }
+  const float fbarf = (float)fbar;
   __syncwarp();
 
   // ---- iterations (all lanes hold the same warp parameters) ----
