@@ -17,8 +17,9 @@
 // partials, fp64 warp reductions. The reference forms e_k (:331) / coeff_k
 // (:258) after gbar and ng are known; the update sums are expanded exactly,
 //   sum e_k sd_k = sum f_k sd_k - (nf/ng) [ sum g'_k sd_k - (gbar - fbar) sum sd_k ],
-// g' = g - fbar, with the reference-side sums precomputed in fp64 (the IC-GN
-// Hessian EXACTLY: (2 grad)^2 * {1,dx,dy,dx^2,dxdy,dy^2} are integers < 2^53).
+// g' = g - fbar, with the reference-side sums (sum f sd, sum sd, Hessian
+// moments) precomputed in ONE pass: fp32 per-lane partials (<= 53 terms),
+// fp64 across lanes; subset_stats sums (sum f, sum f^2) exact in fp64.
 // 6x6 solves: warp-parallel Cholesky H^-1 (H is SPD: J^T J); IC-GN keeps H^-1
 // in registers for all iterations. "Degenerate target" (ng == 0 in the
 // reference) is detected exactly as "all samples equal" (min == max).
@@ -331,6 +332,7 @@ struct WarpConst {
 struct PassCtx {
   const float* T;   // target region
   const float* Rs;  // reference pixel (0,0) of the subset in the reference region
+  const float2* Gs;  // IC-GN: (2 df/dx, 2 df/dy) of that pixel (gradient region)
   int tP, rP;
   float offx, offy;  // subset-local -> target-region coordinates
   float fbar;
@@ -391,7 +393,8 @@ __device__ __forceinline__ void pixel_pass(const PassCtx& c, const ImageView& tg
     acc[1] = fmaf(gp, gp, acc[1]);
     if (KIND != kIcgn) acc[2] = fmaf(q[0] - c.fbar, gp, acc[2]);
     if (KIND == kIcgn) {
-      const float tx = gp * (q[1] - q[-1]), ty = gp * (q[c.rP] - q[-c.rP]);  // g' * 2 grad f
+      const float2 gg = c.Gs[w.roff];  // 2 grad f, staged once per strip
+      const float tx = gp * gg.x, ty = gp * gg.y;
       acc[3] += tx;
       acc[4] = fmaf(tx, dx, acc[4]);
       acc[5] = fmaf(tx, dy, acc[5]);
@@ -503,6 +506,8 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
   const StripGeom g = G;
   float* R = smem_f;                    // reference region [rH][rP]
   float* T = smem_f + g.rH * g.rP;      // target region [tH][tP]
+  // IC-GN: gradient region (2 grad f) [rH][rP] as float2, 8-byte aligned
+  float2* G2 = reinterpret_cast<float2*>(smem_f + ((g.rH * g.rP + g.tH * g.tP + 1) & ~1));
   // ---- stage both regions (fp32), zero outside the images ----
   for (int i = tid; i < g.rH * g.rP; i += kNT) {
     const int y = i / g.rP, x = i - y * g.rP;
@@ -515,6 +520,15 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
     T[i] = (gx >= 0 && gx < p.tgt.width && gy >= 0 && gy < p.tgt.height) ? gpx<Pix>(p.tgt, gx, gy) : 0.f;
   }
   __syncthreads();
+  if (METHOD == 1) {  // central differences of the reference (icgn_precompute, subpixel.cpp:207-208), x2
+    for (int i = tid; i < g.rH * g.rP; i += kNT) {
+      const int y = i / g.rP, x = i - y * g.rP;
+      float2 v = make_float2(0.f, 0.f);
+      if (x >= 1 && x < g.rP - 1 && y >= 1 && y < g.rH - 1) v = make_float2(R[i + 1] - R[i - 1], R[i + g.rP] - R[i - g.rP]);
+      G2[i] = v;
+    }
+    __syncthreads();
+  }
   // ==== from here on every warp is independent (no block barriers) ====
   if (warp >= ts || !s_ok[warp]) return;
   dicb200_poi_record* rec = p.rec + rec0 + warp;
@@ -536,6 +550,7 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
   Walk wk;
   wk.init(M, lane, g.rP);
   const float* Rs = R + g.rP + (cx - p.lat.cx(ix0)) + 1;  // reference pixel (0,0) of this subset
+  const float2* Gs = G2 + g.rP + (cx - p.lat.cx(ix0)) + 1;
 
   // ---- one precompute pass: exact subset_stats sums (fp64) and, for IC-GN,
   // the reference-side update constants in fp32 per lane (<= npl terms):
@@ -557,7 +572,8 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
         sf += (double)f;
         sff = fma((double)f, (double)f, sff);
         if (METHOD == 1) {
-          const float ga = q[1] - q[-1], gb = q[g.rP] - q[-g.rP];  // 2 * gradient (exact)
+          const float2 gg = Gs[w.roff];
+          const float ga = gg.x, gb = gg.y;  // 2 * gradient (exact)
           const float dx = w.dxf, dy = w.dyf;
           const float w6[6] = {1.f, dx, dy, dx * dx, dx * dy, dy * dy};
           const float aa = ga * ga, ab = ga * gb, bb = gb * gb;
@@ -651,6 +667,7 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
   PassCtx pc;
   pc.T = T;
   pc.Rs = Rs;
+  pc.Gs = Gs;
   pc.tP = g.tP;
   pc.rP = g.rP;
   pc.offx = (float)(bx - g.tX0);
@@ -827,25 +844,26 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
 
 }  // namespace
 
-static size_t strip_smem(int M, int step, int spc) {
+static size_t strip_smem(int M, int step, int spc, int method) {
   const int side = 2 * M + 1;
   const int span = step * (spc - 1);
-  return (size_t)4 * ((size_t)(side + 2) * (span + side + 2) +
-                      (size_t)(side + 2 * kPad + 2 * kSpread) * (span + 2 * kSpread + side + 2 * kPad));
+  const size_t ref = (size_t)(side + 2) * (span + side + 2);
+  const size_t tgt = (size_t)(side + 2 * kPad + 2 * kSpread) * (span + 2 * kSpread + side + 2 * kPad);
+  return (size_t)4 * (((ref + tgt + 1) & ~(size_t)1) + (method == 1 ? 2 * ref : 0));
 }
 
 bool refine_plan(int M, int* ppt_out, int* nt_out) {
   *ppt_out = ((2 * M + 1) * (2 * M + 1) + 31) / 32;
   *nt_out = kNT;
-  return M >= 1 && strip_smem(M, 1, 1) <= 100 * 1024;
+  return M >= 1 && strip_smem(M, 1, 1, 1) <= 100 * 1024;
 }
 
 cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st) {
   if (p0.n_records <= 0) return cudaSuccess;
   RefineParams p = p0;
   p.spc = kWarps;
-  while (p.spc > 1 && strip_smem(p.M, p.lat.step, p.spc) > 100 * 1024) --p.spc;
-  const size_t smem = strip_smem(p.M, p.lat.step, p.spc);
+  while (p.spc > 1 && strip_smem(p.M, p.lat.step, p.spc, p.method) > 110 * 1024) --p.spc;
+  const size_t smem = strip_smem(p.M, p.lat.step, p.spc, p.method);
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   const int rows = p.n_records / p.lat.nx;
   dim3 grid((p.lat.nx + p.spc - 1) / p.spc, rows);
