@@ -357,8 +357,9 @@ __device__ __forceinline__ void pixel_pass(const PassCtx& c, const ImageView& tg
   gmax = -3.0e38f;
   bad = 0;
   Walk w = w0;
-  for (int i = 0; i < w.npl; ++i) {
-    if (i == w.npl - 1 && !w.last_valid) break;
+  const int cnt = w.npl - (w.last_valid ? 0 : 1);
+#pragma unroll 2
+  for (int i = 0; i < cnt; ++i) {
     const float dx = w.dxf, dy = w.dyf;
     const float xl = fmaf(c.uy, dy, fmaf(c.ux, dx, dx + c.ul));
     const float yl = fmaf(c.vy, dy, fmaf(c.vx, dx, dy + c.vl));

@@ -4,13 +4,16 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #define ILP 8
+__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d; asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c)); return d; }
 template <int OP>
 __global__ void kern(uint32_t* out, int iters, uint32_t seed) {
   uint32_t a[ILP], b = seed * 3u + threadIdx.x, c = seed ^ 0x9e37u;
   double d[ILP], db = (double)b * 1e-12, dc = 1.0000000001;
   float f[ILP], fb = 1e-7f, fc = 1.0000001f;
+  unsigned long long q[ILP], qb = 0x3f8000003f800000ull, qc = 0x33d6bf9533d6bf95ull;
   #pragma unroll
-  for (int i = 0; i < ILP; ++i) { a[i] = threadIdx.x + i; d[i] = (double)(threadIdx.x + i); f[i] = (float)i; }
+  for (int i = 0; i < ILP; ++i) { a[i] = threadIdx.x + i; d[i] = (double)(threadIdx.x + i); f[i] = (float)i; q[i] = i; }
   for (int it = 0; it < iters; ++it) {
     #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -22,20 +25,22 @@ __global__ void kern(uint32_t* out, int iters, uint32_t seed) {
         if (OP == 3) { a[i] = a[i] * b + c; f[i] = fmaf(f[i], fc, fb); }
         if (OP == 4) { d[i] += (double)(uint16_t)(a[i] + u); }
         if (OP == 5) { a[i] = a[i] * b + c; f[i] = fmaf(f[i], fc, fb); d[i] = fma(d[i], dc, db); }
+        if (OP == 6) { f[i] = fmaf(f[i], fc, fb); }
+        if (OP == 7) { q[i] = fma2(q[i], qb, qc); }
       }
     }
   }
   uint32_t s = 0;
   #pragma unroll
-  for (int i = 0; i < ILP; ++i) s += a[i] + (uint32_t)__double_as_longlong(d[i]) + __float_as_uint(f[i]);
+  for (int i = 0; i < ILP; ++i) s += a[i] + (uint32_t)__double_as_longlong(d[i]) + __float_as_uint(f[i]) + (uint32_t)q[i];
   if (s == 0x12345678u) out[0] = s;
 }
 int main() {
   cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
   uint32_t* out; cudaMalloc(&out, 4);
-  const char* names[] = {"imad", "dfma", "imad+dfma(pairs)", "imad+ffma(pairs)", "i2f64+dadd", "imad+ffma+dfma(triples)"};
+  const char* names[] = {"imad", "dfma", "imad+dfma(pairs)", "imad+ffma(pairs)", "i2f64+dadd", "imad+ffma+dfma(triples)", "ffma", "ffma2(instr)"};
   printf("{");
-  for (int op = 0; op < 6; ++op) {
+  for (int op = 0; op < 8; ++op) {
     int grid = p.multiProcessorCount * 8, block = 256, iters = 2048;
     auto launch = [&]() {
       switch (op) {
@@ -45,6 +50,8 @@ int main() {
         case 3: kern<3><<<grid, block>>>(out, iters, 1); break;
         case 4: kern<4><<<grid, block>>>(out, iters, 1); break;
         case 5: kern<5><<<grid, block>>>(out, iters, 1); break;
+        case 6: kern<6><<<grid, block>>>(out, iters, 1); break;
+        case 7: kern<7><<<grid, block>>>(out, iters, 1); break;
       }
     };
     launch(); cudaDeviceSynchronize();
