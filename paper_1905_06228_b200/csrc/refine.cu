@@ -335,6 +335,7 @@ struct PassCtx {
   const float2* Gs;  // IC-GN: (2 df/dx, 2 df/dy) of that pixel (gradient region)
   int tP, rP;
   float offx, offy;  // subset-local -> target-region coordinates
+  int ioffx, ioffy;  // the same offsets as integers (exact floor/frac in local coordinates)
   float fbar;
   float ul, vl, ux, uy, vx, vy;
   Win wn;
@@ -347,6 +348,87 @@ enum { kIcgn = 0, kNr = 1, kFinal = 2 };
 // kIcgn : acc = {sum g', sum g'^2, -, sum g' 2gx {1,dx,dy}, sum g' 2gy {1,dx,dy}}
 // kNr   : acc = {sum g', sum g'^2, sum cf g', sum cf J[6], sum g' J[6], sum J[6], moments[18]}
 // kFinal: acc = {sum g', sum g'^2, sum cf g'}
+
+// ---- packed FP32x2 (FFMA2 / FADD2 / FMUL2, sm_100a) ----
+typedef unsigned long long f2x;
+__device__ __forceinline__ f2x pk2(float a, float b) {
+  f2x r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void up2(f2x v, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
+__device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c) {
+  f2x d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2x add2(f2x a, f2x b) {
+  f2x d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2x mul2(f2x a, f2x b) {
+  f2x d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// Fast IC-GN pass with packed x/y arithmetic: same sums as pixel_pass<true, kIcgn>.
+__device__ __forceinline__ void icgn_pass_fast2(const PassCtx& c, const Walk& w0, float* acc, float& gmin,
+                                                float& gmax) {
+  float s0 = 0.f, s1 = 0.f;
+  f2x a36 = pk2(0.f, 0.f), a47 = a36, a58 = a36;
+  gmin = 3.0e38f;
+  gmax = -3.0e38f;
+  const f2x uvl = pk2(c.ul, c.vl);
+  const f2x uxvx = pk2(c.ux, c.vx), uyvy = pk2(c.uy, c.vy);
+  const f2x step = pk2(w0.r32f, w0.q32f), wrap = pk2(-w0.sidef, 1.0f);
+  f2x dxy = pk2(w0.dxf, w0.dyf);
+  int roff = w0.roff;
+  const int cnt = w0.npl - (w0.last_valid ? 0 : 1);
+#pragma unroll 2
+  for (int i = 0; i < cnt; ++i) {
+    float dx, dy;
+    up2(dxy, dx, dy);
+    f2x xy = add2(dxy, uvl);
+    xy = fma2(uxvx, pk2(dx, dx), xy);
+    xy = fma2(uyvy, pk2(dy, dy), xy);
+    float xl, yl;
+    up2(xy, xl, yl);
+    const float flx = floorf(xl), fly = floorf(yl);  // subset-local: exact frac
+    const float fx = xl - flx, fy = yl - fly;
+    const float* t = c.T + ((int)fly + c.ioffy) * c.tP + ((int)flx + c.ioffx);
+    const float f00 = t[0], f10 = t[1], f01 = t[c.tP], f11 = t[c.tP + 1];
+    const float a10 = f10 - f00, a01 = f01 - f00, a11 = (f11 - f10) - a01;
+    const float gv = fmaf(a11 * fx, fy, fmaf(a01, fy, fmaf(a10, fx, f00)));
+    gmin = fminf(gmin, gv);
+    gmax = fmaxf(gmax, gv);
+    const float2 gg = c.Gs[roff];
+    const float gp = gv - c.fbar;
+    s0 += gp;
+    s1 = fmaf(gp, gp, s1);
+    const f2x txy = mul2(pk2(gg.x, gg.y), pk2(gp, gp));
+    a36 = add2(a36, txy);
+    a47 = fma2(txy, pk2(dx, dx), a47);
+    a58 = fma2(txy, pk2(dy, dy), a58);
+    // advance the strided walk
+    dxy = add2(dxy, step);
+    roff += w0.roff_step;
+    float ndx, ndy;
+    up2(dxy, ndx, ndy);
+    if (ndx > w0.Mf) {
+      dxy = add2(dxy, wrap);
+      roff += w0.roff_wrap;
+    }
+  }
+  acc[0] = s0;
+  acc[1] = s1;
+  acc[2] = 0.f;
+  up2(a36, acc[3], acc[6]);
+  up2(a47, acc[4], acc[7]);
+  up2(a58, acc[5], acc[8]);
+}
+
 template <bool FAST, int KIND, typename Pix>
 __device__ __forceinline__ void pixel_pass(const PassCtx& c, const ImageView& tgt, const Walk& w0,
                                            float* acc, int& bad, float& gmin, float& gmax) {
@@ -365,10 +447,9 @@ __device__ __forceinline__ void pixel_pass(const PassCtx& c, const ImageView& tg
     const float yl = fmaf(c.vy, dy, fmaf(c.vx, dx, dy + c.vl));
     float gv, gx = 0.f, gy = 0.f;
     if (FAST) {
-      const float wx = xl + c.offx, wy = yl + c.offy;
-      const float flx = floorf(wx), fly = floorf(wy);
-      const float fx = wx - flx, fy = wy - fly;
-      const float* t = c.T + (int)fly * c.tP + (int)flx;
+      const float flx = floorf(xl), fly = floorf(yl);  // subset-local: exact frac
+      const float fx = xl - flx, fy = yl - fly;
+      const float* t = c.T + ((int)fly + c.ioffy) * c.tP + ((int)flx + c.ioffx);
       const float f00 = t[0], f10 = t[1], f01 = t[c.tP], f11 = t[c.tP + 1];
       const float a10 = f10 - f00, a01 = f01 - f00, a11 = (f00 + f11) - f10 - f01;
       gv = fmaf(a11 * fx, fy, fmaf(a01, fy, fmaf(a10, fx, f00)));
@@ -673,6 +754,8 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
   pc.rP = g.rP;
   pc.offx = (float)(bx - g.tX0);
   pc.offy = (float)(by - g.tY0);
+  pc.ioffx = bx - g.tX0;
+  pc.ioffy = by - g.tY0;
   pc.fbar = fbarf;
   pc.wn.w = T;
   pc.wn.S = min(g.tP, g.tH);
@@ -721,7 +804,7 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
         pixel_pass<false, kFinal, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
     } else if (METHOD == 1) {
       if (fast)
-        pixel_pass<true, kIcgn, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
+        icgn_pass_fast2(pc, wk, acc, gmin, gmax);
       else
         pixel_pass<false, kIcgn, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
     } else {
