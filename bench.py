@@ -339,11 +339,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         else:
             a, b = my_pairs[0]
             ia, ib = img(a, host[a].data_ptr()), img(b, host[b].data_ptr())
-            outrec = np.zeros(spp, dtype=_abi.record_dtype())
+            outrec = torch.empty(spp * rec_size, dtype=torch.uint8).pin_memory()
 
             def e2e_step():
                 n = C.c_size_t(0)
-                st = L.dicb200_analyze_pair(C.byref(ia), C.byref(ib), C.byref(cfgc), 0, outrec.ctypes.data, spp,
+                st = L.dicb200_analyze_pair(C.byref(ia), C.byref(ib), C.byref(cfgc), 0, outrec.data_ptr(), spp,
                                             C.byref(n))
                 if st:
                     raise RuntimeError(L.dicb200_last_error_message().decode())
@@ -369,7 +369,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "frame_pairs_per_s": n_pairs * args.steps / float(et.item()),
                "path": "dicb200_analyze_sequence (C-ABI), pinned host frames" if n_pairs > 1 else
-                       "dicb200_analyze_pair (C-ABI), host frames"}
+                       "dicb200_analyze_pair (C-ABI), pinned host frames and records"}
 
     if rank != 0:
         return None

@@ -280,67 +280,208 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
 
 static size_t elem_size(int dtype) { return dtype == DICB200_U8 ? 1 : 2; }
 
-// Upload a host image (tight pitch) on `st`.
-static dicb200_status upload(const dicb200_image* host, dicb200_image* dev, void** buf, cudaStream_t st) {
-  const size_t es = elem_size(host->dtype);
-  const int pitch = host->pitch > 0 ? host->pitch : host->width;
-  const size_t bytes = (size_t)host->width * host->height * es;
-  DICB200_CUDA_TRY(cudaMallocAsync(buf, bytes, st));
-  DICB200_CUDA_TRY(cudaMemcpy2DAsync(*buf, host->width * es, host->data, pitch * es, host->width * es, host->height,
-                                     cudaMemcpyHostToDevice, st));
-  *dev = *host;
-  dev->pitch = host->width;
-  dev->data = *buf;
+// ---- persistent per-device execution contexts ------------------------------
+// Streams, events and grow-only device buffers are created once and reused by
+// every analyze call. Contexts live in a pool so that concurrent callers (and
+// the per-device workers of analyze_sequence) each own one while they run.
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+// Grow `b` to at least `bytes` in stream order on `st`.
+static cudaError_t ensure(DevBuf& b, size_t bytes, cudaStream_t st) {
+  if (b.cap >= bytes) return cudaSuccess;
+  if (b.p) {
+    cudaError_t e = cudaFreeAsync(b.p, st);
+    if (e != cudaSuccess) return e;
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  cudaError_t e = cudaMallocAsync(&b.p, bytes, st);
+  if (e == cudaSuccess) b.cap = bytes;
+  return e;
+}
+
+// A device-resident frame. `key` is the frame's index in the caller's image
+// array for the duration of one analyze_sequence call (-1 = nothing cached).
+struct FrameSlot {
+  DevBuf buf;
+  long key = -1, last_use = -1;
+  cudaEvent_t ready = nullptr;  // upload finished (copy stream)
+  cudaEvent_t idle = nullptr;   // last pair reading the frame finished (compute stream)
+  dicb200_image im{};
+};
+
+// Device records of one pair plus a pinned staging buffer for pageable outputs.
+struct RecSlot {
+  DevBuf dev;
+  void* stage = nullptr;
+  size_t stage_cap = 0;
+  cudaEvent_t computed = nullptr;  // kernels of the pair finished (compute stream)
+  cudaEvent_t done = nullptr;      // records are in host memory (read-back stream)
+  long pair = -1;              // pair in flight (-1 = none)
+  size_t n = 0;
+  bool staged = false;
+};
+
+constexpr int kFrameSlots = 4;
+constexpr int kRecSlots = 2;
+
+struct DeviceContext {
+  int dev = 0;
+  cudaStream_t cs = nullptr;  // compute: kernels + record read-back
+  cudaStream_t xs = nullptr;  // copy: frame uploads ahead of the compute stream
+  cudaStream_t ds = nullptr;  // copy: record read-back behind the compute stream
+  FrameSlot frames[kFrameSlots];
+  RecSlot recs[kRecSlots];
+};
+
+namespace {
+std::mutex g_ctx_mu;
+std::vector<DeviceContext*> g_ctx_idle;
+}  // namespace
+
+static void destroy_context(DeviceContext* c) {
+  cudaSetDevice(c->dev);
+  if (c->cs) cudaStreamSynchronize(c->cs);
+  if (c->xs) cudaStreamSynchronize(c->xs);
+  if (c->ds) cudaStreamSynchronize(c->ds);
+  for (auto& f : c->frames) {
+    if (f.buf.p) cudaFree(f.buf.p);
+    if (f.ready) cudaEventDestroy(f.ready);
+    if (f.idle) cudaEventDestroy(f.idle);
+  }
+  for (auto& r : c->recs) {
+    if (r.dev.p) cudaFree(r.dev.p);
+    if (r.stage) cudaFreeHost(r.stage);
+    if (r.done) cudaEventDestroy(r.done);
+    if (r.computed) cudaEventDestroy(r.computed);
+  }
+  if (c->cs) cudaStreamDestroy(c->cs);
+  if (c->xs) cudaStreamDestroy(c->xs);
+  if (c->ds) cudaStreamDestroy(c->ds);
+  delete c;
+}
+
+// Take an idle context of the current device (or create one).
+static DeviceContext* acquire_context(dicb200_status* st) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    *st = cuda_fail(e, "cudaGetDevice", __FILE__, __LINE__);
+    return nullptr;
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    for (size_t i = 0; i < g_ctx_idle.size(); ++i)
+      if (g_ctx_idle[i]->dev == dev) {
+        DeviceContext* c = g_ctx_idle[i];
+        g_ctx_idle.erase(g_ctx_idle.begin() + (long)i);
+        *st = DICB200_OK;
+        return c;
+      }
+  }
+  auto* c = new DeviceContext;
+  c->dev = dev;
+  e = cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->xs, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->ds, cudaStreamNonBlocking);
+  for (auto& f : c->frames) {
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f.ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f.idle, cudaEventDisableTiming);
+  }
+  for (auto& r : c->recs) {
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r.computed, cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) {
+    *st = cuda_fail(e, "device context creation", __FILE__, __LINE__);
+    destroy_context(c);
+    return nullptr;
+  }
+  *st = DICB200_OK;
+  return c;
+}
+
+// Return a context to the pool once both of its streams are drained.
+static dicb200_status release_context(DeviceContext* c) {
+  cudaError_t e1 = cudaStreamSynchronize(c->xs);
+  cudaError_t e2 = cudaStreamSynchronize(c->cs);
+  cudaError_t e3 = cudaStreamSynchronize(c->ds);
+  if (e2 == cudaSuccess) e2 = e3;
+  for (auto& f : c->frames) f.key = f.last_use = -1;  // LRU state is per call
+  for (auto& r : c->recs) r.pair = -1;
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  g_ctx_idle.push_back(c);
+  if (e1 != cudaSuccess) return cuda_fail(e1, "cudaStreamSynchronize(copy)", __FILE__, __LINE__);
+  if (e2 != cudaSuccess) return cuda_fail(e2, "cudaStreamSynchronize(compute)", __FILE__, __LINE__);
   return DICB200_OK;
 }
 
-struct StreamGuard {
-  cudaStream_t s = nullptr;
-  ~StreamGuard() {
-    if (s) cudaStreamDestroy(s);
-  }
-};
+// H2D of a host image (any pitch) into `buf` on `st`; `dev` describes the copy.
+static dicb200_status upload(const dicb200_image* host, DevBuf& buf, dicb200_image* dev, cudaStream_t st) {
+  const size_t es = elem_size(host->dtype);
+  const int pitch = host->pitch > 0 ? host->pitch : host->width;
+  const size_t row = (size_t)host->width * es;
+  DICB200_CUDA_TRY(ensure(buf, row * host->height, st));
+  DICB200_CUDA_TRY(cudaMemcpy2DAsync(buf.p, row, host->data, pitch * es, row, host->height, cudaMemcpyHostToDevice, st));
+  *dev = *host;
+  dev->pitch = host->width;
+  dev->data = buf.p;
+  return DICB200_OK;
+}
 
-static dicb200_status analyze_pair_on_stream(const dicb200_image* ref, const dicb200_image* tgt,
-                                             const dicb200_run_config* cfg, uint64_t pair_index,
-                                             dicb200_poi_record* out, size_t out_cap, size_t* out_count,
-                                             cudaStream_t st, const dicb200_image* ref_dev_cached) {
+// Make frame `key` resident: reuse its slot, or upload it on the copy stream
+// into the least recently used slot other than `pin` once that slot's last
+// reader has finished.
+static dicb200_status stage_frame(DeviceContext* c, const dicb200_image* host, long key, long use, int pin,
+                                  int* slot) {
+  for (int i = 0; i < kFrameSlots; ++i)
+    if (c->frames[i].key == key) {
+      c->frames[i].last_use = std::max(c->frames[i].last_use, use);
+      *slot = i;
+      return DICB200_OK;
+    }
+  int v = -1;
+  for (int i = 0; i < kFrameSlots; ++i)
+    if (i != pin && (v < 0 || c->frames[i].last_use < c->frames[v].last_use)) v = i;
+  FrameSlot& f = c->frames[v];
+  f.key = -1;
+  DICB200_CUDA_TRY(cudaStreamWaitEvent(c->xs, f.idle, 0));
+  dicb200_status s = upload(host, f.buf, &f.im, c->xs);
+  if (s != DICB200_OK) return s;
+  DICB200_CUDA_TRY(cudaEventRecord(f.ready, c->xs));
+  f.key = key;
+  f.last_use = use;
+  *slot = v;
+  return DICB200_OK;
+}
+
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Shape checks shared by the host-buffer entry points: lattice size and the
+// caller's output capacity.
+static dicb200_status precheck(const dicb200_image* ref, const dicb200_image* tgt, const dicb200_run_config* cfg,
+                               size_t cap, Lattice* lat, size_t* n) {
+  *n = 0;
   dicb200_status s = validate_pair(ref, tgt, cfg);
   if (s != DICB200_OK) return s;
-  Lattice lat;
-  s = make_lattice(ref->width, ref->height, cfg, &lat);
+  s = make_lattice(ref->width, ref->height, cfg, lat);
   if (s != DICB200_OK) return s;
-  const size_t n = (size_t)lat.nx * lat.ny;
-  if (out_count) *out_count = n;
-  if (n > out_cap) {
+  *n = (size_t)lat->nx * lat->ny;
+  if (*n > cap) {
     set_error("output capacity smaller than the grid");
     return DICB200_ERR_CAPACITY;
   }
-  dicb200_image dref, dtgt;
-  void *bref = nullptr, *btgt = nullptr, *brec = nullptr;
-  if (ref_dev_cached) {
-    dref = *ref_dev_cached;
-  } else {
-    s = upload(ref, &dref, &bref, st);
-    if (s != DICB200_OK) return s;
-  }
-  s = upload(tgt, &dtgt, &btgt, st);
-  if (s == DICB200_OK) {
-    cudaError_t e = cudaMallocAsync(&brec, n * sizeof(dicb200_poi_record), st);
-    if (e != cudaSuccess) s = cuda_fail(e, "cudaMallocAsync(records)", __FILE__, __LINE__);
-  }
-  if (s == DICB200_OK)
-    s = enqueue_pair(&dref, &dtgt, cfg, pair_index, lat, 0, lat.ny, (dicb200_poi_record*)brec, st);
-  if (s == DICB200_OK) {
-    cudaError_t e = cudaMemcpyAsync(out, brec, n * sizeof(dicb200_poi_record), cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) s = cuda_fail(e, "cudaMemcpyAsync(records)", __FILE__, __LINE__);
-  }
-  if (brec) cudaFreeAsync(brec, st);
-  if (btgt) cudaFreeAsync(btgt, st);
-  if (bref) cudaFreeAsync(bref, st);
-  cudaError_t e = cudaStreamSynchronize(st);
-  if (s == DICB200_OK && e != cudaSuccess) s = cuda_fail(e, "cudaStreamSynchronize", __FILE__, __LINE__);
-  return s;
+  return DICB200_OK;
 }
 
 }  // namespace dicb200
@@ -440,9 +581,30 @@ dicb200_status dicb200_partition_ranges(size_t n, int32_t workers, size_t* range
 dicb200_status dicb200_analyze_pair(const dicb200_image* ref, const dicb200_image* tgt, const dicb200_run_config* cfg,
                                     uint64_t pair_index, dicb200_poi_record* out, size_t out_cap, size_t* out_count) {
   if (!has_device()) return no_device();
-  StreamGuard g;
-  DICB200_CUDA_TRY(cudaStreamCreateWithFlags(&g.s, cudaStreamNonBlocking));
-  return analyze_pair_on_stream(ref, tgt, cfg, pair_index, out, out_cap, out_count, g.s, nullptr);
+  Lattice lat;
+  size_t n = 0;
+  dicb200_status s = precheck(ref, tgt, cfg, out_cap, &lat, &n);
+  if (out_count) *out_count = n;
+  if (s != DICB200_OK) return s;
+  DeviceContext* c = acquire_context(&s);
+  if (!c) return s;
+  // one pair: everything in order on the compute stream, one sync at the end
+  RecSlot& r = c->recs[0];
+  s = upload(ref, c->frames[0].buf, &c->frames[0].im, c->cs);
+  if (s == DICB200_OK) s = upload(tgt, c->frames[1].buf, &c->frames[1].im, c->cs);
+  if (s == DICB200_OK) {
+    cudaError_t e = ensure(r.dev, n * sizeof(dicb200_poi_record), c->cs);
+    if (e != cudaSuccess) s = cuda_fail(e, "cudaMallocAsync(records)", __FILE__, __LINE__);
+  }
+  if (s == DICB200_OK)
+    s = enqueue_pair(&c->frames[0].im, &c->frames[1].im, cfg, pair_index, lat, 0, lat.ny,
+                     (dicb200_poi_record*)r.dev.p, c->cs);
+  if (s == DICB200_OK) {
+    cudaError_t e = cudaMemcpyAsync(out, r.dev.p, n * sizeof(dicb200_poi_record), cudaMemcpyDeviceToHost, c->cs);
+    if (e != cudaSuccess) s = cuda_fail(e, "cudaMemcpyAsync(records)", __FILE__, __LINE__);
+  }
+  const dicb200_status rs = release_context(c);
+  return s != DICB200_OK ? s : rs;
 }
 
 dicb200_status dicb200_analyze_pair_device(const dicb200_image* ref, const dicb200_image* tgt,
@@ -470,6 +632,7 @@ dicb200_status dicb200_analyze_pair_device(const dicb200_image* ref, const dicb2
 dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_images, const dicb200_run_config* cfg,
                                         dicb200_field* fields, size_t n_fields) {
   if (!has_device()) return no_device();
+  if (!images || !cfg || !fields) return invalid("null argument");
   if (n_images < 2) return invalid("insufficient images");
   if (n_fields != n_images - 1) return invalid("fields must hold one entry per pair");
   std::vector<int32_t> pairs(2 * (n_images - 1));
@@ -484,50 +647,132 @@ dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_im
   cudaGetDevice(&cur);
   std::vector<dicb200_status> result(workers, DICB200_OK);
   std::vector<std::string> errs(workers);
+
+  // One worker per device over a contiguous range of pairs. Per pair: frames are
+  // made resident on the copy stream (each frame uploaded once while it stays in
+  // one of the LRU slots — the fixed_first reference, or the frame an
+  // update_every_pair sequence shares between neighbouring pairs), the compute
+  // stream waits for them, runs the pair and reads its records back. The next
+  // pair's frames are uploaded while the current pair computes, and the host
+  // finalises pair i-1 while the device runs pair i.
   auto run = [&](int wk) {
     const int dev = workers == 1 ? cur : wk;
     cudaSetDevice(dev);
-    StreamGuard g;
-    if (cudaStreamCreateWithFlags(&g.s, cudaStreamNonBlocking) != cudaSuccess) {
-      result[wk] = DICB200_ERR_CUDA;
-      errs[wk] = "stream creation failed";
-      return;
-    }
-    // fixed_first: keep frame 0 resident on this device for all its pairs
-    dicb200_image ref0{};
-    void* ref0_buf = nullptr;
-    const bool fixed = cfg->reference_policy == DICB200_POLICY_FIXED_FIRST;
-    for (size_t i = ranges[2 * wk]; i < ranges[2 * wk + 1]; ++i) {
-      const dicb200_image* a = &images[pairs[2 * i]];
-      const dicb200_image* b = &images[pairs[2 * i + 1]];
-      dicb200_field& f = fields[i];
-      f.pair_index = (int32_t)i;
-      f.ref_id = a->id;
-      f.tgt_id = b->id;
+    auto fail_field = [&](dicb200_field& f, dicb200_status s) {
       f.count = 0;
-      f.error[0] = 0;
-      const dicb200_image* cached = nullptr;
-      if (fixed && validate_pair(a, b, cfg) == DICB200_OK) {
-        if (!ref0_buf && upload(a, &ref0, &ref0_buf, g.s) != DICB200_OK) ref0_buf = nullptr;
-        if (ref0_buf) cached = &ref0;
-      }
-      size_t cnt = 0;
-      const dicb200_status s = analyze_pair_on_stream(a, b, cfg, i, f.records, f.capacity, &cnt, g.s, cached);
-      f.count = s == DICB200_OK ? cnt : 0;
       f.status = s;
-      if (s == DICB200_ERR_INVALID) {
-        std::strncpy(f.error, g_last_error.c_str(), sizeof f.error - 1);
-        f.error[sizeof f.error - 1] = 0;
-      } else if (s != DICB200_OK) {
+      std::strncpy(f.error, g_last_error.c_str(), sizeof f.error - 1);
+      f.error[sizeof f.error - 1] = 0;
+      if (s != DICB200_ERR_INVALID) {  // a pair-level dic::Error does not fail the call (pipeline.cpp:191-198)
         result[wk] = s;
         errs[wk] = g_last_error;
-        std::strncpy(f.error, g_last_error.c_str(), sizeof f.error - 1);
-        f.error[sizeof f.error - 1] = 0;
       }
+    };
+    const size_t lo = ranges[2 * wk], hi = ranges[2 * wk + 1];
+    std::vector<Lattice> lat(hi - lo);
+    std::vector<size_t> cnt(hi - lo, 0);
+    std::vector<dicb200_status> pre(hi - lo);
+    for (size_t i = lo; i < hi; ++i) {
+      dicb200_field& f = fields[i];
+      f.pair_index = (int32_t)i;
+      f.ref_id = images[pairs[2 * i]].id;
+      f.tgt_id = images[pairs[2 * i + 1]].id;
+      f.count = 0;
+      f.status = DICB200_OK;
+      f.error[0] = 0;
+      pre[i - lo] = precheck(&images[pairs[2 * i]], &images[pairs[2 * i + 1]], cfg, f.capacity, &lat[i - lo],
+                             &cnt[i - lo]);
+      if (pre[i - lo] != DICB200_OK) fail_field(f, pre[i - lo]);
     }
-    if (ref0_buf) {
-      cudaFreeAsync(ref0_buf, g.s);
-      cudaStreamSynchronize(g.s);
+    dicb200_status cs_ = DICB200_OK;
+    DeviceContext* c = acquire_context(&cs_);
+    if (!c) {
+      for (size_t i = lo; i < hi; ++i)
+        if (pre[i - lo] == DICB200_OK) fail_field(fields[i], cs_);
+      return;
+    }
+    auto stage_pair = [&](size_t i, int* sa, int* sb) -> dicb200_status {
+      dicb200_status s = stage_frame(c, &images[pairs[2 * i]], pairs[2 * i], (long)i, -1, sa);
+      if (s != DICB200_OK) return s;
+      return stage_frame(c, &images[pairs[2 * i + 1]], pairs[2 * i + 1], (long)i, *sa, sb);
+    };
+    auto finalize = [&](RecSlot& r) {
+      if (r.pair < 0) return;
+      dicb200_field& f = fields[r.pair];
+      r.pair = -1;
+      cudaError_t e = cudaEventSynchronize(r.done);
+      if (e != cudaSuccess) {
+        fail_field(f, cuda_fail(e, "pair execution", __FILE__, __LINE__));
+        return;
+      }
+      if (r.staged) std::memcpy(f.records, r.stage, r.n * sizeof(dicb200_poi_record));
+      f.count = r.n;
+      f.status = DICB200_OK;
+    };
+    auto next_valid = [&](size_t i) {
+      while (i < hi && pre[i - lo] != DICB200_OK) ++i;
+      return i;
+    };
+    for (size_t i = next_valid(lo); i < hi; i = next_valid(i + 1)) {
+      dicb200_field& f = fields[i];
+      const size_t n = cnt[i - lo];
+      const size_t bytes = n * sizeof(dicb200_poi_record);
+      RecSlot& r = c->recs[i % kRecSlots];
+      finalize(r);
+      int sa = 0, sb = 0;
+      dicb200_status s = stage_pair(i, &sa, &sb);
+      cudaError_t e = cudaSuccess;
+      if (s == DICB200_OK) {
+        e = ensure(r.dev, bytes, c->cs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(c->cs, c->frames[sa].ready, 0);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(c->cs, c->frames[sb].ready, 0);
+        if (e != cudaSuccess) s = cuda_fail(e, "compute stream setup", __FILE__, __LINE__);
+      }
+      if (s == DICB200_OK)
+        s = enqueue_pair(&c->frames[sa].im, &c->frames[sb].im, cfg, i, lat[i - lo], 0, lat[i - lo].ny,
+                         (dicb200_poi_record*)r.dev.p, c->cs);
+      if (s == DICB200_OK) {
+        e = cudaEventRecord(c->frames[sa].idle, c->cs);
+        if (e == cudaSuccess) e = cudaEventRecord(c->frames[sb].idle, c->cs);
+        r.staged = !is_pinned(f.records);
+        void* dst = f.records;
+        if (e == cudaSuccess && r.staged) {
+          if (r.stage_cap < bytes) {
+            if (r.stage) cudaFreeHost(r.stage);
+            r.stage = nullptr;
+            r.stage_cap = 0;
+            e = cudaMallocHost(&r.stage, bytes);
+            if (e == cudaSuccess) r.stage_cap = bytes;
+          }
+          dst = r.stage;
+        }
+        // read-back on its own stream so the next pair's kernels start at once;
+        // r.dev is rewritten only after finalize(r) has seen r.done
+        if (e == cudaSuccess) e = cudaEventRecord(r.computed, c->cs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(c->ds, r.computed, 0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dst, r.dev.p, bytes, cudaMemcpyDeviceToHost, c->ds);
+        if (e == cudaSuccess) e = cudaEventRecord(r.done, c->ds);
+        if (e != cudaSuccess) s = cuda_fail(e, "record read-back", __FILE__, __LINE__);
+      }
+      if (s != DICB200_OK) {
+        fail_field(f, s);
+        continue;
+      }
+      r.pair = (long)i;
+      r.n = n;
+      // prefetch the next pair's frames, then retire the previous pair
+      const size_t j = next_valid(i + 1);
+      if (j < hi) {
+        int ja = 0, jb = 0;
+        stage_pair(j, &ja, &jb);  // an upload error resurfaces when pair j stages again
+      }
+      finalize(c->recs[(i + kRecSlots - 1) % kRecSlots]);
+    }
+    for (auto& r : c->recs) finalize(r);
+    const dicb200_status rs = release_context(c);
+    if (rs != DICB200_OK && result[wk] == DICB200_OK) {
+      result[wk] = rs;
+      errs[wk] = g_last_error;
     }
   };
   if (workers == 1) {
@@ -571,9 +816,15 @@ int dicb200_profile_read(double* ms, uint64_t* launches) {
 }
 
 void dicb200_shutdown(void) {
-  int n = dicb200_device_count();
   int cur = 0;
   cudaGetDevice(&cur);
+  std::vector<DeviceContext*> idle;
+  {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    idle.swap(g_ctx_idle);
+  }
+  for (DeviceContext* c : idle) destroy_context(c);
+  int n = dicb200_device_count();
   for (int d = 0; d < n; ++d) {
     cudaSetDevice(d);
     cudaMemPool_t pool;

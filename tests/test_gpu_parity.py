@@ -202,6 +202,28 @@ def test_analyze_sequence_policies_and_pair_errors(gpu, port):
     assert not fields[0].failed() and fields[1].error == "dimension mismatch"
 
 
+def test_analyze_sequence_pipeline_matches_pairwise(gpu):
+    """The pipelined sequence (frame slots reused across pairs, uploads ahead of
+    compute, read-back behind it) returns exactly what independent
+    analyze_pair calls return, for both policies and across an invalid pair."""
+    w = configs.crop(configs.c5(9), 160, 144)
+    frames = [f.render() for f in w.frames]
+    imgs = [dic.GrayImage(f, i) for i, f in enumerate(frames)]
+    imgs[5] = dic.GrayImage(np.zeros((64, 64), np.uint16), 5)  # pairs touching frame 5 fail
+    for policy in (dic.ReferencePolicy.fixed_first, dic.ReferencePolicy.update_every_pair):
+        cfg = copy.deepcopy(w.cfg)
+        cfg.reference_policy = policy
+        fields = dic.analyze_sequence(imgs, cfg)
+        for f, (ra, tb) in zip(fields, dic.sequence_pairs(policy, len(imgs))):
+            if 5 in (ra, tb):
+                assert f.error == "dimension mismatch" and len(f.records) == 0
+                continue
+            assert not f.failed()
+            exp = run_device(frames[ra], frames[tb], cfg, pair_index=f.pair_index)
+            for k in exp.dtype.names:
+                assert np.array_equal(f.records[k], exp[k], equal_nan=True), (policy, f.pair_index, k)
+
+
 def test_failure_semantics_degenerate_target(gpu, port):
     """Constant target regions: skipped candidates, 'all positions degenerate',
     refine failures keep the integer fields (pipeline.cpp:82-133)."""
