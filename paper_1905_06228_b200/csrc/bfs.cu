@@ -431,33 +431,6 @@ __global__ void __launch_bounds__(256, 3) bfs_tile_kernel(BfsParams p) {
   }
 }
 
-__device__ void write_integer_record(dicb200_poi_record& r, int x, int y, const BestPartial& b, int subpixel_none) {
-  r.x = x;
-  r.y = y;
-  r.iterations = 0;
-  r.update_evaluations = 0;
-  r.pad = 0;
-  if (!b.found) {  // "all positions degenerate" (integer_search.cpp:77): record keeps defaults
-    r.u = 0.0;
-    r.v = 0.0;
-    r.zncc = __longlong_as_double(0x7ff8000000000000ULL);
-    r.converged = 0;
-    r.evaluations = 0;
-    r.status = DICB200_POI_ALL_DEGENERATE;
-    r.integer_dx = 0;
-    r.integer_dy = 0;
-    return;
-  }
-  r.u = (double)b.dx;
-  r.v = (double)b.dy;
-  r.zncc = b.c;
-  r.evaluations = b.count;
-  r.converged = subpixel_none ? 1 : 0;
-  r.status = DICB200_POI_OK;
-  r.integer_dx = b.dx;
-  r.integer_dy = b.dy;
-}
-
 __global__ void bfs_reduce_kernel(BfsParams p, int n_subsets) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n_subsets) return;

@@ -24,8 +24,72 @@ struct BfsSmem {
 };
 
 __host__ __device__ BfsSmem bfs_smem_layout(const BfsParams& p);
-__device__ void write_integer_record(dicb200_poi_record& r, int x, int y, const BestPartial& b, int subpixel_none);
+__device__ inline void write_integer_record(dicb200_poi_record& r, int x, int y, const BestPartial& b, int subpixel_none) {
+  r.x = x;
+  r.y = y;
+  r.iterations = 0;
+  r.update_evaluations = 0;
+  r.pad = 0;
+  if (!b.found) {  // "all positions degenerate" (integer_search.cpp:77): record keeps defaults
+    r.u = 0.0;
+    r.v = 0.0;
+    r.zncc = __longlong_as_double(0x7ff8000000000000ULL);
+    r.converged = 0;
+    r.evaluations = 0;
+    r.status = DICB200_POI_ALL_DEGENERATE;
+    r.integer_dx = 0;
+    r.integer_dy = 0;
+    return;
+  }
+  r.u = (double)b.dx;
+  r.v = (double)b.dy;
+  r.zncc = b.c;
+  r.evaluations = b.count;
+  r.converged = subpixel_none ? 1 : 0;
+  r.status = DICB200_POI_OK;
+  r.integer_dx = b.dx;
+  r.integer_dy = b.dy;
+}
+
 bool bfs_plan(BfsParams& p, size_t smem_limit);
 cudaError_t bfs_launch(BfsParams& p, int rows, cudaStream_t st);
+
+// ---- K1 on the tensor cores (bfs_tc.cu) ----------------------------------
+// Window-mode search as an exact u8 x u8 -> s32 tcgen05 GEMM: M = 128 target
+// positions (16 x 8 subset top-left corners), N = the POIs (x byte planes of
+// the reference) whose windows touch them, K = the subset pixels. Wider pixels
+// are split into hi/lo byte planes and recombined exactly.
+struct TcParams {
+  ImageView ref, tgt;
+  Lattice lat;
+  int rb, re;  // POI rows [rb, re)
+  int M, R, side, planes, subpixel_none;
+  int qx_min, qx_max, qy_min, qy_max, SW, SH;  // position domain (subset top-left corners)
+  int ntx, nty, n_tiles;
+  int RG, CG, NX, HT, RWB, n_mma;  // K blocking: 8 rows x 4 columns per MMA
+  int nix_max, niy_max, npoi_max, N_max, tmem_cols;
+  size_t off_rows, off_B, stage_bytes, smem;  // stage = T | rows | B
+  int stages;
+  int grid;
+  long long* dbg_out;  // optional per-CTA MMA-thread clock breakdown (tools)
+  int dbg;  // DICB200_TC_DBG timing experiments (bit 0: no epilogue math, bit 1: no stage build)
+  // buffers (device)
+  uint8_t* bprep;        // [poi][n_mma][planes][32] reference bytes in MMA order
+  int64_t* poi_sf;       // [poi] sum f
+  double* poi_sqrtvf;    // [poi] sqrt(n Sff - Sf^2)
+  uint32_t* S1;          // [SH][SW] window sums of g
+  uint64_t* S2;          // [SH][SW] window sums of g^2
+  int64_t* sfg;          // [poi][2R+1][2R+1] exact cross terms from the tensor cores
+  void* tiles;           // [n_tiles] uint4: tx|ty<<16, ix_lo|iy_lo<<16, nix|niy<<16
+  double* surface;       // optional [poi][2R+1][2R+1]
+  dicb200_poi_record* rec;
+};
+
+// Plans the tensor-core search for POI rows [rb, re); false = not applicable
+// (whole-image domain, too many POIs per tile, shared memory).
+bool tc_plan(TcParams& p);
+// Enqueues stats, reference preparation, the tensor-core kernel and the
+// per-POI merge (or only the surface when p.surface is set) on `st`.
+cudaError_t tc_launch(TcParams& p, cudaStream_t st);
 
 }  // namespace dicb200

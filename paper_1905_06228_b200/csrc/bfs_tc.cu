@@ -1,0 +1,914 @@
+// K1 on the 5th-generation tensor cores: brute-force ZNCC search over a
+// +-R window (bfs_search, integer_search.cpp:52-79; zncc, correlation.cpp:41-72)
+// with every cross term Sfg computed EXACTLY by tcgen05.mma kind::i8
+// (u8 x u8 -> s32 in TMEM).
+//
+// GEMM view. A "position" q = (qx, qy) is the top-left corner of a target
+// subset. For a POI P with reference subset f_P and a position q,
+//   Sfg(P, q) = sum_{r,c} f_P[r][c] * g[qy + r][qx + c].
+// One tile = 128 positions (16 in x, 8 in y) = the MMA's M rows; the tile's N
+// columns are the POIs whose +-R windows touch it (x the reference byte
+// planes); K runs over the subset pixels in blocks of 8 rows x 4 columns.
+//
+// A operand (positions x K) without an im2col: the target rows are staged as
+// 16-pixel windows T[X][y][0..15] = g[Y0 + y][X0 + X + i]. An MN-major,
+// no-swizzle UMMA descriptor with SBO = 16 B (next M chunk = next row y) and
+// LBO = HT*16 B (next K group = next column offset X) then reads
+//   A[(mx, my)][(j, i)] = T[cg*4 + j][rg*8 + my + i][mx]
+//                       = g[Y0 + my + rg*8 + i][X0 + mx + cg*4 + j]
+// directly: the 8-row core matrices of neighbouring M chunks overlap.
+// B operand (K x N): the POIs' reference bytes pre-arranged in MMA order
+// (K-major, no swizzle), gathered per tile with cp.async.
+//
+// 16-bit pixels: g = 256 gh + gl, f = 256 fh + fl; A runs once per g plane
+// into its own accumulator, N holds both f planes, and
+//   Sfg = 65536 D[gh,fh] + 256 (D[gh,fl] + D[gl,fh]) + D[gl,fl]
+// (every partial < 2^31 for side <= 129). Sg and Sgg per position come from a
+// separate exact box-sum pass, Sf and Sff per POI from the preparation pass;
+// ZNCC and every decision are then formed exactly as in bfs.cu.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "bfs.cuh"
+#include "common.cuh"
+
+namespace dicb200 {
+
+namespace {
+
+constexpr int kTX = 16, kTY = 8;  // positions per tile: x, y (M = 128)
+constexpr int kMaxTilePoi = 128;  // per-tile POI limit (N <= 256 for byte planes)
+constexpr int kMaxStages = 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// UMMA shared-memory descriptor, SWIZZLE_NONE (16-byte units; version 1).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+
+// Instruction descriptor: kind::i8, D s32, A u8 MN-major, B u8 K-major, M = 128.
+__device__ __forceinline__ uint32_t idesc_i8(int n) {
+  return (2u << 4) | (1u << 15) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+// Issued by one elected lane of a converged warp (the warp keeps the loop
+// state in uniform registers).
+__device__ __forceinline__ void mma_i8_elect(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                             uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int sleep_ns = 0) {
+  uint32_t done = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) break;
+    if (sleep_ns) __nanosleep(sleep_ns);  // waiting roles yield issue slots to the MMA / working warps
+  }
+}
+
+// Warp-converged wait: the exit condition is warp-uniform (vote), so the
+// caller's loop state stays in uniform registers.
+__device__ __forceinline__ void mbar_wait_warp(uint32_t bar, uint32_t parity) {
+  while (true) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (__all_sync(0xffffffffu, done)) break;
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// int64 -> double without the XU conversion unit (exact for |x| < 2^51: the
+// value sits in the mantissa of 1.5 * 2^52 + x); wider values fall back.
+__device__ __forceinline__ double i64_to_f64(int64_t x) {
+  if (x >= -(1ll << 51) && x < (1ll << 51))
+    return __longlong_as_double(0x4338000000000000ll + x) - 6755399441055744.0;
+  return (double)x;
+}
+
+// Tiles of position space whose rectangle holds positions of P's window
+// (clipped to the launch domain). Empty when hi < lo.
+struct TileRange {
+  int tx_lo, tx_hi, ty_lo, ty_hi;
+};
+
+__host__ __device__ inline TileRange poi_tiles(const TcParams& p, int cx, int cy) {
+  TileRange t;
+  const int wx_lo = max(cx - p.M - p.R, p.qx_min), wx_hi = min(cx - p.M + p.R, p.qx_max);
+  const int wy_lo = max(cy - p.M - p.R, p.qy_min), wy_hi = min(cy - p.M + p.R, p.qy_max);
+  if (wx_lo > wx_hi || wy_lo > wy_hi) {
+    t.tx_lo = t.ty_lo = 0;
+    t.tx_hi = t.ty_hi = -1;
+    return t;
+  }
+  t.tx_lo = (wx_lo - p.qx_min) / kTX;
+  t.tx_hi = (wx_hi - p.qx_min) / kTX;
+  t.ty_lo = (wy_lo - p.qy_min) / kTY;
+  t.ty_hi = (wy_hi - p.qy_min) / kTY;
+  return t;
+}
+
+// POIs (lattice index ranges) whose windows intersect the tile rectangle.
+__host__ __device__ inline void tile_pois(const TcParams& p, int X0, int Y0, int& ix_lo, int& nix, int& iy_lo,
+                                          int& niy) {
+  auto ceil_div = [](int a, int b) { return a >= 0 ? (a + b - 1) / b : -((-a) / b); };
+  auto floor_div = [](int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
+  const int s = p.lat.step;
+  int lo = ceil_div(X0 + p.M - p.R - p.lat.x0, s), hi = floor_div(X0 + kTX - 1 + p.M + p.R - p.lat.x0, s);
+  lo = max(lo, 0);
+  hi = min(hi, p.lat.nx - 1);
+  ix_lo = lo;
+  nix = max(0, hi - lo + 1);
+  lo = ceil_div(Y0 + p.M - p.R - p.lat.y0, s);
+  hi = floor_div(Y0 + kTY - 1 + p.M + p.R - p.lat.y0, s);
+  lo = max(lo, p.rb);
+  hi = min(hi, p.re - 1);
+  iy_lo = lo;
+  niy = max(0, hi - lo + 1);
+}
+
+// ---- exact window sums of g and g^2 at every position of the domain ----
+template <typename Pix>
+__global__ void __launch_bounds__(256) tc_stats_kernel(TcParams p) {
+  constexpr int BX = 64, BY = 32;
+  extern __shared__ __align__(1024) unsigned char stats_smem[];
+  const int side = p.side, CW = BX + side - 1;
+  uint32_t* c1 = reinterpret_cast<uint32_t*>(stats_smem);
+  uint64_t* c2 = reinterpret_cast<uint64_t*>(stats_smem + (((size_t)BY * CW * 4 + 15) & ~size_t(15)));
+  const int sx0 = blockIdx.x * BX, sy0 = blockIdx.y * BY;
+  const int rows = min(BY, p.SH - sy0), cols = min(BX, p.SW - sx0);
+  const Pix* img = reinterpret_cast<const Pix*>(p.tgt.data);
+  const int pitch = p.tgt.pitch, gy0 = p.qy_min + sy0;
+  for (int x = threadIdx.x; x < CW; x += blockDim.x) {
+    const int gx = p.qx_min + sx0 + x;
+    if (gx >= p.tgt.width) {  // only feeds positions past the domain
+      for (int t = 0; t < rows; ++t) {
+        c1[t * CW + x] = 0;
+        c2[t * CW + x] = 0;
+      }
+      continue;
+    }
+    uint32_t s1 = 0;
+    uint64_t s2 = 0;
+    for (int r = 0; r < side; ++r) {
+      const uint32_t v = img[(size_t)(gy0 + r) * pitch + gx];
+      s1 += v;
+      s2 += (uint64_t)v * v;
+    }
+    c1[x] = s1;
+    c2[x] = s2;
+    for (int t = 1; t < rows; ++t) {
+      const uint32_t a = img[(size_t)(gy0 + t + side - 1) * pitch + gx], b = img[(size_t)(gy0 + t - 1) * pitch + gx];
+      s1 += a - b;
+      s2 += (uint64_t)a * a - (uint64_t)b * b;
+      c1[t * CW + x] = s1;
+      c2[t * CW + x] = s2;
+    }
+  }
+  __syncthreads();
+  constexpr int SEG = 16;
+  const int nseg = (cols + SEG - 1) / SEG;
+  for (int item = threadIdx.x; item < rows * nseg; item += blockDim.x) {
+    const int t = item / nseg, x0 = (item % nseg) * SEG, x1 = min(cols, x0 + SEG);
+    const uint32_t* r1 = c1 + t * CW;
+    const uint64_t* r2 = c2 + t * CW;
+    uint32_t s1 = 0;
+    uint64_t s2 = 0;
+    for (int c = 0; c < side; ++c) {
+      s1 += r1[x0 + c];
+      s2 += r2[x0 + c];
+    }
+    const size_t o = (size_t)(sy0 + t) * p.SW + sx0;
+    p.S1[o + x0] = s1;
+    p.S2[o + x0] = s2;
+    for (int x = x0 + 1; x < x1; ++x) {
+      s1 += r1[x + side - 1] - r1[x - 1];
+      s2 += r2[x + side - 1] - r2[x - 1];
+      p.S1[o + x] = s1;
+      p.S2[o + x] = s2;
+    }
+  }
+}
+
+// ---- per POI: exact reference moments + reference bytes in MMA order ----
+template <typename Pix>
+__global__ void __launch_bounds__(256) tc_prep_kernel(TcParams p) {
+  const int warp = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  const int npoi = (p.re - p.rb) * p.lat.nx;
+  if (warp >= npoi) return;
+  const int iy = p.rb + warp / p.lat.nx, ix = warp % p.lat.nx;
+  const int cx = p.lat.cx(ix), cy = p.lat.cy(iy), M = p.M, side = p.side;
+  const int pitch = p.ref.pitch;
+  const Pix* base = reinterpret_cast<const Pix*>(p.ref.data) + (size_t)(cy - M) * pitch + (cx - M);
+  uint64_t sf = 0, sff = 0;
+  for (int k = lane; k < side * side; k += 32) {
+    const int r = k / side, c = k - r * side;
+    const uint64_t v = base[(size_t)r * pitch + c];
+    sf += v;
+    sff += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sf += __shfl_xor_sync(0xffffffffu, sf, o);
+    sff += __shfl_xor_sync(0xffffffffu, sff, o);
+  }
+  if (lane == 0) {
+    const int64_t n = (int64_t)side * side;
+    const int64_t vf = n * (int64_t)sff - (int64_t)sf * (int64_t)sf;
+    p.poi_sf[warp] = (int64_t)sf;
+    p.poi_sqrtvf[warp] = vf > 0 ? sqrt((double)vf) : 0.0;
+  }
+  const int planes = p.planes;
+  uint8_t* dst = p.bprep + (size_t)warp * p.n_mma * planes * 32;
+  for (int item = lane; item < p.n_mma * planes; item += 32) {
+    const int mma = item / planes, plane = item - mma * planes;
+    const int rg = mma / p.CG, cg = mma - rg * p.CG;
+    const int shift = (planes == 2 && plane == 0) ? 8 : 0;
+    uint32_t w[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int k = 4 * q + e, j = k >> 3, i = k & 7;  // k = j*8 + i <-> column cg*4+j, row rg*8+i
+        const int r = rg * 8 + i, c = cg * 4 + j;
+        uint32_t v = 0;
+        if (r < side && c < side) v = ((uint32_t)base[(size_t)r * pitch + c] >> shift) & 0xffu;
+        word |= v << (8 * e);
+      }
+      w[q] = word;
+    }
+    uint4* d = reinterpret_cast<uint4*>(dst + (size_t)item * 32);
+    d[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    d[1] = make_uint4(w[4], w[5], w[6], w[7]);
+  }
+}
+
+// ---- per tile: position tile coordinates and the POI rectangle it serves ----
+__global__ void tc_tiles_kernel(TcParams p) {
+  const int tile = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tile >= p.n_tiles) return;
+  const int tx = tile % p.ntx, ty = tile / p.ntx;
+  int ix_lo, nix, iy_lo, niy;
+  tile_pois(p, p.qx_min + kTX * tx, p.qy_min + kTY * ty, ix_lo, nix, iy_lo, niy);
+  reinterpret_cast<uint4*>(p.tiles)[tile] =
+      make_uint4((uint32_t)tx | ((uint32_t)ty << 16), (uint32_t)ix_lo | ((uint32_t)iy_lo << 16),
+                 (uint32_t)nix | ((uint32_t)niy << 16), 0u);
+}
+
+// ---- the tensor-core kernel: persistent, warp-specialised ----
+//   warps 0-3 : producers — per K stage (8 subset rows): target rows -> byte
+//               planes -> 16-pixel windows (A), reference bytes (B, cp.async)
+//   warp  4   : one thread issues the tcgen05.mma stream
+//   warps 5-8 : epilogue — TMEM -> exact moments -> ZNCC -> per-POI argmax
+// Stages form a ring (full/empty mbarriers); the two TMEM accumulators let the
+// epilogue of tile t overlap the MMAs of tile t+1.
+constexpr int kGroups = 4, kGroupThreads = 64;  // producer groups = ring slots
+constexpr int kProducerWarps = kGroups * kGroupThreads / 32;
+constexpr int kProducers = kGroups * kGroupThreads, kEpilogue = 256;
+constexpr int kTcThreads = kProducers + 32 + kEpilogue;
+constexpr int kStageRows = 16;  // T rows per stage: 8 positions + 8 subset rows - 1, rounded
+
+struct TileInfo {
+  int tx, ty, X0, Y0, ix_lo, nix, iy_lo, niy, npoi, N;
+};
+
+template <int PLANES>
+__device__ __forceinline__ bool tile_info(const TcParams& p, int tile, TileInfo& t) {
+  const uint4 q = __ldg(reinterpret_cast<const uint4*>(p.tiles) + tile);  // tc_tiles_kernel
+  t.tx = (int)(q.x & 0xffffu);
+  t.ty = (int)(q.x >> 16);
+  t.X0 = p.qx_min + kTX * t.tx;
+  t.Y0 = p.qy_min + kTY * t.ty;
+  t.ix_lo = (int)(q.y & 0xffffu);
+  t.iy_lo = (int)(q.y >> 16);
+  t.nix = (int)(q.z & 0xffffu);
+  t.niy = (int)(q.z >> 16);
+  t.npoi = t.nix * t.niy;
+  t.N = max(16, ((t.npoi * PLANES + 15) / 16) * 16);
+  return t.npoi > 0;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+
+template <int PLANES>
+__global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ int prod_poi[kGroups * kMaxTilePoi];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int S = kGroups;  // ring slots: one per producer group
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
+                 "r"(p.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 32) {
+    for (int s = 0; s < kGroups; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&full_bar[s])), "r"(kGroupThreads));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&empty_bar[s])));
+    }
+    for (int a = 0; a < 2; ++a) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&tfull_bar[a])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&tempty_bar[a])), "r"(kEpilogue));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = tmem_base;
+  const int NX = p.NX, RWB = p.RWB, CG = p.CG;
+  const size_t planeT = (size_t)NX * kStageRows * 16;
+
+  if ((p.dbg & 256) && warp != kProducerWarps) {
+    // timing experiment: MMA issuer alone
+  } else if (warp < kProducerWarps) {
+    // ================= producers =================
+    // group g (2 warps) owns ring slot g and builds every stage it with it % S == g,
+    // so S stages (and their global-load latencies) are in flight at once.
+    const int g = warp >> 1, gt = tid & 63;
+    const auto* img = reinterpret_cast<const uint8_t*>(p.tgt.data);
+    const int W = p.tgt.width, H = p.tgt.height, pitch = p.tgt.pitch;
+    const size_t poi_stride = (size_t)p.n_mma * PLANES * 32;
+    const int RW4 = (NX + 15 + 3) / 4;  // words per staged row
+    int* poi_tab = prod_poi + g * kMaxTilePoi;
+    uint32_t ph = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+      TileInfo t;
+      if (!tile_info<PLANES>(p, tile, t)) continue;
+      const int first = (g - it % kGroups + kGroups) % kGroups;  // this group's first stage of the tile
+      it += p.RG;
+      if (first >= p.RG) continue;
+      named_sync(1 + g, kGroupThreads);  // previous tile's readers of poi_tab are done
+      for (int j = gt; j < t.npoi; j += kGroupThreads) {
+        const int jy = j / t.nix, jx = j - jy * t.nix;
+        poi_tab[j] = (t.iy_lo + jy - p.rb) * p.lat.nx + (t.ix_lo + jx);
+      }
+      named_sync(1 + g, kGroupThreads);
+      const int NN = t.npoi * PLANES;
+      unsigned char* base = sm + (size_t)g * p.stage_bytes;
+      uint8_t* T = base;
+      uint32_t* rows = reinterpret_cast<uint32_t*>(base + p.off_rows);
+      uint8_t* Bs = base + p.off_B;
+      for (int rg = first; rg < p.RG; rg += kGroups) {
+        if (!(p.dbg & 16)) mbar_wait(smem_u32(&empty_bar[g]), ph ^ 1u, (p.dbg & 128) ? 2000 : 64);
+        if (p.dbg & 2) {  // timing experiment: no stage build
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          mbar_arrive(smem_u32(&full_bar[g]));
+          ph ^= 1u;
+          continue;
+        }
+        // (a) B: one thread per (POI plane, K half) column, all CG MMA blocks of the stage
+        for (int e = gt; e < NN * 2; e += kGroupThreads) {
+          const int nn = e >> 1, kh = e & 1;
+          const int j = nn / PLANES, pl = nn - j * PLANES;
+          const uint8_t* src = p.bprep + (size_t)poi_tab[j] * poi_stride + ((size_t)rg * CG * PLANES + pl) * 32 + kh * 16;
+          uint8_t* dst = Bs + (nn & 7) * 16 + (nn >> 3) * 256 + kh * 128;
+          for (int cg = 0; cg < CG; ++cg) cp_async16(dst + (size_t)cg * t.N * 32, src + (size_t)cg * PLANES * 32);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        // (b) target rows [Y0 + 8 rg, +16) x [X0, X0 + 4 RW4): 4 pixels -> one word per byte plane
+        {
+          const int gy0 = t.Y0 + rg * 8;
+          for (int w = gt & 15; w < RW4; w += 16) {
+            const int gx0 = t.X0 + 4 * w;
+            uint32_t v[4][4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int gy = gy0 + (gt >> 4) + 4 * k;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int gx = gx0 + i;
+                v[k][i] = 0;
+                if (gy < H && gx < W) {
+                  if (PLANES == 1)
+                    v[k][i] = __ldg(img + (size_t)gy * pitch + gx);
+                  else
+                    v[k][i] = __ldg(reinterpret_cast<const uint16_t*>(img) + (size_t)gy * pitch + gx);
+                }
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int y = (gt >> 4) + 4 * k;
+              if (PLANES == 1) {
+                rows[y * (RWB / 4) + w] = v[k][0] | (v[k][1] << 8) | (v[k][2] << 16) | (v[k][3] << 24);
+              } else {
+                rows[y * (RWB / 4) + w] = __byte_perm(v[k][0], v[k][1], 0x7751) | (__byte_perm(v[k][2], v[k][3], 0x5177) & 0xffff0000u);
+                rows[(kStageRows + y) * (RWB / 4) + w] =
+                    __byte_perm(v[k][0], v[k][1], 0x7740) | (__byte_perm(v[k][2], v[k][3], 0x4077) & 0xffff0000u);
+              }
+            }
+          }
+        }
+        named_sync(1 + g, kGroupThreads);
+        // (c) 16-pixel windows, four column offsets per item:
+        //     T[pl][X][y][0..15] = rows[pl][y][X .. X+15], X = 4 X4 + s
+        {
+          const int y = gt & 15;
+          for (int pl = 0; pl < PLANES; ++pl) {
+            const uint32_t* rw = rows + (size_t)(pl * kStageRows + y) * (RWB / 4);
+            for (int X4 = gt >> 4; X4 < CG; X4 += kGroupThreads / 16) {
+              const uint32_t a0 = rw[X4], a1 = rw[X4 + 1], a2 = rw[X4 + 2], a3 = rw[X4 + 3], a4 = rw[X4 + 4];
+              uint8_t* dst = T + pl * planeT + ((size_t)(4 * X4) * kStageRows + y) * 16;
+#pragma unroll
+              for (int s = 0; s < 4; ++s) {
+                uint4 o;
+                o.x = __funnelshift_r(a0, a1, 8 * s);
+                o.y = __funnelshift_r(a1, a2, 8 * s);
+                o.z = __funnelshift_r(a2, a3, 8 * s);
+                o.w = __funnelshift_r(a3, a4, 8 * s);
+                *reinterpret_cast<uint4*>(dst + s * kStageRows * 16) = o;
+              }
+            }
+          }
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_arrive(smem_u32(&full_bar[g]));
+        ph ^= 1u;
+        named_sync(1 + g, kGroupThreads);  // rows of this slot are rewritten next round
+      }
+    }
+  } else if (warp == kProducerWarps) {
+    // ================= MMA issuer =================
+    // The whole warp runs the loop (descriptors stay in uniform registers);
+    // one elected lane issues each tcgen05.mma / commit.
+    {
+      int it = 0, tc = 0;
+      long long w_full = 0, w_empty = 0, t_issue = 0, t0 = clock64();
+      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+        TileInfo t;
+        if (!tile_info<PLANES>(p, tile, t)) continue;
+        const int a = tc & 1;
+        const uint32_t aph = (uint32_t)(tc >> 1) & 1u;
+        long long c0 = clock64();
+        if (!(p.dbg & 256)) mbar_wait_warp(smem_u32(&tempty_bar[a]), aph ^ 1u);
+        w_empty += clock64() - c0;
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t d0 = tmem + (uint32_t)(a * PLANES * p.N_max);
+        const uint32_t d1 = d0 + (uint32_t)t.N;
+        const uint32_t idesc = idesc_i8((p.dbg & 8) ? 16 : t.N);
+        const uint32_t b_step = (uint32_t)t.N * 2u;  // B block per cg, 16-byte units
+        for (int rg = 0; rg < p.RG; ++rg, ++it) {
+          const int s = it % S;
+          const uint32_t ph = (uint32_t)(it / S) & 1u;
+          long long c1 = clock64();
+          if (!(p.dbg & 256)) mbar_wait_warp(smem_u32(&full_bar[s]), ph);
+          long long c2 = clock64();
+          w_full += c2 - c1;
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const uint32_t base = smem_u32(sm + (size_t)s * p.stage_bytes);
+          uint64_t da = sdesc(base, kStageRows * 16, 16);
+          uint64_t db = sdesc(base + (uint32_t)p.off_B, 128, 256);
+          const uint64_t da_plane = (uint64_t)(uint32_t)(planeT >> 4);
+          for (int cg = 0; cg < CG; ++cg) {
+            const uint32_t acc = (rg | cg) != 0;
+            if (!(p.dbg & 2048)) {
+              mma_i8_elect(d0, da, db, idesc, acc);
+              if (PLANES == 2 && !(p.dbg & 4)) mma_i8_elect(d1, da + da_plane, db, idesc, acc);
+            }
+            da += (uint64_t)(4 * kStageRows);
+            db += (uint64_t)b_step;
+          }
+          umma_commit_elect(smem_u32(&empty_bar[s]));
+          t_issue += clock64() - c2;
+        }
+        umma_commit_elect(smem_u32(&tfull_bar[a]));
+        ++tc;
+      }
+      if (p.dbg_out && lane == 0) {
+        p.dbg_out[blockIdx.x * 4 + 0] = clock64() - t0;
+        p.dbg_out[blockIdx.x * 4 + 1] = w_full;
+        p.dbg_out[blockIdx.x * 4 + 2] = w_empty;
+        p.dbg_out[blockIdx.x * 4 + 3] = t_issue;
+      }
+    }
+  } else if (warp >= kProducerWarps + 1) {
+    // ================= epilogue =================
+    // thread = position (TMEM lane quadrant = warp % 4; the two warps of a
+    // quadrant split the POI column groups): the exact cross terms Sfg of every
+    // in-window position go to sfg[poi][dy + R][dx + R]; ZNCC and the argmax run
+    // in tc_argmax_kernel / tc_surface_kernel.
+    const int quad = warp & 3, half = (warp - kProducerWarps - 1) >> 2;
+    const int m = quad * 32 + lane, mx = m & 15, my = m >> 4;
+    const int R = p.R, EW = 2 * R + 1;
+    constexpr int PER = 8 / PLANES;  // POIs per 8 accumulator columns
+    int tc = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+      TileInfo t;
+      if (!tile_info<PLANES>(p, tile, t)) continue;
+      const int a = tc & 1;
+      const uint32_t aph = (uint32_t)(tc >> 1) & 1u;
+      ++tc;
+      const int qx = t.X0 + mx, qy = t.Y0 + my;
+      const bool in_domain = qx <= p.qx_max && qy <= p.qy_max;
+      const int rx = qx + p.M - t.ix_lo * p.lat.step - p.lat.x0;  // dx = rx - jx * step
+      const int ry = qy + p.M - t.iy_lo * p.lat.step - p.lat.y0;
+      const int ngroups = (t.npoi + PER - 1) / PER;
+      int jy = 0, jx = half * PER;  // lattice offsets of POI gi * PER
+      while (jx >= t.nix) {
+        jx -= t.nix;
+        ++jy;
+      }
+      mbar_wait(smem_u32(&tfull_bar[a]), aph, 64);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t tl = tmem + (uint32_t)(a * PLANES * p.N_max) + ((uint32_t)(quad * 32) << 16);
+      for (int gi = half; gi < ngroups; gi += 2) {
+        const int j0 = gi * PER;
+        uint32_t d0[8], d1[8];
+        tmem_ld8(tl + (uint32_t)(j0 * PLANES), d0);
+        if (PLANES == 2) tmem_ld8(tl + (uint32_t)(t.N + j0 * PLANES), d1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        int ux = jx, uy = jy;
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int dx = rx - ux * p.lat.step, dy = ry - uy * p.lat.step;
+          if (j0 + u < t.npoi && in_domain && dx >= -R && dx <= R && dy >= -R && dy <= R) {
+            int64_t sfg;
+            if (PLANES == 1)
+              sfg = (int64_t)d0[u];
+            else
+              sfg = 65536ll * (int64_t)d0[2 * u] + 256ll * ((int64_t)d0[2 * u + 1] + (int64_t)d1[2 * u]) +
+                    (int64_t)d1[2 * u + 1];
+            const size_t poi = (size_t)(t.iy_lo + uy - p.rb) * p.lat.nx + (t.ix_lo + ux);
+            p.sfg[poi * EW * EW + (size_t)(dy + R) * EW + (dx + R)] = sfg;
+          }
+          if (++ux == t.nix) {
+            ux = 0;
+            ++uy;
+          }
+        }
+        jx += 2 * PER;
+        while (jx >= t.nix) {
+          jx -= t.nix;
+          ++jy;
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      mbar_arrive(smem_u32(&tempty_bar[a]));
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(p.tmem_cols));
+}
+
+// One candidate's exact moments from the tensor-core cross term and the exact
+// window sums (as zncc_from_moments, common.cuh); false = degenerate window.
+struct Cand {
+  int64_t num, vg;
+};
+
+__device__ __forceinline__ bool tc_candidate(const TcParams& p, int64_t n, int64_t sf, int64_t sfg, int qx, int qy,
+                                             Cand& c) {
+  const size_t o = (size_t)(qy - p.qy_min) * p.SW + (qx - p.qx_min);
+  const int64_t sg = p.S1[o], sgg = (int64_t)p.S2[o];
+  c.vg = n * sgg - sg * sg;
+  c.num = n * sfg - sf * sg;
+  return c.vg > 0;  // constant target window: skipped, not counted
+}
+
+// ---- per POI: count, exact argmax in improves() order -> record ----
+// Pass 1 finds the maximum of a cheap quotient num * (1/sqrt(vf)) * rsqrt(vg)
+// (relative error a few ulp, i.e. < 2^-48 absolute as |zncc| <= 1); pass 2 forms
+// the EXACT IEEE quotient num / (sqrt(vf) sqrt(vg)) only for candidates within
+// 2^-40 of it, so the winner and its value are exactly those of the sequential
+// reference loop. Warp per POI, lanes across the window columns.
+__global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p) {
+  const int k = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  const int npoi = (p.re - p.rb) * p.lat.nx;
+  if (k >= npoi) return;
+  const int iy = p.rb + k / p.lat.nx, ix = k % p.lat.nx;
+  const int cx = p.lat.cx(ix), cy = p.lat.cy(iy), M = p.M, R = p.R, EW = 2 * R + 1;
+  const int64_t n = (int64_t)p.side * p.side;
+  const int fx_lo = max(-R, M - cx), fx_hi = min(R, p.tgt.width - 1 - M - cx);   // integer_search.cpp:11-21
+  const int fy_lo = max(-R, M - cy), fy_hi = min(R, p.tgt.height - 1 - M - cy);
+  const int64_t sf = p.poi_sf[k];
+  const double svf = p.poi_sqrtvf[k];
+  BestPartial b;
+  b.c = -2.0;
+  b.dx = b.dy = 0;
+  b.count = 0;
+  b.found = 0;
+  if (fx_lo <= fx_hi && fy_lo <= fy_hi && svf > 0.0) {
+    const int64_t* buf = p.sfg + (size_t)k * EW * EW;
+    const double rsvf = 1.0 / svf;
+    int cnt = 0;
+    double amax = -3.0;
+    for (int dy = fy_lo; dy <= fy_hi; ++dy)
+      for (int dx = fx_lo + lane; dx <= fx_hi; dx += 32) {
+        Cand c;
+        if (tc_candidate(p, n, sf, buf[(dy + R) * EW + (dx + R)], cx - M + dx, cy - M + dy, c)) {
+          ++cnt;
+          amax = fmax(amax, i64_to_f64(c.num) * rsvf * rsqrt(i64_to_f64(c.vg)));
+        }
+      }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    }
+    const double thr = amax - 0x1p-40;
+    for (int dy = fy_lo; dy <= fy_hi; ++dy)
+      for (int dx = fx_lo + lane; dx <= fx_hi; dx += 32) {
+        Cand c;
+        if (tc_candidate(p, n, sf, buf[(dy + R) * EW + (dx + R)], cx - M + dx, cy - M + dy, c)) {
+          const double nd = i64_to_f64(c.num), vd = i64_to_f64(c.vg);
+          if (nd * rsvf * rsqrt(vd) >= thr) {
+            const double z = nd / (svf * sqrt(vd));  // exact IEEE quotient (zncc_from_moments)
+            if (!b.found || improves(z, dx, dy, b.c, b.dx, b.dy)) {
+              b.found = 1;
+              b.c = z;
+              b.dx = dx;
+              b.dy = dy;
+            }
+          }
+        }
+      }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      BestPartial q;
+      q.c = __shfl_xor_sync(0xffffffffu, b.c, o);
+      q.dx = __shfl_xor_sync(0xffffffffu, b.dx, o);
+      q.dy = __shfl_xor_sync(0xffffffffu, b.dy, o);
+      q.count = 0;
+      q.found = __shfl_xor_sync(0xffffffffu, b.found, o);
+      merge_best(b, q);
+    }
+    b.count = cnt;
+  }
+  if (lane == 0) write_integer_record(p.rec[k], cx, cy, b, p.subpixel_none);
+}
+
+// ---- per POI: the full exact ZNCC surface over the +-R window (NaN = no result) ----
+__global__ void __launch_bounds__(256) tc_surface_kernel(TcParams p) {
+  const int k = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  const int npoi = (p.re - p.rb) * p.lat.nx;
+  if (k >= npoi) return;
+  const int iy = p.rb + k / p.lat.nx, ix = k % p.lat.nx;
+  const int cx = p.lat.cx(ix), cy = p.lat.cy(iy), M = p.M, R = p.R, EW = 2 * R + 1;
+  const int64_t n = (int64_t)p.side * p.side;
+  const int fx_lo = max(-R, M - cx), fx_hi = min(R, p.tgt.width - 1 - M - cx);
+  const int fy_lo = max(-R, M - cy), fy_hi = min(R, p.tgt.height - 1 - M - cy);
+  const int64_t sf = p.poi_sf[k];
+  const double svf = p.poi_sqrtvf[k];
+  const int64_t* buf = p.sfg + (size_t)k * EW * EW;
+  double* out = p.surface + (size_t)k * EW * EW;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ULL);
+  for (int idx = lane; idx < EW * EW; idx += 32) {
+    const int ry = idx / EW, dx = idx - ry * EW - R, dy = ry - R;
+    double z = qnan;
+    Cand c;
+    if (svf > 0.0 && dx >= fx_lo && dx <= fx_hi && dy >= fy_lo && dy <= fy_hi &&
+        tc_candidate(p, n, sf, buf[idx], cx - M + dx, cy - M + dy, c))
+      z = i64_to_f64(c.num) / (svf * sqrt(i64_to_f64(c.vg)));  // exact, as bfs.cu
+    out[idx] = z;
+  }
+}
+
+template <typename K>
+cudaError_t set_smem(K kern, size_t bytes) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace
+
+bool tc_plan(TcParams& p) {
+  if (std::getenv("DICB200_BFS_LEGACY")) return false;  // A/B switch: CUDA-core kernel
+  p.dbg = std::getenv("DICB200_TC_DBG") ? std::atoi(std::getenv("DICB200_TC_DBG")) : 0;  // timing experiments only
+  if (p.R < 0 || p.M < 0) return false;
+  p.side = 2 * p.M + 1;
+  if (p.side > 129) return false;
+  const int side = p.side, W = p.tgt.width, H = p.tgt.height;
+  const int rows = p.re - p.rb;
+  if (rows <= 0 || p.lat.nx <= 0) return false;
+  p.qx_min = std::max(0, p.lat.cx(0) - p.M - p.R);
+  p.qx_max = std::min(W - side, p.lat.cx(p.lat.nx - 1) - p.M + p.R);
+  p.qy_min = std::max(0, p.lat.cy(p.rb) - p.M - p.R);
+  p.qy_max = std::min(H - side, p.lat.cy(p.re - 1) - p.M + p.R);
+  if (p.qx_min > p.qx_max || p.qy_min > p.qy_max) {
+    p.SW = p.SH = p.ntx = p.nty = p.n_tiles = 0;
+  } else {
+    p.SW = p.qx_max - p.qx_min + 1;
+    p.SH = p.qy_max - p.qy_min + 1;
+    p.ntx = (p.SW + kTX - 1) / kTX;
+    p.nty = (p.SH + kTY - 1) / kTY;
+    p.n_tiles = p.ntx * p.nty;
+  }
+  p.RG = (side + 7) / 8;
+  p.CG = (side + 3) / 4;
+  p.NX = 4 * p.CG;
+  p.HT = 16;
+  int rwb = ((p.NX + 16 + 3) / 4) * 4 + 4;  // +1 word for the funnel shift reads
+  if (((rwb / 4) & 1) == 0) rwb += 4;      // odd word pitch
+  p.RWB = rwb;
+  p.n_mma = p.RG * p.CG;
+  const int s = p.lat.step;
+  p.nix_max = std::min(p.lat.nx, (kTX - 1 + 2 * p.R) / s + 1);
+  p.niy_max = std::min(rows, (kTY - 1 + 2 * p.R) / s + 1);
+  p.npoi_max = p.nix_max * p.niy_max;
+  if (p.npoi_max > kMaxTilePoi) return false;
+  p.N_max = std::max(16, ((p.npoi_max * p.planes + 15) / 16) * 16);
+  if (p.N_max > 256) return false;
+  int cols = 32;
+  while (cols < 2 * p.planes * p.N_max) cols *= 2;  // two accumulators
+  if (cols > 512) return false;
+  p.tmem_cols = cols;
+  // shared memory: a ring of K stages (T | rows | B), one per producer group
+  auto al = [](size_t v, size_t a) { return (v + a - 1) & ~(a - 1); };
+  p.off_rows = al((size_t)p.planes * p.NX * 16 * 16, 128);
+  p.off_B = al(p.off_rows + (size_t)p.planes * 16 * p.RWB, 128);
+  p.stage_bytes = al(p.off_B + (size_t)p.CG * p.N_max * 32, 1024);
+  p.stages = kGroups;
+  p.smem = (size_t)p.stages * p.stage_bytes;
+  if (p.smem > 220 * 1024) return false;
+  // cross-term buffer: one window per POI of the launch
+  const size_t EW = 2 * (size_t)p.R + 1;
+  if ((size_t)rows * p.lat.nx * EW * EW * 8 > ((size_t)3 << 30)) return false;
+  p.grid = std::max(1, std::min(p.n_tiles, sm_count()));
+  return true;
+}
+
+cudaError_t tc_launch(TcParams& p, cudaStream_t st) {
+  const int rows = p.re - p.rb;
+  const size_t npoi = (size_t)rows * p.lat.nx;
+  cudaError_t e = cudaSuccess;
+  void *bprep = nullptr, *psf = nullptr, *pvf = nullptr, *s1 = nullptr, *s2 = nullptr, *part = nullptr,
+       *tiles = nullptr;
+  auto cleanup = [&]() {
+    for (void* q : {bprep, psf, pvf, s1, s2, part, tiles})
+      if (q) cudaFreeAsync(q, st);
+  };
+  const size_t sbytes = (size_t)std::max(1, p.SW) * std::max(1, p.SH);
+  e = cudaMallocAsync(&bprep, npoi * p.n_mma * p.planes * 32, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&psf, npoi * 8, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&pvf, npoi * 8, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&s1, sbytes * 4, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&s2, sbytes * 8, st);
+  const size_t EW = 2 * (size_t)p.R + 1;
+  if (e == cudaSuccess) e = cudaMallocAsync(&part, npoi * EW * EW * sizeof(int64_t), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&tiles, (size_t)std::max(1, p.n_tiles) * 16, st);
+  if (e != cudaSuccess) {
+    cleanup();
+    return e;
+  }
+  p.bprep = (uint8_t*)bprep;
+  p.poi_sf = (int64_t*)psf;
+  p.poi_sqrtvf = (double*)pvf;
+  p.S1 = (uint32_t*)s1;
+  p.S2 = (uint64_t*)s2;
+  p.sfg = (int64_t*)part;
+  p.tiles = tiles;
+  const bool u8 = p.planes == 1;
+  // (a) window sums of the target
+  if (e == cudaSuccess && p.n_tiles > 0) {
+    const int CW = 64 + p.side - 1;
+    const size_t sm = (((size_t)32 * CW * 4 + 15) & ~size_t(15)) + (size_t)32 * CW * 8;
+    dim3 grid((p.SW + 63) / 64, (p.SH + 31) / 32);
+    if (u8) {
+      e = set_smem(tc_stats_kernel<uint8_t>, sm);
+      if (e == cudaSuccess) tc_stats_kernel<uint8_t><<<grid, 256, sm, st>>>(p);
+    } else {
+      e = set_smem(tc_stats_kernel<uint16_t>, sm);
+      if (e == cudaSuccess) tc_stats_kernel<uint16_t><<<grid, 256, sm, st>>>(p);
+    }
+    count_launch();
+    if (e == cudaSuccess) e = cudaGetLastError();
+  }
+  // (b) reference moments + MMA-ordered bytes
+  if (e == cudaSuccess) {
+    const int blocks = (int)((npoi * 32 + 255) / 256);
+    if (u8)
+      tc_prep_kernel<uint8_t><<<blocks, 256, 0, st>>>(p);
+    else
+      tc_prep_kernel<uint16_t><<<blocks, 256, 0, st>>>(p);
+    count_launch();
+    e = cudaGetLastError();
+  }
+  // (c) tensor-core search
+  if (e == cudaSuccess && p.n_tiles > 0) {
+    tc_tiles_kernel<<<(p.n_tiles + 255) / 256, 256, 0, st>>>(p);
+    count_launch();
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess && p.n_tiles > 0) {
+    long long* dbg_buf = nullptr;
+    if (p.dbg & 32) {  // tools: MMA-thread clock breakdown
+      cudaMalloc(&dbg_buf, (size_t)p.grid * 8 * sizeof(long long));
+      cudaMemsetAsync(dbg_buf, 0, (size_t)p.grid * 8 * sizeof(long long), st);
+      p.dbg_out = dbg_buf;
+    }
+    if (u8) {
+      e = set_smem(bfs_tc_kernel<1>, p.smem);
+      if (e == cudaSuccess) bfs_tc_kernel<1><<<p.grid, kTcThreads, p.smem, st>>>(p);
+    } else {
+      e = set_smem(bfs_tc_kernel<2>, p.smem);
+      if (e == cudaSuccess) bfs_tc_kernel<2><<<p.grid, kTcThreads, p.smem, st>>>(p);
+    }
+    count_launch();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (dbg_buf) {
+      std::vector<long long> h((size_t)p.grid * 8);
+      cudaStreamSynchronize(st);
+      cudaMemcpy(h.data(), dbg_buf, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+      double a[4] = {0, 0, 0, 0};
+      for (int b = 0; b < p.grid; ++b)
+        for (int k = 0; k < 4; ++k) a[k] += (double)h[(size_t)b * 4 + k] / p.grid;
+      fprintf(stderr, "[tc dbg] clk total %.0f  wait_full %.0f  wait_tmem %.0f  mma-loop %.0f  (tiles/cta %.1f)\n", a[0],
+              a[1], a[2], a[3], (double)p.n_tiles / p.grid);
+      double b[4] = {0, 0, 0, 0};
+      for (int bb = 0; bb < p.grid; ++bb)
+        for (int k = 0; k < 4; ++k) b[k] += (double)h[(size_t)(p.grid + bb) * 4 + k] / p.grid;
+      fprintf(stderr, "[tc dbg] epilogue: pre %.0f  end-barrier %.0f  tmem->smem %.0f  per-poi(incl barrier) %.0f\n", b[0], b[1], b[2], b[3]);
+      cudaFree(dbg_buf);
+      p.dbg_out = nullptr;
+    }
+  }
+  // (d) per POI: exact ZNCC -> argmax record, or the full surface for the swarm walk
+  if (e == cudaSuccess) {
+    const int blocks = (int)((npoi * 32 + 255) / 256);
+    if (p.surface)
+      tc_surface_kernel<<<blocks, 256, 0, st>>>(p);
+    else
+      tc_argmax_kernel<<<blocks, 256, 0, st>>>(p);
+    count_launch();
+    e = cudaGetLastError();
+  }
+  cleanup();
+  return e;
+}
+
+}  // namespace dicb200

@@ -172,6 +172,24 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
     p.subpixel_none = cfg->subpixel_method == DICB200_SUB_NONE;
     p.rec = out_dev;
     if (!p.whole && p.R < 0) return invalid("search radius must be >= 0");
+    if (!p.whole) {  // tensor-core search when the window shape allows it
+      TcParams t{};
+      t.ref = p.ref;
+      t.tgt = p.tgt;
+      t.lat = lat;
+      t.rb = rb;
+      t.re = re;
+      t.M = p.M;
+      t.R = p.R;
+      t.planes = p.u8 ? 1 : 2;
+      t.subpixel_none = p.subpixel_none;
+      t.rec = out_dev;
+      if (tc_plan(t)) {
+        StageTimer tm(0, st);
+        DICB200_CUDA_TRY(tc_launch(t, st));
+        goto refine;
+      }
+    }
     if (!bfs_plan(p, 72 * 1024) && !bfs_plan(p, 200 * 1024)) return invalid("subset too large for the BFS tile (shared memory)");
     BestPartial* partial = nullptr;
     if (p.n_chunks > 1) {
@@ -214,12 +232,24 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
       b.subpixel_none = 1;
       b.rec = out_chunk;
       b.surface = surface;
-      if (!bfs_plan(b, 72 * 1024) && !bfs_plan(b, 200 * 1024)) {
+      TcParams t{};
+      t.ref = b.ref;
+      t.tgt = b.tgt;
+      t.lat = lat;
+      t.rb = r0;
+      t.re = r1;
+      t.M = b.M;
+      t.R = b.R;
+      t.planes = b.u8 ? 1 : 2;
+      t.subpixel_none = 1;
+      t.surface = surface;
+      const bool use_tc = tc_plan(t);
+      if (!use_tc && !bfs_plan(b, 72 * 1024) && !bfs_plan(b, 200 * 1024)) {
         s = invalid("subset too large for the BFS tile (shared memory)");
         break;
       }
       BestPartial* partial = nullptr;
-      if (b.n_chunks > 1) {
+      if (!use_tc && b.n_chunks > 1) {
         cudaError_t e = cudaMallocAsync((void**)&partial, (size_t)(r1 - r0) * lat.nx * b.n_chunks * sizeof(BestPartial), st);
         if (e != cudaSuccess) {
           s = cuda_fail(e, "cudaMallocAsync(partial)", __FILE__, __LINE__);
@@ -251,7 +281,7 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
       p.surface = surface;
       {
         StageTimer tm(1, st);
-        cudaError_t e = bfs_launch(b, r1 - r0, st);
+        cudaError_t e = use_tc ? tc_launch(t, st) : bfs_launch(b, r1 - r0, st);
         if (e != cudaSuccess) s = cuda_fail(e, "bfs_launch(surface)", __FILE__, __LINE__);
         if (s == DICB200_OK) s = pso_walk_launch(p, st);
       }
@@ -260,6 +290,7 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
     cudaFreeAsync(surface, st);
     if (s != DICB200_OK) return s;
   }
+refine:
   if (cfg->subpixel_method != DICB200_SUB_NONE) {
     RefineParams r{};
     r.ref = view(ref);
