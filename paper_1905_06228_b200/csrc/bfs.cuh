@@ -74,7 +74,8 @@ struct TcParams {
   long long* dbg_out;  // optional per-CTA MMA-thread clock breakdown (tools)
   int dbg;  // DICB200_TC_DBG timing experiments (bit 0: no epilogue math, bit 1: no stage build)
   // buffers (device)
-  uint8_t* bprep;        // [poi][n_mma][planes][32] reference bytes in MMA order
+  uint8_t* strips;       // [planes][8][W][strip_h] row-shifted column-major reference byte planes
+  int strip_h;
   int64_t* poi_sf;       // [poi] sum f
   double* poi_sqrtvf;    // [poi] sqrt(n Sff - Sf^2)
   uint32_t* S1;          // [SH][SW] window sums of g

@@ -17,15 +17,18 @@
 //   A[(mx, my)][(j, i)] = T[cg*4 + j][rg*8 + my + i][mx]
 //                       = g[Y0 + my + rg*8 + i][X0 + mx + cg*4 + j]
 // directly: the 8-row core matrices of neighbouring M chunks overlap.
-// B operand (K x N): the POIs' reference bytes pre-arranged in MMA order
-// (K-major, no swizzle), gathered per tile with cp.async.
+// B operand (K x N, K-major, no swizzle): each POI's 8-row x 4-column
+// reference blocks, gathered per stage with 8-byte cp.async from row-shifted
+// column-major copies of the reference byte planes (tc_strips_kernel).
 //
 // 16-bit pixels: g = 256 gh + gl, f = 256 fh + fl; A runs once per g plane
 // into its own accumulator, N holds both f planes, and
 //   Sfg = 65536 D[gh,fh] + 256 (D[gh,fl] + D[gl,fh]) + D[gl,fl]
 // (every partial < 2^31 for side <= 129). Sg and Sgg per position come from a
-// separate exact box-sum pass, Sf and Sff per POI from the preparation pass;
-// ZNCC and every decision are then formed exactly as in bfs.cu.
+// separate exact box-sum pass, Sf and Sff per POI from the preparation pass.
+// The kernel streams the exact Sfg of every in-window position to HBM; ZNCC,
+// the evaluation count and the argmax (or the PSO surface) are then formed
+// exactly as in bfs.cu by tc_argmax_kernel / tc_surface_kernel.
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -52,14 +55,6 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 // Instruction descriptor: kind::i8, D s32, A u8 MN-major, B u8 K-major, M = 128.
 __device__ __forceinline__ uint32_t idesc_i8(int n) {
   return (2u << 4) | (1u << 15) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
 // Issued by one elected lane of a converged warp (the warp keeps the loop
@@ -119,10 +114,6 @@ __device__ __forceinline__ void mbar_wait_warp(uint32_t bar, uint32_t parity) {
   }
 }
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-
 // int64 -> double without the XU conversion unit (exact for |x| < 2^51: the
 // value sits in the mantissa of 1.5 * 2^52 + x); wider values fall back.
 __device__ __forceinline__ double i64_to_f64(int64_t x) {
@@ -131,26 +122,10 @@ __device__ __forceinline__ double i64_to_f64(int64_t x) {
   return (double)x;
 }
 
-// Tiles of position space whose rectangle holds positions of P's window
-// (clipped to the launch domain). Empty when hi < lo.
-struct TileRange {
-  int tx_lo, tx_hi, ty_lo, ty_hi;
-};
-
-__host__ __device__ inline TileRange poi_tiles(const TcParams& p, int cx, int cy) {
-  TileRange t;
-  const int wx_lo = max(cx - p.M - p.R, p.qx_min), wx_hi = min(cx - p.M + p.R, p.qx_max);
-  const int wy_lo = max(cy - p.M - p.R, p.qy_min), wy_hi = min(cy - p.M + p.R, p.qy_max);
-  if (wx_lo > wx_hi || wy_lo > wy_hi) {
-    t.tx_lo = t.ty_lo = 0;
-    t.tx_hi = t.ty_hi = -1;
-    return t;
-  }
-  t.tx_lo = (wx_lo - p.qx_min) / kTX;
-  t.tx_hi = (wx_hi - p.qx_min) / kTX;
-  t.ty_lo = (wy_lo - p.qy_min) / kTY;
-  t.ty_hi = (wy_hi - p.qy_min) / kTY;
-  return t;
+// 8-byte async copy; bytes past src_size (0..8) are zero-filled.
+__device__ __forceinline__ void cp_async8_zfill(void* dst, const void* src, int src_size) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_size)
+               : "memory");
 }
 
 // POIs (lattice index ranges) whose windows intersect the tile rectangle.
@@ -235,57 +210,74 @@ __global__ void __launch_bounds__(256) tc_stats_kernel(TcParams p) {
   }
 }
 
-// ---- per POI: exact reference moments + reference bytes in MMA order ----
+// ---- per POI: exact reference moments (separable window sums at the lattice) ----
+// One CTA per POI row: column sums over the subset rows for every column, then
+// each POI sums its `side` columns. Exact in integers.
 template <typename Pix>
 __global__ void __launch_bounds__(256) tc_prep_kernel(TcParams p) {
-  const int warp = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
-  const int npoi = (p.re - p.rb) * p.lat.nx;
-  if (warp >= npoi) return;
-  const int iy = p.rb + warp / p.lat.nx, ix = warp % p.lat.nx;
-  const int cx = p.lat.cx(ix), cy = p.lat.cy(iy), M = p.M, side = p.side;
-  const int pitch = p.ref.pitch;
-  const Pix* base = reinterpret_cast<const Pix*>(p.ref.data) + (size_t)(cy - M) * pitch + (cx - M);
-  uint64_t sf = 0, sff = 0;
-  for (int k = lane; k < side * side; k += 32) {
-    const int r = k / side, c = k - r * side;
-    const uint64_t v = base[(size_t)r * pitch + c];
-    sf += v;
-    sff += v * v;
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    sf += __shfl_xor_sync(0xffffffffu, sf, o);
-    sff += __shfl_xor_sync(0xffffffffu, sff, o);
-  }
-  if (lane == 0) {
-    const int64_t n = (int64_t)side * side;
-    const int64_t vf = n * (int64_t)sff - (int64_t)sf * (int64_t)sf;
-    p.poi_sf[warp] = (int64_t)sf;
-    p.poi_sqrtvf[warp] = vf > 0 ? sqrt((double)vf) : 0.0;
-  }
-  const int planes = p.planes;
-  uint8_t* dst = p.bprep + (size_t)warp * p.n_mma * planes * 32;
-  for (int item = lane; item < p.n_mma * planes; item += 32) {
-    const int mma = item / planes, plane = item - mma * planes;
-    const int rg = mma / p.CG, cg = mma - rg * p.CG;
-    const int shift = (planes == 2 && plane == 0) ? 8 : 0;
-    uint32_t w[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      uint32_t word = 0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int k = 4 * q + e, j = k >> 3, i = k & 7;  // k = j*8 + i <-> column cg*4+j, row rg*8+i
-        const int r = rg * 8 + i, c = cg * 4 + j;
-        uint32_t v = 0;
-        if (r < side && c < side) v = ((uint32_t)base[(size_t)r * pitch + c] >> shift) & 0xffu;
-        word |= v << (8 * e);
-      }
-      w[q] = word;
+  extern __shared__ __align__(16) unsigned char prep_smem[];
+  const int W = p.ref.width, pitch = p.ref.pitch, M = p.M, side = p.side;
+  uint32_t* c1 = reinterpret_cast<uint32_t*>(prep_smem);
+  uint64_t* c2 = reinterpret_cast<uint64_t*>(prep_smem + (((size_t)W * 4 + 15) & ~size_t(15)));
+  const int iy = p.rb + blockIdx.x, y0 = p.lat.cy(iy) - M;
+  const Pix* img = reinterpret_cast<const Pix*>(p.ref.data);
+  for (int x = threadIdx.x; x < W; x += blockDim.x) {
+    uint32_t s1 = 0;
+    uint64_t s2 = 0;
+    for (int r = 0; r < side; ++r) {
+      const uint32_t v = img[(size_t)(y0 + r) * pitch + x];
+      s1 += v;
+      s2 += (uint64_t)v * v;
     }
-    uint4* d = reinterpret_cast<uint4*>(dst + (size_t)item * 32);
-    d[0] = make_uint4(w[0], w[1], w[2], w[3]);
-    d[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    c1[x] = s1;
+    c2[x] = s2;
+  }
+  __syncthreads();
+  const int64_t n = (int64_t)side * side;
+  for (int ix = threadIdx.x; ix < p.lat.nx; ix += blockDim.x) {
+    const int x0 = p.lat.cx(ix) - M;
+    uint64_t sf = 0, sff = 0;
+    for (int c = 0; c < side; ++c) {
+      sf += c1[x0 + c];
+      sff += c2[x0 + c];
+    }
+    const int64_t vf = n * (int64_t)sff - (int64_t)sf * (int64_t)sf;
+    const size_t k = (size_t)blockIdx.x * p.lat.nx + ix;
+    p.poi_sf[k] = (int64_t)sf;
+    p.poi_sqrtvf[k] = vf > 0 ? sqrt((double)vf) : 0.0;
+  }
+}
+
+// ---- reference byte planes as 8 row-shifted strip images ----
+// strips[pl][s][y8][x][i] = plane_pl(ref[8 y8 + i + s][x]): the 8-row column
+// runs of one 8-row band lie side by side, so the MMA's B block of a POI (8
+// subset rows x 4 consecutive columns, K-major = column runs) is 32 contiguous
+// bytes of strip s = (first row) % 8 — gathered with cp.async straight from
+// here, no per-POI copies of the reference.
+template <typename Pix>
+__global__ void __launch_bounds__(256) tc_strips_kernel(TcParams p) {
+  constexpr int CX = 32, CY = 64;
+  __shared__ uint16_t tile[CY + 8][CX + 1];
+  const int x0 = blockIdx.x * CX, y0 = blockIdx.y * CY;
+  const Pix* img = reinterpret_cast<const Pix*>(p.ref.data);
+  const int W = p.ref.width, H = p.ref.height, pitch = p.ref.pitch, Hs = p.strip_h;
+  for (int i = threadIdx.x; i < (CY + 8) * CX; i += blockDim.x) {
+    const int r = i / CX, c = i - r * CX, gy = y0 + r, gx = x0 + c;
+    tile[r][c] = (gy < H && gx < W) ? (uint16_t)img[(size_t)gy * pitch + gx] : (uint16_t)0;
+  }
+  __syncthreads();
+  const int per_plane = 8 * CX * (CY / 4);
+  for (int item = threadIdx.x; item < p.planes * per_plane; item += blockDim.x) {
+    const int q = item % (CY / 4), c = (item / (CY / 4)) % CX, sft = (item / (CX * (CY / 4))) % 8,
+              pl = item / per_plane;
+    if (x0 + c >= W) continue;
+    const int shift = (p.planes == 2 && pl == 0) ? 8 : 0;
+    uint32_t w = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) w |= (((uint32_t)tile[q * 4 + e + sft][c] >> shift) & 0xffu) << (8 * e);
+    const int yy = y0 + q * 4;  // strip row of the word's first byte
+    *reinterpret_cast<uint32_t*>(p.strips + ((size_t)(pl * 8 + sft) * (Hs / 8) + (yy >> 3)) * W * 8 +
+                                 (size_t)(x0 + c) * 8 + (yy & 7)) = w;
   }
 }
 
@@ -311,7 +303,8 @@ __global__ void tc_tiles_kernel(TcParams p) {
 constexpr int kGroups = 4, kGroupThreads = 64;  // producer groups = ring slots
 constexpr int kProducerWarps = kGroups * kGroupThreads / 32;
 constexpr int kProducers = kGroups * kGroupThreads, kEpilogue = 256;
-constexpr int kTcThreads = kProducers + 32 + kEpilogue;
+constexpr int kMmaWarps = 2;  // one tcgen05 issuer per byte plane of the target
+constexpr int kTcThreads = kProducers + 32 * kMmaWarps + kEpilogue;
 constexpr int kStageRows = 16;  // T rows per stage: 8 positions + 8 subset rows - 1, rounded
 
 struct TileInfo {
@@ -338,11 +331,6 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
 
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
-               : "memory");
-}
-
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 
 template <int PLANES>
@@ -350,7 +338,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base;
-  __shared__ int prod_poi[kGroups * kMaxTilePoi];
+  __shared__ int2 prod_poi[kGroups * kMaxTilePoi];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int S = kGroups;  // ring slots: one per producer group
 
@@ -362,10 +350,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
   if (tid == 32) {
     for (int s = 0; s < kGroups; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&full_bar[s])), "r"(kGroupThreads));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&empty_bar[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&empty_bar[s])), "r"(PLANES));
     }
     for (int a = 0; a < 2; ++a) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&tfull_bar[a])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&tfull_bar[a])), "r"(PLANES));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&tempty_bar[a])), "r"(kEpilogue));
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -381,14 +369,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
     // timing experiment: MMA issuer alone
   } else if (warp < kProducerWarps) {
     // ================= producers =================
-    // group g (2 warps) owns ring slot g and builds every stage it with it % S == g,
+    // group g (kGroupThreads threads) owns ring slot g and builds every stage it with it % S == g,
     // so S stages (and their global-load latencies) are in flight at once.
-    const int g = warp >> 1, gt = tid & 63;
+    const int g = tid / kGroupThreads, gt = tid % kGroupThreads;
     const auto* img = reinterpret_cast<const uint8_t*>(p.tgt.data);
     const int W = p.tgt.width, H = p.tgt.height, pitch = p.tgt.pitch;
-    const size_t poi_stride = (size_t)p.n_mma * PLANES * 32;
     const int RW4 = (NX + 15 + 3) / 4;  // words per staged row
-    int* poi_tab = prod_poi + g * kMaxTilePoi;
+    int2* poi_tab = prod_poi + g * kMaxTilePoi;
     uint32_t ph = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
@@ -400,7 +387,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
       named_sync(1 + g, kGroupThreads);  // previous tile's readers of poi_tab are done
       for (int j = gt; j < t.npoi; j += kGroupThreads) {
         const int jy = j / t.nix, jx = j - jy * t.nix;
-        poi_tab[j] = (t.iy_lo + jy - p.rb) * p.lat.nx + (t.ix_lo + jx);
+        poi_tab[j] = make_int2(p.lat.cx(t.ix_lo + jx) - p.M, p.lat.cy(t.iy_lo + jy) - p.M);
       }
       named_sync(1 + g, kGroupThreads);
       const int NN = t.npoi * PLANES;
@@ -416,13 +403,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
           ph ^= 1u;
           continue;
         }
-        // (a) B: one thread per (POI plane, K half) column, all CG MMA blocks of the stage
-        for (int e = gt; e < NN * 2; e += kGroupThreads) {
-          const int nn = e >> 1, kh = e & 1;
-          const int j = nn / PLANES, pl = nn - j * PLANES;
-          const uint8_t* src = p.bprep + (size_t)poi_tab[j] * poi_stride + ((size_t)rg * CG * PLANES + pl) * 32 + kh * 16;
-          uint8_t* dst = Bs + (nn & 7) * 16 + (nn >> 3) * 256 + kh * 128;
-          for (int cg = 0; cg < CG; ++cg) cp_async16(dst + (size_t)cg * t.N * 32, src + (size_t)cg * PLANES * 32);
+        // (a) B: the tile's reference blocks (8 subset rows x 4 columns per MMA,
+        //     K-major) as 8-byte column runs from the strip images; rows/columns
+        //     past the subset are zero-filled (cp.async src-size)
+        {
+          const int r0 = rg * 8, vrows = min(8, p.side - r0);
+          const int W = p.ref.width, Hs = p.strip_h;
+          for (int jp = gt >> 2; jp < NN; jp += kGroupThreads / 4) {
+            const int jc = gt & 3;
+            const int j = jp / PLANES, pl = jp - j * PLANES;
+            const int2 o = poi_tab[j];  // subset top-left (x, y) in the reference
+            const int ry = o.y + r0, sft = ry & 7;
+            const uint8_t* strip = p.strips + ((size_t)(pl * 8 + sft) * (Hs / 8) + (ry >> 3)) * W * 8;
+            const uint8_t* src = strip + (size_t)(o.x + jc) * 8;
+            const size_t src_step = 32;  // next column group: 4 columns x 8 bytes
+            uint8_t* dst = Bs + (jp & 7) * 16 + (jp >> 3) * 256 + (jc >> 1) * 128 + (jc & 1) * 8;
+            const size_t dst_step = (size_t)t.N * 32;
+            const int cg_full = (p.side - jc + 3) / 4;  // column groups holding column jc + 4 cg < side
+            for (int cg = 0; cg < CG; ++cg, src += src_step, dst += dst_step)
+              cp_async8_zfill(dst, cg < cg_full ? src : strip, cg < cg_full ? vrows : 0);
+          }
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
         // (b) target rows [Y0 + 8 rg, +16) x [X0, X0 + 4 RW4): 4 pixels -> one word per byte plane
@@ -430,10 +430,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
           const int gy0 = t.Y0 + rg * 8;
           for (int w = gt & 15; w < RW4; w += 16) {
             const int gx0 = t.X0 + 4 * w;
-            uint32_t v[4][4];
+            constexpr int RY = kStageRows * 16 / kGroupThreads;  // rows per thread
+            constexpr int YS = kGroupThreads / 16;                // row stride
+            uint32_t v[RY][4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int gy = gy0 + (gt >> 4) + 4 * k;
+            for (int k = 0; k < RY; ++k) {
+              const int gy = gy0 + (gt >> 4) + YS * k;
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 const int gx = gx0 + i;
@@ -447,8 +449,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
               }
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int y = (gt >> 4) + 4 * k;
+            for (int k = 0; k < RY; ++k) {
+              const int y = (gt >> 4) + YS * k;
               if (PLANES == 1) {
                 rows[y * (RWB / 4) + w] = v[k][0] | (v[k][1] << 8) | (v[k][2] << 16) | (v[k][3] << 24);
               } else {
@@ -488,8 +490,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
         named_sync(1 + g, kGroupThreads);  // rows of this slot are rewritten next round
       }
     }
-  } else if (warp == kProducerWarps) {
-    // ================= MMA issuer =================
+  } else if (warp < kProducerWarps + kMmaWarps) {
+    if (warp - kProducerWarps >= PLANES) {
+      // spare issuer (single-plane data)
+    } else {
+    // ================= MMA issuers =================
+    // issuer pl handles target byte plane pl into its own accumulator
     // The whole warp runs the loop (descriptors stay in uniform registers);
     // one elected lane issues each tcgen05.mma / commit.
     {
@@ -504,8 +510,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
         if (!(p.dbg & 256)) mbar_wait_warp(smem_u32(&tempty_bar[a]), aph ^ 1u);
         w_empty += clock64() - c0;
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const uint32_t d0 = tmem + (uint32_t)(a * PLANES * p.N_max);
-        const uint32_t d1 = d0 + (uint32_t)t.N;
+        const int pl = warp - kProducerWarps;
+        const uint32_t d0 = tmem + (uint32_t)(a * PLANES * p.N_max) + (uint32_t)(pl * t.N);
         const uint32_t idesc = idesc_i8((p.dbg & 8) ? 16 : t.N);
         const uint32_t b_step = (uint32_t)t.N * 2u;  // B block per cg, 16-byte units
         for (int rg = 0; rg < p.RG; ++rg, ++it) {
@@ -517,15 +523,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
           w_full += c2 - c1;
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           const uint32_t base = smem_u32(sm + (size_t)s * p.stage_bytes);
-          uint64_t da = sdesc(base, kStageRows * 16, 16);
+          uint64_t da = sdesc(base + (uint32_t)(pl * planeT), kStageRows * 16, 16);
           uint64_t db = sdesc(base + (uint32_t)p.off_B, 128, 256);
-          const uint64_t da_plane = (uint64_t)(uint32_t)(planeT >> 4);
           for (int cg = 0; cg < CG; ++cg) {
             const uint32_t acc = (rg | cg) != 0;
-            if (!(p.dbg & 2048)) {
-              mma_i8_elect(d0, da, db, idesc, acc);
-              if (PLANES == 2 && !(p.dbg & 4)) mma_i8_elect(d1, da + da_plane, db, idesc, acc);
-            }
+            if (!(p.dbg & 2048) && !(pl == 1 && (p.dbg & 4))) mma_i8_elect(d0, da, db, idesc, acc);
             da += (uint64_t)(4 * kStageRows);
             db += (uint64_t)b_step;
           }
@@ -535,20 +537,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
         umma_commit_elect(smem_u32(&tfull_bar[a]));
         ++tc;
       }
-      if (p.dbg_out && lane == 0) {
+      if (p.dbg_out && lane == 0 && warp == kProducerWarps) {
         p.dbg_out[blockIdx.x * 4 + 0] = clock64() - t0;
         p.dbg_out[blockIdx.x * 4 + 1] = w_full;
         p.dbg_out[blockIdx.x * 4 + 2] = w_empty;
         p.dbg_out[blockIdx.x * 4 + 3] = t_issue;
       }
     }
-  } else if (warp >= kProducerWarps + 1) {
+    }
+  } else if (warp >= kProducerWarps + kMmaWarps) {
     // ================= epilogue =================
     // thread = position (TMEM lane quadrant = warp % 4; the two warps of a
     // quadrant split the POI column groups): the exact cross terms Sfg of every
     // in-window position go to sfg[poi][dy + R][dx + R]; ZNCC and the argmax run
     // in tc_argmax_kernel / tc_surface_kernel.
-    const int quad = warp & 3, half = (warp - kProducerWarps - 1) >> 2;
+    const int quad = warp & 3, half = (warp - kProducerWarps - kMmaWarps) >> 2;
     const int m = quad * 32 + lane, mx = m & 15, my = m >> 4;
     const int R = p.R, EW = 2 * R + 1;
     constexpr int PER = 8 / PLANES;  // POIs per 8 accumulator columns
@@ -654,38 +657,61 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p) {
   if (fx_lo <= fx_hi && fy_lo <= fy_hi && svf > 0.0) {
     const int64_t* buf = p.sfg + (size_t)k * EW * EW;
     const double rsvf = 1.0 / svf;
+    // one pass over memory: count, and each lane's two best candidates by the
+    // approximate quotient
     int cnt = 0;
-    double amax = -3.0;
+    double a1 = -3.0, a2 = -3.0;
+    Cand c1{0, 1};
+    int x1 = 0, y1 = 0;
     for (int dy = fy_lo; dy <= fy_hi; ++dy)
       for (int dx = fx_lo + lane; dx <= fx_hi; dx += 32) {
         Cand c;
         if (tc_candidate(p, n, sf, buf[(dy + R) * EW + (dx + R)], cx - M + dx, cy - M + dy, c)) {
           ++cnt;
-          amax = fmax(amax, i64_to_f64(c.num) * rsvf * rsqrt(i64_to_f64(c.vg)));
+          const double av = i64_to_f64(c.num) * rsvf * rsqrt(i64_to_f64(c.vg));
+          if (av > a1) {  // a2: the lane's runner-up (only its value is needed)
+            a2 = a1;
+            a1 = av, c1 = c, x1 = dx, y1 = dy;
+          } else if (av > a2) {
+            a2 = av;
+          }
         }
       }
+    double amax = a1;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
       amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     }
     const double thr = amax - 0x1p-40;
-    for (int dy = fy_lo; dy <= fy_hi; ++dy)
-      for (int dx = fx_lo + lane; dx <= fx_hi; dx += 32) {
-        Cand c;
-        if (tc_candidate(p, n, sf, buf[(dy + R) * EW + (dx + R)], cx - M + dx, cy - M + dy, c)) {
-          const double nd = i64_to_f64(c.num), vd = i64_to_f64(c.vg);
-          if (nd * rsvf * rsqrt(vd) >= thr) {
-            const double z = nd / (svf * sqrt(vd));  // exact IEEE quotient (zncc_from_moments)
-            if (!b.found || improves(z, dx, dy, b.c, b.dx, b.dy)) {
-              b.found = 1;
-              b.c = z;
-              b.dx = dx;
-              b.dy = dy;
+    if (!__any_sync(0xffffffffu, a2 >= thr)) {
+      // every near-maximal candidate is some lane's best: exact quotients for those
+      if (a1 >= thr) {
+        const double z = i64_to_f64(c1.num) / (svf * sqrt(i64_to_f64(c1.vg)));  // exact (zncc_from_moments)
+        b.found = 1;
+        b.c = z;
+        b.dx = x1;
+        b.dy = y1;
+      }
+    } else {
+      // near-ties beyond two per lane: second pass over the window
+      for (int dy = fy_lo; dy <= fy_hi; ++dy)
+        for (int dx = fx_lo + lane; dx <= fx_hi; dx += 32) {
+          Cand c;
+          if (tc_candidate(p, n, sf, buf[(dy + R) * EW + (dx + R)], cx - M + dx, cy - M + dy, c)) {
+            const double nd = i64_to_f64(c.num), vd = i64_to_f64(c.vg);
+            if (nd * rsvf * rsqrt(vd) >= thr) {
+              const double z = nd / (svf * sqrt(vd));
+              if (!b.found || improves(z, dx, dy, b.c, b.dx, b.dy)) {
+                b.found = 1;
+                b.c = z;
+                b.dx = dx;
+                b.dy = dy;
+              }
             }
           }
         }
-      }
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       BestPartial q;
@@ -752,6 +778,7 @@ bool tc_plan(TcParams& p) {
   if (p.R < 0 || p.M < 0) return false;
   p.side = 2 * p.M + 1;
   if (p.side > 129) return false;
+  if ((size_t)p.ref.width * 12 + 16 > 200 * 1024) return false;  // tc_prep_kernel column sums
   const int side = p.side, W = p.tgt.width, H = p.tgt.height;
   const int rows = p.re - p.rb;
   if (rows <= 0 || p.lat.nx <= 0) return false;
@@ -813,7 +840,8 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st) {
       if (q) cudaFreeAsync(q, st);
   };
   const size_t sbytes = (size_t)std::max(1, p.SW) * std::max(1, p.SH);
-  e = cudaMallocAsync(&bprep, npoi * p.n_mma * p.planes * 32, st);
+  p.strip_h = ((p.ref.height + 63) / 64) * 64;
+  e = cudaMallocAsync(&bprep, (size_t)p.planes * 8 * p.ref.width * p.strip_h, st);
   if (e == cudaSuccess) e = cudaMallocAsync(&psf, npoi * 8, st);
   if (e == cudaSuccess) e = cudaMallocAsync(&pvf, npoi * 8, st);
   if (e == cudaSuccess) e = cudaMallocAsync(&s1, sbytes * 4, st);
@@ -825,7 +853,7 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st) {
     cleanup();
     return e;
   }
-  p.bprep = (uint8_t*)bprep;
+  p.strips = (uint8_t*)bprep;
   p.poi_sf = (int64_t*)psf;
   p.poi_sqrtvf = (double*)pvf;
   p.S1 = (uint32_t*)s1;
@@ -848,13 +876,25 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st) {
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
   }
-  // (b) reference moments + MMA-ordered bytes
+  // (b) reference moments + strip images
   if (e == cudaSuccess) {
-    const int blocks = (int)((npoi * 32 + 255) / 256);
+    dim3 sg((p.ref.width + 31) / 32, p.strip_h / 64);
     if (u8)
-      tc_prep_kernel<uint8_t><<<blocks, 256, 0, st>>>(p);
+      tc_strips_kernel<uint8_t><<<sg, 256, 0, st>>>(p);
     else
-      tc_prep_kernel<uint16_t><<<blocks, 256, 0, st>>>(p);
+      tc_strips_kernel<uint16_t><<<sg, 256, 0, st>>>(p);
+    count_launch();
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) {
+    const size_t sm = (((size_t)p.ref.width * 4 + 15) & ~size_t(15)) + (size_t)p.ref.width * 8;
+    if (u8) {
+      e = set_smem(tc_prep_kernel<uint8_t>, sm);
+      if (e == cudaSuccess) tc_prep_kernel<uint8_t><<<rows, 256, sm, st>>>(p);
+    } else {
+      e = set_smem(tc_prep_kernel<uint16_t>, sm);
+      if (e == cudaSuccess) tc_prep_kernel<uint16_t><<<rows, 256, sm, st>>>(p);
+    }
     count_launch();
     e = cudaGetLastError();
   }
