@@ -42,6 +42,20 @@ import numpy as np  # noqa: E402
 from paper_1905_06228_b200 import _abi, configs, dic  # noqa: E402
 
 PIPES_BIN = os.path.join(ROOT, "tools", "microbench", "pipes")
+N_STAGES = 6  # DICB200_N_STAGES
+
+
+def _measured_peaks() -> dict:
+    """MEASURED_PEAKS.json (driver-written); else the profiling recipe's fallback."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        d["source"] = "MEASURED_PEAKS.json"
+        return d
+    except Exception:  # noqa: BLE001
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+MEASURED_PEAKS = _measured_peaks()
 
 
 def parse():
@@ -261,7 +275,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     peaks = pipe_peaks() if rank == 0 else {}
     # timed region: K steps, CUDA events on the launch stream, stage events live
     clocks = Clocks(local_rank)
-    L.dicb200_profile_read((C.c_double * 4)(), (C.c_uint64 * 4)())  # clear
+    L.dicb200_profile_read((C.c_double * N_STAGES)(), (C.c_uint64 * N_STAGES)())  # clear
     barrier()
     torch.cuda.synchronize()
     L.dicb200_reset_launch_count()
@@ -288,8 +302,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize()
     barrier()
     ms_total = ev0.elapsed_time(ev1)
-    stage_ms = (C.c_double * 4)()
-    stage_n = (C.c_uint64 * 4)()
+    stage_ms = (C.c_double * N_STAGES)()
+    stage_n = (C.c_uint64 * N_STAGES)()
     L.dicb200_profile_read(stage_ms, stage_n)
     # flush time is not analysis work: subtract it (measured on the same stream)
     ms = ms_total - sum(a.elapsed_time(b) for a, b in flush_ev)
@@ -375,13 +389,29 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         return None
 
     # ---- roofline of the dominant stage ----
-    names = ["bfs_zncc", "pso", "nr", "icgn"]
+    names = ["bfs_zncc", "pso", "nr", "icgn", "tc_cross_terms", "tc_zncc"]
     stage = {names[i]: {"ms_total": float(stage_ms[i]), "launches": int(stage_n[i]),
-                        "avg_ms": float(stage_ms[i]) / max(1, int(stage_n[i]))} for i in range(4) if stage_n[i]}
-    dom = max(stage, key=lambda k: stage[k]["ms_total"]) if stage else None
+                        "avg_ms": float(stage_ms[i]) / max(1, int(stage_n[i]))} for i in range(N_STAGES) if stage_n[i]}
+    top = {k: v for k, v in stage.items() if k in names[:4]}
+    dom = max(top, key=lambda k: top[k]["ms_total"]) if top else None
     n_px = (2 * cfg.grid.half_width + 1) ** 2
+    planes = 1 if u8 else 2
     roof = None
-    if dom == "bfs_zncc":
+    if dom in ("bfs_zncc", "pso") and "tc_cross_terms" in stage:
+        # tensor-core search: algorithmic u8 x u8 MACs = sum(evaluations) x n x planes^2
+        # (a 16-bit product is 4 exact byte products), per launch of bfs_tc_kernel
+        st_tc = stage["tc_cross_terms"]
+        evals_launch = evals * args.steps / max(1, st_tc["launches"])  # evals: one step of my pairs
+        macs_per_launch = evals_launch * n_px * planes * planes
+        achieved = macs_per_launch / (st_tc["avg_ms"] * 1e-3) / 1e12
+        i8_peak = MEASURED_PEAKS.get("bf16_tflops", 0.0)  # dense i8 = 2x bf16 ops = bf16 TFLOP/s in TMAC/s
+        roof = {"kernel": "bfs_tc_kernel", "bound": "tensor", "pipe": "tcgen05.mma kind::i8 (u8 x u8 -> s32)",
+                "achieved": achieved, "peak": i8_peak, "unit": "TMAC/s (i8)",
+                "frac": achieved / i8_peak if i8_peak else None, "traffic": None,
+                "peak_source": MEASURED_PEAKS["source"] + " bf16_tflops (dense bf16 FLOP/s == dense i8 MAC/s on B200)",
+                "work_per_launch": f"sum(evaluations) x (2M+1)^2 x planes^2 = {macs_per_launch:.4g} i8 MACs",
+                "launch_ms": st_tc["avg_ms"]}
+    elif dom == "bfs_zncc":
         # algorithmic work per launch: (sum of evaluations over the launch's POIs) x n MACs
         macs_per_launch = evals / max(1, len(my_pairs)) * n_px
         achieved = macs_per_launch / (stage[dom]["avg_ms"] * 1e-3) / 1e12

@@ -201,8 +201,10 @@ void dicb200_reset_launch_count(void);
 /* Stage timing (bench evidence): while enabled, every enqueued stage kernel
  * is bracketed by CUDA events on the stream it runs on. dicb200_profile_read
  * waits for them and returns per-stage totals (ms) and launch counts, then
- * clears. Stages: 0 BFS-ZNCC, 1 PSO/mPSO, 2 NR, 3 IC-GN. */
-#define DICB200_N_STAGES 4
+ * clears. Stages: 0 BFS-ZNCC, 1 PSO/mPSO, 2 NR, 3 IC-GN (whole stages);
+ * 4 the tensor-core cross-term kernel and 5 the ZNCC argmax/surface kernel
+ * inside stage 0 or 1 when the tensor-core search runs. */
+#define DICB200_N_STAGES 6
 void dicb200_profile_enable(int on);
 int dicb200_profile_read(double* ms_out, uint64_t* launches_out);
 

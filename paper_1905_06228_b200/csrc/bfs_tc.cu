@@ -782,6 +782,7 @@ bool tc_plan(TcParams& p) {
   const int side = p.side, W = p.tgt.width, H = p.tgt.height;
   const int rows = p.re - p.rb;
   if (rows <= 0 || p.lat.nx <= 0) return false;
+  if ((size_t)rows * p.lat.nx < 1024) return false;  // tiny grids: the single-launch CUDA-core kernel wins
   p.qx_min = std::max(0, p.lat.cx(0) - p.M - p.R);
   p.qx_max = std::min(W - side, p.lat.cx(p.lat.nx - 1) - p.M + p.R);
   p.qy_min = std::max(0, p.lat.cy(p.rb) - p.M - p.R);
@@ -911,12 +912,15 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st) {
       cudaMemsetAsync(dbg_buf, 0, (size_t)p.grid * 8 * sizeof(long long), st);
       p.dbg_out = dbg_buf;
     }
-    if (u8) {
-      e = set_smem(bfs_tc_kernel<1>, p.smem);
-      if (e == cudaSuccess) bfs_tc_kernel<1><<<p.grid, kTcThreads, p.smem, st>>>(p);
-    } else {
-      e = set_smem(bfs_tc_kernel<2>, p.smem);
-      if (e == cudaSuccess) bfs_tc_kernel<2><<<p.grid, kTcThreads, p.smem, st>>>(p);
+    {
+      StageTimer tm(4, st);
+      if (u8) {
+        e = set_smem(bfs_tc_kernel<1>, p.smem);
+        if (e == cudaSuccess) bfs_tc_kernel<1><<<p.grid, kTcThreads, p.smem, st>>>(p);
+      } else {
+        e = set_smem(bfs_tc_kernel<2>, p.smem);
+        if (e == cudaSuccess) bfs_tc_kernel<2><<<p.grid, kTcThreads, p.smem, st>>>(p);
+      }
     }
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
@@ -940,6 +944,7 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st) {
   // (d) per POI: exact ZNCC -> argmax record, or the full surface for the swarm walk
   if (e == cudaSuccess) {
     const int blocks = (int)((npoi * 32 + 255) / 256);
+    StageTimer tm(5, st);
     if (p.surface)
       tc_surface_kernel<<<blocks, 256, 0, st>>>(p);
     else

@@ -65,6 +65,15 @@ __device__ inline double zncc_from_moments(int64_t n, int64_t sfg, int64_t sf, i
 // Launch accounting (bench.py "gpu_launches").
 void count_launch(int n = 1);
 
+// Stage timing scope (dicb200_profile_*): CUDA events around the enqueued work.
+struct StageTimer {
+  int stage;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  StageTimer(int s, cudaStream_t stream);
+  ~StageTimer();
+};
+
 }  // namespace dicb200
 
 #define DICB200_CUDA_TRY(expr)                                              \

@@ -33,24 +33,21 @@ std::atomic<int> g_profile{0};
 std::mutex g_profile_mu;
 std::vector<StageEvent> g_events;
 
-struct StageTimer {
-  int stage;
-  cudaStream_t st;
-  cudaEvent_t a = nullptr, b = nullptr;
-  StageTimer(int s, cudaStream_t stream) : stage(s), st(stream) {
-    if (!g_profile.load()) return;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
-    cudaEventRecord(a, st);
-  }
-  ~StageTimer() {
-    if (!a) return;
-    cudaEventRecord(b, st);
-    std::lock_guard<std::mutex> lk(g_profile_mu);
-    g_events.push_back({stage, a, b});
-  }
-};
 }  // namespace
+
+StageTimer::StageTimer(int s, cudaStream_t stream) : stage(s), st(stream) {
+  if (!g_profile.load()) return;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, st);
+}
+
+StageTimer::~StageTimer() {
+  if (!a) return;
+  cudaEventRecord(b, st);
+  std::lock_guard<std::mutex> lk(g_profile_mu);
+  g_events.push_back({stage, a, b});
+}
 
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 

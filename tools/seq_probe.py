@@ -38,8 +38,8 @@ for i in range(npairs):
     fields[i].records = C.cast(C.c_void_p(recs[i].data_ptr()), C.POINTER(_abi.PoiRecordC))
     fields[i].capacity = n
 arr = (_abi.Image * (npairs + 1))(*ims_h)
-ms = (C.c_double * 4)()
-nl = (C.c_uint64 * 4)()
+ms = (C.c_double * 6)()
+nl = (C.c_uint64 * 6)()
 
 
 def seq():
