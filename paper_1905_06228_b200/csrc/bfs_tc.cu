@@ -663,8 +663,13 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p) {
     double a1 = -3.0, a2 = -3.0;
     Cand c1{0, 1};
     int x1 = 0, y1 = 0;
-    for (int dy = fy_lo; dy <= fy_hi; ++dy)
-      for (int dx = fx_lo + lane; dx <= fx_hi; dx += 32) {
+    // flattened (dy, dx) walk: lane l takes candidates l, l + 32, ... in row-major order
+    const int fw = fx_hi - fx_lo + 1, total = fw * (fy_hi - fy_lo + 1);
+    int ry = lane / fw, rx = lane - ry * fw;
+    const int jump_y = 32 / fw, jump_x = 32 - jump_y * fw;
+    for (int idx = lane; idx < total; idx += 32) {
+      {
+        const int dx = fx_lo + rx, dy = fy_lo + ry;
         Cand c;
         if (tc_candidate(p, n, sf, buf[(dy + R) * EW + (dx + R)], cx - M + dx, cy - M + dy, c)) {
           ++cnt;
@@ -677,6 +682,13 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p) {
           }
         }
       }
+      rx += jump_x;
+      ry += jump_y;
+      if (rx >= fw) {
+        rx -= fw;
+        ++ry;
+      }
+    }
     double amax = a1;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
