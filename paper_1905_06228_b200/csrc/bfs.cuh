@@ -86,11 +86,26 @@ struct TcParams {
   dicb200_poi_record* rec;
 };
 
+// Reference-side inputs of the tensor-core search (strip images, POI moments)
+// kept across pairs that share a reference frame (analyze_sequence). `key`
+// identifies the frame within one call; reset() between calls.
+struct TcRefCache {
+  void* strips = nullptr;
+  void* psf = nullptr;
+  void* pvf = nullptr;
+  size_t strips_cap = 0, psf_cap = 0, pvf_cap = 0;
+  long key = -1;
+  const void* data = nullptr;
+  int W = 0, H = 0, M = 0, x0 = 0, y0 = 0, step = 0, nx = 0, rb = 0, re = 0;
+  void reset() { key = -1; }
+};
+
 // Plans the tensor-core search for POI rows [rb, re); false = not applicable
 // (whole-image domain, too many POIs per tile, shared memory).
 bool tc_plan(TcParams& p);
 // Enqueues stats, reference preparation, the tensor-core kernel and the
 // per-POI merge (or only the surface when p.surface is set) on `st`.
-cudaError_t tc_launch(TcParams& p, cudaStream_t st);
+cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache = nullptr, long ref_key = -1);
+void tc_cache_free(TcRefCache& c);
 
 }  // namespace dicb200

@@ -842,7 +842,26 @@ bool tc_plan(TcParams& p) {
   return true;
 }
 
-cudaError_t tc_launch(TcParams& p, cudaStream_t st) {
+namespace {
+cudaError_t grow(void*& ptr, size_t& cap, size_t bytes, cudaStream_t st) {
+  if (cap >= bytes) return cudaSuccess;
+  if (ptr) cudaFreeAsync(ptr, st);
+  ptr = nullptr;
+  cap = 0;
+  cudaError_t e = cudaMallocAsync(&ptr, bytes, st);
+  if (e == cudaSuccess) cap = bytes;
+  return e;
+}
+}  // namespace
+
+void tc_cache_free(TcRefCache& c) {
+  if (c.strips) cudaFree(c.strips);
+  if (c.psf) cudaFree(c.psf);
+  if (c.pvf) cudaFree(c.pvf);
+  c = TcRefCache{};
+}
+
+cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_key) {
   const int rows = p.re - p.rb;
   const size_t npoi = (size_t)rows * p.lat.nx;
   cudaError_t e = cudaSuccess;
@@ -854,9 +873,31 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st) {
   };
   const size_t sbytes = (size_t)std::max(1, p.SW) * std::max(1, p.SH);
   p.strip_h = ((p.ref.height + 63) / 64) * 64;
-  e = cudaMallocAsync(&bprep, (size_t)p.planes * 8 * p.ref.width * p.strip_h, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&psf, npoi * 8, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&pvf, npoi * 8, st);
+  const size_t strip_bytes = (size_t)p.planes * 8 * p.ref.width * p.strip_h;
+  // reference-side inputs: from the cache when this reference frame's were built already
+  bool ref_ready = false;
+  if (cache && ref_key >= 0) {
+    ref_ready = cache->key == ref_key && cache->data == p.ref.data && cache->W == p.ref.width &&
+                cache->H == p.ref.height && cache->M == p.M && cache->x0 == p.lat.x0 && cache->y0 == p.lat.y0 &&
+                cache->step == p.lat.step && cache->nx == p.lat.nx && cache->rb == p.rb && cache->re == p.re;
+    if (!ref_ready) {
+      cache->key = -1;
+      e = grow(cache->strips, cache->strips_cap, strip_bytes, st);
+      if (e == cudaSuccess) e = grow(cache->psf, cache->psf_cap, npoi * 8, st);
+      if (e == cudaSuccess) e = grow(cache->pvf, cache->pvf_cap, npoi * 8, st);
+      if (e != cudaSuccess) return e;
+    }
+    p.strips = (uint8_t*)cache->strips;
+    p.poi_sf = (int64_t*)cache->psf;
+    p.poi_sqrtvf = (double*)cache->pvf;
+  } else {
+    e = cudaMallocAsync(&bprep, strip_bytes, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&psf, npoi * 8, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&pvf, npoi * 8, st);
+    p.strips = (uint8_t*)bprep;
+    p.poi_sf = (int64_t*)psf;
+    p.poi_sqrtvf = (double*)pvf;
+  }
   if (e == cudaSuccess) e = cudaMallocAsync(&s1, sbytes * 4, st);
   if (e == cudaSuccess) e = cudaMallocAsync(&s2, sbytes * 8, st);
   const size_t EW = 2 * (size_t)p.R + 1;
@@ -866,9 +907,6 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st) {
     cleanup();
     return e;
   }
-  p.strips = (uint8_t*)bprep;
-  p.poi_sf = (int64_t*)psf;
-  p.poi_sqrtvf = (double*)pvf;
   p.S1 = (uint32_t*)s1;
   p.S2 = (uint64_t*)s2;
   p.sfg = (int64_t*)part;
@@ -889,8 +927,8 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st) {
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
   }
-  // (b) reference moments + strip images
-  if (e == cudaSuccess) {
+  // (b) reference moments + strip images (skipped when cached)
+  if (e == cudaSuccess && !ref_ready) {
     dim3 sg((p.ref.width + 31) / 32, p.strip_h / 64);
     if (u8)
       tc_strips_kernel<uint8_t><<<sg, 256, 0, st>>>(p);
@@ -898,18 +936,31 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st) {
       tc_strips_kernel<uint16_t><<<sg, 256, 0, st>>>(p);
     count_launch();
     e = cudaGetLastError();
-  }
-  if (e == cudaSuccess) {
-    const size_t sm = (((size_t)p.ref.width * 4 + 15) & ~size_t(15)) + (size_t)p.ref.width * 8;
-    if (u8) {
-      e = set_smem(tc_prep_kernel<uint8_t>, sm);
-      if (e == cudaSuccess) tc_prep_kernel<uint8_t><<<rows, 256, sm, st>>>(p);
-    } else {
-      e = set_smem(tc_prep_kernel<uint16_t>, sm);
-      if (e == cudaSuccess) tc_prep_kernel<uint16_t><<<rows, 256, sm, st>>>(p);
+    if (e == cudaSuccess) {
+      const size_t sm = (((size_t)p.ref.width * 4 + 15) & ~size_t(15)) + (size_t)p.ref.width * 8;
+      if (u8) {
+        e = set_smem(tc_prep_kernel<uint8_t>, sm);
+        if (e == cudaSuccess) tc_prep_kernel<uint8_t><<<rows, 256, sm, st>>>(p);
+      } else {
+        e = set_smem(tc_prep_kernel<uint16_t>, sm);
+        if (e == cudaSuccess) tc_prep_kernel<uint16_t><<<rows, 256, sm, st>>>(p);
+      }
+      count_launch();
+      if (e == cudaSuccess) e = cudaGetLastError();
     }
-    count_launch();
-    e = cudaGetLastError();
+    if (e == cudaSuccess && cache && ref_key >= 0) {
+      cache->key = ref_key;
+      cache->data = p.ref.data;
+      cache->W = p.ref.width;
+      cache->H = p.ref.height;
+      cache->M = p.M;
+      cache->x0 = p.lat.x0;
+      cache->y0 = p.lat.y0;
+      cache->step = p.lat.step;
+      cache->nx = p.lat.nx;
+      cache->rb = p.rb;
+      cache->re = p.re;
+    }
   }
   // (c) tensor-core search
   if (e == cudaSuccess && p.n_tiles > 0) {

@@ -146,7 +146,8 @@ static dicb200_status validate_pair(const dicb200_image* a, const dicb200_image*
 // Enqueue the whole per-pair chain for grid rows [rb, re) on `st`.
 static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image* tgt, const dicb200_run_config* cfg,
                                    uint64_t pair_index, const Lattice& lat, int rb, int re,
-                                   dicb200_poi_record* out_dev, cudaStream_t st) {
+                                   dicb200_poi_record* out_dev, cudaStream_t st, TcRefCache* tcache = nullptr,
+                                   long ref_key = -1) {
   const int rows = re - rb;
   if (rows <= 0) return DICB200_OK;
   const size_t nrec = (size_t)rows * lat.nx;
@@ -183,7 +184,7 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
       t.rec = out_dev;
       if (tc_plan(t)) {
         StageTimer tm(0, st);
-        DICB200_CUDA_TRY(tc_launch(t, st));
+        DICB200_CUDA_TRY(tc_launch(t, st, tcache, ref_key));
         goto refine;
       }
     }
@@ -278,7 +279,7 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
       p.surface = surface;
       {
         StageTimer tm(1, st);
-        cudaError_t e = use_tc ? tc_launch(t, st) : bfs_launch(b, r1 - r0, st);
+        cudaError_t e = use_tc ? tc_launch(t, st, tcache, ref_key) : bfs_launch(b, r1 - r0, st);
         if (e != cudaSuccess) s = cuda_fail(e, "bfs_launch(surface)", __FILE__, __LINE__);
         if (s == DICB200_OK) s = pso_walk_launch(p, st);
       }
@@ -363,6 +364,7 @@ struct DeviceContext {
   cudaStream_t ds = nullptr;  // copy: record read-back behind the compute stream
   FrameSlot frames[kFrameSlots];
   RecSlot recs[kRecSlots];
+  TcRefCache tcache;  // reference-side tensor-core inputs, reused while the reference frame repeats
 };
 
 namespace {
@@ -386,6 +388,7 @@ static void destroy_context(DeviceContext* c) {
     if (r.done) cudaEventDestroy(r.done);
     if (r.computed) cudaEventDestroy(r.computed);
   }
+  tc_cache_free(c->tcache);
   if (c->cs) cudaStreamDestroy(c->cs);
   if (c->xs) cudaStreamDestroy(c->xs);
   if (c->ds) cudaStreamDestroy(c->ds);
@@ -439,6 +442,7 @@ static dicb200_status release_context(DeviceContext* c) {
   cudaError_t e3 = cudaStreamSynchronize(c->ds);
   if (e2 == cudaSuccess) e2 = e3;
   for (auto& f : c->frames) f.key = f.last_use = -1;  // LRU state is per call
+  c->tcache.reset();
   for (auto& r : c->recs) r.pair = -1;
   std::lock_guard<std::mutex> lk(g_ctx_mu);
   g_ctx_idle.push_back(c);
@@ -758,7 +762,7 @@ dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_im
       }
       if (s == DICB200_OK)
         s = enqueue_pair(&c->frames[sa].im, &c->frames[sb].im, cfg, i, lat[i - lo], 0, lat[i - lo].ny,
-                         (dicb200_poi_record*)r.dev.p, c->cs);
+                         (dicb200_poi_record*)r.dev.p, c->cs, &c->tcache, (long)pairs[2 * i]);
       if (s == DICB200_OK) {
         e = cudaEventRecord(c->frames[sa].idle, c->cs);
         if (e == cudaSuccess) e = cudaEventRecord(c->frames[sb].idle, c->cs);
