@@ -148,64 +148,99 @@ __host__ __device__ inline void tile_pois(const TcParams& p, int X0, int Y0, int
 }
 
 // ---- exact window sums of g and g^2 at every position of the domain ----
+// CTA = 64 x 32 positions. The target region is staged in shared memory by
+// rows; row sums over `side` columns go to shared memory, then column sums over
+// `side` rows slide down each output column, so the global stores of S1/S2 are
+// coalesced rows. Exact in integers (u32 sums, u64 sums of squares).
+constexpr int kStatsBX = 64, kStatsBY = 32;
+
+__host__ __device__ inline size_t stats_smem_bytes(int side) {
+  const size_t RW = kStatsBX + side - 1, RH = kStatsBY + side - 1;
+  return ((RH * RW * 2 + 15) & ~size_t(15)) + ((RH * kStatsBX * 4 + 15) & ~size_t(15)) + RH * kStatsBX * 8;
+}
+
 template <typename Pix>
 __global__ void __launch_bounds__(256) tc_stats_kernel(TcParams p) {
-  constexpr int BX = 64, BY = 32;
   extern __shared__ __align__(1024) unsigned char stats_smem[];
-  const int side = p.side, CW = BX + side - 1;
-  uint32_t* c1 = reinterpret_cast<uint32_t*>(stats_smem);
-  uint64_t* c2 = reinterpret_cast<uint64_t*>(stats_smem + (((size_t)BY * CW * 4 + 15) & ~size_t(15)));
-  const int sx0 = blockIdx.x * BX, sy0 = blockIdx.y * BY;
-  const int rows = min(BY, p.SH - sy0), cols = min(BX, p.SW - sx0);
+  const int side = p.side, RW = kStatsBX + side - 1, RH = kStatsBY + side - 1;
+  uint16_t* reg = reinterpret_cast<uint16_t*>(stats_smem);
+  uint32_t* h1 = reinterpret_cast<uint32_t*>(stats_smem + (((size_t)RH * RW * 2 + 15) & ~size_t(15)));
+  uint64_t* h2 = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(h1) +
+                                             (((size_t)RH * kStatsBX * 4 + 15) & ~size_t(15)));
+  const int sx0 = blockIdx.x * kStatsBX, sy0 = blockIdx.y * kStatsBY;
+  const int rows = min(kStatsBY, p.SH - sy0), cols = min(kStatsBX, p.SW - sx0);
   const Pix* img = reinterpret_cast<const Pix*>(p.tgt.data);
-  const int pitch = p.tgt.pitch, gy0 = p.qy_min + sy0;
-  for (int x = threadIdx.x; x < CW; x += blockDim.x) {
-    const int gx = p.qx_min + sx0 + x;
-    if (gx >= p.tgt.width) {  // only feeds positions past the domain
-      for (int t = 0; t < rows; ++t) {
-        c1[t * CW + x] = 0;
-        c2[t * CW + x] = 0;
+  const int pitch = p.tgt.pitch, gx0 = p.qx_min + sx0, gy0 = p.qy_min + sy0;
+  const int W = p.tgt.width, H = p.tgt.height;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int rh = rows + side - 1;  // region rows this CTA needs
+  {
+    // batches of 8 independent loads per thread (memory-level parallelism)
+    const int E = rh * RW;
+    constexpr int U = 8;
+    for (int base = threadIdx.x; base < E; base += U * 256) {
+      uint16_t v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = base + u * 256, r = i / RW, c = i - r * RW, gy = gy0 + r, gx = gx0 + c;
+        v[u] = (i < E && gy < H && gx < W) ? (uint16_t)img[(size_t)gy * pitch + gx] : (uint16_t)0;
       }
-      continue;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (base + u * 256 < E) reg[base + u * 256] = v[u];
     }
+  }
+  (void)warp;
+  (void)lane;
+  (void)nw;
+  __syncthreads();
+  // row sums over `side` columns: h[r][x], 8 outputs per item
+  constexpr int SEG = 8;
+  for (int item = threadIdx.x; item < rh * (kStatsBX / SEG); item += blockDim.x) {
+    const int r = item / (kStatsBX / SEG), x0 = (item % (kStatsBX / SEG)) * SEG;
+    const uint16_t* row = reg + r * RW;
     uint32_t s1 = 0;
     uint64_t s2 = 0;
-    for (int r = 0; r < side; ++r) {
-      const uint32_t v = img[(size_t)(gy0 + r) * pitch + gx];
+#pragma unroll 8
+    for (int c = 0; c < side; ++c) {
+      const uint32_t v = row[x0 + c];
       s1 += v;
       s2 += (uint64_t)v * v;
     }
-    c1[x] = s1;
-    c2[x] = s2;
-    for (int t = 1; t < rows; ++t) {
-      const uint32_t a = img[(size_t)(gy0 + t + side - 1) * pitch + gx], b = img[(size_t)(gy0 + t - 1) * pitch + gx];
+    h1[r * kStatsBX + x0] = s1;
+    h2[r * kStatsBX + x0] = s2;
+#pragma unroll
+    for (int x = x0 + 1; x < x0 + SEG; ++x) {
+      const uint32_t a = row[x + side - 1], b = row[x - 1];
       s1 += a - b;
       s2 += (uint64_t)a * a - (uint64_t)b * b;
-      c1[t * CW + x] = s1;
-      c2[t * CW + x] = s2;
+      h1[r * kStatsBX + x] = s1;
+      h2[r * kStatsBX + x] = s2;
     }
   }
   __syncthreads();
-  constexpr int SEG = 16;
-  const int nseg = (cols + SEG - 1) / SEG;
-  for (int item = threadIdx.x; item < rows * nseg; item += blockDim.x) {
-    const int t = item / nseg, x0 = (item % nseg) * SEG, x1 = min(cols, x0 + SEG);
-    const uint32_t* r1 = c1 + t * CW;
-    const uint64_t* r2 = c2 + t * CW;
+  // column sums over `side` rows, sliding down 16 outputs per item (coalesced stores)
+  constexpr int CH = 16;
+  for (int item = threadIdx.x; item < kStatsBX * (kStatsBY / CH); item += blockDim.x) {
+    const int x = item % kStatsBX, t0 = (item / kStatsBX) * CH;
+    if (t0 >= rows || x >= cols) continue;
     uint32_t s1 = 0;
     uint64_t s2 = 0;
-    for (int c = 0; c < side; ++c) {
-      s1 += r1[x0 + c];
-      s2 += r2[x0 + c];
+#pragma unroll 8
+    for (int r = 0; r < side; ++r) {
+      s1 += h1[(t0 + r) * kStatsBX + x];
+      s2 += h2[(t0 + r) * kStatsBX + x];
     }
-    const size_t o = (size_t)(sy0 + t) * p.SW + sx0;
-    p.S1[o + x0] = s1;
-    p.S2[o + x0] = s2;
-    for (int x = x0 + 1; x < x1; ++x) {
-      s1 += r1[x + side - 1] - r1[x - 1];
-      s2 += r2[x + side - 1] - r2[x - 1];
-      p.S1[o + x] = s1;
-      p.S2[o + x] = s2;
+    size_t o = (size_t)(sy0 + t0) * p.SW + sx0 + x;
+    p.S1[o] = s1;
+    p.S2[o] = s2;
+    const int t1 = min(t0 + CH, rows);
+    for (int t = t0 + 1; t < t1; ++t) {
+      s1 += h1[(t + side - 1) * kStatsBX + x] - h1[(t - 1) * kStatsBX + x];
+      s2 += h2[(t + side - 1) * kStatsBX + x] - h2[(t - 1) * kStatsBX + x];
+      o += p.SW;
+      p.S1[o] = s1;
+      p.S2[o] = s2;
     }
   }
 }
@@ -791,6 +826,7 @@ bool tc_plan(TcParams& p) {
   p.side = 2 * p.M + 1;
   if (p.side > 129) return false;
   if ((size_t)p.ref.width * 12 + 16 > 200 * 1024) return false;  // tc_prep_kernel column sums
+  if (stats_smem_bytes(p.side) > 200 * 1024) return false;
   const int side = p.side, W = p.tgt.width, H = p.tgt.height;
   const int rows = p.re - p.rb;
   if (rows <= 0 || p.lat.nx <= 0) return false;
@@ -914,9 +950,8 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
   const bool u8 = p.planes == 1;
   // (a) window sums of the target
   if (e == cudaSuccess && p.n_tiles > 0) {
-    const int CW = 64 + p.side - 1;
-    const size_t sm = (((size_t)32 * CW * 4 + 15) & ~size_t(15)) + (size_t)32 * CW * 8;
-    dim3 grid((p.SW + 63) / 64, (p.SH + 31) / 32);
+    const size_t sm = stats_smem_bytes(p.side);
+    dim3 grid((p.SW + kStatsBX - 1) / kStatsBX, (p.SH + kStatsBY - 1) / kStatsBY);
     if (u8) {
       e = set_smem(tc_stats_kernel<uint8_t>, sm);
       if (e == cudaSuccess) tc_stats_kernel<uint8_t><<<grid, 256, sm, st>>>(p);
