@@ -67,6 +67,7 @@ struct TcParams {
   int qx_min, qx_max, qy_min, qy_max, SW, SH;  // position domain (subset top-left corners)
   int ntx, nty, n_tiles;
   int RG, CG, NX, HT, RWB, n_mma;  // K blocking: 8 rows x 4 columns per MMA
+  int rem, rem_rows, n_h, NX2, HT2, RWB2;  // row-major remainder stage (last subset rows)
   int nix_max, niy_max, npoi_max, N_max, tmem_cols;
   size_t off_rows, off_B, stage_bytes, smem;  // stage = T | rows | B
   int stages;
@@ -76,6 +77,7 @@ struct TcParams {
   // buffers (device)
   uint8_t* strips;       // [planes][8][W][strip_h] row-shifted column-major reference byte planes
   int strip_h;
+  uint8_t* tail;          // [poi][rem_rows * n_h][planes][32] remainder-row reference blocks
   int64_t* poi_sf;       // [poi] sum f
   double* poi_sqrtvf;    // [poi] sqrt(n Sff - Sf^2)
   uint32_t* S1;          // [SH][SW] window sums of g
@@ -93,7 +95,8 @@ struct TcRefCache {
   void* strips = nullptr;
   void* psf = nullptr;
   void* pvf = nullptr;
-  size_t strips_cap = 0, psf_cap = 0, pvf_cap = 0;
+  void* tail = nullptr;
+  size_t strips_cap = 0, psf_cap = 0, pvf_cap = 0, tail_cap = 0;
   long key = -1;
   const void* data = nullptr;
   int W = 0, H = 0, M = 0, x0 = 0, y0 = 0, step = 0, nx = 0, rb = 0, re = 0;

@@ -122,6 +122,10 @@ __device__ __forceinline__ double i64_to_f64(int64_t x) {
   return (double)x;
 }
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
 // 8-byte async copy; bytes past src_size (0..8) are zero-filled.
 __device__ __forceinline__ void cp_async8_zfill(void* dst, const void* src, int src_size) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_size)
@@ -281,6 +285,26 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(TcParams p) {
     p.poi_sf[k] = (int64_t)sf;
     p.poi_sqrtvf[k] = vf > 0 ? sqrt((double)vf) : 0.0;
   }
+  // remainder-row blocks of every POI of the row: tail[poi][q = ry n_h + h][plane][32 bytes]
+  if (p.rem) {
+    const int Q = p.rem_rows * p.n_h, r0 = 8 * (p.RG - 1);
+    const int per_poi = Q * p.planes * 8;  // words
+    for (int e = threadIdx.x; e < p.lat.nx * per_poi; e += blockDim.x) {
+      const int ix = e / per_poi, rest = e - ix * per_poi;
+      const int w = rest & 7, qp = rest >> 3, pl = qp % p.planes, q = qp / p.planes;
+      const int ry = q / p.n_h, h = q - ry * p.n_h;
+      const int x0 = p.lat.cx(ix) - M + 32 * h + 4 * w;
+      const Pix* row = img + (size_t)(y0 + r0 + ry) * pitch;
+      const int shift = (p.planes == 2 && pl == 0) ? 8 : 0;
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int c = 32 * h + 4 * w + b;
+        if (c < side) word |= (((uint32_t)row[x0 + b] >> shift) & 0xffu) << (8 * b);
+      }
+      reinterpret_cast<uint32_t*>(p.tail)[((size_t)blockIdx.x * p.lat.nx + ix) * per_poi + rest] = word;
+    }
+  }
 }
 
 // ---- reference byte planes as 8 row-shifted strip images ----
@@ -368,12 +392,84 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 
+// Remainder stage of a tile: subset rows r0 .. r0 + rem_rows - 1 (< 8 of them).
+//   T2[pl][y][X][0..15] = plane_pl(g[Y0 + r0 + y][X0 + X + i]), y < HT2, X < NX2
+//   B2[q = ry * n_h + h][n][k] = plane(f_n[r0 + ry][32 h + k]) (0 past the subset),
+//   copied from the per-POI tails written by tc_prep_kernel
+template <int PLANES>
+__device__ __forceinline__ void build_remainder_stage(const TcParams& p, const TileInfo& t, const int* poi_idx,
+                                                      int r0, uint8_t* T, uint8_t* rows8, uint8_t* Bs, int gt,
+                                                      int g) {
+  const auto* img = reinterpret_cast<const uint8_t*>(p.tgt.data);
+  const int W = p.tgt.width, H = p.tgt.height, pitch = p.tgt.pitch;
+  const int NX2 = p.NX2, HT2 = p.HT2, RWB2 = p.RWB2, RW42 = (NX2 + 15 + 3) / 4;
+  uint32_t* rows = reinterpret_cast<uint32_t*>(rows8);
+  // (a) B2: the POIs' precomputed remainder blocks (tc_prep_kernel), 16 bytes per cp.async
+  {
+    const int NN = t.npoi * PLANES, Q = p.rem_rows * p.n_h;
+    const int items = Q * NN * 2;
+    for (int e = gt; e < items; e += kGroupThreads) {
+      const int kh = e & 1, rest = e >> 1;
+      const int nn = rest % NN, q = rest / NN;
+      const int j = nn / PLANES, pl = nn - j * PLANES;
+      const uint8_t* src = p.tail + (((size_t)poi_idx[j] * Q + q) * PLANES + pl) * 32 + kh * 16;
+      cp_async16(Bs + (size_t)q * t.N * 32 + (nn & 7) * 16 + (nn >> 3) * 256 + kh * 128, src);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  // (b) target rows -> byte planes (4 pixels per word)
+  for (int e = gt; e < HT2 * RW42; e += kGroupThreads) {
+    const int y = e / RW42, w = e - y * RW42;
+    const int gy = t.Y0 + r0 + y, gx0 = t.X0 + 4 * w;
+    uint32_t v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int gx = gx0 + i;
+      v[i] = 0;
+      if (gy < H && gx < W) {
+        if (PLANES == 1)
+          v[i] = __ldg(img + (size_t)gy * pitch + gx);
+        else
+          v[i] = __ldg(reinterpret_cast<const uint16_t*>(img) + (size_t)gy * pitch + gx);
+      }
+    }
+    if (PLANES == 1) {
+      rows[y * (RWB2 / 4) + w] = v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24);
+    } else {
+      rows[y * (RWB2 / 4) + w] = __byte_perm(v[0], v[1], 0x7751) | (__byte_perm(v[2], v[3], 0x5177) & 0xffff0000u);
+      rows[(HT2 + y) * (RWB2 / 4) + w] =
+          __byte_perm(v[0], v[1], 0x7740) | (__byte_perm(v[2], v[3], 0x4077) & 0xffff0000u);
+    }
+  }
+  named_sync(1 + g, kGroupThreads);
+  // (c) row-major 16-pixel windows, four column offsets per item
+  const size_t planeT2 = (size_t)HT2 * NX2 * 16;
+  (void)g;
+  for (int e = gt; e < PLANES * HT2 * (NX2 / 4); e += kGroupThreads) {
+    const int X4 = e % (NX2 / 4), rest = e / (NX2 / 4), y = rest % HT2, pl = rest / HT2;
+    const uint32_t* rw = rows + (size_t)(pl * HT2 + y) * (RWB2 / 4);
+    const uint32_t a0 = rw[X4], a1 = rw[X4 + 1], a2 = rw[X4 + 2], a3 = rw[X4 + 3], a4 = rw[X4 + 4];
+    uint8_t* dst = T + pl * planeT2 + ((size_t)y * NX2 + 4 * X4) * 16;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      uint4 o;
+      o.x = __funnelshift_r(a0, a1, 8 * s);
+      o.y = __funnelshift_r(a1, a2, 8 * s);
+      o.z = __funnelshift_r(a2, a3, 8 * s);
+      o.w = __funnelshift_r(a3, a4, 8 * s);
+      *reinterpret_cast<uint4*>(dst + s * 16) = o;
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 template <int PLANES>
 __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base;
   __shared__ int2 prod_poi[kGroups * kMaxTilePoi];
+  __shared__ int prod_poi_ix[kGroups * kMaxTilePoi];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int S = kGroups;  // ring slots: one per producer group
 
@@ -411,6 +507,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
     const int W = p.tgt.width, H = p.tgt.height, pitch = p.tgt.pitch;
     const int RW4 = (NX + 15 + 3) / 4;  // words per staged row
     int2* poi_tab = prod_poi + g * kMaxTilePoi;
+    int* poi_ix = prod_poi_ix + g * kMaxTilePoi;
     uint32_t ph = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
@@ -423,6 +520,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
       for (int j = gt; j < t.npoi; j += kGroupThreads) {
         const int jy = j / t.nix, jx = j - jy * t.nix;
         poi_tab[j] = make_int2(p.lat.cx(t.ix_lo + jx) - p.M, p.lat.cy(t.iy_lo + jy) - p.M);
+        poi_ix[j] = (t.iy_lo + jy - p.rb) * p.lat.nx + (t.ix_lo + jx);
       }
       named_sync(1 + g, kGroupThreads);
       const int NN = t.npoi * PLANES;
@@ -436,6 +534,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
           mbar_arrive(smem_u32(&full_bar[g]));
           ph ^= 1u;
+          continue;
+        }
+        if (p.rem && rg == p.RG - 1) {
+          // remainder rows (e.g. row 40 of a 41-row subset): row-major stage,
+          // K = 32 consecutive columns of one subset row per MMA
+          build_remainder_stage<PLANES>(p, t, poi_ix, rg * 8, T, reinterpret_cast<uint8_t*>(rows), Bs, gt, g);
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          mbar_arrive(smem_u32(&full_bar[g]));
+          ph ^= 1u;
+          named_sync(1 + g, kGroupThreads);
           continue;
         }
         // (a) B: the tile's reference blocks (8 subset rows x 4 columns per MMA,
@@ -558,6 +666,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
           w_full += c2 - c1;
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           const uint32_t base = smem_u32(sm + (size_t)s * p.stage_bytes);
+          if (p.rem && rg == p.RG - 1) {
+            // row-major remainder stage: M chunks = rows (SBO = NX2 x 16 B),
+            // K rows = consecutive columns (16 B), K groups = +8 columns (LBO = 128 B)
+            const uint32_t planeT2 = (uint32_t)(p.HT2 * p.NX2 * 16);
+            for (int ry = 0; ry < p.rem_rows; ++ry)
+              for (int h = 0; h < p.n_h; ++h) {
+                const uint64_t da = sdesc(base + pl * planeT2 + (uint32_t)((ry * p.NX2 + 32 * h) * 16), 128,
+                                          (uint32_t)(p.NX2 * 16));
+                const uint64_t db =
+                    sdesc(base + (uint32_t)p.off_B + (uint32_t)((ry * p.n_h + h) * t.N * 32), 128, 256);
+                if (!(p.dbg & 2048) && !(pl == 1 && (p.dbg & 4))) mma_i8_elect(d0, da, db, idesc, 1u);
+              }
+            umma_commit_elect(smem_u32(&empty_bar[s]));
+            t_issue += clock64() - c2;
+            continue;
+          }
           uint64_t da = sdesc(base + (uint32_t)(pl * planeT), kStageRows * 16, 16);
           uint64_t db = sdesc(base + (uint32_t)p.off_B, 128, 256);
           for (int cg = 0; cg < CG; ++cg) {
@@ -852,6 +976,18 @@ bool tc_plan(TcParams& p) {
   if (((rwb / 4) & 1) == 0) rwb += 4;      // odd word pitch
   p.RWB = rwb;
   p.n_mma = p.RG * p.CG;
+  // remainder rows (side = 8 (RG - 1) + rem_rows): a row-major last stage with
+  // K = 32 columns per MMA when that needs fewer MMAs than CG (e.g. side 41: 2 vs 11)
+  p.rem_rows = side - 8 * (p.RG - 1);
+  p.n_h = (side + 31) / 32;
+  p.NX2 = 32 * p.n_h;
+  p.HT2 = 8 + p.rem_rows - 1;
+  {
+    int rwb2 = ((p.NX2 + 16 + 3) / 4) * 4 + 4;
+    if (((rwb2 / 4) & 1) == 0) rwb2 += 4;
+    p.RWB2 = rwb2;
+  }
+  p.rem = p.RG >= 2 && p.rem_rows * p.n_h < p.CG && !std::getenv("DICB200_TC_NOREM");
   const int s = p.lat.step;
   p.nix_max = std::min(p.lat.nx, (kTX - 1 + 2 * p.R) / s + 1);
   p.niy_max = std::min(rows, (kTY - 1 + 2 * p.R) / s + 1);
@@ -868,6 +1004,10 @@ bool tc_plan(TcParams& p) {
   p.off_rows = al((size_t)p.planes * p.NX * 16 * 16, 128);
   p.off_B = al(p.off_rows + (size_t)p.planes * 16 * p.RWB, 128);
   p.stage_bytes = al(p.off_B + (size_t)p.CG * p.N_max * 32, 1024);
+  if (p.rem && ((size_t)p.planes * p.HT2 * p.NX2 * 16 > p.off_rows ||
+                (size_t)p.planes * p.HT2 * p.RWB2 > p.off_B - p.off_rows ||
+                (size_t)p.rem_rows * p.n_h * p.N_max * 32 > p.stage_bytes - p.off_B))
+    p.rem = 0;
   p.stages = kGroups;
   p.smem = (size_t)p.stages * p.stage_bytes;
   if (p.smem > 220 * 1024) return false;
@@ -891,6 +1031,7 @@ cudaError_t grow(void*& ptr, size_t& cap, size_t bytes, cudaStream_t st) {
 }  // namespace
 
 void tc_cache_free(TcRefCache& c) {
+  if (c.tail) cudaFree(c.tail);
   if (c.strips) cudaFree(c.strips);
   if (c.psf) cudaFree(c.psf);
   if (c.pvf) cudaFree(c.pvf);
@@ -902,9 +1043,10 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
   const size_t npoi = (size_t)rows * p.lat.nx;
   cudaError_t e = cudaSuccess;
   void *bprep = nullptr, *psf = nullptr, *pvf = nullptr, *s1 = nullptr, *s2 = nullptr, *part = nullptr,
-       *tiles = nullptr;
+       *tiles = nullptr, *tailb = nullptr;
+  const size_t tail_bytes = p.rem ? npoi * (size_t)p.rem_rows * p.n_h * p.planes * 32 : 0;
   auto cleanup = [&]() {
-    for (void* q : {bprep, psf, pvf, s1, s2, part, tiles})
+    for (void* q : {bprep, psf, pvf, s1, s2, part, tiles, tailb})
       if (q) cudaFreeAsync(q, st);
   };
   const size_t sbytes = (size_t)std::max(1, p.SW) * std::max(1, p.SH);
@@ -921,15 +1063,19 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
       e = grow(cache->strips, cache->strips_cap, strip_bytes, st);
       if (e == cudaSuccess) e = grow(cache->psf, cache->psf_cap, npoi * 8, st);
       if (e == cudaSuccess) e = grow(cache->pvf, cache->pvf_cap, npoi * 8, st);
+      if (e == cudaSuccess) e = grow(cache->tail, cache->tail_cap, std::max<size_t>(16, tail_bytes), st);
       if (e != cudaSuccess) return e;
     }
     p.strips = (uint8_t*)cache->strips;
     p.poi_sf = (int64_t*)cache->psf;
     p.poi_sqrtvf = (double*)cache->pvf;
+    p.tail = (uint8_t*)cache->tail;
   } else {
     e = cudaMallocAsync(&bprep, strip_bytes, st);
     if (e == cudaSuccess) e = cudaMallocAsync(&psf, npoi * 8, st);
     if (e == cudaSuccess) e = cudaMallocAsync(&pvf, npoi * 8, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&tailb, std::max<size_t>(16, tail_bytes), st);
+    p.tail = (uint8_t*)tailb;
     p.strips = (uint8_t*)bprep;
     p.poi_sf = (int64_t*)psf;
     p.poi_sqrtvf = (double*)pvf;
