@@ -81,7 +81,8 @@ struct TcParams {
   int64_t* poi_sf;       // [poi] sum f
   double* poi_sqrtvf;    // [poi] sqrt(n Sff - Sf^2)
   uint32_t* S1;          // [SH][SW] window sums of g
-  uint64_t* S2;          // [SH][SW] window sums of g^2
+  double* SQ;            // [SH][SW] sqrt(n Sgg - Sg^2) (0: constant window)
+  float* RSQ;            // [SH][SW] ~1 / SQ (argmax candidate filter)
   int64_t* sfg;          // [poi][2R+1][2R+1] exact cross terms from the tensor cores
   void* tiles;           // [n_tiles] uint4: tx|ty<<16, ix_lo|iy_lo<<16, nix|niy<<16
   double* surface;       // optional [poi][2R+1][2R+1]

@@ -236,15 +236,22 @@ __global__ void __launch_bounds__(256) tc_stats_kernel(TcParams p) {
       s2 += h2[(t0 + r) * kStatsBX + x];
     }
     size_t o = (size_t)(sy0 + t0) * p.SW + sx0 + x;
-    p.S1[o] = s1;
-    p.S2[o] = s2;
+    const int64_t nn = (int64_t)side * side;
+    auto put = [&](size_t oo, uint32_t a1, uint64_t a2) {
+      // sqrt(vg) exactly as zncc_from_moments forms it (0 = degenerate window)
+      const int64_t vg = nn * (int64_t)a2 - (int64_t)a1 * (int64_t)a1;
+      const double sq = vg > 0 ? sqrt((double)vg) : 0.0;
+      p.S1[oo] = a1;
+      p.SQ[oo] = sq;
+      p.RSQ[oo] = vg > 0 ? (float)(1.0 / sq) : 0.0f;
+    };
+    put(o, s1, s2);
     const int t1 = min(t0 + CH, rows);
     for (int t = t0 + 1; t < t1; ++t) {
       s1 += h1[(t + side - 1) * kStatsBX + x] - h1[(t - 1) * kStatsBX + x];
       s2 += h2[(t + side - 1) * kStatsBX + x] - h2[(t - 1) * kStatsBX + x];
       o += p.SW;
-      p.S1[o] = s1;
-      p.S2[o] = s2;
+      put(o, s1, s2);
     }
   }
 }
@@ -776,37 +783,86 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(p.tmem_cols));
 }
 
-// One candidate's exact moments from the tensor-core cross term and the exact
-// window sums (as zncc_from_moments, common.cuh); false = degenerate window.
+// One candidate's exact numerator n Sfg - Sf Sg from the tensor-core cross
+// term and the exact window sums (as zncc_from_moments, common.cuh).
 struct Cand {
-  int64_t num, vg;
+  int64_t num;
+  double sq;   // sqrt(n Sgg - Sg^2), computed once per position by tc_stats_kernel
+  float rsq;   // ~1 / sq (candidate filter only)
 };
 
-__device__ __forceinline__ bool tc_candidate(const TcParams& p, int64_t n, int64_t sf, int64_t sfg, int qx, int qy,
-                                             Cand& c) {
-  const size_t o = (size_t)(qy - p.qy_min) * p.SW + (qx - p.qx_min);
-  const int64_t sg = p.S1[o], sgg = (int64_t)p.S2[o];
-  c.vg = n * sgg - sg * sg;
-  c.num = n * sfg - sf * sg;
-  return c.vg > 0;  // constant target window: skipped, not counted
+// Position data (Sg, sqrt(vg), ~1/sqrt(vg)) of the union of a strip's windows,
+// staged in shared memory once per CTA (neighbouring POIs share most positions).
+struct PosView {
+  const double* sq;
+  const uint32_t* s1;
+  const float* rsq;
+  int x0, y0, W;
+};
+
+__host__ __device__ inline size_t pos_smem_bytes(const TcParams& p, int sp) {
+  const size_t W = (size_t)(sp - 1) * p.lat.step + 2 * p.R + 1, H = 2 * (size_t)p.R + 1;
+  return W * H * 16;
+}
+
+__device__ __forceinline__ PosView stage_positions(const TcParams& p, int iy, int ix0, int ts, unsigned char* sm) {
+  PosView v;
+  const int M = p.M, R = p.R;
+  v.x0 = max(p.lat.cx(ix0) - M - R, p.qx_min);
+  const int x1 = min(p.lat.cx(ix0 + ts - 1) - M + R, p.qx_max);
+  v.y0 = max(p.lat.cy(iy) - M - R, p.qy_min);
+  const int y1 = min(p.lat.cy(iy) - M + R, p.qy_max);
+  v.W = max(0, x1 - v.x0 + 1);
+  const int H = max(0, y1 - v.y0 + 1), N = v.W * H;
+  double* sq = reinterpret_cast<double*>(sm);
+  uint32_t* s1 = reinterpret_cast<uint32_t*>(sm + (size_t)N * 8);
+  float* rsq = reinterpret_cast<float*>(sm + (size_t)N * 12);
+  for (int r = threadIdx.x >> 5; r < H; r += blockDim.x >> 5) {
+    const size_t o = (size_t)(v.y0 + r - p.qy_min) * p.SW + (v.x0 - p.qx_min);
+    for (int c = threadIdx.x & 31; c < v.W; c += 32) {
+      sq[r * v.W + c] = p.SQ[o + c];
+      s1[r * v.W + c] = p.S1[o + c];
+      rsq[r * v.W + c] = p.RSQ[o + c];
+    }
+  }
+  __syncthreads();
+  v.sq = sq;
+  v.s1 = s1;
+  v.rsq = rsq;
+  return v;
+}
+
+// n <= 129^2 and Sf, Sg <= 129^2 * 65535 < 2^31 fit 32 bits, Sfg (>= 0) 64: two
+// wide multiplies, exact in wrap-around 64-bit arithmetic.
+__device__ __forceinline__ bool tc_candidate_s(const PosView& v, uint32_t n, uint32_t sf, int64_t sfg, int qx, int qy,
+                                               Cand& c) {
+  const int o = (qy - v.y0) * v.W + (qx - v.x0);
+  c.sq = v.sq[o];
+  if (!(c.sq > 0.0)) return false;  // constant target window: skipped, not counted
+  c.rsq = v.rsq[o];
+  c.num = (int64_t)((uint64_t)sfg * n - (uint64_t)sf * v.s1[o]);
+  return true;
 }
 
 // ---- per POI: count, exact argmax in improves() order -> record ----
-// Pass 1 finds the maximum of a cheap quotient num * (1/sqrt(vf)) * rsqrt(vg)
-// (relative error a few ulp, i.e. < 2^-48 absolute as |zncc| <= 1); pass 2 forms
-// the EXACT IEEE quotient num / (sqrt(vf) sqrt(vg)) only for candidates within
-// 2^-40 of it, so the winner and its value are exactly those of the sequential
-// reference loop. Warp per POI, lanes across the window columns.
-__global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p) {
-  const int k = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
-  const int npoi = (p.re - p.rb) * p.lat.nx;
-  if (k >= npoi) return;
-  const int iy = p.rb + k / p.lat.nx, ix = k % p.lat.nx;
+// One pass finds the maximum of a cheap quotient num * (1/sqrt(vf)) * rsq with
+// rsq the fp32 reciprocal of sqrt(vg) (relative error < 2^-22, i.e. absolute as
+// |zncc| <= 1); the EXACT IEEE quotient num / (sqrt(vf) sqrt(vg)) is formed only
+// for candidates within 2^-20 of it (a second pass when more than one per lane
+// qualifies), so the winner and its value are exactly those of the sequential
+// reference loop. Warp per POI, lanes across the window candidates.
+__global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p, int sp) {
+  extern __shared__ __align__(16) unsigned char pos_smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int iy = p.rb + blockIdx.y, ix0 = blockIdx.x * sp, ts = min(sp, p.lat.nx - ix0);
+  const PosView pv = stage_positions(p, iy, ix0, ts, pos_smem);
+  if (w >= ts) return;
+  const int ix = ix0 + w, k = (iy - p.rb) * p.lat.nx + ix;
   const int cx = p.lat.cx(ix), cy = p.lat.cy(iy), M = p.M, R = p.R, EW = 2 * R + 1;
-  const int64_t n = (int64_t)p.side * p.side;
+  const uint32_t n = (uint32_t)(p.side * p.side);
   const int fx_lo = max(-R, M - cx), fx_hi = min(R, p.tgt.width - 1 - M - cx);   // integer_search.cpp:11-21
   const int fy_lo = max(-R, M - cy), fy_hi = min(R, p.tgt.height - 1 - M - cy);
-  const int64_t sf = p.poi_sf[k];
+  const uint32_t sf = (uint32_t)p.poi_sf[k];
   const double svf = p.poi_sqrtvf[k];
   BestPartial b;
   b.c = -2.0;
@@ -820,7 +876,7 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p) {
     // approximate quotient
     int cnt = 0;
     double a1 = -3.0, a2 = -3.0;
-    Cand c1{0, 1};
+    Cand c1{0, 1.0, 1.0f};
     int x1 = 0, y1 = 0;
     // flattened (dy, dx) walk: lane l takes candidates l, l + 32, ... in row-major order
     const int fw = fx_hi - fx_lo + 1, total = fw * (fy_hi - fy_lo + 1);
@@ -830,9 +886,9 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p) {
       {
         const int dx = fx_lo + rx, dy = fy_lo + ry;
         Cand c;
-        if (tc_candidate(p, n, sf, buf[(dy + R) * EW + (dx + R)], cx - M + dx, cy - M + dy, c)) {
+        if (tc_candidate_s(pv, n, sf, buf[(dy + R) * EW + (dx + R)], cx - M + dx, cy - M + dy, c)) {
           ++cnt;
-          const double av = i64_to_f64(c.num) * rsvf * rsqrt(i64_to_f64(c.vg));
+          const double av = i64_to_f64(c.num) * rsvf * (double)c.rsq;
           if (av > a1) {  // a2: the lane's runner-up (only its value is needed)
             a2 = a1;
             a1 = av, c1 = c, x1 = dx, y1 = dy;
@@ -854,11 +910,11 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p) {
       cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
       amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     }
-    const double thr = amax - 0x1p-40;
+    const double thr = amax - 0x1p-20;  // the filter's error (fp32 1/sqrt(vg)) is < 2^-22
     if (!__any_sync(0xffffffffu, a2 >= thr)) {
       // every near-maximal candidate is some lane's best: exact quotients for those
       if (a1 >= thr) {
-        const double z = i64_to_f64(c1.num) / (svf * sqrt(i64_to_f64(c1.vg)));  // exact (zncc_from_moments)
+        const double z = i64_to_f64(c1.num) / (svf * c1.sq);  // exact (zncc_from_moments)
         b.found = 1;
         b.c = z;
         b.dx = x1;
@@ -869,10 +925,10 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p) {
       for (int dy = fy_lo; dy <= fy_hi; ++dy)
         for (int dx = fx_lo + lane; dx <= fx_hi; dx += 32) {
           Cand c;
-          if (tc_candidate(p, n, sf, buf[(dy + R) * EW + (dx + R)], cx - M + dx, cy - M + dy, c)) {
-            const double nd = i64_to_f64(c.num), vd = i64_to_f64(c.vg);
-            if (nd * rsvf * rsqrt(vd) >= thr) {
-              const double z = nd / (svf * sqrt(vd));
+          if (tc_candidate_s(pv, n, sf, buf[(dy + R) * EW + (dx + R)], cx - M + dx, cy - M + dy, c)) {
+            const double nd = i64_to_f64(c.num);
+            if (nd * rsvf * (double)c.rsq >= thr) {
+              const double z = nd / (svf * c.sq);
               if (!b.found || improves(z, dx, dy, b.c, b.dx, b.dy)) {
                 b.found = 1;
                 b.c = z;
@@ -900,15 +956,23 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p) {
 
 // ---- per POI: the full exact ZNCC surface over the +-R window (NaN = no result) ----
 __global__ void __launch_bounds__(256) tc_surface_kernel(TcParams p) {
-  const int k = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
-  const int npoi = (p.re - p.rb) * p.lat.nx;
-  if (k >= npoi) return;
+  // every candidate is written: position data read straight from global memory (L2)
+  const int lane = threadIdx.x & 31;
+  const int k = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  if (k >= (p.re - p.rb) * p.lat.nx) return;
   const int iy = p.rb + k / p.lat.nx, ix = k % p.lat.nx;
+  PosView pv;
+  pv.sq = p.SQ;
+  pv.s1 = p.S1;
+  pv.rsq = p.RSQ;
+  pv.x0 = p.qx_min;
+  pv.y0 = p.qy_min;
+  pv.W = p.SW;
   const int cx = p.lat.cx(ix), cy = p.lat.cy(iy), M = p.M, R = p.R, EW = 2 * R + 1;
-  const int64_t n = (int64_t)p.side * p.side;
+  const uint32_t n = (uint32_t)(p.side * p.side);
   const int fx_lo = max(-R, M - cx), fx_hi = min(R, p.tgt.width - 1 - M - cx);
   const int fy_lo = max(-R, M - cy), fy_hi = min(R, p.tgt.height - 1 - M - cy);
-  const int64_t sf = p.poi_sf[k];
+  const uint32_t sf = (uint32_t)p.poi_sf[k];
   const double svf = p.poi_sqrtvf[k];
   const int64_t* buf = p.sfg + (size_t)k * EW * EW;
   double* out = p.surface + (size_t)k * EW * EW;
@@ -918,8 +982,8 @@ __global__ void __launch_bounds__(256) tc_surface_kernel(TcParams p) {
     double z = qnan;
     Cand c;
     if (svf > 0.0 && dx >= fx_lo && dx <= fx_hi && dy >= fy_lo && dy <= fy_hi &&
-        tc_candidate(p, n, sf, buf[idx], cx - M + dx, cy - M + dy, c))
-      z = i64_to_f64(c.num) / (svf * sqrt(i64_to_f64(c.vg)));  // exact, as bfs.cu
+        tc_candidate_s(pv, n, sf, buf[idx], cx - M + dx, cy - M + dy, c))
+      z = i64_to_f64(c.num) / (svf * c.sq);  // exact, as bfs.cu
     out[idx] = z;
   }
 }
@@ -951,6 +1015,7 @@ bool tc_plan(TcParams& p) {
   if (p.side > 129) return false;
   if ((size_t)p.ref.width * 12 + 16 > 200 * 1024) return false;  // tc_prep_kernel column sums
   if (stats_smem_bytes(p.side) > 200 * 1024) return false;
+  if (pos_smem_bytes(p, 1) > 200 * 1024) return false;
   const int side = p.side, W = p.tgt.width, H = p.tgt.height;
   const int rows = p.re - p.rb;
   if (rows <= 0 || p.lat.nx <= 0) return false;
@@ -1081,7 +1146,7 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
     p.poi_sqrtvf = (double*)pvf;
   }
   if (e == cudaSuccess) e = cudaMallocAsync(&s1, sbytes * 4, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&s2, sbytes * 8, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&s2, sbytes * 12, st);  // SQ (double) + RSQ (float)
   const size_t EW = 2 * (size_t)p.R + 1;
   if (e == cudaSuccess) e = cudaMallocAsync(&part, npoi * EW * EW * sizeof(int64_t), st);
   if (e == cudaSuccess) e = cudaMallocAsync(&tiles, (size_t)std::max(1, p.n_tiles) * 16, st);
@@ -1090,7 +1155,8 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
     return e;
   }
   p.S1 = (uint32_t*)s1;
-  p.S2 = (uint64_t*)s2;
+  p.SQ = (double*)s2;
+  p.RSQ = (float*)((char*)s2 + sbytes * 8);
   p.sfg = (int64_t*)part;
   p.tiles = tiles;
   const bool u8 = p.planes == 1;
@@ -1187,14 +1253,19 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
   }
   // (d) per POI: exact ZNCC -> argmax record, or the full surface for the swarm walk
   if (e == cudaSuccess) {
-    const int blocks = (int)((npoi * 32 + 255) / 256);
+    int sp = 8;  // POIs per CTA strip (one warp each), sharing the staged position data
+    while (sp > 1 && pos_smem_bytes(p, sp) > 96 * 1024) sp /= 2;
+    const size_t sm = pos_smem_bytes(p, sp);
+    dim3 grid((p.lat.nx + sp - 1) / sp, rows);
     StageTimer tm(5, st);
-    if (p.surface)
-      tc_surface_kernel<<<blocks, 256, 0, st>>>(p);
-    else
-      tc_argmax_kernel<<<blocks, 256, 0, st>>>(p);
+    if (p.surface) {
+      tc_surface_kernel<<<(int)((npoi * 32 + 255) / 256), 256, 0, st>>>(p);
+    } else {
+      e = set_smem(tc_argmax_kernel, sm);
+      if (e == cudaSuccess) tc_argmax_kernel<<<grid, 256, sm, st>>>(p, sp);
+    }
     count_launch();
-    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
   }
   cleanup();
   return e;
