@@ -73,7 +73,7 @@ struct TcParams {
   int stages;
   int grid;
   long long* dbg_out;  // optional per-CTA MMA-thread clock breakdown (tools)
-  int dbg;  // DICB200_TC_DBG timing experiments (bit 0: no epilogue math, bit 1: no stage build)
+  int dbg;  // DICB200_TC_DBG=32: MMA-issuer clock breakdown (tools)
   // buffers (device)
   uint8_t* strips;       // [planes][8][W][strip_h] row-shifted column-major reference byte planes
   int strip_h;

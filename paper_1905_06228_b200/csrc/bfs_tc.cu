@@ -503,9 +503,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
   const int NX = p.NX, RWB = p.RWB, CG = p.CG;
   const size_t planeT = (size_t)NX * kStageRows * 16;
 
-  if ((p.dbg & 256) && warp != kProducerWarps) {
-    // timing experiment: MMA issuer alone
-  } else if (warp < kProducerWarps) {
+  if (warp < kProducerWarps) {
     // ================= producers =================
     // group g (kGroupThreads threads) owns ring slot g and builds every stage it with it % S == g,
     // so S stages (and their global-load latencies) are in flight at once.
@@ -536,13 +534,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
       uint32_t* rows = reinterpret_cast<uint32_t*>(base + p.off_rows);
       uint8_t* Bs = base + p.off_B;
       for (int rg = first; rg < p.RG; rg += kGroups) {
-        if (!(p.dbg & 16)) mbar_wait(smem_u32(&empty_bar[g]), ph ^ 1u, (p.dbg & 128) ? 2000 : 64);
-        if (p.dbg & 2) {  // timing experiment: no stage build
-          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          mbar_arrive(smem_u32(&full_bar[g]));
-          ph ^= 1u;
-          continue;
-        }
+        mbar_wait(smem_u32(&empty_bar[g]), ph ^ 1u, 64);
         if (p.rem && rg == p.RG - 1) {
           // remainder rows (e.g. row 40 of a 41-row subset): row-major stage,
           // K = 32 consecutive columns of one subset row per MMA
@@ -657,18 +649,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
         const int a = tc & 1;
         const uint32_t aph = (uint32_t)(tc >> 1) & 1u;
         long long c0 = clock64();
-        if (!(p.dbg & 256)) mbar_wait_warp(smem_u32(&tempty_bar[a]), aph ^ 1u);
+        mbar_wait_warp(smem_u32(&tempty_bar[a]), aph ^ 1u);
         w_empty += clock64() - c0;
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const int pl = warp - kProducerWarps;
         const uint32_t d0 = tmem + (uint32_t)(a * PLANES * p.N_max) + (uint32_t)(pl * t.N);
-        const uint32_t idesc = idesc_i8((p.dbg & 8) ? 16 : t.N);
+        const uint32_t idesc = idesc_i8(t.N);
         const uint32_t b_step = (uint32_t)t.N * 2u;  // B block per cg, 16-byte units
         for (int rg = 0; rg < p.RG; ++rg, ++it) {
           const int s = it % S;
           const uint32_t ph = (uint32_t)(it / S) & 1u;
           long long c1 = clock64();
-          if (!(p.dbg & 256)) mbar_wait_warp(smem_u32(&full_bar[s]), ph);
+          mbar_wait_warp(smem_u32(&full_bar[s]), ph);
           long long c2 = clock64();
           w_full += c2 - c1;
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -683,7 +675,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
                                           (uint32_t)(p.NX2 * 16));
                 const uint64_t db =
                     sdesc(base + (uint32_t)p.off_B + (uint32_t)((ry * p.n_h + h) * t.N * 32), 128, 256);
-                if (!(p.dbg & 2048) && !(pl == 1 && (p.dbg & 4))) mma_i8_elect(d0, da, db, idesc, 1u);
+                mma_i8_elect(d0, da, db, idesc, 1u);
               }
             umma_commit_elect(smem_u32(&empty_bar[s]));
             t_issue += clock64() - c2;
@@ -693,7 +685,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
           uint64_t db = sdesc(base + (uint32_t)p.off_B, 128, 256);
           for (int cg = 0; cg < CG; ++cg) {
             const uint32_t acc = (rg | cg) != 0;
-            if (!(p.dbg & 2048) && !(pl == 1 && (p.dbg & 4))) mma_i8_elect(d0, da, db, idesc, acc);
+            mma_i8_elect(d0, da, db, idesc, acc);
             da += (uint64_t)(4 * kStageRows);
             db += (uint64_t)b_step;
           }
@@ -1009,7 +1001,8 @@ int sm_count() {
 
 bool tc_plan(TcParams& p) {
   if (std::getenv("DICB200_BFS_LEGACY")) return false;  // A/B switch: CUDA-core kernel
-  p.dbg = std::getenv("DICB200_TC_DBG") ? std::atoi(std::getenv("DICB200_TC_DBG")) : 0;  // timing experiments only
+  // DICB200_TC_DBG=32: per-CTA clock breakdown of the MMA issuer (tools)
+  p.dbg = std::getenv("DICB200_TC_DBG") ? std::atoi(std::getenv("DICB200_TC_DBG")) : 0;
   if (p.R < 0 || p.M < 0) return false;
   p.side = 2 * p.M + 1;
   if (p.side > 129) return false;
@@ -1243,10 +1236,6 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
         for (int k = 0; k < 4; ++k) a[k] += (double)h[(size_t)b * 4 + k] / p.grid;
       fprintf(stderr, "[tc dbg] clk total %.0f  wait_full %.0f  wait_tmem %.0f  mma-loop %.0f  (tiles/cta %.1f)\n", a[0],
               a[1], a[2], a[3], (double)p.n_tiles / p.grid);
-      double b[4] = {0, 0, 0, 0};
-      for (int bb = 0; bb < p.grid; ++bb)
-        for (int k = 0; k < 4; ++k) b[k] += (double)h[(size_t)(p.grid + bb) * 4 + k] / p.grid;
-      fprintf(stderr, "[tc dbg] epilogue: pre %.0f  end-barrier %.0f  tmem->smem %.0f  per-poi(incl barrier) %.0f\n", b[0], b[1], b[2], b[3]);
       cudaFree(dbg_buf);
       p.dbg_out = nullptr;
     }
