@@ -43,6 +43,11 @@ namespace {
 constexpr int kTX = 16, kTY = 8;  // positions per tile: x, y (M = 128)
 constexpr int kMaxTilePoi = 128;  // per-tile POI limit (N <= 256 for byte planes)
 constexpr int kMaxStages = 8;
+// MMA-issuer clock breakdown (DICB200_TC_DBG=32 with -DDICB200_TC_CLOCKS=1; tools)
+#ifndef DICB200_TC_CLOCKS
+#define DICB200_TC_CLOCKS 0
+#endif
+constexpr bool kClocks = DICB200_TC_CLOCKS;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -642,15 +647,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
     // one elected lane issues each tcgen05.mma / commit.
     {
       int it = 0, tc = 0;
-      long long w_full = 0, w_empty = 0, t_issue = 0, t0 = clock64();
+      long long w_full = 0, w_empty = 0, t_issue = 0, t0 = kClocks ? clock64() : 0;
       for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
         TileInfo t;
         if (!tile_info<PLANES>(p, tile, t)) continue;
         const int a = tc & 1;
         const uint32_t aph = (uint32_t)(tc >> 1) & 1u;
-        long long c0 = clock64();
+        const long long c0 = kClocks ? clock64() : 0;
         mbar_wait_warp(smem_u32(&tempty_bar[a]), aph ^ 1u);
-        w_empty += clock64() - c0;
+        if (kClocks) w_empty += clock64() - c0;
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const int pl = warp - kProducerWarps;
         const uint32_t d0 = tmem + (uint32_t)(a * PLANES * p.N_max) + (uint32_t)(pl * t.N);
@@ -659,10 +664,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
         for (int rg = 0; rg < p.RG; ++rg, ++it) {
           const int s = it % S;
           const uint32_t ph = (uint32_t)(it / S) & 1u;
-          long long c1 = clock64();
+          const long long c1 = kClocks ? clock64() : 0;
           mbar_wait_warp(smem_u32(&full_bar[s]), ph);
-          long long c2 = clock64();
-          w_full += c2 - c1;
+          const long long c2 = kClocks ? clock64() : 0;
+          if (kClocks) w_full += c2 - c1;
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           const uint32_t base = smem_u32(sm + (size_t)s * p.stage_bytes);
           if (p.rem && rg == p.RG - 1) {
@@ -678,7 +683,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
                 mma_i8_elect(d0, da, db, idesc, 1u);
               }
             umma_commit_elect(smem_u32(&empty_bar[s]));
-            t_issue += clock64() - c2;
+            if (kClocks) t_issue += clock64() - c2;
             continue;
           }
           uint64_t da = sdesc(base + (uint32_t)(pl * planeT), kStageRows * 16, 16);
@@ -690,12 +695,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
             db += (uint64_t)b_step;
           }
           umma_commit_elect(smem_u32(&empty_bar[s]));
-          t_issue += clock64() - c2;
+          if (kClocks) t_issue += clock64() - c2;
         }
         umma_commit_elect(smem_u32(&tfull_bar[a]));
         ++tc;
       }
-      if (p.dbg_out && lane == 0 && warp == kProducerWarps) {
+      if (kClocks && p.dbg_out && lane == 0 && warp == kProducerWarps) {
         p.dbg_out[blockIdx.x * 4 + 0] = clock64() - t0;
         p.dbg_out[blockIdx.x * 4 + 1] = w_full;
         p.dbg_out[blockIdx.x * 4 + 2] = w_empty;
