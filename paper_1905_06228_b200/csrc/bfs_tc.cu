@@ -539,8 +539,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
       uint32_t* rows = reinterpret_cast<uint32_t*>(base + p.off_rows);
       uint8_t* Bs = base + p.off_B;
       for (int rg = first; rg < p.RG; rg += kGroups) {
-        mbar_wait(smem_u32(&empty_bar[g]), ph ^ 1u, 64);
         if (p.rem && rg == p.RG - 1) {
+          mbar_wait(smem_u32(&empty_bar[g]), ph ^ 1u, 64);
           // remainder rows (e.g. row 40 of a 41-row subset): row-major stage,
           // K = 32 consecutive columns of one subset row per MMA
           build_remainder_stage<PLANES>(p, t, poi_ix, rg * 8, T, reinterpret_cast<uint8_t*>(rows), Bs, gt, g);
@@ -550,29 +550,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
           named_sync(1 + g, kGroupThreads);
           continue;
         }
-        // (a) B: the tile's reference blocks (8 subset rows x 4 columns per MMA,
-        //     K-major) as 8-byte column runs from the strip images; rows/columns
-        //     past the subset are zero-filled (cp.async src-size)
-        {
-          const int r0 = rg * 8, vrows = min(8, p.side - r0);
-          const int W = p.ref.width, Hs = p.strip_h;
-          for (int jp = gt >> 2; jp < NN; jp += kGroupThreads / 4) {
-            const int jc = gt & 3;
-            const int j = jp / PLANES, pl = jp - j * PLANES;
-            const int2 o = poi_tab[j];  // subset top-left (x, y) in the reference
-            const int ry = o.y + r0, sft = ry & 7;
-            const uint8_t* strip = p.strips + ((size_t)(pl * 8 + sft) * (Hs / 8) + (ry >> 3)) * W * 8;
-            const uint8_t* src = strip + (size_t)(o.x + jc) * 8;
-            const size_t src_step = 32;  // next column group: 4 columns x 8 bytes
-            uint8_t* dst = Bs + (jp & 7) * 16 + (jp >> 3) * 256 + (jc >> 1) * 128 + (jc & 1) * 8;
-            const size_t dst_step = (size_t)t.N * 32;
-            const int cg_full = (p.side - jc + 3) / 4;  // column groups holding column jc + 4 cg < side
-            for (int cg = 0; cg < CG; ++cg, src += src_step, dst += dst_step)
-              cp_async8_zfill(dst, cg < cg_full ? src : strip, cg < cg_full ? vrows : 0);
-          }
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-        // (b) target rows [Y0 + 8 rg, +16) x [X0, X0 + 4 RW4): 4 pixels -> one word per byte plane
+        // (b) target rows (no wait: the MMAs never read the row buffer) [Y0 + 8 rg, +16) x [X0, X0 + 4 RW4): 4 pixels -> one word per byte plane
         {
           const int gy0 = t.Y0 + rg * 8;
           for (int w = gt & 15; w < RW4; w += 16) {
@@ -608,6 +586,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) bfs_tc_kernel(TcParams p) {
             }
           }
         }
+        mbar_wait(smem_u32(&empty_bar[g]), ph ^ 1u, 64);  // T and B of this slot are free
+        // (a) B: the tile's reference blocks (8 subset rows x 4 columns per MMA,
+        //     K-major) as 8-byte column runs from the strip images; rows/columns
+        //     past the subset are zero-filled (cp.async src-size)
+        {
+          const int r0 = rg * 8, vrows = min(8, p.side - r0);
+          const int W = p.ref.width, Hs = p.strip_h;
+          for (int jp = gt >> 2; jp < NN; jp += kGroupThreads / 4) {
+            const int jc = gt & 3;
+            const int j = jp / PLANES, pl = jp - j * PLANES;
+            const int2 o = poi_tab[j];  // subset top-left (x, y) in the reference
+            const int ry = o.y + r0, sft = ry & 7;
+            const uint8_t* strip = p.strips + ((size_t)(pl * 8 + sft) * (Hs / 8) + (ry >> 3)) * W * 8;
+            const uint8_t* src = strip + (size_t)(o.x + jc) * 8;
+            const size_t src_step = 32;  // next column group: 4 columns x 8 bytes
+            uint8_t* dst = Bs + (jp & 7) * 16 + (jp >> 3) * 256 + (jc >> 1) * 128 + (jc & 1) * 8;
+            const size_t dst_step = (size_t)t.N * 32;
+            const int cg_full = (p.side - jc + 3) / 4;  // column groups holding column jc + 4 cg < side
+            for (int cg = 0; cg < CG; ++cg, src += src_step, dst += dst_step)
+              cp_async8_zfill(dst, cg < cg_full ? src : strip, cg < cg_full ? vrows : 0);
+          }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
         named_sync(1 + g, kGroupThreads);
         // (c) 16-pixel windows, four column offsets per item:
         //     T[pl][X][y][0..15] = rows[pl][y][X .. X+15], X = 4 X4 + s
