@@ -371,7 +371,7 @@ __global__ void tc_tiles_kernel(TcParams p) {
 //   warps 5-8 : epilogue — TMEM -> exact moments -> ZNCC -> per-POI argmax
 // Stages form a ring (full/empty mbarriers); the two TMEM accumulators let the
 // epilogue of tile t overlap the MMAs of tile t+1.
-constexpr int kGroups = 4, kGroupThreads = 64;  // producer groups = ring slots
+constexpr int kGroups = 5, kGroupThreads = 64;  // producer groups = ring slots
 constexpr int kProducerWarps = kGroups * kGroupThreads / 32;
 constexpr int kProducers = kGroups * kGroupThreads, kEpilogue = 256;
 constexpr int kMmaWarps = 2;  // one tcgen05 issuer per byte plane of the target
