@@ -386,6 +386,7 @@ __device__ __forceinline__ void icgn_pass_fast2(const PassCtx& c, const Walk& w0
   f2x dxy = pk2(w0.dxf, w0.dyf);
   int roff = w0.roff;
   const int cnt = w0.npl - (w0.last_valid ? 0 : 1);
+  const float* Tb = c.T + c.ioffy * c.tP + c.ioffx;  // target-region origin in subset-local coordinates
 #pragma unroll 2
   for (int i = 0; i < cnt; ++i) {
     float dx, dy;
@@ -397,7 +398,7 @@ __device__ __forceinline__ void icgn_pass_fast2(const PassCtx& c, const Walk& w0
     up2(xy, xl, yl);
     const float flx = floorf(xl), fly = floorf(yl);  // subset-local: exact frac
     const float fx = xl - flx, fy = yl - fly;
-    const float* t = c.T + ((int)fly + c.ioffy) * c.tP + ((int)flx + c.ioffx);
+    const float* t = Tb + (int)fly * c.tP + (int)flx;
     const float f00 = t[0], f10 = t[1], f01 = t[c.tP], f11 = t[c.tP + 1];
     const float a10 = f10 - f00, a01 = f01 - f00, a11 = (f11 - f10) - a01;
     const float gv = fmaf(a11 * fx, fy, fmaf(a01, fy, fmaf(a10, fx, f00)));
@@ -440,6 +441,7 @@ __device__ __forceinline__ void pixel_pass(const PassCtx& c, const ImageView& tg
   bad = 0;
   Walk w = w0;
   const int cnt = w.npl - (w.last_valid ? 0 : 1);
+  const float* Tb = c.T + c.ioffy * c.tP + c.ioffx;  // target-region origin in subset-local coordinates
 #pragma unroll 2
   for (int i = 0; i < cnt; ++i) {
     const float dx = w.dxf, dy = w.dyf;
@@ -449,7 +451,7 @@ __device__ __forceinline__ void pixel_pass(const PassCtx& c, const ImageView& tg
     if (FAST) {
       const float flx = floorf(xl), fly = floorf(yl);  // subset-local: exact frac
       const float fx = xl - flx, fy = yl - fly;
-      const float* t = c.T + ((int)fly + c.ioffy) * c.tP + ((int)flx + c.ioffx);
+      const float* t = Tb + (int)fly * c.tP + (int)flx;
       const float f00 = t[0], f10 = t[1], f01 = t[c.tP], f11 = t[c.tP + 1];
       const float a10 = f10 - f00, a01 = f01 - f00, a11 = (f00 + f11) - f10 - f01;
       gv = fmaf(a11 * fx, fy, fmaf(a01, fy, fmaf(a10, fx, f00)));
