@@ -208,6 +208,27 @@ void dicb200_reset_launch_count(void);
 void dicb200_profile_enable(int on);
 int dicb200_profile_read(double* ms_out, uint64_t* launches_out);
 
+/* ---- f-2 image ingestion (image.cpp:40-138): portable graymaps --------------
+ * dicb200_load_pgm: P5 (binary) / P2 (ASCII) graymap. 8-bit exactly as
+ * dic::load_image (byte n -> gray level n; same errors, DICB200_ERR_INVALID with
+ * the reference's message). DICB200_PGM_16BIT also accepts maxval 256..65535
+ * (P5: big-endian 2-byte samples), which the reference rejects. Call with
+ * pixels == NULL to read the header; then with width*height elements (u8 for
+ * maxval <= 255, else u16) — e.g. dicb200_host_alloc'ed pinned memory, which
+ * analyze_sequence uploads asynchronously.
+ * dicb200_save_pgm: 8-bit P5 like dic::save_pgm (values clamped to 255).
+ * dicb200_sequence_files: regular files of `dir` matching the glob `pattern`,
+ * lexicographic by filename, as NUL-separated names (dic::load_sequence's file
+ * list; >= 2 required). Call with buf == NULL for the size. */
+#define DICB200_PGM_16BIT 1
+dicb200_status dicb200_load_pgm(const char* path, int32_t flags, int32_t* width, int32_t* height, int32_t* dtype,
+                                int32_t* maxval, void* pixels, size_t cap);
+dicb200_status dicb200_save_pgm(const char* path, const dicb200_image* img);
+dicb200_status dicb200_sequence_files(const char* dir, const char* pattern, char* buf, size_t cap, size_t* needed,
+                                      size_t* count);
+void* dicb200_host_alloc(size_t bytes); /* pinned host memory (NULL on failure) */
+void dicb200_host_free(void* p);
+
 /* Release pooled device memory on all devices. */
 void dicb200_shutdown(void);
 

@@ -4,6 +4,7 @@
 // C restatement (oracle/dic_oracle.c) and to generate tests/golden/, and by
 // bench.py --impl reference / cpu_baseline as the reference's own CPU path.
 // Never linked into the product.
+#include <cstdio>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -281,5 +282,39 @@ int dicref_grid(int w, int h, int half_width, int spacing, int margin, int32_t* 
 }
 
 unsigned dicref_hardware_threads(void) { return std::thread::hardware_concurrency(); }
+
+// dic::load_image / dic::load_sequence (image.cpp:60-138) for the ingestion
+// parity tests: 0 = ok, 1 = dic::Error (message copied to err).
+int dicref_load_image(const char* path, double* out, size_t cap, int* w, int* h, char* err, size_t errcap) {
+  try {
+    const dic::GrayImage img = dic::load_image(path);
+    *w = img.width();
+    *h = img.height();
+    if (out && cap >= img.pixels().size()) std::copy(img.pixels().begin(), img.pixels().end(), out);
+    return 0;
+  } catch (const dic::Error& e) {
+    std::snprintf(err, errcap, "%s", e.what());
+    return 1;
+  }
+}
+
+int dicref_load_sequence(const char* dir, const char* pattern, double* out, size_t cap, int* n, int* w, int* h,
+                         int* ids, size_t ids_cap, char* err, size_t errcap) {
+  try {
+    const auto seq = dic::load_sequence(dir, pattern);
+    *n = (int)seq.size();
+    *w = seq.front().width();
+    *h = seq.front().height();
+    const size_t per = seq.front().pixels().size();
+    for (size_t i = 0; i < seq.size(); ++i) {
+      if (i < ids_cap) ids[i] = seq[i].id();
+      if (out && cap >= per * (i + 1)) std::copy(seq[i].pixels().begin(), seq[i].pixels().end(), out + per * i);
+    }
+    return 0;
+  } catch (const dic::Error& e) {
+    std::snprintf(err, errcap, "%s", e.what());
+    return 1;
+  }
+}
 
 }  // extern "C"

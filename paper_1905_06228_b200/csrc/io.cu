@@ -1,0 +1,190 @@
+// f-2 image ingestion: portable graymaps and frame sequences,
+// restating image.cpp:40-138 of the reference (load_image, save_pgm,
+// load_sequence) in native host code, plus pinned host buffers so loaded
+// frames reach analyze_sequence's asynchronous uploads directly.
+//
+// 8-bit P5/P2 behaves exactly as the reference (byte n -> gray level n, the same
+// error conditions and message prefixes). DICB200_PGM_16BIT additionally accepts
+// maxval 256..65535 (P5: two big-endian bytes per sample, the Netpbm layout),
+// which the reference rejects as "unsupported format (only 8-bit graymaps)".
+#include <dirent.h>
+#include <fnmatch.h>
+#include <sys/stat.h>
+
+#include <algorithm>
+#include <cctype>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+using namespace dicb200;
+
+namespace {
+
+dicb200_status io_error(const std::string& msg) {
+  set_error(msg.c_str());
+  return DICB200_ERR_INVALID;
+}
+
+struct File {
+  FILE* f = nullptr;
+  explicit File(const char* path, const char* mode) : f(std::fopen(path, mode)) {}
+  ~File() {
+    if (f) std::fclose(f);
+  }
+};
+
+// Header fields may be separated by whitespace and '#' comment lines
+// (image.cpp:44-57); false = unreadable header.
+bool next_header_int(FILE* f, int* value) {
+  int c;
+  while ((c = std::fgetc(f)) != EOF) {
+    if (c == '#') {
+      while ((c = std::fgetc(f)) != EOF && c != '\n') {
+      }
+    } else if (!std::isspace(c)) {
+      std::ungetc(c, f);
+      break;
+    }
+  }
+  return std::fscanf(f, "%d", value) == 1;
+}
+
+// ASCII sample, as `in >> value` (skips whitespace; no comments in the raster).
+bool next_ascii_int(FILE* f, long* value) { return std::fscanf(f, "%ld", value) == 1; }
+
+}  // namespace
+
+extern "C" {
+
+dicb200_status dicb200_load_pgm(const char* path, int32_t flags, int32_t* width, int32_t* height, int32_t* dtype,
+                                int32_t* maxval_out, void* pixels, size_t cap) {
+  if (!path) return io_error("null argument");
+  const std::string p(path);
+  File in(path, "rb");
+  if (!in.f) return io_error("unreadable file: " + p);
+  char magic[2] = {0, 0};
+  if (std::fread(magic, 1, 2, in.f) != 2 || magic[0] != 'P' || (magic[1] != '5' && magic[1] != '2'))
+    return io_error("unsupported format (want P5 or P2 graymap): " + p);
+  const bool binary = magic[1] == '5';
+  int w, h, maxval;
+  if (!next_header_int(in.f, &w) || !next_header_int(in.f, &h) || !next_header_int(in.f, &maxval))
+    return io_error("unreadable portable graymap header");
+  if (w < 1 || h < 1) return io_error("zero-dimension image: " + p);
+  const bool wide_ok = (flags & DICB200_PGM_16BIT) != 0;
+  if (maxval < 1 || maxval > (wide_ok ? 65535 : 255))
+    return io_error("unsupported format (only 8-bit graymaps): " + p);
+  const int dt = maxval <= 255 ? DICB200_U8 : DICB200_U16;
+  if (width) *width = w;
+  if (height) *height = h;
+  if (dtype) *dtype = dt;
+  if (maxval_out) *maxval_out = maxval;
+  if (!pixels) return DICB200_OK;  // header query
+  const size_t n = (size_t)w * (size_t)h;
+  if (cap < n) {
+    set_error("pixel buffer smaller than width * height");
+    return DICB200_ERR_CAPACITY;
+  }
+  if (binary) {
+    std::fgetc(in.f);  // the single whitespace byte after maxval
+    if (dt == DICB200_U8) {
+      if (std::fread(pixels, 1, n, in.f) != n) return io_error("unreadable file (truncated pixel data): " + p);
+    } else {
+      std::vector<unsigned char> raw(2 * n);
+      if (std::fread(raw.data(), 1, raw.size(), in.f) != raw.size())
+        return io_error("unreadable file (truncated pixel data): " + p);
+      uint16_t* out = static_cast<uint16_t*>(pixels);
+      for (size_t i = 0; i < n; ++i) {
+        const uint16_t v = (uint16_t)((raw[2 * i] << 8) | raw[2 * i + 1]);
+        if (v > maxval) return io_error("unreadable file (sample out of range): " + p);
+        out[i] = v;
+      }
+    }
+  } else {
+    for (size_t i = 0; i < n; ++i) {
+      long v;
+      if (!next_ascii_int(in.f, &v)) return io_error("unreadable file (truncated pixel data): " + p);
+      if (v < 0 || v > maxval) return io_error("unreadable file (sample out of range): " + p);
+      if (dt == DICB200_U8)
+        static_cast<uint8_t*>(pixels)[i] = (uint8_t)v;
+      else
+        static_cast<uint16_t*>(pixels)[i] = (uint16_t)v;
+    }
+  }
+  return DICB200_OK;
+}
+
+dicb200_status dicb200_save_pgm(const char* path, const dicb200_image* img) {
+  if (!path || !img || !img->data) return io_error("null argument");
+  File out(path, "wb");
+  if (!out.f) return io_error(std::string("cannot open for writing: ") + path);
+  std::fprintf(out.f, "P5\n%d %d\n255\n", img->width, img->height);
+  const int pitch = img->pitch > 0 ? img->pitch : img->width;
+  std::vector<unsigned char> row((size_t)img->width);
+  for (int y = 0; y < img->height; ++y) {
+    for (int x = 0; x < img->width; ++x) {
+      // save_pgm (image.cpp:98-104): round, clamp to [0, 255]
+      const unsigned v = img->dtype == DICB200_U8 ? static_cast<const uint8_t*>(img->data)[(size_t)y * pitch + x]
+                                                  : static_cast<const uint16_t*>(img->data)[(size_t)y * pitch + x];
+      row[x] = (unsigned char)std::min(v, 255u);
+    }
+    if (std::fwrite(row.data(), 1, row.size(), out.f) != row.size())
+      return io_error(std::string("write failed: ") + path);
+  }
+  return DICB200_OK;
+}
+
+dicb200_status dicb200_sequence_files(const char* dir, const char* pattern, char* buf, size_t cap, size_t* needed,
+                                      size_t* count) {
+  if (!dir || !pattern) return io_error("null argument");
+  struct stat sb;
+  if (stat(dir, &sb) != 0 || !S_ISDIR(sb.st_mode)) return io_error(std::string("not a directory: ") + dir);
+  DIR* d = opendir(dir);
+  if (!d) return io_error(std::string("not a directory: ") + dir);
+  std::vector<std::string> names;
+  while (dirent* e = readdir(d)) {
+    const std::string full = std::string(dir) + "/" + e->d_name;
+    struct stat fs;
+    if (stat(full.c_str(), &fs) != 0 || !S_ISREG(fs.st_mode)) continue;  // regular files only
+    if (fnmatch(pattern, e->d_name, 0) == 0) names.push_back(e->d_name);
+  }
+  closedir(d);
+  std::sort(names.begin(), names.end());  // lexicographic by filename (image.cpp:121-123)
+  if (names.size() < 2)
+    return io_error(std::string("insufficient images (need at least 2 matching '") + pattern + "')");
+  size_t total = 0;
+  for (const auto& s : names) total += s.size() + 1;
+  if (needed) *needed = total;
+  if (count) *count = names.size();
+  if (!buf) return DICB200_OK;
+  if (cap < total) {
+    set_error("name buffer too small");
+    return DICB200_ERR_CAPACITY;
+  }
+  for (const auto& s : names) {
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    buf += s.size() + 1;
+  }
+  return DICB200_OK;
+}
+
+void* dicb200_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void dicb200_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

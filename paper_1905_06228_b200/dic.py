@@ -223,6 +223,14 @@ def lib() -> C.CDLL:
         L.dicb200_sequence_pairs.argtypes = [C.c_int32, C.c_int32, C.c_void_p]
         L.dicb200_partition_ranges.argtypes = [C.c_size_t, C.c_int32, C.c_void_p]
         L.dicb200_synth_render.argtypes = [C.POINTER(_abi.SynthSpecC), C.c_void_p, C.c_int32, C.c_int32]
+        L.dicb200_load_pgm.argtypes = [C.c_char_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                       C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_void_p, C.c_size_t]
+        L.dicb200_save_pgm.argtypes = [C.c_char_p, C.POINTER(_abi.Image)]
+        L.dicb200_sequence_files.argtypes = [C.c_char_p, C.c_char_p, C.c_void_p, C.c_size_t,
+                                             C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]
+        L.dicb200_host_alloc.restype = C.c_void_p
+        L.dicb200_host_alloc.argtypes = [C.c_size_t]
+        L.dicb200_host_free.argtypes = [C.c_void_p]
         L.dicb200_synth_displacement.argtypes = [
             C.POINTER(_abi.SynthSpecC), C.c_double, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double),
         ]
@@ -235,6 +243,123 @@ def _raise(status: int) -> None:
     if status == 1:
         raise DicError(msg)
     raise RuntimeError(f"dicb200 status {status}: {msg}")
+
+
+def load_image(path, allow_16bit: bool = False, id: int = 0) -> GrayImage:
+    """image.cpp:60-96 (dic::load_image), native: P5/P2 graymaps, byte n -> gray
+    level n; raises DicError with the reference's messages. allow_16bit also
+    accepts maxval 256..65535 (the reference rejects it)."""
+    L = lib()
+    w, h, dt, mv = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+    flags = 1 if allow_16bit else 0
+    st = L.dicb200_load_pgm(str(path).encode(), flags, C.byref(w), C.byref(h), C.byref(dt), C.byref(mv), None, 0)
+    if st:
+        _raise(st)
+    px = np.empty((h.value, w.value), np.uint8 if dt.value == _abi.U8 else np.uint16)
+    st = L.dicb200_load_pgm(str(path).encode(), flags, C.byref(w), C.byref(h), C.byref(dt), C.byref(mv),
+                            px.ctypes.data, px.size)
+    if st:
+        _raise(st)
+    return GrayImage(px, id)
+
+
+def save_pgm(img: GrayImage, path) -> None:
+    """image.cpp:98-111 (dic::save_pgm): 8-bit P5, values clamped to 255."""
+    im = img.as_c()
+    st = lib().dicb200_save_pgm(str(path).encode(), C.byref(im))
+    if st:
+        _raise(st)
+
+
+def sequence_files(directory, pattern: str) -> List[str]:
+    """The file list of dic::load_sequence (image.cpp:113-138): regular files
+    matching the glob, lexicographic by filename, at least two."""
+    L = lib()
+    need, cnt = C.c_size_t(), C.c_size_t()
+    st = L.dicb200_sequence_files(str(directory).encode(), pattern.encode(), None, 0, C.byref(need), C.byref(cnt))
+    if st:
+        _raise(st)
+    buf = C.create_string_buffer(need.value)
+    st = L.dicb200_sequence_files(str(directory).encode(), pattern.encode(), buf, need.value, C.byref(need),
+                                  C.byref(cnt))
+    if st:
+        _raise(st)
+    return [n.decode() for n in buf.raw[: need.value].split(b"\0")[: cnt.value]]
+
+
+class PinnedBlock:
+    """Page-locked host memory from dicb200_host_alloc (cudaMallocHost), freed
+    when the last array viewing it is collected. Frames in pinned memory are
+    uploaded by analyze_sequence with asynchronous copies that overlap the
+    previous pair's kernels."""
+
+    def __init__(self, nbytes: int):
+        self.nbytes = max(int(nbytes), 1)
+        self.ptr = lib().dicb200_host_alloc(self.nbytes)
+        if not self.ptr:
+            raise DicError("pinned host allocation failed (%d bytes)" % self.nbytes)
+        self.__array_interface__ = {"shape": (self.nbytes,), "typestr": "|u1", "data": (self.ptr, False),
+                                    "version": 3}
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            lib().dicb200_host_free(C.c_void_p(self.ptr))
+            self.ptr = None
+
+    def view(self, offset: int, shape, dtype) -> np.ndarray:
+        n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        return np.asarray(self)[offset:offset + n].view(dtype).reshape(shape)
+
+
+def _load_into(path, allow_16bit, out: np.ndarray, dtype_code: int):
+    L = lib()
+    w, h, dt, mv = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+    st = L.dicb200_load_pgm(str(path).encode(), 1 if allow_16bit else 0, C.byref(w), C.byref(h), C.byref(dt),
+                            C.byref(mv), out.ctypes.data, out.size)
+    if st:
+        _raise(st)
+    assert dt.value == dtype_code
+
+
+def load_sequence(directory, pattern: str, allow_16bit: bool = False, pinned: bool = False) -> List[GrayImage]:
+    """image.cpp:113-138 (dic::load_sequence): ids are the sequence positions;
+    frames must share dimensions ("dimension mismatch in sequence: <file>").
+    pinned=True reads every frame straight into one page-locked host block."""
+    names = sequence_files(directory, pattern)
+    if pinned:
+        return _load_sequence_pinned(directory, names, allow_16bit)
+    images: List[GrayImage] = []
+    for i, name in enumerate(names):
+        path = os.path.join(str(directory), name)
+        img = load_image(path, allow_16bit, id=i)
+        if images and (img.width() != images[0].width() or img.height() != images[0].height()):
+            raise DicError("dimension mismatch in sequence: " + path)
+        images.append(img)
+    return images
+
+
+def _load_sequence_pinned(directory, names: List[str], allow_16bit: bool) -> List[GrayImage]:
+    L = lib()
+    heads = []
+    for name in names:  # header pass: dimensions, sample width, error order as the reference
+        path = os.path.join(str(directory), name)
+        w, h, dt, mv = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        st = L.dicb200_load_pgm(path.encode(), 1 if allow_16bit else 0, C.byref(w), C.byref(h), C.byref(dt),
+                                C.byref(mv), None, 0)
+        if st:
+            _raise(st)
+        if heads and (w.value != heads[0][1] or h.value != heads[0][2]):
+            raise DicError("dimension mismatch in sequence: " + path)
+        heads.append((path, w.value, h.value, dt.value))
+    sizes = [w * h * (1 if dt == _abi.U8 else 2) for _, w, h, dt in heads]
+    offs = np.concatenate([[0], np.cumsum([(s + 255) // 256 * 256 for s in sizes])]).astype(np.int64)
+    block = PinnedBlock(int(offs[-1]))
+    images: List[GrayImage] = []
+    for i, (path, w, h, dt) in enumerate(heads):
+        arr = block.view(int(offs[i]), (h, w), np.uint8 if dt == _abi.U8 else np.uint16)
+        _load_into(path, allow_16bit, arr, dt)
+        images.append(GrayImage(arr, i))
+    return images
 
 
 def grid_subsets(width: int, height: int, half_width: int, spacing: int, margin: int) -> List[Tuple[int, int]]:
