@@ -229,6 +229,73 @@ dicb200_status dicb200_sequence_files(const char* dir, const char* pattern, char
 void* dicb200_host_alloc(size_t bytes); /* pinned host memory (NULL on failure) */
 void dicb200_host_free(void* p);
 
+/* ---- f-4 accuracy sweep (accuracy.hpp:15-50, accuracy.cpp:10-78; synth.hpp:14-66) ----
+ * dicb200_synth_speckle / dicb200_synth_warped_pair restate dic::synth_speckle
+ * (synth.cpp:55-93) and dic::synth_warped_pair (synth.cpp:127-172) on the host,
+ * bit-identical doubles (same mt19937_64 stream, same libm calls, same
+ * evaluation order); errors as the reference ("textureless pattern", "zero-dimension
+ * image", "invalid blob radius range", "warp not invertible", "warp out of bounds").
+ * dicb200_accuracy_sweep replaces dic::run_accuracy_sweep: the frames are
+ * synthesized as above, quantized to integer gray levels (round(value * gray_scale):
+ * gray_scale 1 = the reference's own 8-bit PGM round trip, 256 = 16-bit, keeping
+ * 8 fractional bits of the reference's doubles), and every (offset, fraction)
+ * warp of every combo is analysed on the GPU — one pipelined fixed-first
+ * sequence per combo, so pair_index == warp index as in accuracy.cpp:49-50.
+ * Pass / flag rules are the reference's (accuracy.cpp:64-72). */
+typedef struct {  /* SpeckleParams, synth.hpp:14-23 */
+  int32_t blob_count;      /* <= 0 in a sweep: scale by area (default_blob_count) */
+  int32_t texture_window;  /* 31 */
+  double sigma_min;        /* 1.0 */
+  double sigma_max;        /* 2.5 */
+  double amp_min;          /* 40 */
+  double amp_max;          /* 140 */
+  double background;       /* 128 */
+  double variance_floor;   /* 25 */
+} dicb200_speckle_params;
+
+typedef struct {  /* WarpSpec, synth.hpp:30-35 */
+  double u, v, ux, uy, vx, vy;
+} dicb200_warp_spec;
+
+typedef struct {  /* SweepConfig, accuracy.hpp:15-23 */
+  int32_t width;                 /* 160 */
+  int32_t height;                /* 160 */
+  uint64_t seed;                 /* 7 */
+  dicb200_speckle_params speckle;
+  dicb200_run_config base;       /* methods overridden per combo */
+  const double* fractions;       /* {0.1, 0.25, 0.5, 0.75, 0.9} */
+  int32_t n_fractions;
+  int32_t n_offsets;
+  const int32_t* offsets;        /* {-3, 0, 4} */
+  int32_t gray_scale;            /* B200: 1 (u8) or 256 (u16, default) */
+  int32_t pad;
+} dicb200_sweep_config;
+
+typedef struct {  /* ComboAccuracy, accuracy.hpp:25-34 */
+  int32_t integer_method;
+  int32_t subpixel_method;
+  double max_err;
+  double mean_err;
+  int32_t measurements;
+  int32_t unconverged;
+  int32_t pass;
+  int32_t mean_flagged;
+} dicb200_combo_accuracy;
+
+void dicb200_default_speckle(dicb200_speckle_params* p);
+int32_t dicb200_default_blob_count(int32_t width, int32_t height); /* synth.cpp:14-16 */
+/* fractions/offsets point at static default arrays. */
+void dicb200_default_sweep(dicb200_sweep_config* cfg);
+dicb200_status dicb200_synth_speckle(int32_t width, int32_t height, uint64_t seed,
+                                     const dicb200_speckle_params* params, double* out /* w*h */);
+dicb200_status dicb200_synth_warped_pair(const double* reference, int32_t width, int32_t height,
+                                         const dicb200_warp_spec* warp, double* target /* w*h */,
+                                         uint8_t* valid_mask /* w*h, may be NULL */);
+/* combos: n pairs (integer_method, subpixel_method). */
+dicb200_status dicb200_accuracy_sweep(const int32_t* combos, size_t n_combos, const dicb200_sweep_config* cfg,
+                                      dicb200_combo_accuracy* out, int32_t* warp_count, int32_t* poi_count,
+                                      double* elapsed_s);
+
 /* Release pooled device memory on all devices. */
 void dicb200_shutdown(void);
 

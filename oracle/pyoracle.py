@@ -224,3 +224,50 @@ class Oracle:
         out = np.zeros(n, np.float64)
         self._f("uniform01")(seed, n, out.ctypes.data)
         return out
+
+
+# -- f-4: the reference's generators and accuracy sweep (reference build only) ----
+def _ref_lib():
+    L = C.CDLL(PATHS["reference"])
+    L.dicref_synth_speckle.argtypes = [C.c_int, C.c_int, C.c_uint64, C.POINTER(_abi.SpeckleParamsC), C.c_void_p,
+                                       C.c_char_p, C.c_size_t]
+    L.dicref_synth_warped_pair.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(_abi.WarpSpecC), C.c_void_p,
+                                           C.c_void_p, C.c_char_p, C.c_size_t]
+    L.dicref_accuracy_sweep.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(_abi.SweepConfigC),
+                                        C.POINTER(_abi.ComboAccuracyC), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                        C.POINTER(C.c_double), C.c_char_p, C.c_size_t]
+    return L
+
+
+def ref_synth_speckle(width: int, height: int, seed: int, params) -> np.ndarray:
+    """dic::synth_speckle (synth.cpp:55-93); params: dic.SpeckleParams."""
+    out = np.zeros((height, width), np.float64)
+    err = C.create_string_buffer(160)
+    if _ref_lib().dicref_synth_speckle(width, height, seed, C.byref(params.to_c()), out.ctypes.data, err, 160):
+        raise OracleError(err.value.decode())
+    return out
+
+
+def ref_synth_warped_pair(reference: np.ndarray, warp) -> Tuple[np.ndarray, np.ndarray]:
+    """dic::synth_warped_pair (synth.cpp:127-172); warp: dic.WarpSpec."""
+    ref = _as_double(reference)
+    tgt, mask = np.zeros_like(ref), np.zeros(ref.shape, np.uint8)
+    err = C.create_string_buffer(160)
+    if _ref_lib().dicref_synth_warped_pair(ref.ctypes.data, ref.shape[1], ref.shape[0], C.byref(warp.to_c()),
+                                           tgt.ctypes.data, mask.ctypes.data, err, 160):
+        raise OracleError(err.value.decode())
+    return tgt, mask
+
+
+def ref_accuracy_sweep(combos, cfg):
+    """dic::run_accuracy_sweep (accuracy.cpp:10-78) on the reference's own
+    double frames. Returns (list of ComboAccuracyC, warp_count, poi_count, elapsed_s)."""
+    arr = np.array([[int(a), int(b)] for a, b in combos], np.int32)
+    out = (_abi.ComboAccuracyC * len(combos))()
+    c, keep = cfg.to_c()
+    wc, pc, el = C.c_int(), C.c_int(), C.c_double()
+    err = C.create_string_buffer(160)
+    if _ref_lib().dicref_accuracy_sweep(arr.ctypes.data, len(combos), C.byref(c), out, C.byref(wc), C.byref(pc),
+                                        C.byref(el), err, 160):
+        raise OracleError(err.value.decode())
+    return list(out), wc.value, pc.value, el.value

@@ -318,3 +318,100 @@ int dicref_load_sequence(const char* dir, const char* pattern, double* out, size
 }
 
 }  // extern "C"
+
+// ---- f-4: the reference's generators and accuracy sweep (synth.cpp, accuracy.cpp) ----
+#include "dic/accuracy.hpp"
+#include "dic/synth.hpp"
+
+namespace {
+dic::SpeckleParams to_speckle(const dicb200_speckle_params& p) {
+  dic::SpeckleParams s;
+  s.blob_count = p.blob_count;
+  s.sigma_min = p.sigma_min;
+  s.sigma_max = p.sigma_max;
+  s.amp_min = p.amp_min;
+  s.amp_max = p.amp_max;
+  s.background = p.background;
+  s.variance_floor = p.variance_floor;
+  s.texture_window = p.texture_window;
+  return s;
+}
+dic::WarpSpec to_warp(const dicb200_warp_spec& w) {
+  dic::WarpSpec s;
+  s.u = w.u;
+  s.v = w.v;
+  s.ux = w.ux;
+  s.uy = w.uy;
+  s.vx = w.vx;
+  s.vy = w.vy;
+  return s;
+}
+}  // namespace
+
+extern "C" {
+
+int dicref_synth_speckle(int w, int h, uint64_t seed, const dicb200_speckle_params* p, double* out, char* err,
+                         size_t errcap) {
+  try {
+    const dic::GrayImage img = dic::synth_speckle(w, h, seed, to_speckle(*p));
+    std::copy(img.pixels().begin(), img.pixels().end(), out);
+    return 0;
+  } catch (const dic::Error& e) {
+    copy_err(e.what(), err, errcap);
+    return 1;
+  }
+}
+
+int dicref_synth_warped_pair(const double* ref, int w, int h, const dicb200_warp_spec* warp, double* target,
+                             uint8_t* mask, char* err, size_t errcap) {
+  try {
+    const auto [tgt, truth] = dic::synth_warped_pair(make_image(ref, w, h), to_warp(*warp));
+    std::copy(tgt.pixels().begin(), tgt.pixels().end(), target);
+    if (mask)
+      for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) mask[(size_t)y * w + x] = truth.valid(x, y) ? 1 : 0;
+    return 0;
+  } catch (const dic::Error& e) {
+    copy_err(e.what(), err, errcap);
+    return 1;
+  }
+}
+
+// dic::run_accuracy_sweep on the reference's own (unquantized) frames.
+int dicref_accuracy_sweep(const int32_t* combos, size_t n, const dicb200_sweep_config* c, dicb200_combo_accuracy* out,
+                          int* warp_count, int* poi_count, double* elapsed, char* err, size_t errcap) {
+  try {
+    dic::SweepConfig s;
+    s.width = c->width;
+    s.height = c->height;
+    s.seed = c->seed;
+    s.speckle = to_speckle(c->speckle);
+    s.base = to_run_config(c->base);
+    s.fractions.assign(c->fractions, c->fractions + c->n_fractions);
+    s.offsets.assign(c->offsets, c->offsets + c->n_offsets);
+    std::vector<std::pair<dic::IntegerMethod, dic::SubpixelMethod>> cs;
+    for (size_t i = 0; i < n; ++i)
+      cs.emplace_back(static_cast<dic::IntegerMethod>(combos[2 * i]), static_cast<dic::SubpixelMethod>(combos[2 * i + 1]));
+    const dic::SweepReport r = dic::run_accuracy_sweep(cs, s);
+    for (size_t i = 0; i < n; ++i) {
+      const auto& a = r.combos[i];
+      out[i].integer_method = static_cast<int32_t>(a.integer_method);
+      out[i].subpixel_method = static_cast<int32_t>(a.subpixel_method);
+      out[i].max_err = a.max_err;
+      out[i].mean_err = a.mean_err;
+      out[i].measurements = a.measurements;
+      out[i].unconverged = a.unconverged;
+      out[i].pass = a.pass ? 1 : 0;
+      out[i].mean_flagged = a.mean_flagged ? 1 : 0;
+    }
+    *warp_count = r.warp_count;
+    *poi_count = r.poi_count;
+    *elapsed = r.elapsed_s;
+    return 0;
+  } catch (const dic::Error& e) {
+    copy_err(e.what(), err, errcap);
+    return 1;
+  }
+}
+
+}  // extern "C"

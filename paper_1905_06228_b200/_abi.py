@@ -137,3 +137,49 @@ def record_dtype():
             "itemsize": C.sizeof(PoiRecordC),
         }
     )
+
+
+class SpeckleParamsC(C.Structure):  # dicb200_speckle_params (synth.hpp:14-23)
+    _fields_ = [
+        ("blob_count", C.c_int32),
+        ("texture_window", C.c_int32),
+        ("sigma_min", C.c_double),
+        ("sigma_max", C.c_double),
+        ("amp_min", C.c_double),
+        ("amp_max", C.c_double),
+        ("background", C.c_double),
+        ("variance_floor", C.c_double),
+    ]
+
+
+class WarpSpecC(C.Structure):  # dicb200_warp_spec (synth.hpp:30-35)
+    _fields_ = [(k, C.c_double) for k in ("u", "v", "ux", "uy", "vx", "vy")]
+
+
+class SweepConfigC(C.Structure):  # dicb200_sweep_config (accuracy.hpp:15-23)
+    _fields_ = [
+        ("width", C.c_int32),
+        ("height", C.c_int32),
+        ("seed", C.c_uint64),
+        ("speckle", SpeckleParamsC),
+        ("base", RunConfigC),
+        ("fractions", C.POINTER(C.c_double)),
+        ("n_fractions", C.c_int32),
+        ("n_offsets", C.c_int32),
+        ("offsets", C.POINTER(C.c_int32)),
+        ("gray_scale", C.c_int32),
+        ("pad", C.c_int32),
+    ]
+
+
+class ComboAccuracyC(C.Structure):  # dicb200_combo_accuracy (accuracy.hpp:25-34)
+    _fields_ = [
+        ("integer_method", C.c_int32),
+        ("subpixel_method", C.c_int32),
+        ("max_err", C.c_double),
+        ("mean_err", C.c_double),
+        ("measurements", C.c_int32),
+        ("unconverged", C.c_int32),
+        ("pass_", C.c_int32),
+        ("mean_flagged", C.c_int32),
+    ]

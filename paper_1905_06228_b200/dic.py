@@ -234,6 +234,15 @@ def lib() -> C.CDLL:
         L.dicb200_synth_displacement.argtypes = [
             C.POINTER(_abi.SynthSpecC), C.c_double, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double),
         ]
+        L.dicb200_synth_speckle.argtypes = [C.c_int32, C.c_int32, C.c_uint64, C.POINTER(_abi.SpeckleParamsC),
+                                            C.c_void_p]
+        L.dicb200_synth_warped_pair.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(_abi.WarpSpecC),
+                                                C.c_void_p, C.c_void_p]
+        L.dicb200_accuracy_sweep.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(_abi.SweepConfigC),
+                                             C.POINTER(_abi.ComboAccuracyC), C.POINTER(C.c_int32),
+                                             C.POINTER(C.c_int32), C.POINTER(C.c_double)]
+        L.dicb200_default_speckle.argtypes = [C.POINTER(_abi.SpeckleParamsC)]
+        L.dicb200_default_sweep.argtypes = [C.POINTER(_abi.SweepConfigC)]
         _lib_handle = L
     return _lib_handle
 
@@ -452,3 +461,132 @@ def field_csv_string(field_: DisplacementField) -> str:
             % (r["x"], r["y"], r["u"], r["v"], r["zncc"], 1 if r["converged"] else 0, r["iterations"], r["evaluations"])
         )
     return "".join(lines)
+
+
+# ---- f-4 accuracy sweep (accuracy.hpp / synth.hpp) --------------------------------
+
+
+@dataclass
+class SpeckleParams:  # synth.hpp:14-23
+    blob_count: int = 0
+    sigma_min: float = 1.0
+    sigma_max: float = 2.5
+    amp_min: float = 40.0
+    amp_max: float = 140.0
+    background: float = 128.0
+    variance_floor: float = 25.0
+    texture_window: int = 31
+
+    def to_c(self) -> _abi.SpeckleParamsC:
+        c = _abi.SpeckleParamsC()
+        for k in ("blob_count", "sigma_min", "sigma_max", "amp_min", "amp_max", "background", "variance_floor",
+                  "texture_window"):
+            setattr(c, k, getattr(self, k))
+        return c
+
+
+@dataclass
+class WarpSpec:  # synth.hpp:30-35
+    u: float = 0.0
+    v: float = 0.0
+    ux: float = 0.0
+    uy: float = 0.0
+    vx: float = 0.0
+    vy: float = 0.0
+
+    def to_c(self) -> _abi.WarpSpecC:
+        return _abi.WarpSpecC(self.u, self.v, self.ux, self.uy, self.vx, self.vy)
+
+
+@dataclass
+class SweepConfig:  # accuracy.hpp:15-23
+    width: int = 160
+    height: int = 160
+    seed: int = 7
+    speckle: SpeckleParams = field(default_factory=SpeckleParams)
+    base: RunConfig = field(default_factory=RunConfig)
+    fractions: List[float] = field(default_factory=lambda: [0.1, 0.25, 0.5, 0.75, 0.9])
+    offsets: List[int] = field(default_factory=lambda: [-3, 0, 4])
+    gray_scale: int = 256  # B200: integer gray levels round(v * scale); 1 = 8-bit PGM round trip
+
+    def to_c(self):
+        """(struct, keep-alive arrays)."""
+        fr = (C.c_double * max(1, len(self.fractions)))(*self.fractions)
+        of = (C.c_int32 * max(1, len(self.offsets)))(*self.offsets)
+        c = _abi.SweepConfigC()
+        c.width, c.height, c.seed = self.width, self.height, self.seed & 0xFFFFFFFFFFFFFFFF
+        c.speckle = self.speckle.to_c()
+        c.base = self.base.to_c()
+        c.fractions, c.n_fractions = C.cast(fr, C.POINTER(C.c_double)), len(self.fractions)
+        c.offsets, c.n_offsets = C.cast(of, C.POINTER(C.c_int32)), len(self.offsets)
+        c.gray_scale = self.gray_scale
+        return c, (fr, of)
+
+
+@dataclass
+class ComboAccuracy:  # accuracy.hpp:25-34
+    integer_method: IntegerMethod = IntegerMethod.bfs
+    subpixel_method: SubpixelMethod = SubpixelMethod.none
+    max_err: float = 0.0
+    mean_err: float = 0.0
+    measurements: int = 0
+    unconverged: int = 0
+    passed: bool = False  # `pass` in the reference
+    mean_flagged: bool = False
+
+
+@dataclass
+class SweepReport:  # accuracy.hpp:36-41
+    combos: List[ComboAccuracy] = field(default_factory=list)
+    warp_count: int = 0
+    poi_count: int = 0
+    elapsed_s: float = 0.0
+
+
+def default_blob_count(width: int, height: int) -> int:
+    """synth.cpp:14-16."""
+    return int(lib().dicb200_default_blob_count(width, height))
+
+
+def synth_speckle(width: int, height: int, seed: int, params: SpeckleParams) -> np.ndarray:
+    """synth.cpp:55-93 (dic::synth_speckle): float64 frame, bit-identical to the
+    reference's doubles. Raises DicError("textureless pattern") etc."""
+    out = np.zeros((max(height, 0), max(width, 0)), np.float64)
+    st = lib().dicb200_synth_speckle(width, height, seed & 0xFFFFFFFFFFFFFFFF, C.byref(params.to_c()),
+                                     out.ctypes.data)
+    if st:
+        _raise(st)
+    return out
+
+
+def synth_warped_pair(reference: np.ndarray, warp: WarpSpec) -> Tuple[np.ndarray, np.ndarray]:
+    """synth.cpp:127-172 (dic::synth_warped_pair): (target float64, valid mask u8)."""
+    ref = np.ascontiguousarray(reference, np.float64)
+    h, w = ref.shape
+    tgt = np.zeros_like(ref)
+    mask = np.zeros(ref.shape, np.uint8)
+    st = lib().dicb200_synth_warped_pair(ref.ctypes.data, w, h, C.byref(warp.to_c()), tgt.ctypes.data,
+                                         mask.ctypes.data)
+    if st:
+        _raise(st)
+    return tgt, mask
+
+
+def run_accuracy_sweep(combos: Sequence[Tuple[IntegerMethod, SubpixelMethod]], cfg: SweepConfig) -> SweepReport:
+    """accuracy.cpp:10-78 (dic::run_accuracy_sweep) with every pair analysed on
+    the GPU (one pipelined fixed-first sequence per combo)."""
+    arr = np.array([[int(a), int(b)] for a, b in combos] or [[0, 0]], np.int32)
+    out = (_abi.ComboAccuracyC * max(1, len(combos)))()
+    c, keep = cfg.to_c()
+    wc, pc, el = C.c_int32(), C.c_int32(), C.c_double()
+    st = lib().dicb200_accuracy_sweep(arr.ctypes.data, len(combos), C.byref(c), out, C.byref(wc), C.byref(pc),
+                                      C.byref(el))
+    if st:
+        _raise(st)
+    rep = SweepReport(warp_count=wc.value, poi_count=pc.value, elapsed_s=el.value)
+    for i in range(len(combos)):
+        o = out[i]
+        rep.combos.append(ComboAccuracy(IntegerMethod(o.integer_method), SubpixelMethod(o.subpixel_method), o.max_err,
+                                        o.mean_err, o.measurements, o.unconverged, bool(o.pass_),
+                                        bool(o.mean_flagged)))
+    return rep
