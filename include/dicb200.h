@@ -296,6 +296,65 @@ dicb200_status dicb200_accuracy_sweep(const int32_t* combos, size_t n_combos, co
                                       dicb200_combo_accuracy* out, int32_t* warp_count, int32_t* poi_count,
                                       double* elapsed_s);
 
+/* ---- f-3 output format (pipeline.cpp:216-238) ----
+ * dicb200_field_csv: dic::field_csv_string (header + "%d,%d,%.17g,%.17g,%.17g,%d,%d,%ld"
+ * rows); buf == NULL returns the size (incl. NUL) in *needed.
+ * dicb200_write_field_csv: dic::write_field_csv. dicb200_field_filename:
+ * "field_%04d.csv" (dic::field_filename). */
+dicb200_status dicb200_field_csv(const dicb200_field* field, char* buf, size_t cap, size_t* needed);
+dicb200_status dicb200_write_field_csv(const dicb200_field* field, const char* path);
+dicb200_status dicb200_field_filename(int32_t pair_index, char* buf, size_t cap);
+
+/* ---- f-4 bench matrix (bench.hpp:12-90, bench.cpp:14-293) ----
+ * dicb200_run_bench replaces dic::run_bench: every cell strictly in order; per
+ * cell one untimed warm-up repetition, then `repeats` timed repetitions
+ * (auto_repeats bands from the warm-up unless auto_bands == 0), each = load the
+ * sequence from disk (native PGM loader, pinned frames), analyze_sequence on
+ * the GPU, write every field CSV under scratch_dir/cell-<int>-<sub>-<mode>/.
+ * Cell failures (a failed pair, changing evaluation counts) are recorded in the
+ * record, as the reference does; the call itself fails only on bad arguments.
+ * dicb200_derive_ratios / dicb200_write_*_csv: dic::derive_ratios and the
+ * reference's three CSV layouts, byte-identical formatting. */
+typedef struct {  /* BenchCell, bench.hpp:12-16 */
+  int32_t integer_method;
+  int32_t subpixel_method;
+  int32_t mode;
+} dicb200_bench_cell;
+
+typedef struct {  /* BenchRecord, bench.hpp:18-31 */
+  dicb200_bench_cell cell;
+  int32_t repeats;
+  int32_t pair_count;
+  int32_t failed;
+  double mean_s;
+  double stddev_s;
+  double per_pair_s;
+  double frame_rate_hz;  /* pair_count / mean_s */
+  int64_t total_evaluations;
+  char dataset_id[128];
+  char error[160];
+} dicb200_bench_record;
+
+typedef struct {  /* RatioRow, bench.hpp:56-61 */
+  char kind[32];     /* bfs_vs_pso | image_speedup_vs_serial | subimage_speedup_vs_serial */
+  char detail[160];
+  double value;      /* NaN when a needed cell is missing / failed */
+  char note[32];
+} dicb200_ratio_row;
+
+int32_t dicb200_auto_repeats(double warmup_seconds); /* bench.cpp:14-19 */
+dicb200_status dicb200_run_bench(const dicb200_bench_cell* cells, size_t n_cells, const char* dataset_dir,
+                                 const char* pattern, const dicb200_run_config* base, int32_t auto_bands,
+                                 int32_t fixed_repeats, const char* scratch_dir, int32_t load_flags,
+                                 dicb200_bench_record* out);
+/* rows: at most 3*3 + 3*3*2 = 27. */
+dicb200_status dicb200_derive_ratios(const dicb200_bench_record* records, size_t n, const char* dataset_id,
+                                     dicb200_ratio_row* rows, size_t cap, size_t* count);
+dicb200_status dicb200_write_times_csv(const dicb200_bench_record* records, size_t n, const char* dataset_id,
+                                       const char* path);
+dicb200_status dicb200_write_records_csv(const dicb200_bench_record* records, size_t n, const char* path);
+dicb200_status dicb200_write_ratios_csv(const dicb200_ratio_row* rows, size_t n, const char* path);
+
 /* Release pooled device memory on all devices. */
 void dicb200_shutdown(void);
 

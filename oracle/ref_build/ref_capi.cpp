@@ -415,3 +415,111 @@ int dicref_accuracy_sweep(const int32_t* combos, size_t n, const dicb200_sweep_c
 }
 
 }  // extern "C"
+
+// ---- f-3 / f-4: field CSV and the bench matrix (pipeline.cpp:216-238, bench.cpp) ----
+#include "dic/bench.hpp"
+
+namespace {
+dic::BenchRecord to_bench(const dicb200_bench_record& r) {
+  dic::BenchRecord b;
+  b.cell.integer_method = static_cast<dic::IntegerMethod>(r.cell.integer_method);
+  b.cell.subpixel_method = static_cast<dic::SubpixelMethod>(r.cell.subpixel_method);
+  b.cell.mode = static_cast<dic::ExecMode>(r.cell.mode);
+  b.dataset_id = r.dataset_id;
+  b.repeats = r.repeats;
+  b.pair_count = r.pair_count;
+  b.mean_s = r.mean_s;
+  b.stddev_s = r.stddev_s;
+  b.per_pair_s = r.per_pair_s;
+  b.frame_rate_hz = r.frame_rate_hz;
+  b.total_evaluations = r.total_evaluations;
+  b.failed = r.failed != 0;
+  b.error = r.error;
+  return b;
+}
+dic::BenchReport to_report(const dicb200_bench_record* recs, size_t n, const char* dataset_id) {
+  dic::BenchReport rep;
+  rep.dataset_id = dataset_id;
+  for (size_t i = 0; i < n; ++i) rep.records.push_back(to_bench(recs[i]));
+  return rep;
+}
+}  // namespace
+
+extern "C" {
+
+int dicref_field_csv(const dicb200_poi_record* recs, size_t n, char* out, size_t cap, size_t* needed) {
+  dic::DisplacementField f;
+  for (size_t i = 0; i < n; ++i) {
+    dic::PoiRecord r;
+    r.x = recs[i].x;
+    r.y = recs[i].y;
+    r.u = recs[i].u;
+    r.v = recs[i].v;
+    r.zncc = recs[i].zncc;
+    r.converged = recs[i].converged != 0;
+    r.iterations = recs[i].iterations;
+    r.evaluations = recs[i].evaluations;
+    f.records.push_back(r);
+  }
+  const std::string s = dic::field_csv_string(f);
+  *needed = s.size() + 1;
+  if (out && cap > s.size()) std::memcpy(out, s.c_str(), s.size() + 1);
+  return 0;
+}
+
+int dicref_bench_csvs(const dicb200_bench_record* recs, size_t n, const char* dataset_id, const char* times,
+                      const char* records, const char* ratios, char* err, size_t errcap) {
+  try {
+    const dic::BenchReport rep = to_report(recs, n, dataset_id);
+    dic::write_times_csv(rep, times);
+    dic::write_records_csv(rep, records);
+    dic::write_ratios_csv(dic::derive_ratios(rep), ratios);
+    return 0;
+  } catch (const dic::Error& e) {
+    copy_err(e.what(), err, errcap);
+    return 1;
+  }
+}
+
+int dicref_auto_repeats(double s) { return dic::auto_repeats(s); }
+
+// dic::run_bench on the CPU (tiny datasets only: tests).
+int dicref_run_bench(const dicb200_bench_cell* cells, size_t n, const char* dir, const char* pattern,
+                     const dicb200_run_config* base, int auto_bands, int fixed, const char* scratch,
+                     dicb200_bench_record* out, char* err, size_t errcap) {
+  try {
+    std::vector<dic::BenchCell> cs;
+    for (size_t i = 0; i < n; ++i) {
+      dic::BenchCell c;
+      c.integer_method = static_cast<dic::IntegerMethod>(cells[i].integer_method);
+      c.subpixel_method = static_cast<dic::SubpixelMethod>(cells[i].subpixel_method);
+      c.mode = static_cast<dic::ExecMode>(cells[i].mode);
+      cs.push_back(c);
+    }
+    dic::RepeatsPolicy rp;
+    rp.auto_bands = auto_bands != 0;
+    rp.fixed = fixed;
+    const dic::BenchReport rep = dic::run_bench(cs, dir, pattern, to_run_config(*base), rp, scratch);
+    for (size_t i = 0; i < n; ++i) {
+      const dic::BenchRecord& r = rep.records[i];
+      std::memset(&out[i], 0, sizeof out[i]);
+      out[i].cell = cells[i];
+      out[i].repeats = r.repeats;
+      out[i].pair_count = r.pair_count;
+      out[i].failed = r.failed ? 1 : 0;
+      out[i].mean_s = r.mean_s;
+      out[i].stddev_s = r.stddev_s;
+      out[i].per_pair_s = r.per_pair_s;
+      out[i].frame_rate_hz = r.frame_rate_hz;
+      out[i].total_evaluations = r.total_evaluations;
+      std::snprintf(out[i].dataset_id, sizeof out[i].dataset_id, "%s", r.dataset_id.c_str());
+      std::snprintf(out[i].error, sizeof out[i].error, "%s", r.error.c_str());
+    }
+    return 0;
+  } catch (const dic::Error& e) {
+    copy_err(e.what(), err, errcap);
+    return 1;
+  }
+}
+
+}  // extern "C"

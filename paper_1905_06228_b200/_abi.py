@@ -183,3 +183,27 @@ class ComboAccuracyC(C.Structure):  # dicb200_combo_accuracy (accuracy.hpp:25-34
         ("pass_", C.c_int32),
         ("mean_flagged", C.c_int32),
     ]
+
+
+class BenchCellC(C.Structure):  # dicb200_bench_cell (bench.hpp:12-16)
+    _fields_ = [("integer_method", C.c_int32), ("subpixel_method", C.c_int32), ("mode", C.c_int32)]
+
+
+class BenchRecordC(C.Structure):  # dicb200_bench_record (bench.hpp:18-31)
+    _fields_ = [
+        ("cell", BenchCellC),
+        ("repeats", C.c_int32),
+        ("pair_count", C.c_int32),
+        ("failed", C.c_int32),
+        ("mean_s", C.c_double),
+        ("stddev_s", C.c_double),
+        ("per_pair_s", C.c_double),
+        ("frame_rate_hz", C.c_double),
+        ("total_evaluations", C.c_int64),
+        ("dataset_id", C.c_char * 128),
+        ("error", C.c_char * 160),
+    ]
+
+
+class RatioRowC(C.Structure):  # dicb200_ratio_row (bench.hpp:56-61)
+    _fields_ = [("kind", C.c_char * 32), ("detail", C.c_char * 160), ("value", C.c_double), ("note", C.c_char * 32)]

@@ -243,6 +243,18 @@ def lib() -> C.CDLL:
                                              C.POINTER(C.c_int32), C.POINTER(C.c_double)]
         L.dicb200_default_speckle.argtypes = [C.POINTER(_abi.SpeckleParamsC)]
         L.dicb200_default_sweep.argtypes = [C.POINTER(_abi.SweepConfigC)]
+        L.dicb200_field_csv.argtypes = [C.POINTER(_abi.FieldC), C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
+        L.dicb200_write_field_csv.argtypes = [C.POINTER(_abi.FieldC), C.c_char_p]
+        L.dicb200_field_filename.argtypes = [C.c_int32, C.c_char_p, C.c_size_t]
+        L.dicb200_auto_repeats.argtypes = [C.c_double]
+        L.dicb200_run_bench.argtypes = [C.POINTER(_abi.BenchCellC), C.c_size_t, C.c_char_p, C.c_char_p,
+                                        C.POINTER(_abi.RunConfigC), C.c_int32, C.c_int32, C.c_char_p, C.c_int32,
+                                        C.POINTER(_abi.BenchRecordC)]
+        L.dicb200_derive_ratios.argtypes = [C.POINTER(_abi.BenchRecordC), C.c_size_t, C.c_char_p,
+                                            C.POINTER(_abi.RatioRowC), C.c_size_t, C.POINTER(C.c_size_t)]
+        L.dicb200_write_times_csv.argtypes = [C.POINTER(_abi.BenchRecordC), C.c_size_t, C.c_char_p, C.c_char_p]
+        L.dicb200_write_records_csv.argtypes = [C.POINTER(_abi.BenchRecordC), C.c_size_t, C.c_char_p]
+        L.dicb200_write_ratios_csv.argtypes = [C.POINTER(_abi.RatioRowC), C.c_size_t, C.c_char_p]
         _lib_handle = L
     return _lib_handle
 
@@ -452,15 +464,44 @@ def analyze_sequence(images: Sequence[GrayImage], cfg: RunConfig) -> List[Displa
     return out
 
 
+def _field_c(field_: DisplacementField):
+    recs = np.ascontiguousarray(field_.records if field_.records is not None else
+                                np.zeros(0, _abi.record_dtype()), dtype=_abi.record_dtype())
+    f = _abi.FieldC()
+    f.pair_index, f.ref_id, f.tgt_id = field_.pair_index, field_.ref_id, field_.tgt_id
+    f.records = C.cast(recs.ctypes.data, C.POINTER(_abi.PoiRecordC))
+    f.capacity = f.count = len(recs)
+    return f, recs
+
+
 def field_csv_string(field_: DisplacementField) -> str:
-    """pipeline.cpp:216-231 (same printf formats)."""
-    lines = ["x,y,u,v,zncc,converged,iterations,evaluations\n"]
-    for r in field_.records:
-        lines.append(
-            "%d,%d,%.17g,%.17g,%.17g,%d,%d,%d\n"
-            % (r["x"], r["y"], r["u"], r["v"], r["zncc"], 1 if r["converged"] else 0, r["iterations"], r["evaluations"])
-        )
-    return "".join(lines)
+    """pipeline.cpp:222-231 (dic::field_csv_string), formatted natively with the
+    reference's printf formats."""
+    f, keep = _field_c(field_)
+    need = C.c_size_t(0)
+    lib().dicb200_field_csv(C.byref(f), None, 0, C.byref(need))
+    buf = C.create_string_buffer(need.value)
+    st = lib().dicb200_field_csv(C.byref(f), buf, need.value, C.byref(need))
+    if st:
+        _raise(st)
+    return buf.value.decode()
+
+
+def write_field_csv(field_: DisplacementField, path) -> None:
+    """pipeline.cpp:233-238 (dic::write_field_csv)."""
+    f, keep = _field_c(field_)
+    st = lib().dicb200_write_field_csv(C.byref(f), str(path).encode())
+    if st:
+        _raise(st)
+
+
+def field_filename(pair_index: int) -> str:
+    """pipeline.cpp:216-220: field_%04d.csv."""
+    buf = C.create_string_buffer(32)
+    st = lib().dicb200_field_filename(pair_index, buf, 32)
+    if st:
+        _raise(st)
+    return buf.value.decode()
 
 
 # ---- f-4 accuracy sweep (accuracy.hpp / synth.hpp) --------------------------------
@@ -590,3 +631,170 @@ def run_accuracy_sweep(combos: Sequence[Tuple[IntegerMethod, SubpixelMethod]], c
                                         o.mean_err, o.measurements, o.unconverged, bool(o.pass_),
                                         bool(o.mean_flagged)))
     return rep
+
+
+# ---- f-4 bench matrix (bench.hpp / bench.cpp) --------------------------------------
+
+
+@dataclass
+class BenchCell:  # bench.hpp:12-16
+    integer_method: IntegerMethod = IntegerMethod.pso
+    subpixel_method: SubpixelMethod = SubpixelMethod.nr
+    mode: ExecMode = ExecMode.serial
+
+
+@dataclass
+class BenchRecord:  # bench.hpp:18-31
+    cell: BenchCell = field(default_factory=BenchCell)
+    dataset_id: str = ""
+    repeats: int = 0
+    pair_count: int = 0
+    mean_s: float = 0.0
+    stddev_s: float = 0.0
+    per_pair_s: float = 0.0
+    frame_rate_hz: float = 0.0
+    total_evaluations: int = 0
+    failed: bool = False
+    error: str = ""
+
+    def to_c(self) -> _abi.BenchRecordC:
+        c = _abi.BenchRecordC()
+        c.cell = _abi.BenchCellC(int(self.cell.integer_method), int(self.cell.subpixel_method), int(self.cell.mode))
+        for k in ("repeats", "pair_count", "mean_s", "stddev_s", "per_pair_s", "frame_rate_hz", "total_evaluations"):
+            setattr(c, k, getattr(self, k))
+        c.failed = 1 if self.failed else 0
+        c.dataset_id = self.dataset_id.encode()[:127]
+        c.error = self.error.encode()[:159]
+        return c
+
+    @staticmethod
+    def from_c(c: _abi.BenchRecordC) -> "BenchRecord":
+        return BenchRecord(BenchCell(IntegerMethod(c.cell.integer_method), SubpixelMethod(c.cell.subpixel_method),
+                                     ExecMode(c.cell.mode)), c.dataset_id.decode(), c.repeats, c.pair_count, c.mean_s,
+                           c.stddev_s, c.per_pair_s, c.frame_rate_hz, c.total_evaluations, bool(c.failed),
+                           c.error.decode())
+
+
+@dataclass
+class BenchReport:  # bench.hpp:33-42
+    records: List[BenchRecord] = field(default_factory=list)
+    dataset_id: str = ""
+    cpu_model: str = ""
+    hardware_threads: int = 0
+    worker_count: int = 0
+    timestamp: str = ""
+
+
+@dataclass
+class RepeatsPolicy:  # bench.hpp:44-47
+    auto_bands: bool = True
+    fixed: int = 1
+
+
+@dataclass
+class RatioRow:  # bench.hpp:56-61
+    kind: str = ""
+    detail: str = ""
+    value: float = 0.0
+    note: str = ""
+
+
+def auto_repeats(warmup_seconds: float) -> int:
+    """bench.cpp:14-19."""
+    return int(lib().dicb200_auto_repeats(warmup_seconds))
+
+
+def cpu_model_name() -> str:
+    """bench.cpp:293-306 (/proc/cpuinfo "model name")."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name") and ":" in line:
+                    name = line.split(":", 1)[1].rstrip("\n")
+                    return name[1:] if name.startswith(" ") else name
+    except OSError:
+        pass
+    return "unknown"
+
+
+def timestamp_utc() -> str:
+    """bench.cpp:308-315."""
+    import time
+
+    return time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())
+
+
+def run_bench(cells: Sequence[BenchCell], dataset_dir, pattern: str, base: RunConfig,
+              repeats: RepeatsPolicy = RepeatsPolicy(), scratch_dir=None, allow_16bit: bool = False) -> BenchReport:
+    """bench.cpp:60-120 (dic::run_bench): cells in order, each repeat = load the
+    sequence (native PGM loader, pinned), analyze it on the GPU, write the field
+    CSVs under scratch_dir/cell-<int>-<sub>-<mode>/; host wall clock per repeat."""
+    import tempfile
+
+    if scratch_dir is None:
+        scratch_dir = tempfile.mkdtemp(prefix="dicb200_bench_")
+    arr = (_abi.BenchCellC * max(1, len(cells)))(
+        *[_abi.BenchCellC(int(c.integer_method), int(c.subpixel_method), int(c.mode)) for c in cells])
+    out = (_abi.BenchRecordC * max(1, len(cells)))()
+    st = lib().dicb200_run_bench(arr, len(cells), str(dataset_dir).encode(), pattern.encode(), C.byref(base.to_c()),
+                                 1 if repeats.auto_bands else 0, repeats.fixed, str(scratch_dir).encode(),
+                                 1 if allow_16bit else 0, out)
+    if st:
+        _raise(st)
+    d = str(dataset_dir)
+    rep = BenchReport(dataset_id=os.path.basename(d) or d, cpu_model=cpu_model_name(),
+                      hardware_threads=os.cpu_count() or 0, worker_count=base.worker_count, timestamp=timestamp_utc())
+    rep.records = [BenchRecord.from_c(out[i]) for i in range(len(cells))]
+    return rep
+
+
+def _records_c(report: BenchReport):
+    return (_abi.BenchRecordC * max(1, len(report.records)))(*[r.to_c() for r in report.records])
+
+
+def derive_ratios(report: BenchReport) -> List[RatioRow]:
+    """bench.cpp:142-208 (dic::derive_ratios)."""
+    recs = _records_c(report)
+    rows = (_abi.RatioRowC * 32)()
+    n = C.c_size_t(0)
+    st = lib().dicb200_derive_ratios(recs, len(report.records), report.dataset_id.encode(), rows, 32, C.byref(n))
+    if st:
+        _raise(st)
+    return [RatioRow(rows[i].kind.decode(), rows[i].detail.decode(), rows[i].value, rows[i].note.decode())
+            for i in range(n.value)]
+
+
+def write_times_csv(report: BenchReport, path) -> None:
+    """bench.cpp:210-251: one row per (integer, subpixel), one mean-seconds column per mode."""
+    st = lib().dicb200_write_times_csv(_records_c(report), len(report.records), report.dataset_id.encode(),
+                                       str(path).encode())
+    if st:
+        _raise(st)
+
+
+def write_records_csv(report: BenchReport, path) -> None:
+    """bench.cpp:253-269."""
+    st = lib().dicb200_write_records_csv(_records_c(report), len(report.records), str(path).encode())
+    if st:
+        _raise(st)
+
+
+def write_ratios_csv(rows: Sequence[RatioRow], path) -> None:
+    """bench.cpp:271-283."""
+    arr = (_abi.RatioRowC * max(1, len(rows)))()
+    for i, r in enumerate(rows):
+        arr[i].kind, arr[i].detail = r.kind.encode()[:31], r.detail.encode()[:159]
+        arr[i].value, arr[i].note = r.value, r.note.encode()[:31]
+    st = lib().dicb200_write_ratios_csv(arr, len(rows), str(path).encode())
+    if st:
+        _raise(st)
+
+
+def write_manifest(entries: Sequence[Tuple[str, str]], path) -> None:
+    """bench.cpp:285-291: "key = value" lines."""
+    try:
+        with open(path, "w") as f:
+            for k, v in entries:
+                f.write(f"{k} = {v}\n")
+    except OSError:
+        raise DicError("cannot open for writing: " + str(path))
