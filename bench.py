@@ -244,7 +244,20 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     recbuf = torch.empty(max(1, len(my_pairs) * recs_per_pair * rec_size), dtype=torch.uint8, device=dev)
     cnt = C.c_size_t(0)
 
+    seq_imgs = (_abi.Image * len(needed))(*[dev_imgs[i] for i in needed])
+    assert [(needed[a], needed[b]) for a, b in dic.sequence_pairs(cfg.reference_policy, len(needed))] == my_pairs
+    L.dicb200_analyze_sequence_device.argtypes = [
+        C.c_void_p, C.c_size_t, C.POINTER(_abi.RunConfigC), C.c_uint64, C.c_int32, C.c_int32, C.c_void_p,
+        C.c_size_t, C.POINTER(C.c_size_t), C.c_void_p]
+
     def step():
+        if len(my_pairs) > 1:  # device-resident sequence: reference-side inputs built once per step
+            st = L.dicb200_analyze_sequence_device(
+                seq_imgs, len(needed), C.byref(cfgc), all_pairs.index(my_pairs[0]), row_range[0], row_range[1],
+                C.c_void_p(recbuf.data_ptr()), recs_per_pair, C.byref(cnt), sptr)
+            if st:
+                raise RuntimeError(L.dicb200_last_error_message().decode())
+            return
         for j, (a, b) in enumerate(my_pairs):
             st = L.dicb200_analyze_pair_device(
                 C.byref(dev_imgs[a]), C.byref(dev_imgs[b]), C.byref(cfgc), all_pairs.index((a, b)),

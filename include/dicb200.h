@@ -193,6 +193,17 @@ dicb200_status dicb200_analyze_pair_device(const dicb200_image* reference, const
                                            dicb200_poi_record* out_dev, size_t out_cap,
                                            size_t* out_count, void* stream);
 
+/* Device-resident sequence: images hold device pointers; the pairs of
+ * dicb200_sequence_pairs(cfg->reference_policy, n_images) are enqueued on
+ * `stream` in order, pair i writing out_dev + i * pair_stride and using pair
+ * index first_pair_index + i (RNG keys; lets image-parallel ranks pass a
+ * contiguous sub-sequence). Like analyze_sequence, reference-side inputs are
+ * built once per reference frame and reused by the following pairs on it. */
+dicb200_status dicb200_analyze_sequence_device(const dicb200_image* images, size_t n_images,
+                                               const dicb200_run_config* cfg, uint64_t first_pair_index,
+                                               int32_t row_begin, int32_t row_end, dicb200_poi_record* out_dev,
+                                               size_t pair_stride, size_t* per_pair_count, void* stream);
+
 /* Kernel launches issued by this thread since the last reset (evidence for
  * bench.py "gpu_launches"). */
 uint64_t dicb200_launch_count(void);

@@ -110,6 +110,7 @@ bool tc_plan(TcParams& p);
 // Enqueues stats, reference preparation, the tensor-core kernel and the
 // per-POI merge (or only the surface when p.surface is set) on `st`.
 cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache = nullptr, long ref_key = -1);
-void tc_cache_free(TcRefCache& c);
+// async: stream-ordered release on `st` (device-resident callers); else cudaFree.
+void tc_cache_free(TcRefCache& c, cudaStream_t st = nullptr, bool async = false);
 
 }  // namespace dicb200

@@ -1094,11 +1094,9 @@ cudaError_t grow(void*& ptr, size_t& cap, size_t bytes, cudaStream_t st) {
 }
 }  // namespace
 
-void tc_cache_free(TcRefCache& c) {
-  if (c.tail) cudaFree(c.tail);
-  if (c.strips) cudaFree(c.strips);
-  if (c.psf) cudaFree(c.psf);
-  if (c.pvf) cudaFree(c.pvf);
+void tc_cache_free(TcRefCache& c, cudaStream_t st, bool async) {
+  for (void* q : {c.tail, c.strips, c.psf, c.pvf})
+    if (q) async ? cudaFreeAsync(q, st) : cudaFree(q);
   c = TcRefCache{};
 }
 

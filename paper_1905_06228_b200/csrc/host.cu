@@ -147,7 +147,7 @@ static dicb200_status validate_pair(const dicb200_image* a, const dicb200_image*
 static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image* tgt, const dicb200_run_config* cfg,
                                    uint64_t pair_index, const Lattice& lat, int rb, int re,
                                    dicb200_poi_record* out_dev, cudaStream_t st, TcRefCache* tcache = nullptr,
-                                   long ref_key = -1) {
+                                   long ref_key = -1, IcgnRefCache* icache = nullptr) {
   const int rows = re - rb;
   if (rows <= 0) return DICB200_OK;
   const size_t nrec = (size_t)rows * lat.nx;
@@ -302,7 +302,7 @@ refine:
     r.max_iter = cfg->max_iter;
     r.rec = out_dev;
     StageTimer tm(r.method == 0 ? 2 : 3, st);
-    DICB200_CUDA_TRY(refine_launch(r, ref->dtype == DICB200_U8, st));
+    DICB200_CUDA_TRY(refine_launch(r, ref->dtype == DICB200_U8, st, icache, ref_key));
   }
   return DICB200_OK;
 }
@@ -365,6 +365,7 @@ struct DeviceContext {
   FrameSlot frames[kFrameSlots];
   RecSlot recs[kRecSlots];
   TcRefCache tcache;  // reference-side tensor-core inputs, reused while the reference frame repeats
+  IcgnRefCache icache;  // reference-side IC-GN constants (Hessian inverse, sums), likewise
 };
 
 namespace {
@@ -389,6 +390,7 @@ static void destroy_context(DeviceContext* c) {
     if (r.computed) cudaEventDestroy(r.computed);
   }
   tc_cache_free(c->tcache);
+  icgn_cache_free(c->icache);
   if (c->cs) cudaStreamDestroy(c->cs);
   if (c->xs) cudaStreamDestroy(c->xs);
   if (c->ds) cudaStreamDestroy(c->ds);
@@ -443,6 +445,7 @@ static dicb200_status release_context(DeviceContext* c) {
   if (e2 == cudaSuccess) e2 = e3;
   for (auto& f : c->frames) f.key = f.last_use = -1;  // LRU state is per call
   c->tcache.reset();
+  c->icache.reset();
   for (auto& r : c->recs) r.pair = -1;
   std::lock_guard<std::mutex> lk(g_ctx_mu);
   g_ctx_idle.push_back(c);
@@ -661,6 +664,45 @@ dicb200_status dicb200_analyze_pair_device(const dicb200_image* ref, const dicb2
   return enqueue_pair(ref, tgt, cfg, pair_index, lat, rb, re, out_dev, (cudaStream_t)stream);
 }
 
+dicb200_status dicb200_analyze_sequence_device(const dicb200_image* images, size_t n_images,
+                                               const dicb200_run_config* cfg, uint64_t first_pair_index,
+                                               int32_t row_begin, int32_t row_end, dicb200_poi_record* out_dev,
+                                               size_t pair_stride, size_t* per_pair_count, void* stream) {
+  if (!has_device()) return no_device();
+  if (!images || !cfg || !out_dev) return invalid("null argument");
+  if (n_images < 2) return invalid("insufficient images");
+  std::vector<int32_t> pairs(2 * (n_images - 1));
+  dicb200_sequence_pairs(cfg->reference_policy, (int32_t)n_images, pairs.data());
+  for (size_t i = 1; i < n_images; ++i)
+    if (images[i].width != images[0].width || images[i].height != images[0].height)
+      return invalid("dimension mismatch");
+  dicb200_status s = validate_pair(&images[0], &images[1], cfg);
+  if (s != DICB200_OK) return s;
+  Lattice lat;
+  s = make_lattice(images[0].width, images[0].height, cfg, &lat);
+  if (s != DICB200_OK) return s;
+  const int rb = row_begin < 0 ? 0 : row_begin;
+  const int re = std::max(rb, row_end < 0 ? lat.ny : std::min(row_end, lat.ny));
+  const size_t n = (size_t)(re - rb) * lat.nx;
+  if (per_pair_count) *per_pair_count = n;
+  if (n > pair_stride) {
+    set_error("pair stride smaller than the grid rows");
+    return DICB200_ERR_CAPACITY;
+  }
+  // Reference-side inputs (tensor-core strips/moments, IC-GN constants) live for
+  // this call only and are rebuilt whenever the pair's reference frame changes.
+  const cudaStream_t st = (cudaStream_t)stream;
+  TcRefCache tc;
+  IcgnRefCache ic;
+  const bool fixed = cfg->reference_policy == DICB200_POLICY_FIXED_FIRST;
+  for (size_t i = 0; i + 1 < n_images && s == DICB200_OK; ++i)
+    s = enqueue_pair(&images[pairs[2 * i]], &images[pairs[2 * i + 1]], cfg, first_pair_index + i, lat, rb, re,
+                     out_dev + i * pair_stride, st, &tc, (long)pairs[2 * i], fixed ? &ic : nullptr);
+  tc_cache_free(tc, st, true);
+  icgn_cache_free(ic, st, true);
+  return s;
+}
+
 dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_images, const dicb200_run_config* cfg,
                                         dicb200_field* fields, size_t n_fields) {
   if (!has_device()) return no_device();
@@ -762,7 +804,8 @@ dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_im
       }
       if (s == DICB200_OK)
         s = enqueue_pair(&c->frames[sa].im, &c->frames[sb].im, cfg, i, lat[i - lo], 0, lat[i - lo].ny,
-                         (dicb200_poi_record*)r.dev.p, c->cs, &c->tcache, (long)pairs[2 * i]);
+                         (dicb200_poi_record*)r.dev.p, c->cs, &c->tcache, (long)pairs[2 * i],
+                         cfg->reference_policy == DICB200_POLICY_FIXED_FIRST ? &c->icache : nullptr);
       if (s == DICB200_OK) {
         e = cudaEventRecord(c->frames[sa].idle, c->cs);
         if (e == cudaSuccess) e = cudaEventRecord(c->frames[sb].idle, c->cs);

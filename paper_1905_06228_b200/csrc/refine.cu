@@ -636,13 +636,34 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
   const float* Rs = R + g.rP + (cx - p.lat.cx(ix0)) + 1;  // reference pixel (0,0) of this subset
   const float2* Gs = G2 + g.rP + (cx - p.lat.cx(ix0)) + 1;
 
+  double* crec = (METHOD == 1 && p.cache)
+                     ? p.cache + ((size_t)iy * p.lat.nx + ix0 + warp) * kIcgnCacheStride
+                     : nullptr;
+  auto store_fail = [&](int code) {
+    if (crec && lane == 0) crec[0] = 1.0 + code;
+  };
+  WarpConst& C = s_const[warp];
+  double fbar, nf;
+  double hinv[6] = {0, 0, 0, 0, 0, 0};
+  const double tag = crec ? crec[0] : 0.0;
+  if (tag != 0.0) {  // reference-side constants of this POI from an earlier pair
+    if (tag != 1.0) {
+      fail((int)tag - 1);
+      return;
+    }
+    fbar = crec[1];
+    nf = crec[2];
+    if (lane == 0) C.scf = crec[3];
+    if (lane < 12) (lane < 6 ? C.A[lane] : C.S[lane - 6]) = crec[4 + lane];
+    if (lane < 6)
+#pragma unroll
+      for (int j = 0; j < 6; ++j) hinv[j] = crec[16 + 6 * lane + j];
+    if (lane == 0) C.nf = nf;
+  } else {
   // ---- one precompute pass: exact subset_stats sums (fp64) and, for IC-GN,
   // the reference-side update constants in fp32 per lane (<= npl terms):
   // sum f*sd, sum sd, and the Hessian moments of sd = (2 grad) x {1,dx,dy}.
   // A = sum (f - fbar) sd = sum f sd - fbar sum sd needs no second pass.
-  WarpConst& C = s_const[warp];
-  double fbar, nf;
-  double hinv[6] = {0, 0, 0, 0, 0, 0};
   {
     double sf = 0.0, sff = 0.0;
     float a[30];
@@ -689,6 +710,7 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
     const int64_t vf = (int64_t)n * (int64_t)sff - (int64_t)sf * (int64_t)sf;
     if (vf <= 0) {  // constant subset (exact test)
       fail(METHOD == 1 ? DICB200_POI_DEGENERATE_TEXTURE : DICB200_POI_DEGENERATE_SUBSET);
+      store_fail(DICB200_POI_DEGENERATE_TEXTURE);
       return;
     }
     fbar = sf / (double)n;  // correlation.cpp:25: exact sum / n
@@ -736,10 +758,29 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
       }
       if (!accept) {
         fail(DICB200_POI_DEGENERATE_TEXTURE);
+        store_fail(DICB200_POI_DEGENERATE_TEXTURE);
         return;
+      }
+      if (crec) {  // keep this POI's constants for the next pair on the same reference
+        __syncwarp();
+        if (lane == 0) {
+          crec[1] = fbar;
+          crec[2] = nf;
+          crec[3] = C.scf;
+        }
+        if (lane < 12) crec[4 + lane] = lane < 6 ? C.A[lane] : C.S[lane - 6];
+        if (lane < 6)
+#pragma unroll
+          for (int j = 0; j < 6; ++j) crec[16 + 6 * lane + j] = hinv[j];
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          crec[0] = 1.0;
+        }
       }
     }
   }
+  }  // precompute
   const float fbarf = (float)fbar;
   __syncwarp();
 
@@ -944,9 +985,48 @@ bool refine_plan(int M, int* ppt_out, int* nt_out) {
   return M >= 1 && strip_smem(M, 1, 1, 1) <= 100 * 1024;
 }
 
-cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st) {
+void icgn_cache_free(IcgnRefCache& c, cudaStream_t st, bool async) {
+  if (c.data) async ? cudaFreeAsync(c.data, st) : cudaFree(c.data);
+  c = IcgnRefCache{};
+}
+
+cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st, IcgnRefCache* cache, long ref_key) {
   if (p0.n_records <= 0) return cudaSuccess;
   RefineParams p = p0;
+  p.cache = nullptr;
+  if (p.method == 1 && cache && ref_key >= 0) {
+    // entries are filled lazily (tag 0 = not yet computed), so a new key only clears them
+    const bool same = cache->key == ref_key && cache->ref == p.ref.data && cache->W == p.ref.width &&
+                      cache->H == p.ref.height && cache->M == p.M && cache->x0 == p.lat.x0 &&
+                      cache->y0 == p.lat.y0 && cache->step == p.lat.step && cache->nx == p.lat.nx &&
+                      cache->ny == p.lat.ny;
+    const size_t bytes = (size_t)p.lat.nx * p.lat.ny * kIcgnCacheStride * sizeof(double);
+    cudaError_t e = cudaSuccess;
+    if (!same) {
+      cache->key = -1;
+      if (cache->cap < bytes) {
+        if (cache->data) cudaFreeAsync(cache->data, st);
+        cache->data = nullptr;
+        cache->cap = 0;
+        e = cudaMallocAsync((void**)&cache->data, bytes, st);
+        if (e != cudaSuccess) return e;
+        cache->cap = bytes;
+      }
+      e = cudaMemsetAsync(cache->data, 0, bytes, st);
+      if (e != cudaSuccess) return e;
+      cache->key = ref_key;
+      cache->ref = p.ref.data;
+      cache->W = p.ref.width;
+      cache->H = p.ref.height;
+      cache->M = p.M;
+      cache->x0 = p.lat.x0;
+      cache->y0 = p.lat.y0;
+      cache->step = p.lat.step;
+      cache->nx = p.lat.nx;
+      cache->ny = p.lat.ny;
+    }
+    p.cache = cache->data;
+  }
   p.spc = kWarps;
   while (p.spc > 1 && strip_smem(p.M, p.lat.step, p.spc, p.method) > 110 * 1024) --p.spc;
   const size_t smem = strip_smem(p.M, p.lat.step, p.spc, p.method);

@@ -15,9 +15,30 @@ struct RefineParams {
   int max_iter;
   dicb200_poi_record* rec;
   int spc;  // POIs per CTA strip (<= 8), chosen by refine_launch to fit shared memory
+  // IC-GN reference-side constants per POI (kIcgnCacheStride doubles, global
+  // POI index), reused while the reference frame repeats (fixed_first
+  // sequences): [0] tag (0 = not computed, 1 = ok, 1 + status = failed),
+  // [1] fbar, [2] nf, [3] scf, [4..9] A, [10..15] S, [16..51] H^-1 rows.
+  double* cache;
+};
+
+constexpr int kIcgnCacheStride = 52;
+
+// Device buffer + key of the IC-GN reference-side constants (see RefineParams::cache).
+struct IcgnRefCache {
+  double* data = nullptr;
+  size_t cap = 0;
+  long key = -1;
+  const void* ref = nullptr;
+  int W = 0, H = 0, M = 0, x0 = 0, y0 = 0, step = 0, nx = 0, ny = 0;
+  void reset() { key = -1; }
 };
 
 bool refine_plan(int M, int* ppt, int* nt);
-cudaError_t refine_launch(const RefineParams& p, bool u8, cudaStream_t st);
+// cache/ref_key: reuse the IC-GN reference-side constants across calls with
+// the same reference frame (ref_key >= 0, same device pointer, lattice and M).
+cudaError_t refine_launch(const RefineParams& p, bool u8, cudaStream_t st, IcgnRefCache* cache = nullptr,
+                          long ref_key = -1);
+void icgn_cache_free(IcgnRefCache& c, cudaStream_t st = nullptr, bool async = false);
 
 }  // namespace dicb200

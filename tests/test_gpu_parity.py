@@ -224,6 +224,43 @@ def test_analyze_sequence_pipeline_matches_pairwise(gpu):
                 assert np.array_equal(f.records[k], exp[k], equal_nan=True), (policy, f.pair_index, k)
 
 
+def test_sequence_device_matches_pairwise(gpu):
+    """dicb200_analyze_sequence_device (device-resident frames, reference-side
+    inputs reused along the sequence) == independent analyze_pair calls, for
+    both policies, BFS/IC-GN and mPSO/NR, with a pair-index offset (RNG keys)."""
+    import ctypes as C
+    import torch
+
+    w = configs.crop(configs.c5(6), 170, 150)
+    frames = [f.render() for f in w.frames]
+    dev = [torch.from_numpy(f.astype(np.int16) if f.dtype == np.uint16 else f).cuda() for f in frames]
+    L = dic.lib()
+    L.dicb200_analyze_sequence_device.argtypes = [
+        C.c_void_p, C.c_size_t, C.POINTER(_abi.RunConfigC), C.c_uint64, C.c_int32, C.c_int32, C.c_void_p,
+        C.c_size_t, C.POINTER(C.c_size_t), C.c_void_p]
+    ims = (_abi.Image * len(frames))()
+    for i, t in enumerate(dev):
+        im = dic.GrayImage(frames[i], i).as_c()
+        im.data = t.data_ptr()
+        ims[i] = im
+    for policy in (dic.ReferencePolicy.fixed_first, dic.ReferencePolicy.update_every_pair):
+        for im_, sm in ((dic.IntegerMethod.bfs, dic.SubpixelMethod.icgn), (dic.IntegerMethod.mpso, dic.SubpixelMethod.nr)):
+            cfg = copy.deepcopy(w.cfg)
+            cfg.reference_policy, cfg.integer_method, cfg.subpixel_method = policy, im_, sm
+            n = len(dic.grid_subsets(170, 150, cfg.grid.half_width, cfg.grid.spacing, cfg.effective_margin()))
+            out = torch.empty(len(frames) * n * C.sizeof(_abi.PoiRecordC), dtype=torch.uint8, device="cuda")
+            cnt = C.c_size_t(0)
+            assert L.dicb200_analyze_sequence_device(ims, len(frames), C.byref(cfg.to_c()), 7, -1, -1,
+                                                     C.c_void_p(out.data_ptr()), n, C.byref(cnt), None) == 0
+            torch.cuda.synchronize()
+            recs = np.frombuffer(out.cpu().numpy().tobytes(), dtype=_abi.record_dtype())
+            for k, (ra, tb) in enumerate(dic.sequence_pairs(policy, len(frames))):
+                exp = run_device(frames[ra], frames[tb], cfg, pair_index=7 + k)
+                got = recs[k * n:(k + 1) * n]
+                for f in exp.dtype.names:
+                    assert np.array_equal(got[f], exp[f], equal_nan=True), (policy, im_, k, f)
+
+
 def test_failure_semantics_degenerate_target(gpu, port):
     """Constant target regions: skipped candidates, 'all positions degenerate',
     refine failures keep the integer fields (pipeline.cpp:82-133)."""
