@@ -64,6 +64,7 @@ struct TcParams {
   Lattice lat;
   int rb, re;  // POI rows [rb, re)
   int M, R, side, planes, subpixel_none;
+  double maxv;  // largest gray level of either image (0 = full dtype range)
   int qx_min, qx_max, qy_min, qy_max, SW, SH;  // position domain (subset top-left corners)
   int ntx, nty, n_tiles;
   int RG, CG, NX, HT, RWB, n_mma;  // K blocking: 8 rows x 4 columns per MMA
@@ -110,6 +111,17 @@ bool tc_plan(TcParams& p);
 // Enqueues stats, reference preparation, the tensor-core kernel and the
 // per-POI merge (or only the surface when p.surface is set) on `st`.
 cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache = nullptr, long ref_key = -1);
+// ---- K1-BS: shared block sums on CUDA cores (bfs_bs.cu) ----
+struct BsGeom {
+  int S, RR, q, PX, PY, nbx, nby, nblk, EW, DXC, nchunk, dy_per, nsplit;  // s, r, L / s, POI tile, blocks
+  int RWp, RHp, TWp, THp;                                                // staged regions (pixels)
+  size_t off_tgt, off_blk, smem;
+  int threads;
+  int async_ok;  // u16 images with 8-byte aligned rows: cp.async staging
+};
+bool bs_plan(const TcParams& p, BsGeom& g);
+cudaError_t bs_launch(const TcParams& p, const BsGeom& g, cudaStream_t st);
+
 // async: stream-ordered release on `st` (device-resident callers); else cudaFree.
 void tc_cache_free(TcRefCache& c, cudaStream_t st = nullptr, bool async = false);
 

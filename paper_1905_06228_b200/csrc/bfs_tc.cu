@@ -1171,15 +1171,20 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
   }
-  // (b) reference moments + strip images (skipped when cached)
+  // (b) reference moments + strip images (skipped when cached; the block-sum
+  //     kernel reads the reference directly and needs no strips)
+  BsGeom bsg{};
+  const bool use_bs = bs_plan(p, bsg);
   if (e == cudaSuccess && !ref_ready) {
-    dim3 sg((p.ref.width + 31) / 32, p.strip_h / 64);
-    if (u8)
-      tc_strips_kernel<uint8_t><<<sg, 256, 0, st>>>(p);
-    else
-      tc_strips_kernel<uint16_t><<<sg, 256, 0, st>>>(p);
-    count_launch();
-    e = cudaGetLastError();
+    if (!use_bs) {
+      dim3 sg((p.ref.width + 31) / 32, p.strip_h / 64);
+      if (u8)
+        tc_strips_kernel<uint8_t><<<sg, 256, 0, st>>>(p);
+      else
+        tc_strips_kernel<uint16_t><<<sg, 256, 0, st>>>(p);
+      count_launch();
+      e = cudaGetLastError();
+    }
     if (e == cudaSuccess) {
       const size_t sm = (((size_t)p.ref.width * 4 + 15) & ~size_t(15)) + (size_t)p.ref.width * 8;
       if (u8) {
@@ -1207,12 +1212,16 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
     }
   }
   // (c) tensor-core search
-  if (e == cudaSuccess && p.n_tiles > 0) {
+  if (e == cudaSuccess && use_bs) {
+    StageTimer tm(4, st);
+    e = bs_launch(p, bsg, st);
+  }
+  if (e == cudaSuccess && p.n_tiles > 0 && !use_bs) {
     tc_tiles_kernel<<<(p.n_tiles + 255) / 256, 256, 0, st>>>(p);
     count_launch();
     e = cudaGetLastError();
   }
-  if (e == cudaSuccess && p.n_tiles > 0) {
+  if (e == cudaSuccess && p.n_tiles > 0 && !use_bs) {
     long long* dbg_buf = nullptr;
     if (p.dbg & 32) {  // tools: MMA-thread clock breakdown
       cudaMalloc(&dbg_buf, (size_t)p.grid * 8 * sizeof(long long));

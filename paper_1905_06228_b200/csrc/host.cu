@@ -143,6 +143,13 @@ static dicb200_status validate_pair(const dicb200_image* a, const dicb200_image*
   return DICB200_OK;
 }
 
+// Largest representable gray level of the pair (dicb200_image.bits, else the dtype's).
+static double pixel_max(const dicb200_image* a, const dicb200_image* b) {
+  const int bits = std::max(a->bits, b->bits);
+  if (a->dtype == DICB200_U8 && b->dtype == DICB200_U8) return 255.0;
+  return (bits > 0 && bits < 16) ? (double)((1 << bits) - 1) : 65535.0;
+}
+
 // Enqueue the whole per-pair chain for grid rows [rb, re) on `st`.
 static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image* tgt, const dicb200_run_config* cfg,
                                    uint64_t pair_index, const Lattice& lat, int rb, int re,
@@ -181,6 +188,7 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
       t.R = p.R;
       t.planes = p.u8 ? 1 : 2;
       t.subpixel_none = p.subpixel_none;
+      t.maxv = pixel_max(ref, tgt);
       t.rec = out_dev;
       if (tc_plan(t)) {
         StageTimer tm(0, st);
@@ -240,6 +248,7 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
       t.R = b.R;
       t.planes = b.u8 ? 1 : 2;
       t.subpixel_none = 1;
+      t.maxv = pixel_max(ref, tgt);
       t.surface = surface;
       const bool use_tc = tc_plan(t);
       if (!use_tc && !bfs_plan(b, 72 * 1024) && !bfs_plan(b, 200 * 1024)) {

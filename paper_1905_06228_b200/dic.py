@@ -175,8 +175,16 @@ class GrayImage:
         im.pitch = self.width()
         im.dtype = _abi.U8 if self._px.dtype == np.uint8 else _abi.U16
         im.id = self._id
+        im.bits = self.bits()
         im.data = self._px.ctypes.data
         return im
+
+    def bits(self) -> int:
+        """Significant bits of the largest gray level (dicb200_image.bits): lets
+        12-bit data in u16 storage take the exact 32-bit integer paths."""
+        if not hasattr(self, "_bits"):
+            self._bits = max(1, int(self._px.max()).bit_length())
+        return self._bits
 
 
 @dataclass

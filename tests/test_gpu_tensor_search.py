@@ -31,15 +31,22 @@ def _frames(width, height, dtype, max_value, seed, u, v):
     return f.render(), g.render()
 
 
-def _run(a, b, cfg, legacy):
+def _run(a, b, cfg, legacy, path=None):
+    """path: None = the library's choice, "tc" = force the tensor-core kernel,
+    "bs" = the block-sum kernel wherever it has an instantiation (also u8)."""
+    for k in ("DICB200_BFS_LEGACY", "DICB200_BFS_TC", "DICB200_BFS_BS"):
+        os.environ.pop(k, None)
     if legacy:
         os.environ["DICB200_BFS_LEGACY"] = "1"
-    else:
-        os.environ.pop("DICB200_BFS_LEGACY", None)
+    if path == "tc":
+        os.environ["DICB200_BFS_TC"] = "1"
+    if path == "bs":
+        os.environ["DICB200_BFS_BS"] = "1"
     try:
         return dic.analyze_pair(dic.GrayImage(a, 0), dic.GrayImage(b, 1), cfg).records
     finally:
-        os.environ.pop("DICB200_BFS_LEGACY", None)
+        for k in ("DICB200_BFS_LEGACY", "DICB200_BFS_TC", "DICB200_BFS_BS"):
+            os.environ.pop(k, None)
 
 
 def _cfg(M, R, step, method=IntegerMethod.bfs, margin=-1):
@@ -127,3 +134,41 @@ def test_tensor_surface_matches_cuda_core_for_pso(gpu):
         assert len(got) >= 1024
         for f in FIELDS:
             assert np.array_equal(got[f], exp[f], equal_nan=True), (method, f)
+
+
+# Shared-block-sum kernel (csrc/bfs_bs.cu): lattices whose spacing / remainder
+# match an instantiation; bit-identical to the tensor-core and CUDA-core kernels.
+BS_CASES = [
+    # (width, height, dtype, max_value, M, R, step, u, v, method)
+    (420, 400, _abi.U16, 4095, 20, 12, 10, 2.6, -3.3, IntegerMethod.bfs),   # c5 shape (s 10, r 1)
+    (337, 301, _abi.U16, 4095, 20, 5, 5, -1.4, 0.8, IntegerMethod.bfs),     # c4 shape (s 5, r 1), odd frame
+    (420, 400, _abi.U8, 255, 15, 15, 10, 4.2, 3.1, IntegerMethod.bfs),      # c2 shape (u8, EW 31)
+    (330, 320, _abi.U8, 255, 15, 20, 8, -6.3, 5.5, IntegerMethod.mpso),     # c3 shape (s 8, r 7), surface
+]
+
+
+@pytest.mark.parametrize("case", BS_CASES, ids=[f"bsM{c[4]}R{c[5]}s{c[6]}d{c[2]}{c[9].name}" for c in BS_CASES])
+def test_block_sum_search_bit_identical(gpu, case):
+    width, height, dtype, maxv, M, R, step, u, v, method = case
+    a, b = _frames(width, height, dtype, maxv, 5 + M + R, u, v)
+    cfg = _cfg(M, R, step, method=method)
+    got = _run(a, b, cfg, legacy=False, path="bs")
+    tc = _run(a, b, cfg, legacy=False, path="tc")
+    exp = _run(a, b, cfg, legacy=True)
+    assert len(got) >= 1024
+    for f in FIELDS:
+        assert np.array_equal(tc[f], exp[f], equal_nan=True), ("tc", f)
+        assert np.array_equal(got[f], exp[f], equal_nan=True), ("bs", f, np.nonzero(got[f] != exp[f])[0][:5])
+
+
+def test_block_sum_row_shards_and_degenerate(gpu):
+    """Row-range launches and constant regions through the block-sum kernel."""
+    a, b = _frames(420, 400, _abi.U16, 4095, 77, 1.2, -2.2)
+    b[:, :80] = 2000
+    a[120:180, 200:260] = 900
+    cfg = _cfg(20, 12, 10)
+    got = _run(a, b, cfg, legacy=False)
+    exp = _run(a, b, cfg, legacy=True)
+    assert (exp["status"] != 0).any()
+    for f in FIELDS:
+        assert np.array_equal(got[f], exp[f], equal_nan=True), f
