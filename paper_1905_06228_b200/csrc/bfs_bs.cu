@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(NT, 1) bs_kernel(TcParams p, BsGeom g) {
   const int nx_here = min(g.PX, p.lat.nx - ix0), ny_here = min(g.PY, p.re - iy0);
   const int nbx = g.nbx;  // block-record row stride
   const int nbx_here = nx_here + Q - (RR == 0 ? 1 : 0), nby = ny_here + Q - (RR == 0 ? 1 : 0);  // blocks needed
-  const int BS = 4 * EW;  // words per block record
+  const int BS = 4 * EW + 1;  // words per block record (odd: conflict-free stores across blocks)
   const size_t ew2 = (size_t)EW * EW;
   for (int dy = dy_lo; dy <= dy_hi; ++dy) {
     // ---- phase A: block partials, DXC displacements per thread
@@ -120,11 +120,13 @@ __global__ void __launch_bounds__(NT, 1) bs_kernel(TcParams p, BsGeom g) {
       const int c = task / (nbx_here * nby), bb = task - c * (nbx_here * nby);
       const int by = bb / nbx_here, bx = bb - by * nbx_here, b = by * nbx + bx;
       const int dx0 = c * DXC;  // chunk start, as an index dx + R
+      const uint16_t* fr = Rf + (by * S) * RP + shR + bx * S;
+      const uint16_t* gr = Tg + (by * S + dy + R) * TP + shT + bx * S + dx0;
+      uint32_t* o = blk + b * BS + dx0;
+      const int nd = min(DXC, EW - dx0);
       uint32_t F[DXC], Cc[DXC], Wr[DXC], Kc[DXC];
 #pragma unroll
       for (int j = 0; j < DXC; ++j) F[j] = Cc[j] = Wr[j] = Kc[j] = 0u;
-      const uint16_t* fr = Rf + (by * S) * RP + shR + bx * S;
-      const uint16_t* gr = Tg + (by * S + dy + R) * TP + shT + bx * S + dx0;
 #pragma unroll
       for (int yy = 0; yy < S; ++yy) {
         uint32_t f[S], gg[S + DXC - 1];
@@ -132,26 +134,32 @@ __global__ void __launch_bounds__(NT, 1) bs_kernel(TcParams p, BsGeom g) {
         for (int k = 0; k < S; ++k) f[k] = fr[yy * RP + k];
 #pragma unroll
         for (int k = 0; k < S + DXC - 1; ++k) gg[k] = gr[yy * TP + k];
+        // k outer, j inner: DXC independent multiply-add chains per pixel column
+        uint32_t part[DXC], full[DXC];
+#pragma unroll
+        for (int j = 0; j < DXC; ++j) part[j] = RR > 0 ? f[0] * gg[j] : 0u;
+#pragma unroll
+        for (int k = 1; k < RR; ++k)
+#pragma unroll
+          for (int j = 0; j < DXC; ++j) part[j] += f[k] * gg[k + j];
+#pragma unroll
+        for (int j = 0; j < DXC; ++j) full[j] = part[j];
+#pragma unroll
+        for (int k = RR; k < S; ++k)
+#pragma unroll
+          for (int j = 0; j < DXC; ++j) full[j] += f[k] * gg[k + j];
 #pragma unroll
         for (int j = 0; j < DXC; ++j) {
-          uint32_t part = 0u;
-#pragma unroll
-          for (int k = 0; k < RR; ++k) part += f[k] * gg[k + j];
-          uint32_t full = part;
-#pragma unroll
-          for (int k = RR; k < S; ++k) full += f[k] * gg[k + j];
-          F[j] += full;
+          F[j] += full[j];
           if (RR > 0) {
-            Cc[j] += part;
+            Cc[j] += part[j];
             if (yy < RR) {
-              Wr[j] += full;
-              Kc[j] += part;
+              Wr[j] += full[j];
+              Kc[j] += part[j];
             }
           }
         }
       }
-      uint32_t* o = blk + b * BS + dx0;
-      const int nd = min(DXC, EW - dx0);
 #pragma unroll
       for (int j = 0; j < DXC; ++j)
         if (j < nd) {
@@ -218,6 +226,7 @@ struct BsVariant {
 };
 constexpr BsVariant kVariants[] = {
     {10, 1, 4, 25, 256},  // c5: L 41, s 10, R 12
+    {10, 1, 4, 13, 512},  // c5, two dx chunks, twice the warps
     {10, 1, 3, 31, 256},  // c2: L 31, s 10, R 15
     {5, 1, 8, 11, 384},   // c4: L 41, s 5, R 5
     {8, 7, 3, 41, 256},   // c3: L 31, s 8, R 20
@@ -268,6 +277,7 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
   int best = -1, waste = 1 << 30;
   for (int v = 0; v < (int)(sizeof(kVariants) / sizeof(kVariants[0])); ++v) {
     if (kVariants[v].S != s || kVariants[v].RR != g.RR || kVariants[v].Q != g.q) continue;
+    if (std::getenv("DICB200_BS_DXC") && kVariants[v].DXC != std::atoi(std::getenv("DICB200_BS_DXC"))) continue;
     const int nch = (g.EW + kVariants[v].DXC - 1) / kVariants[v].DXC;
     const int w = nch * kVariants[v].DXC - g.EW;
     if (w < waste) {
@@ -305,7 +315,7 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
     auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };
     g.off_tgt = al((size_t)g.RWp * g.RHp * pix);
     g.off_blk = al(g.off_tgt + (size_t)g.TWp * g.THp * pix);
-    g.smem = g.off_blk + (size_t)g.nblk * 4 * g.EW * 4;
+    g.smem = g.off_blk + (size_t)g.nblk * (4 * g.EW + 1) * 4;
     if (g.smem <= 220 * 1024) break;
     if (g.PY > 2)
       g.PY /= 2;
@@ -327,6 +337,7 @@ cudaError_t bs_launch(const TcParams& p, const BsGeom& g, cudaStream_t st) {
   dim3 grid((p.lat.nx + g.PX - 1) / g.PX, (rows + g.PY - 1) / g.PY, g.nsplit);
   cudaError_t e = cudaErrorInvalidValue;
   if (g.S == 10 && g.RR == 1 && g.q == 4 && g.DXC == 25) e = launch_variant<10, 1, 4, 25, 256>(p, g, grid, st);
+  if (g.S == 10 && g.RR == 1 && g.q == 4 && g.DXC == 13) e = launch_variant<10, 1, 4, 13, 512>(p, g, grid, st);
   if (g.S == 10 && g.RR == 1 && g.q == 3 && g.DXC == 31) e = launch_variant<10, 1, 3, 31, 256>(p, g, grid, st);
   if (g.S == 5 && g.RR == 1 && g.q == 8 && g.DXC == 11) e = launch_variant<5, 1, 8, 11, 384>(p, g, grid, st);
   if (g.S == 8 && g.RR == 7 && g.q == 3 && g.DXC == 41) e = launch_variant<8, 7, 3, 41, 256>(p, g, grid, st);
