@@ -42,7 +42,7 @@ import numpy as np  # noqa: E402
 from paper_1905_06228_b200 import _abi, configs, dic  # noqa: E402
 
 PIPES_BIN = os.path.join(ROOT, "tools", "microbench", "pipes")
-N_STAGES = 6  # DICB200_N_STAGES
+N_STAGES = 7  # DICB200_N_STAGES
 
 
 def _measured_peaks() -> dict:
@@ -202,8 +202,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     # shard: image-parallel over pairs, or subset-parallel over grid rows for single-pair configs
     spp = w.subsets_per_pair()
-    lat_rows = len({y for _, y in dic.grid_subsets(f0.width, f0.height, cfg.grid.half_width, cfg.grid.spacing,
-                                                   cfg.effective_margin())})
+    grid_pts = dic.grid_subsets(f0.width, f0.height, cfg.grid.half_width, cfg.grid.spacing, cfg.effective_margin())
+    lat_rows = len({y for _, y in grid_pts})
     if n_pairs > 1:
         base, extra = divmod(n_pairs, world)
         lo = rank * base + min(rank, extra)
@@ -402,7 +402,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         return None
 
     # ---- roofline of the dominant stage ----
-    names = ["bfs_zncc", "pso", "nr", "icgn", "tc_cross_terms", "tc_zncc"]
+    names = ["bfs_zncc", "pso", "nr", "icgn", "tc_cross_terms", "tc_zncc", "bs_cross_terms"]
     stage = {names[i]: {"ms_total": float(stage_ms[i]), "launches": int(stage_n[i]),
                         "avg_ms": float(stage_ms[i]) / max(1, int(stage_n[i]))} for i in range(N_STAGES) if stage_n[i]}
     top = {k: v for k, v in stage.items() if k in names[:4]}
@@ -424,6 +424,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "peak_source": MEASURED_PEAKS["source"] + " bf16_tflops (dense bf16 FLOP/s == dense i8 MAC/s on B200)",
                 "work_per_launch": f"sum(evaluations) x (2M+1)^2 x planes^2 = {macs_per_launch:.4g} i8 MACs",
                 "launch_ms": st_tc["avg_ms"]}
+    elif dom in ("bfs_zncc", "pso") and "bs_cross_terms" in stage:
+        roof = None  # block-sum search: reported below as roofline_search
     elif dom == "bfs_zncc":
         # algorithmic work per launch: (sum of evaluations over the launch's POIs) x n MACs
         macs_per_launch = evals / max(1, len(my_pairs)) * n_px
@@ -456,6 +458,32 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "unit": "TMAC/s", "frac": achieved / peak if peak else None, "traffic": None,
                 "peak_source": "measured live by tools/microbench/pipes",
                 "work_per_launch": f"sum(evaluations) x n = {macs_per_launch:.4g} MACs"}
+    roof_search = None
+    if "bs_cross_terms" in stage:
+        # block-sum search (csrc/bfs_bs.cu): its algorithmic work is every
+        # (reference pixel of the union of subsets) x (displacement) product once;
+        # the per-POI formulation's sum(evaluations) x n is reported beside it
+        xs = sorted({x for x, _ in grid_pts})
+        ys = sorted({y for _, y in grid_pts})
+        side = 2 * cfg.grid.half_width + 1
+        ew = 2 * cfg.search.search_radius + 1
+        union_px = (xs[-1] - xs[0] + side) * (ys[-1] - ys[0] + side)
+        st_bs = stage["bs_cross_terms"]
+        pairs_per_launch = len(my_pairs) * args.steps / max(1, st_bs["launches"])
+        macs_launch = union_px * ew * ew * pairs_per_launch
+        achieved = macs_launch / (st_bs["avg_ms"] * 1e-3) / 1e12
+        peak = peaks.get("imad_Ginstr_per_s", 0) / 1e3
+        per_poi = evals * args.steps / max(1, st_bs["launches"]) * n_px / (st_bs["avg_ms"] * 1e-3) / 1e12
+        roof_search = {"kernel": "bs_kernel", "bound": "alu", "pipe": "IMAD (exact u32 products)",
+                       "achieved": achieved, "peak": peak, "unit": "TMAC/s", "frac": achieved / peak if peak else None,
+                       "traffic": None, "launch_ms": st_bs["avg_ms"],
+                       "peak_source": "measured live by tools/microbench/pipes (IMAD issue rate)",
+                       "work_per_launch": f"|union of subsets| x (2R+1)^2 = {macs_launch:.4g} MACs",
+                       "per_poi_equivalent_tmacs": per_poi,
+                       "note": "the per-POI formulation (sum(evaluations) x n) would need per_poi_equivalent "
+                               "TMAC/s of IMAD; the block partials are shared by the (L/s)^2 overlapping subsets"}
+        if roof is None:
+            roof = roof_search
     prof_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if roof and os.path.exists(prof_path):
         try:
@@ -488,6 +516,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "gpu_launches": launches,
         "stages": stage,
         "roofline": roof,
+        "roofline_search": roof_search,
         "clocks": clk,
         "parity_in_run": {"records": int(n_all), "status_ok": int(ok_all), "mean_iterations": iters_all / max(1, n_all)},
         "pipe_peaks": {k: v for k, v in peaks.items() if k.endswith("per_s")},

@@ -213,9 +213,10 @@ void dicb200_reset_launch_count(void);
  * is bracketed by CUDA events on the stream it runs on. dicb200_profile_read
  * waits for them and returns per-stage totals (ms) and launch counts, then
  * clears. Stages: 0 BFS-ZNCC, 1 PSO/mPSO, 2 NR, 3 IC-GN (whole stages);
- * 4 the tensor-core cross-term kernel and 5 the ZNCC argmax/surface kernel
- * inside stage 0 or 1 when the tensor-core search runs. */
-#define DICB200_N_STAGES 6
+ * inside stage 0 or 1 when the window search runs on the cross-term path:
+ * 4 the tensor-core cross-term kernel, 5 the ZNCC argmax/surface kernel,
+ * 6 the block-sum cross-term kernel (whichever of 4 / 6 the plan picked). */
+#define DICB200_N_STAGES 7
 void dicb200_profile_enable(int on);
 int dicb200_profile_read(double* ms_out, uint64_t* launches_out);
 

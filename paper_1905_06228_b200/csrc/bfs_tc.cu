@@ -1213,7 +1213,7 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
   }
   // (c) tensor-core search
   if (e == cudaSuccess && use_bs) {
-    StageTimer tm(4, st);
+    StageTimer tm(6, st);
     e = bs_launch(p, bsg, st);
   }
   if (e == cudaSuccess && p.n_tiles > 0 && !use_bs) {

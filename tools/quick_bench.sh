@@ -9,7 +9,7 @@ try:
     d = json.loads(open(f"gpurun_out/qb_{c}.json").read())
 except Exception as e:
     print(c, "FAILED", open(f"gpurun_out/qb_{c}.err").read()[-800:]); sys.exit()
-st = {k: round(v["avg_ms"], 4) for k, v in d["stages"].items()}
-print(c, "value %.4g" % d["value"], "e2e %.4g" % d["e2e"]["value"], st, "roof", d["roofline"].get("kernel"), round(d["roofline"]["frac"], 3), "ok", d["parity_in_run"]["status_ok"], "/", d["parity_in_run"]["records"])
+st = {k: round(v["avg_ms"], 4) for k, v in d["stages"].items()}; rs = d.get("roofline_search") or {}
+print(c, "value %.4g" % d["value"], "e2e %.4g" % d["e2e"]["value"], st, "roof", d["roofline"].get("kernel"), round(d["roofline"]["frac"], 3), "search_roof", rs.get("kernel"), round(rs.get("frac") or 0, 3), "ok", d["parity_in_run"]["status_ok"], "/", d["parity_in_run"]["records"])
 PY
 done
