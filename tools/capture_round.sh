@@ -12,7 +12,8 @@ timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/c
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/cap/launches_bench_c5.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/cap/ncu_bench.log 2>&1
 python tools/profile_case.py c5 1 > /dev/null
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:bfs_tc_kernel -c 1 -o gpurun_out/cap/full_bfs_tc_c5 python tools/profile_case.py c5 1 > gpurun_out/cap/full_bfs_tc_c5.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:bs_kernel -c 1 -o gpurun_out/cap/full_bs_c5 python tools/profile_case.py c5 1 > gpurun_out/cap/full_bs_c5.log 2>&1
+DICB200_BFS_TC=1 timeout 900 ncu --set full --import-source on --clock-control none -k regex:bfs_tc_kernel -c 1 -o gpurun_out/cap/full_bfs_tc_c5 python tools/profile_case.py c5 1 > gpurun_out/cap/full_bfs_tc_c5.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:refine_strip -c 1 -o gpurun_out/cap/full_refine_c5 python tools/profile_case.py c5 1 > gpurun_out/cap/full_refine_c5.log 2>&1
 timeout 900 ncu --set full --clock-control none -k regex:"tc_argmax|tc_stats|tc_strips|tc_prep" -c 4 -o gpurun_out/cap/full_aux_c5 python tools/profile_case.py c5 1 > gpurun_out/cap/full_aux_c5.log 2>&1
 ls -la gpurun_out/cap
