@@ -277,15 +277,20 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
             dist.barrier()
 
-    # warm-up
+    # the live pipe-rate microbenchmark runs in its own process before the warm-up,
+    # so nothing it leaves behind (context switch, clocks) lands in the timed steps
+    peaks = pipe_peaks() if rank == 0 else {}
+    # warm-up (the last step with stage timing on, so the timing events are
+    # created here and only recycled inside the timed region)
     with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
+        for wi in range(args.warmup):
+            L.dicb200_profile_enable(1 if wi == args.warmup - 1 else 0)
             step()
             if flush is not None:
                 flush.fill_(1)
     stream.synchronize()
+    L.dicb200_profile_enable(0)
 
-    peaks = pipe_peaks() if rank == 0 else {}
     # timed region: K steps, CUDA events on the launch stream, stage events live
     clocks = Clocks(local_rank)
     L.dicb200_profile_read((C.c_double * N_STAGES)(), (C.c_uint64 * N_STAGES)())  # clear
@@ -299,8 +304,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     L.dicb200_profile_enable(1)
     with torch.cuda.stream(stream):
         ev0.record(stream)
+        step_ev = []
         for _ in range(args.steps):
             step()
+            step_ev.append(torch.cuda.Event(enable_timing=True))
+            step_ev[-1].record(stream)
             if flush is not None:
                 fa, fb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 fa.record(stream)
@@ -315,6 +323,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize()
     barrier()
     ms_total = ev0.elapsed_time(ev1)
+    step_ms = [round(a.elapsed_time(b), 3) for a, b in zip([ev0] + step_ev[:-1], step_ev)]
     stage_ms = (C.c_double * N_STAGES)()
     stage_n = (C.c_uint64 * N_STAGES)()
     L.dicb200_profile_read(stage_ms, stage_n)
@@ -517,6 +526,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "stages": stage,
         "roofline": roof,
         "roofline_search": roof_search,
+        "step_ms": step_ms,
         "clocks": clk,
         "parity_in_run": {"records": int(n_all), "status_ok": int(ok_all), "mean_iterations": iters_all / max(1, n_all)},
         "pipe_peaks": {k: v for k, v in peaks.items() if k.endswith("per_s")},

@@ -880,11 +880,49 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p, int sp) {
     const int fw = fx_hi - fx_lo + 1, total = fw * (fy_hi - fy_lo + 1);
     int ry = lane / fw, rx = lane - ry * fw;
     const int jump_y = 32 / fw, jump_x = 32 - jump_y * fw;
+    // cross terms U at a time per lane: their loads are issued together
+    constexpr int U = 4;
+    int64_t pre[U];
+    {
+      int px = rx, py = ry;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        pre[u] = lane + 32 * u < total ? buf[(fy_lo + py + R) * EW + (fx_lo + px + R)] : 0;
+        px += jump_x;
+        py += jump_y;
+        if (px >= fw) {
+          px -= fw;
+          ++py;
+        }
+      }
+    }
+    int ahead_x = rx, ahead_y = ry;  // position of candidate idx + 32 U
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      ahead_x += jump_x;
+      ahead_y += jump_y;
+      if (ahead_x >= fw) {
+        ahead_x -= fw;
+        ++ahead_y;
+      }
+    }
+    int slot = 0;
     for (int idx = lane; idx < total; idx += 32) {
       {
         const int dx = fx_lo + rx, dy = fy_lo + ry;
+        const int64_t sfg_v = pre[0];
+#pragma unroll
+        for (int u = 0; u < U - 1; ++u) pre[u] = pre[u + 1];
+        pre[U - 1] = idx + 32 * U < total ? buf[(fy_lo + ahead_y + R) * EW + (fx_lo + ahead_x + R)] : 0;
+        ahead_x += jump_x;
+        ahead_y += jump_y;
+        if (ahead_x >= fw) {
+          ahead_x -= fw;
+          ++ahead_y;
+        }
+        (void)slot;
         Cand c;
-        if (tc_candidate_s(pv, n, sf, buf[(dy + R) * EW + (dx + R)], cx - M + dx, cy - M + dy, c)) {
+        if (tc_candidate_s(pv, n, sf, sfg_v, cx - M + dx, cy - M + dy, c)) {
           ++cnt;
           const double av = i64_to_f64(c.num) * rsvf * (double)c.rsq;
           if (av > a1) {  // a2: the lane's runner-up (only its value is needed)

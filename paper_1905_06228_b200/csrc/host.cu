@@ -32,13 +32,28 @@ struct StageEvent {
 std::atomic<int> g_profile{0};
 std::mutex g_profile_mu;
 std::vector<StageEvent> g_events;
+std::vector<cudaEvent_t> g_event_pool;  // recycled timing events (creation is slow on the hot path)
+
+cudaEvent_t take_event() {
+  {
+    std::lock_guard<std::mutex> lk(g_profile_mu);
+    if (!g_event_pool.empty()) {
+      cudaEvent_t e = g_event_pool.back();
+      g_event_pool.pop_back();
+      return e;
+    }
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
 
 }  // namespace
 
 StageTimer::StageTimer(int s, cudaStream_t stream) : stage(s), st(stream) {
   if (!g_profile.load()) return;
-  cudaEventCreate(&a);
-  cudaEventCreate(&b);
+  a = take_event();
+  b = take_event();
   cudaEventRecord(a, st);
 }
 
@@ -893,8 +908,13 @@ int dicb200_profile_read(double* ms, uint64_t* launches) {
     if (cudaEventSynchronize(e.b) != cudaSuccess || cudaEventElapsedTime(&t, e.a, e.b) != cudaSuccess) rc = 1;
     ms[e.stage] += t;
     launches[e.stage] += 1;
-    cudaEventDestroy(e.a);
-    cudaEventDestroy(e.b);
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_profile_mu);
+    for (auto& e : ev) {
+      g_event_pool.push_back(e.a);
+      g_event_pool.push_back(e.b);
+    }
   }
   return rc;
 }
