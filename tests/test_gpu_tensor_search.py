@@ -142,6 +142,8 @@ BS_CASES = [
     # (width, height, dtype, max_value, M, R, step, u, v, method)
     (420, 400, _abi.U16, 4095, 20, 12, 10, 2.6, -3.3, IntegerMethod.bfs),   # c5 shape (s 10, r 1)
     (337, 301, _abi.U16, 4095, 20, 5, 5, -1.4, 0.8, IntegerMethod.bfs),     # c4 shape (s 5, r 1), odd frame
+    (300, 290, _abi.U16, 4095, 20, 10, 5, 6.3, -7.7, IntegerMethod.bfs),    # two dx chunks (EW 21 > DXC 11)
+    (310, 300, _abi.U16, 4095, 20, 10, 5, -2.2, 1.9, IntegerMethod.pso),    # block sums feeding the PSO surface
     (420, 400, _abi.U8, 255, 15, 15, 10, 4.2, 3.1, IntegerMethod.bfs),      # c2 shape (u8, EW 31)
     (330, 320, _abi.U8, 255, 15, 20, 8, -6.3, 5.5, IntegerMethod.mpso),     # c3 shape (s 8, r 7), surface
 ]
