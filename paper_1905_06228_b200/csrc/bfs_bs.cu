@@ -226,7 +226,6 @@ struct BsVariant {
 };
 constexpr BsVariant kVariants[] = {
     {10, 1, 4, 25, 256},  // c5: L 41, s 10, R 12
-    {10, 1, 4, 13, 512},  // c5, two dx chunks, twice the warps
     {10, 1, 3, 31, 256},  // c2: L 31, s 10, R 15
     {5, 1, 8, 11, 384},   // c4: L 41, s 5, R 5
     {8, 7, 3, 41, 256},   // c3: L 31, s 8, R 20
@@ -277,7 +276,6 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
   int best = -1, waste = 1 << 30;
   for (int v = 0; v < (int)(sizeof(kVariants) / sizeof(kVariants[0])); ++v) {
     if (kVariants[v].S != s || kVariants[v].RR != g.RR || kVariants[v].Q != g.q) continue;
-    if (std::getenv("DICB200_BS_DXC") && kVariants[v].DXC != std::atoi(std::getenv("DICB200_BS_DXC"))) continue;
     const int nch = (g.EW + kVariants[v].DXC - 1) / kVariants[v].DXC;
     const int w = nch * kVariants[v].DXC - g.EW;
     if (w < waste) {
@@ -337,7 +335,6 @@ cudaError_t bs_launch(const TcParams& p, const BsGeom& g, cudaStream_t st) {
   dim3 grid((p.lat.nx + g.PX - 1) / g.PX, (rows + g.PY - 1) / g.PY, g.nsplit);
   cudaError_t e = cudaErrorInvalidValue;
   if (g.S == 10 && g.RR == 1 && g.q == 4 && g.DXC == 25) e = launch_variant<10, 1, 4, 25, 256>(p, g, grid, st);
-  if (g.S == 10 && g.RR == 1 && g.q == 4 && g.DXC == 13) e = launch_variant<10, 1, 4, 13, 512>(p, g, grid, st);
   if (g.S == 10 && g.RR == 1 && g.q == 3 && g.DXC == 31) e = launch_variant<10, 1, 3, 31, 256>(p, g, grid, st);
   if (g.S == 5 && g.RR == 1 && g.q == 8 && g.DXC == 11) e = launch_variant<5, 1, 8, 11, 384>(p, g, grid, st);
   if (g.S == 8 && g.RR == 7 && g.q == 3 && g.DXC == 41) e = launch_variant<8, 7, 3, 41, 256>(p, g, grid, st);
