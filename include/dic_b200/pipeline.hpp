@@ -11,7 +11,8 @@
 // Semantics: identical records to dic::analyze_pair (same grid order, same
 // per-POI failure semantics). Pair-level failures throw dic::Error with the
 // reference's message. GrayImage values must be integers in [0, 65535]
-// (every 8/16-bit camera frame is); anything else throws dic::Error.
+// (every 8/16-bit camera frame is) or fractional levels in [0, 255], which are
+// carried as 8.8 fixed point (see detail::pack); anything else throws dic::Error.
 #pragma once
 
 #include <cmath>
@@ -52,26 +53,47 @@ inline dicb200_run_config to_c(const RunConfig& c) {
   return r;
 }
 
-// GrayImage (doubles) -> packed u8/u16 + descriptor. Throws on non-integer levels.
+// GrayImage (doubles) -> packed u8/u16 + descriptor. Integer gray levels in
+// [0, 65535] map losslessly. Non-integer levels in [0, 255] (e.g. the
+// reference's synth_speckle / synth_warped_pair frames) are carried with 8
+// fractional bits: u16 = round(256 v). ZNCC, the IC-GN / NR steps and every
+// decision derived from them are invariant to a positive gray-level scale, so
+// only the 2^-9 quantisation of each sample separates the result from the
+// reference's doubles. Anything else (negative, > 65535, fractional above
+// 255, non-finite) throws dic::Error.
 struct Packed {
   std::vector<uint8_t> u8;
   std::vector<uint16_t> u16;
   dicb200_image img{};
 };
 
+inline bool is_integral(const GrayImage& g) {
+  for (double v : g.pixels())
+    if (v != std::floor(v)) return false;
+  return true;
+}
+
 inline void pack(const GrayImage& g, Packed& out, bool force16) {
   const auto& px = g.pixels();
+  const bool frac = !is_integral(g);
   double mx = 0.0;
   for (double v : px) {
-    if (v < 0.0 || v > 65535.0 || v != std::floor(v))
-      throw Error("dicb200: gray levels must be integers in [0, 65535]");
+    if (!(v >= 0.0) || v > (frac ? 255.0 : 65535.0))
+      throw Error(frac ? "dicb200: fractional gray levels must lie in [0, 255]"
+                       : "dicb200: gray levels must be integers in [0, 65535]");
     mx = v > mx ? v : mx;
   }
   out.img.width = g.width();
   out.img.height = g.height();
   out.img.pitch = g.width();
   out.img.id = g.id();
-  if (mx <= 255.0 && !force16) {
+  if (frac) {
+    out.u16.resize(px.size());
+    for (size_t i = 0; i < px.size(); ++i) out.u16[i] = static_cast<uint16_t>(std::lround(px[i] * 256.0));
+    out.img.dtype = DICB200_U16;
+    out.img.bits = 16;
+    out.img.data = out.u16.data();
+  } else if (mx <= 255.0 && !force16) {
     out.u8.assign(px.begin(), px.end());
     out.img.dtype = DICB200_U8;
     out.img.bits = 8;
@@ -103,7 +125,7 @@ inline PoiRecord to_record(const dicb200_poi_record& r) {
 inline bool max_is_u8(const GrayImage& g) {
   for (double v : g.pixels())
     if (v > 255.0) return false;
-  return true;
+  return is_integral(g);  // fractional frames travel as 8.8 fixed point (u16)
 }
 
 }  // namespace detail

@@ -132,23 +132,34 @@ class GrayImage:
     """Immutable single-channel image (image.hpp:14-31).
 
     The reference stores doubles; the device path stores the integer gray
-    levels losslessly as uint8 / uint16. A float array is accepted only when
-    every value is an integer in [0, 65535] (raises DicError otherwise).
+    levels losslessly as uint8 / uint16. Fractional levels in [0, 255] (the
+    reference's synthetic frames) are carried as 8.8 fixed point, round(256 v)
+    in uint16 — ZNCC and the refinement steps are invariant to a positive
+    gray-level scale, so only the 2^-9 quantisation differs from the doubles
+    (`scale` = 256; `at()` returns the level in the caller's units). Anything
+    else raises DicError, as the C++ shim (include/dic_b200/pipeline.hpp) does.
     """
 
     def __init__(self, pixels: np.ndarray, id: int = 0):
         a = np.asarray(pixels)
         if a.ndim != 2 or a.shape[0] < 1 or a.shape[1] < 1:
             raise DicError("zero-dimension image")
+        self.scale = 1
         if a.dtype == np.uint8 or a.dtype == np.uint16:
             px = np.ascontiguousarray(a)
         else:
             f = a.astype(np.float64)
             if not np.all(np.isfinite(f)):
                 raise DicError("non-finite gray level")
-            if np.any(f != np.round(f)) or f.min() < 0 or f.max() > 65535:
-                raise DicError("device path requires integer gray levels in [0, 65535]")
-            px = np.ascontiguousarray(f.astype(np.uint8 if f.max() <= 255 else np.uint16))
+            if np.all(f == np.round(f)):
+                if f.min() < 0 or f.max() > 65535:
+                    raise DicError("device path requires integer gray levels in [0, 65535]")
+                px = np.ascontiguousarray(f.astype(np.uint8 if f.max() <= 255 else np.uint16))
+            else:
+                if f.min() < 0 or f.max() > 255:
+                    raise DicError("fractional gray levels must lie in [0, 255]")
+                px = np.ascontiguousarray(np.round(f * 256.0).astype(np.uint16))
+                self.scale = 256
         px.setflags(write=False)
         self._px = px
         self._id = int(id)
@@ -166,7 +177,7 @@ class GrayImage:
         return self._px
 
     def at(self, x: int, y: int) -> float:
-        return float(self._px[y, x])
+        return float(self._px[y, x]) / self.scale
 
     def as_c(self) -> _abi.Image:
         im = _abi.Image()

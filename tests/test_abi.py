@@ -101,11 +101,16 @@ def test_dimension_mismatch_and_no_cpu_fallback():
                                                   search=dic.SearchConfig(search_radius=3)))
 
 
-def test_grayimage_rejects_non_integer_levels():
-    with pytest.raises(dic.DicError):
-        dic.GrayImage(np.full((8, 8), 1.5))
+def test_grayimage_gray_level_mapping():
+    """Integer levels map losslessly; fractional levels in [0, 255] become 8.8
+    fixed point (as the C++ shim packs them); anything else is rejected."""
     g = dic.GrayImage(np.full((8, 8), 300.0))
-    assert g.pixels().dtype == np.uint16
+    assert g.pixels().dtype == np.uint16 and g.scale == 1 and g.at(0, 0) == 300.0
+    f = dic.GrayImage(np.array([[1.5, 0.0], [254.99609375, 17.25]]))
+    assert f.scale == 256 and f.pixels().tolist() == [[384, 0], [65279, 4416]] and f.at(0, 1) == 254.99609375
+    for bad in (np.full((8, 8), 300.5), np.full((8, 8), -0.5), np.full((8, 8), np.nan), np.full((8, 8), 70000.0)):
+        with pytest.raises(dic.DicError):
+            dic.GrayImage(bad)
 
 
 def test_synth_generator_is_deterministic_and_in_range():

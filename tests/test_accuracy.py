@@ -158,3 +158,24 @@ def test_sweep_tracks_reference_sweep_on_doubles(gpu):
         assert got.unconverged == e.unconverged
         assert got.passed == bool(e.pass_) and got.mean_flagged == bool(e.mean_flagged)
         assert abs(got.max_err - e.max_err) <= 2e-3 and abs(got.mean_err - e.mean_err) <= 2e-3
+
+
+@pytest.mark.gpu
+@needs_ref
+def test_fractional_frames_track_reference_doubles(gpu):
+    """The reference's own (non-integer) synthetic frames go through the 8.8
+    fixed-point image path: same grid, integer decisions and convergence as the
+    reference on its doubles, u/v within the 1e-3 px tolerance."""
+    ref = po.ref_synth_speckle(200, 180, 21, _params(200, 180))
+    tgt, _ = po.ref_synth_warped_pair(ref, dic.WarpSpec(2.35, -1.6, 0.003, 0.0, 0.0, -0.002))
+    oracle = po.Oracle("reference")
+    for im, sm in ((I.bfs, S.icgn), (I.bfs, S.nr), (I.mpso, S.icgn)):
+        cfg = _sweep_cfg(256).base
+        cfg.integer_method, cfg.subpixel_method = im, sm
+        got = dic.analyze_pair(dic.GrayImage(ref), dic.GrayImage(tgt, 1), cfg).records
+        exp = oracle.analyze_pair(ref, tgt, cfg)
+        assert len(got) == len(exp) and np.array_equal(got["x"], exp["x"]) and np.array_equal(got["y"], exp["y"])
+        assert np.array_equal(got["converged"], exp["converged"]), (im, sm)
+        assert np.mean(got["evaluations"] == exp["evaluations"]) > 0.98, (im, sm)
+        ok = exp["converged"] == 1
+        assert np.abs(got["u"] - exp["u"])[ok].max() < 1e-3 and np.abs(got["v"] - exp["v"])[ok].max() < 1e-3, (im, sm)

@@ -17,4 +17,4 @@ def test_cpp_shim_matches_reference_analyze_pair(gpu):
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count(" ok") == 3 and "dimension mismatch" in r.stdout
+    assert r.stdout.count(" ok") == 6 and "dimension mismatch" in r.stdout  # 3 integer + 3 fractional frames
