@@ -53,8 +53,13 @@ typedef enum {
   DICB200_ERR_NO_DEVICE = 5 /* no CUDA device: the product path never falls back to the CPU */
 } dicb200_status;
 
-/* Pixel storage. */
-enum { DICB200_U8 = 0, DICB200_U16 = 1 };
+/* Pixel storage. U8/U16: integer gray levels, used as they are (exact
+ * integer search). F32/F64: gray levels in [0, 255] with fractions (e.g. the
+ * reference's synthetic doubles), carried as 8.8 fixed point round(256 v) in
+ * u16 — ZNCC and the refinement steps are invariant to that scale, so only the
+ * 2^-9 quantisation differs from computing on the doubles. Host entry points
+ * reject levels outside [0, 255]; device entry points saturate them. */
+enum { DICB200_U8 = 0, DICB200_U16 = 1, DICB200_F32 = 2, DICB200_F64 = 3 };
 
 /* Enum values follow the declaration order of the reference enums. */
 enum { DICB200_INT_BFS = 0, DICB200_INT_PSO = 1, DICB200_INT_MPSO = 2 };   /* IntegerMethod, pipeline.hpp:17 */

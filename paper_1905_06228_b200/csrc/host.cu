@@ -146,8 +146,8 @@ static dicb200_status validate_pair(const dicb200_image* a, const dicb200_image*
   if (!a || !b || !cfg || !a->data || !b->data) return invalid("null argument");
   if (a->width != b->width || a->height != b->height) return invalid("dimension mismatch");
   if (a->width < 1 || a->height < 1) return invalid("zero-dimension image");
-  if (a->dtype != b->dtype || (a->dtype != DICB200_U8 && a->dtype != DICB200_U16))
-    return invalid("unsupported pixel type (u8 or u16, identical for both images)");
+  if (a->dtype != b->dtype || a->dtype < DICB200_U8 || a->dtype > DICB200_F64)
+    return invalid("unsupported pixel type (u8, u16, f32 or f64, identical for both images)");
   if (cfg->integer_method < 0 || cfg->integer_method > 2) return invalid("unknown integer method");
   if (cfg->subpixel_method < 0 || cfg->subpixel_method > 2) return invalid("unknown subpixel method");
   if (cfg->subpixel_method != DICB200_SUB_NONE) {
@@ -331,7 +331,53 @@ refine:
   return DICB200_OK;
 }
 
-static size_t elem_size(int dtype) { return dtype == DICB200_U8 ? 1 : 2; }
+static size_t elem_size(int dtype) {
+  return dtype == DICB200_U8 ? 1 : dtype == DICB200_U16 ? 2 : dtype == DICB200_F32 ? 4 : 8;
+}
+static bool is_float(int dtype) { return dtype == DICB200_F32 || dtype == DICB200_F64; }
+
+// Fractional gray levels -> 8.8 fixed point (see DICB200_F32 in dicb200.h).
+template <typename T>
+__global__ void fixed88_kernel(const T* src, int pitch, uint16_t* dst, int w, int h) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (x >= w) return;
+  const double v = (double)src[(size_t)y * pitch + x] * 256.0;
+  dst[(size_t)y * w + x] = (uint16_t)fmin(fmax(round(v), 0.0), 65535.0);  // half away from zero, as lround; NaN -> 0
+}
+
+// Device image `im` (f32/f64) converted into `buf` (w*h u16, stream-ordered).
+static dicb200_status to_fixed88_device(const dicb200_image* im, uint16_t** buf, dicb200_image* out,
+                                        cudaStream_t st) {
+  const int pitch = im->pitch > 0 ? im->pitch : im->width;
+  DICB200_CUDA_TRY(cudaMallocAsync((void**)buf, (size_t)im->width * im->height * 2, st));
+  const dim3 g((im->width + 255) / 256, im->height);
+  if (im->dtype == DICB200_F32)
+    fixed88_kernel<float><<<g, 256, 0, st>>>(static_cast<const float*>(im->data), pitch, *buf, im->width, im->height);
+  else
+    fixed88_kernel<double><<<g, 256, 0, st>>>(static_cast<const double*>(im->data), pitch, *buf, im->width, im->height);
+  count_launch();
+  DICB200_CUDA_TRY(cudaGetLastError());
+  *out = *im;
+  out->dtype = DICB200_U16;
+  out->bits = 16;
+  out->pitch = im->width;
+  out->data = *buf;
+  return DICB200_OK;
+}
+
+// Host image (f32/f64) -> 8.8 fixed point on the host; levels outside [0, 255] are an error.
+static dicb200_status to_fixed88_host(const dicb200_image* im, std::vector<uint16_t>& v) {
+  const int pitch = im->pitch > 0 ? im->pitch : im->width;
+  v.resize((size_t)im->width * im->height);
+  for (int y = 0; y < im->height; ++y)
+    for (int x = 0; x < im->width; ++x) {
+      const double g = im->dtype == DICB200_F32 ? (double)static_cast<const float*>(im->data)[(size_t)y * pitch + x]
+                                                : static_cast<const double*>(im->data)[(size_t)y * pitch + x];
+      if (!(g >= 0.0 && g <= 255.0)) return invalid("fractional gray levels must lie in [0, 255]");
+      v[(size_t)y * im->width + x] = (uint16_t)std::lround(g * 256.0);
+    }
+  return DICB200_OK;
+}
 
 // ---- persistent per-device execution contexts ------------------------------
 // Streams, events and grow-only device buffers are created once and reused by
@@ -480,6 +526,20 @@ static dicb200_status release_context(DeviceContext* c) {
 
 // H2D of a host image (any pitch) into `buf` on `st`; `dev` describes the copy.
 static dicb200_status upload(const dicb200_image* host, DevBuf& buf, dicb200_image* dev, cudaStream_t st) {
+  if (is_float(host->dtype)) {  // converted on the host, then uploaded as u16
+    std::vector<uint16_t> v;
+    dicb200_status s = to_fixed88_host(host, v);
+    if (s != DICB200_OK) return s;
+    DICB200_CUDA_TRY(ensure(buf, v.size() * 2, st));
+    DICB200_CUDA_TRY(cudaMemcpyAsync(buf.p, v.data(), v.size() * 2, cudaMemcpyHostToDevice, st));
+    DICB200_CUDA_TRY(cudaStreamSynchronize(st));  // v is a temporary
+    *dev = *host;
+    dev->dtype = DICB200_U16;
+    dev->bits = 16;
+    dev->pitch = host->width;
+    dev->data = buf.p;
+    return DICB200_OK;
+  }
   const size_t es = elem_size(host->dtype);
   const int pitch = host->pitch > 0 ? host->pitch : host->width;
   const size_t row = (size_t)host->width * es;
@@ -685,6 +745,17 @@ dicb200_status dicb200_analyze_pair_device(const dicb200_image* ref, const dicb2
     set_error("output capacity smaller than the grid rows");
     return DICB200_ERR_CAPACITY;
   }
+  if (is_float(ref->dtype)) {  // fractional levels: 8.8 fixed-point copies for this call
+    const cudaStream_t st = (cudaStream_t)stream;
+    uint16_t *ba = nullptr, *bb = nullptr;
+    dicb200_image ra, rt;
+    s = to_fixed88_device(ref, &ba, &ra, st);
+    if (s == DICB200_OK) s = to_fixed88_device(tgt, &bb, &rt, st);
+    if (s == DICB200_OK) s = enqueue_pair(&ra, &rt, cfg, pair_index, lat, rb, re, out_dev, st);
+    if (ba) cudaFreeAsync(ba, st);
+    if (bb) cudaFreeAsync(bb, st);
+    return s;
+  }
   return enqueue_pair(ref, tgt, cfg, pair_index, lat, rb, re, out_dev, (cudaStream_t)stream);
 }
 
@@ -697,9 +768,11 @@ dicb200_status dicb200_analyze_sequence_device(const dicb200_image* images, size
   if (n_images < 2) return invalid("insufficient images");
   std::vector<int32_t> pairs(2 * (n_images - 1));
   dicb200_sequence_pairs(cfg->reference_policy, (int32_t)n_images, pairs.data());
-  for (size_t i = 1; i < n_images; ++i)
+  for (size_t i = 1; i < n_images; ++i) {
     if (images[i].width != images[0].width || images[i].height != images[0].height)
       return invalid("dimension mismatch");
+    if (images[i].dtype != images[0].dtype) return invalid("unsupported pixel type (identical for every image)");
+  }
   dicb200_status s = validate_pair(&images[0], &images[1], cfg);
   if (s != DICB200_OK) return s;
   Lattice lat;
@@ -716,6 +789,14 @@ dicb200_status dicb200_analyze_sequence_device(const dicb200_image* images, size
   // Reference-side inputs (tensor-core strips/moments, IC-GN constants) live for
   // this call only and are rebuilt whenever the pair's reference frame changes.
   const cudaStream_t st = (cudaStream_t)stream;
+  std::vector<dicb200_image> conv;  // fractional levels: 8.8 fixed-point copies for this call
+  std::vector<uint16_t*> conv_buf;
+  if (is_float(images[0].dtype)) {
+    conv.resize(n_images);
+    conv_buf.assign(n_images, nullptr);
+    for (size_t i = 0; i < n_images && s == DICB200_OK; ++i) s = to_fixed88_device(&images[i], &conv_buf[i], &conv[i], st);
+    if (s == DICB200_OK) images = conv.data();
+  }
   TcRefCache tc;
   IcgnRefCache ic;
   const bool fixed = cfg->reference_policy == DICB200_POLICY_FIXED_FIRST;
@@ -724,6 +805,8 @@ dicb200_status dicb200_analyze_sequence_device(const dicb200_image* images, size
                      out_dev + i * pair_stride, st, &tc, (long)pairs[2 * i], fixed ? &ic : nullptr);
   tc_cache_free(tc, st, true);
   icgn_cache_free(ic, st, true);
+  for (uint16_t* b : conv_buf)
+    if (b) cudaFreeAsync(b, st);
   return s;
 }
 

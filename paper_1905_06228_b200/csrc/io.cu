@@ -130,9 +130,15 @@ dicb200_status dicb200_save_pgm(const char* path, const dicb200_image* img) {
   for (int y = 0; y < img->height; ++y) {
     for (int x = 0; x < img->width; ++x) {
       // save_pgm (image.cpp:98-104): round, clamp to [0, 255]
-      const unsigned v = img->dtype == DICB200_U8 ? static_cast<const uint8_t*>(img->data)[(size_t)y * pitch + x]
-                                                  : static_cast<const uint16_t*>(img->data)[(size_t)y * pitch + x];
-      row[x] = (unsigned char)std::min(v, 255u);
+      const size_t i = (size_t)y * pitch + x;
+      double v;
+      switch (img->dtype) {
+        case DICB200_U8: v = static_cast<const uint8_t*>(img->data)[i]; break;
+        case DICB200_U16: v = static_cast<const uint16_t*>(img->data)[i]; break;
+        case DICB200_F32: v = static_cast<const float*>(img->data)[i]; break;
+        default: v = static_cast<const double*>(img->data)[i]; break;
+      }
+      row[x] = (unsigned char)std::min(std::max(std::round(v), 0.0), 255.0);
     }
     if (std::fwrite(row.data(), 1, row.size(), out.f) != row.size())
       return io_error(std::string("write failed: ") + path);

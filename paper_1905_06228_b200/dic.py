@@ -158,7 +158,7 @@ class GrayImage:
             else:
                 if f.min() < 0 or f.max() > 255:
                     raise DicError("fractional gray levels must lie in [0, 255]")
-                px = np.ascontiguousarray(np.round(f * 256.0).astype(np.uint16))
+                px = np.ascontiguousarray(np.floor(f * 256.0 + 0.5).astype(np.uint16))  # half away from zero, as lround
                 self.scale = 256
         px.setflags(write=False)
         self._px = px

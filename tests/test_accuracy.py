@@ -179,3 +179,61 @@ def test_fractional_frames_track_reference_doubles(gpu):
         assert np.mean(got["evaluations"] == exp["evaluations"]) > 0.98, (im, sm)
         ok = exp["converged"] == 1
         assert np.abs(got["u"] - exp["u"])[ok].max() < 1e-3 and np.abs(got["v"] - exp["v"])[ok].max() < 1e-3, (im, sm)
+
+
+@pytest.mark.gpu
+def test_float_image_dtypes_through_the_c_abi(gpu):
+    """DICB200_F32 / DICB200_F64 images (host and device entry points) are
+    carried as 8.8 fixed point: bit-identical records to the same frames handed
+    over as that u16 data; levels outside [0, 255] are rejected on the host."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1905_06228_b200 import _abi
+
+    ref = dic.synth_speckle(180, 170, 4, _params(180, 170))
+    tgt, _ = dic.synth_warped_pair(ref, dic.WarpSpec(1.7, 2.2, -0.002, 0.0, 0.001, 0.0))
+    cfg = _sweep_cfg(256).base
+    cfg.subpixel_method = S.icgn
+    exp = dic.analyze_pair(dic.GrayImage(ref), dic.GrayImage(tgt, 1), cfg).records
+    L = dic.lib()
+    n = len(exp)
+    for dtype, npt in ((_abi.F64, np.float64), (_abi.F32, np.float32)):
+        a, b = ref.astype(npt), tgt.astype(npt)
+        if npt == np.float32:  # the fixed-point grid is exact in f32 too
+            exp32 = dic.analyze_pair(dic.GrayImage(a.astype(np.float64)), dic.GrayImage(b.astype(np.float64), 1),
+                                     cfg).records
+        else:
+            exp32 = exp
+        ims = []
+        for arr, i in ((a, 0), (b, 1)):
+            im = _abi.Image()
+            im.width, im.height, im.pitch, im.dtype, im.id, im.bits = arr.shape[1], arr.shape[0], arr.shape[1], dtype, i, 0
+            im.data = arr.ctypes.data
+            ims.append(im)
+        out = np.zeros(n, _abi.record_dtype())
+        cnt = C.c_size_t(0)
+        assert L.dicb200_analyze_pair(C.byref(ims[0]), C.byref(ims[1]), C.byref(cfg.to_c()), 0, out.ctypes.data, n,
+                                      C.byref(cnt)) == 0
+        for k in exp.dtype.names:
+            assert np.array_equal(out[k], exp32[k], equal_nan=True), (dtype, k)
+        # device entry point
+        ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        ims[0].data, ims[1].data = ta.data_ptr(), tb.data_ptr()
+        dout = torch.empty(n * C.sizeof(_abi.PoiRecordC), dtype=torch.uint8, device="cuda")
+        assert L.dicb200_analyze_pair_device(C.byref(ims[0]), C.byref(ims[1]), C.byref(cfg.to_c()), 0, -1, -1,
+                                             C.c_void_p(dout.data_ptr()), n, C.byref(cnt), None) == 0
+        torch.cuda.synchronize()
+        drec = np.frombuffer(dout.cpu().numpy().tobytes(), dtype=_abi.record_dtype())
+        for k in exp.dtype.names:
+            assert np.array_equal(drec[k], exp32[k], equal_nan=True), (dtype, "device", k)
+    bad = ref.copy()
+    bad[3, 3] = 300.0
+    im = _abi.Image()
+    im.width, im.height, im.pitch, im.dtype, im.id, im.bits = 180, 170, 180, _abi.F64, 0, 0
+    im.data = bad.ctypes.data
+    out = np.zeros(n, _abi.record_dtype())
+    cnt = C.c_size_t(0)
+    assert L.dicb200_analyze_pair(C.byref(im), C.byref(ims[1]), C.byref(cfg.to_c()), 0, out.ctypes.data, n,
+                                  C.byref(cnt)) == 1
