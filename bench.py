@@ -459,6 +459,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": None,
                 "peak_source": "measured live by tools/microbench/pipes",
                 "work_per_launch": f"sum(iterations) x n x {flop_px_it:.0f} flop"}
+        # gathered-tap bytes against the staged tiles' shared-memory bandwidth
+        tap_b = 4 * 4 + (8 if dom == "icgn" else 8 * 4)  # 4 fp32 target taps (+ gradient / difference taps)
+        taps = iters / max(1, len(my_pairs)) * n_px * tap_b
+        tap_ach = taps / (stage[dom]["avg_ms"] * 1e-3) / 1e9
+        smem_peak = 128.0 * (torch.cuda.get_device_properties(dev).multi_processor_count) * 1.965e9 / 1e9
+        roof["taps"] = {"achieved": tap_ach, "peak": smem_peak, "unit": "GB/s", "frac": tap_ach / smem_peak,
+                        "work_per_launch": f"sum(iterations) x n x {tap_b} B gathered from shared memory",
+                        "peak_source": "128 B/clk/SM (32 banks x 4 B) x SMs x 1965 MHz max SM clock"}
     elif dom == "pso":
         macs_per_launch = evals / max(1, len(my_pairs)) * n_px
         achieved = macs_per_launch / (stage[dom]["avg_ms"] * 1e-3) / 1e12
