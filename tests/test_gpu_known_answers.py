@@ -1,0 +1,81 @@
+"""The reference's own known-answer unit tests for the integer search
+(test_integer_search.cpp:57-121), replayed through the device path on every
+integer-search kernel: the CUDA-core tile kernel (small grids, or forced), the
+tensor-core kernel and the block-sum kernel."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_1905_06228_b200 import configs, dic, _abi
+from paper_1905_06228_b200.dic import BfsDomain, GridParams, IntegerMethod, RunConfig, SearchConfig, SubpixelMethod
+
+pytestmark = pytest.mark.gpu
+PATHS = {"legacy": {"DICB200_BFS_LEGACY": "1"}, "tensor": {"DICB200_BFS_TC": "1"}, "default": {}}
+
+
+def _run(a, b, cfg, path):
+    keys = ("DICB200_BFS_LEGACY", "DICB200_BFS_TC", "DICB200_BFS_BS")
+    for k in keys:
+        os.environ.pop(k, None)
+    os.environ.update(PATHS[path])
+    try:
+        return dic.analyze_pair(dic.GrayImage(a), dic.GrayImage(b, 1), cfg).records
+    finally:
+        for k in keys:
+            os.environ.pop(k, None)
+
+
+def _cfg(M, R, step):
+    return RunConfig(integer_method=IntegerMethod.bfs, subpixel_method=SubpixelMethod.none,
+                     search=SearchConfig(search_radius=R, bfs_domain=BfsDomain.window),
+                     grid=GridParams(half_width=M, spacing=step))
+
+
+def _speckle(w, h, seed, dtype=_abi.U8, maxv=255):
+    if dtype == _abi.U8:
+        return configs.FrameSpec(w, h, _abi.U8, 255, seed, w * h // 60, (2.0, 4.0), (60.0, 200.0)).render()
+    return configs.FrameSpec(w, h, _abi.U16, maxv, seed, w * h // 42, (1.5, 3.5), (0.23 * maxv, 0.78 * maxv)).render()
+
+
+@pytest.mark.parametrize("path", sorted(PATHS))
+@pytest.mark.parametrize("dtype", [_abi.U8, _abi.U16], ids=["u8", "u16"])
+def test_exact_integer_shift_everywhere(gpu, path, dtype):
+    """test_integer_search.cpp:57-69: a pure integer shift is found at every
+    POI, with the full window counted (no degenerate windows in speckle)."""
+    ref = _speckle(420, 400, 17, dtype, 4095)
+    tgt = np.roll(np.roll(ref, -2, axis=0), 3, axis=1)  # content moves by (+3, -2)
+    cfg = _cfg(20, 12, 10)
+    r = _run(ref, tgt, cfg, path)
+    assert len(r) >= 1024  # large enough for the tensor-core / block-sum kernels
+    inner = (r["x"] < 420 - 20 - 3) & (r["y"] >= 20 + 2)  # subsets not wrapped by np.roll
+    assert inner.mean() > 0.9
+    assert np.all(r["integer_dx"][inner] == 3) and np.all(r["integer_dy"][inner] == -2)
+    assert np.all(np.abs(r["zncc"][inner] - 1.0) < 1e-12)
+    assert np.all(r["evaluations"][inner] == 25 * 25)
+
+
+@pytest.mark.parametrize("path", sorted(PATHS))
+@pytest.mark.parametrize("dtype", [_abi.U8, _abi.U16], ids=["u8", "u16"])
+def test_ties_break_toward_smallest_dy_dx(gpu, path, dtype):
+    """test_integer_search.cpp:104-121: on a period-8 checkerboard every
+    displacement that is a multiple of 8 on both axes (or 4 mod 8 on both)
+    correlates perfectly; with R = 8 the winner is the smallest (dy, dx) =
+    (-8, -8) at every POI (R = 12 would make it (-12, -12))."""
+    y, x = np.mgrid[0:400, 0:420]
+    cb = np.where(((x % 8) < 4) ^ ((y % 8) < 4), 200, 50)
+    cb = cb.astype(np.uint8) if dtype == _abi.U8 else (cb * 16).astype(np.uint16)
+    r = _run(cb, cb, _cfg(20, 8, 10), path)
+    assert len(r) >= 1024
+    assert np.all(r["integer_dx"] == -8) and np.all(r["integer_dy"] == -8)
+    assert np.all(np.abs(r["zncc"] - 1.0) < 1e-12)
+
+
+def test_small_grid_tie_break_reference_case(gpu):
+    """The reference's own 32x32 checkerboard case (M = 7, R = 8, POI (16, 16))."""
+    y, x = np.mgrid[0:32, 0:32]
+    cb = np.where(((x % 8) < 4) ^ ((y % 8) < 4), 200, 50).astype(np.uint8)
+    r = _run(cb, cb, _cfg(7, 8, 1), "default")
+    k = np.nonzero((r["x"] == 16) & (r["y"] == 16))[0]
+    assert len(k) == 1
+    assert (r["integer_dx"][k[0]], r["integer_dy"][k[0]]) == (-8, -8)
