@@ -327,6 +327,19 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     stage_ms = (C.c_double * N_STAGES)()
     stage_n = (C.c_uint64 * N_STAGES)()
     L.dicb200_profile_read(stage_ms, stage_n)
+    # The sequence path runs two pairs concurrently (internal streams), so the
+    # live per-launch times above include time-sharing. One extra, untimed step
+    # with the pairs serialised gives each kernel's isolated launch time too.
+    iso_ms, iso_n = (C.c_double * N_STAGES)(), (C.c_uint64 * N_STAGES)()
+    if len(my_pairs) > 1:
+        os.environ["DICB200_SEQ_STREAMS"] = "1"
+        L.dicb200_profile_enable(1)
+        with torch.cuda.stream(stream):
+            step()
+        stream.synchronize()
+        L.dicb200_profile_enable(0)
+        os.environ.pop("DICB200_SEQ_STREAMS", None)
+        L.dicb200_profile_read(iso_ms, iso_n)
     # flush time is not analysis work: subtract it (measured on the same stream)
     ms = ms_total - sum(a.elapsed_time(b) for a, b in flush_ev)
     ms_tensor = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -501,6 +514,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                "TMAC/s of IMAD; the block partials are shared by the (L/s)^2 overlapping subsets"}
         if roof is None:
             roof = roof_search
+    iso = {names[i]: float(iso_ms[i]) / int(iso_n[i]) for i in range(N_STAGES) if iso_n[i]}
+    stage_of = {"bfs_tc_kernel": "tc_cross_terms", "bs_kernel": "bs_cross_terms", "refine_kernel": dom}
+    for rf in (roof, roof_search):
+        if rf and iso.get(stage_of.get(rf["kernel"])) and stage.get(stage_of.get(rf["kernel"])):
+            live = stage[stage_of[rf["kernel"]]]["avg_ms"]
+            rf["launch_ms_live"] = live
+            rf["launch_ms_isolated"] = iso[stage_of[rf["kernel"]]]
+            rf["frac_isolated"] = rf["frac"] * live / rf["launch_ms_isolated"] if rf.get("frac") else None
     prof_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if roof and os.path.exists(prof_path):
         try:
@@ -535,6 +556,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "roofline": roof,
         "roofline_search": roof_search,
         "step_ms": step_ms,
+        "stages_isolated": {k: {"avg_ms": v} for k, v in iso.items()},
         "clocks": clk,
         "parity_in_run": {"records": int(n_all), "status_ok": int(ok_all), "mean_iterations": iters_all / max(1, n_all)},
         "pipe_peaks": {k: v for k, v in peaks.items() if k.endswith("per_s")},

@@ -425,6 +425,7 @@ struct RecSlot {
 };
 
 constexpr int kFrameSlots = 4;
+constexpr int kSeqStreams = 2;  // concurrent pairs of analyze_sequence_device
 constexpr int kRecSlots = 2;
 
 struct DeviceContext {
@@ -797,14 +798,48 @@ dicb200_status dicb200_analyze_sequence_device(const dicb200_image* images, size
     for (size_t i = 0; i < n_images && s == DICB200_OK; ++i) s = to_fixed88_device(&images[i], &conv_buf[i], &conv[i], st);
     if (s == DICB200_OK) images = conv.data();
   }
-  TcRefCache tc;
-  IcgnRefCache ic;
+  // Pairs alternate over kSeqStreams internal streams forked from (and joined
+  // back into) the caller's stream, so one pair's kernels fill the tail waves
+  // of the other's. Each stream owns its reference-side caches: nothing is
+  // shared between concurrently running pairs.
   const bool fixed = cfg->reference_policy == DICB200_POLICY_FIXED_FIRST;
-  for (size_t i = 0; i + 1 < n_images && s == DICB200_OK; ++i)
+  const char* env = std::getenv("DICB200_SEQ_STREAMS");
+  const int ns = std::max(1, std::min<int>(env ? std::atoi(env) : kSeqStreams, (int)(n_images - 1)));
+  std::vector<cudaStream_t> ss(ns, st);
+  std::vector<TcRefCache> tc(ns);
+  std::vector<IcgnRefCache> ic(ns);
+  cudaEvent_t fork = nullptr;
+  if (s == DICB200_OK && ns > 1) {
+    cudaError_t e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(fork, st);
+    for (int k = 0; k < ns && e == cudaSuccess; ++k) {
+      e = cudaStreamCreateWithFlags(&ss[k], cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(ss[k], fork, 0);
+    }
+    if (e != cudaSuccess) s = cuda_fail(e, "sequence stream fork", __FILE__, __LINE__);
+  }
+  for (size_t i = 0; i + 1 < n_images && s == DICB200_OK; ++i) {
+    const int k = (int)(i % ns);
     s = enqueue_pair(&images[pairs[2 * i]], &images[pairs[2 * i + 1]], cfg, first_pair_index + i, lat, rb, re,
-                     out_dev + i * pair_stride, st, &tc, (long)pairs[2 * i], fixed ? &ic : nullptr);
-  tc_cache_free(tc, st, true);
-  icgn_cache_free(ic, st, true);
+                     out_dev + i * pair_stride, ss[k], &tc[k], (long)pairs[2 * i], fixed ? &ic[k] : nullptr);
+  }
+  for (int k = 0; k < ns; ++k) {
+    tc_cache_free(tc[k], ss[k], true);
+    icgn_cache_free(ic[k], ss[k], true);
+  }
+  if (ns > 1) {  // join: the caller's stream waits for every internal stream
+    for (int k = 0; k < ns; ++k) {
+      if (ss[k] == st) continue;
+      cudaEvent_t j = nullptr;
+      if (cudaEventCreateWithFlags(&j, cudaEventDisableTiming) == cudaSuccess) {
+        cudaEventRecord(j, ss[k]);
+        cudaStreamWaitEvent(st, j, 0);
+        cudaEventDestroy(j);
+      }
+      cudaStreamDestroy(ss[k]);
+    }
+    if (fork) cudaEventDestroy(fork);
+  }
   for (uint16_t* b : conv_buf)
     if (b) cudaFreeAsync(b, st);
   return s;
