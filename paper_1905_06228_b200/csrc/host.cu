@@ -409,6 +409,7 @@ struct FrameSlot {
   long key = -1, last_use = -1;
   cudaEvent_t ready = nullptr;  // upload finished (copy stream)
   cudaEvent_t idle = nullptr;   // last pair reading the frame finished (compute stream)
+  cudaEvent_t idle2 = nullptr;  // the same on the second compute stream
   dicb200_image im{};
 };
 
@@ -426,17 +427,20 @@ struct RecSlot {
 
 constexpr int kFrameSlots = 4;
 constexpr int kSeqStreams = 2;  // concurrent pairs of analyze_sequence_device
-constexpr int kRecSlots = 2;
+constexpr int kRecSlots = 4;
 
 struct DeviceContext {
   int dev = 0;
   cudaStream_t cs = nullptr;  // compute: kernels + record read-back
+  cudaStream_t cs2 = nullptr;  // second compute stream: analyze_sequence keeps two pairs in flight
   cudaStream_t xs = nullptr;  // copy: frame uploads ahead of the compute stream
   cudaStream_t ds = nullptr;  // copy: record read-back behind the compute stream
   FrameSlot frames[kFrameSlots];
   RecSlot recs[kRecSlots];
   TcRefCache tcache;  // reference-side tensor-core inputs, reused while the reference frame repeats
   IcgnRefCache icache;  // reference-side IC-GN constants (Hessian inverse, sums), likewise
+  TcRefCache tcache2;   // the second compute stream's own caches (no sharing between
+  IcgnRefCache icache2;  // concurrently running pairs)
 };
 
 namespace {
@@ -447,12 +451,14 @@ std::vector<DeviceContext*> g_ctx_idle;
 static void destroy_context(DeviceContext* c) {
   cudaSetDevice(c->dev);
   if (c->cs) cudaStreamSynchronize(c->cs);
+  if (c->cs2) cudaStreamSynchronize(c->cs2);
   if (c->xs) cudaStreamSynchronize(c->xs);
   if (c->ds) cudaStreamSynchronize(c->ds);
   for (auto& f : c->frames) {
     if (f.buf.p) cudaFree(f.buf.p);
     if (f.ready) cudaEventDestroy(f.ready);
     if (f.idle) cudaEventDestroy(f.idle);
+    if (f.idle2) cudaEventDestroy(f.idle2);
   }
   for (auto& r : c->recs) {
     if (r.dev.p) cudaFree(r.dev.p);
@@ -462,7 +468,10 @@ static void destroy_context(DeviceContext* c) {
   }
   tc_cache_free(c->tcache);
   icgn_cache_free(c->icache);
+  tc_cache_free(c->tcache2);
+  icgn_cache_free(c->icache2);
   if (c->cs) cudaStreamDestroy(c->cs);
+  if (c->cs2) cudaStreamDestroy(c->cs2);
   if (c->xs) cudaStreamDestroy(c->xs);
   if (c->ds) cudaStreamDestroy(c->ds);
   delete c;
@@ -489,11 +498,13 @@ static DeviceContext* acquire_context(dicb200_status* st) {
   auto* c = new DeviceContext;
   c->dev = dev;
   e = cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->cs2, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->xs, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->ds, cudaStreamNonBlocking);
   for (auto& f : c->frames) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f.ready, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f.idle, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f.idle2, cudaEventDisableTiming);
   }
   for (auto& r : c->recs) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming);
@@ -512,11 +523,14 @@ static DeviceContext* acquire_context(dicb200_status* st) {
 static dicb200_status release_context(DeviceContext* c) {
   cudaError_t e1 = cudaStreamSynchronize(c->xs);
   cudaError_t e2 = cudaStreamSynchronize(c->cs);
+  if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(c->cs2);
   cudaError_t e3 = cudaStreamSynchronize(c->ds);
   if (e2 == cudaSuccess) e2 = e3;
   for (auto& f : c->frames) f.key = f.last_use = -1;  // LRU state is per call
   c->tcache.reset();
   c->icache.reset();
+  c->tcache2.reset();
+  c->icache2.reset();
   for (auto& r : c->recs) r.pair = -1;
   std::lock_guard<std::mutex> lk(g_ctx_mu);
   g_ctx_idle.push_back(c);
@@ -569,6 +583,7 @@ static dicb200_status stage_frame(DeviceContext* c, const dicb200_image* host, l
   FrameSlot& f = c->frames[v];
   f.key = -1;
   DICB200_CUDA_TRY(cudaStreamWaitEvent(c->xs, f.idle, 0));
+  DICB200_CUDA_TRY(cudaStreamWaitEvent(c->xs, f.idle2, 0));
   dicb200_status s = upload(host, f.buf, &f.im, c->xs);
   if (s != DICB200_OK) return s;
   DICB200_CUDA_TRY(cudaEventRecord(f.ready, c->xs));
@@ -929,28 +944,33 @@ dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_im
       while (i < hi && pre[i - lo] != DICB200_OK) ++i;
       return i;
     };
-    for (size_t i = next_valid(lo); i < hi; i = next_valid(i + 1)) {
+    // valid pairs alternate over the two compute streams (two pairs in flight)
+    size_t q = 0;
+    for (size_t i = next_valid(lo); i < hi; i = next_valid(i + 1), ++q) {
       dicb200_field& f = fields[i];
       const size_t n = cnt[i - lo];
       const size_t bytes = n * sizeof(dicb200_poi_record);
-      RecSlot& r = c->recs[i % kRecSlots];
+      const int k = (int)(q & 1);
+      const cudaStream_t cst = k ? c->cs2 : c->cs;
+      RecSlot& r = c->recs[q % kRecSlots];
       finalize(r);
       int sa = 0, sb = 0;
       dicb200_status s = stage_pair(i, &sa, &sb);
       cudaError_t e = cudaSuccess;
       if (s == DICB200_OK) {
-        e = ensure(r.dev, bytes, c->cs);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(c->cs, c->frames[sa].ready, 0);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(c->cs, c->frames[sb].ready, 0);
+        e = ensure(r.dev, bytes, cst);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(cst, c->frames[sa].ready, 0);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(cst, c->frames[sb].ready, 0);
         if (e != cudaSuccess) s = cuda_fail(e, "compute stream setup", __FILE__, __LINE__);
       }
       if (s == DICB200_OK)
         s = enqueue_pair(&c->frames[sa].im, &c->frames[sb].im, cfg, i, lat[i - lo], 0, lat[i - lo].ny,
-                         (dicb200_poi_record*)r.dev.p, c->cs, &c->tcache, (long)pairs[2 * i],
-                         cfg->reference_policy == DICB200_POLICY_FIXED_FIRST ? &c->icache : nullptr);
+                         (dicb200_poi_record*)r.dev.p, cst, k ? &c->tcache2 : &c->tcache, (long)pairs[2 * i],
+                         cfg->reference_policy == DICB200_POLICY_FIXED_FIRST ? (k ? &c->icache2 : &c->icache)
+                                                                             : nullptr);
       if (s == DICB200_OK) {
-        e = cudaEventRecord(c->frames[sa].idle, c->cs);
-        if (e == cudaSuccess) e = cudaEventRecord(c->frames[sb].idle, c->cs);
+        e = cudaEventRecord(k ? c->frames[sa].idle2 : c->frames[sa].idle, cst);
+        if (e == cudaSuccess) e = cudaEventRecord(k ? c->frames[sb].idle2 : c->frames[sb].idle, cst);
         r.staged = !is_pinned(f.records);
         void* dst = f.records;
         if (e == cudaSuccess && r.staged) {
@@ -965,7 +985,7 @@ dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_im
         }
         // read-back on its own stream so the next pair's kernels start at once;
         // r.dev is rewritten only after finalize(r) has seen r.done
-        if (e == cudaSuccess) e = cudaEventRecord(r.computed, c->cs);
+        if (e == cudaSuccess) e = cudaEventRecord(r.computed, cst);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(c->ds, r.computed, 0);
         if (e == cudaSuccess) e = cudaMemcpyAsync(dst, r.dev.p, bytes, cudaMemcpyDeviceToHost, c->ds);
         if (e == cudaSuccess) e = cudaEventRecord(r.done, c->ds);
@@ -977,13 +997,14 @@ dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_im
       }
       r.pair = (long)i;
       r.n = n;
-      // prefetch the next pair's frames, then retire the previous pair
+      // prefetch the next pair's frames, then retire the pair two back (the one
+      // before is still running beside this one)
       const size_t j = next_valid(i + 1);
       if (j < hi) {
         int ja = 0, jb = 0;
         stage_pair(j, &ja, &jb);  // an upload error resurfaces when pair j stages again
       }
-      finalize(c->recs[(i + kRecSlots - 1) % kRecSlots]);
+      finalize(c->recs[(q + kRecSlots - 2) % kRecSlots]);
     }
     for (auto& r : c->recs) finalize(r);
     const dicb200_status rs = release_context(c);
