@@ -121,8 +121,8 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) { retur
 
 struct Win {
   int lo_dx, hi_dx, lo_dy, hi_dy, R, W;
-  const double* surf;  // [W][W], entry (dy+R)*W + (dx+R)
-  __device__ __forceinline__ double val(int dx, int dy) const { return __ldg(surf + (dy + R) * W + (dx + R)); }
+  const double* surf;  // [W][W], entry (dy+R)*W + (dx+R): the warp's shared-memory copy
+  __device__ __forceinline__ double val(int dx, int dy) const { return surf[(dy + R) * W + (dx + R)]; }
   __device__ __forceinline__ int pos(int dx, int dy) const { return (dy + R) * W + (dx + R); }
 };
 
@@ -204,11 +204,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) pso_walk_kernel(PsoParams p
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k = blockIdx.x * kWarpsPerCta + warp;
   if (k >= p.n_records) return;
-  // per-warp smem: mt[312] u64 | draws[4*P] double | visited[W*W/32] u32 | ctl
+  // per-warp smem: mt[312] u64 | draws[4*P] double | visited[W*W/32] u32 | ctl | surface[W*W] double
   const int P = p.P;
   const int Wd = 2 * p.R + 1;
   const int nvis = (Wd * Wd + 31) / 32;
-  const size_t per_warp = ((312 * 8 + 4 * (size_t)(P > 0 ? P : 1) * 8 + (size_t)nvis * 4 + sizeof(Ctl)) + 15) & ~size_t(15);
+  const size_t head = ((312 * 8 + 4 * (size_t)(P > 0 ? P : 1) * 8 + (size_t)nvis * 4 + sizeof(Ctl)) + 15) & ~size_t(15);
+  const size_t per_warp = head + (p.stage_surface ? (size_t)Wd * Wd * 8 : 0);
   unsigned char* base = smem_raw + per_warp * warp;
   uint64_t* mt = reinterpret_cast<uint64_t*>(base);
   double* draws = reinterpret_cast<double*>(base + 312 * 8);
@@ -236,6 +237,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) pso_walk_kernel(PsoParams p
     return;
   }
   w.surf = p.surface + (size_t)k * Wd * Wd;
+  if (p.stage_surface) {  // the POI's ZNCC surface, staged once: every swarm probe then reads shared memory
+    double* ss = reinterpret_cast<double*>(base + head);
+    for (int i = lane; i < Wd * Wd; i += 32) ss[i] = __ldg(w.surf + i);
+    w.surf = ss;
+  }
   for (int i = lane; i < nvis; i += 32) visited[i] = 0u;
   if (lane == 0) {
     // std::mt19937_64 seeding (StreamRng(derive_stream_seed(...)), pipeline.cpp:84)
@@ -440,12 +446,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) pso_walk_kernel(PsoParams p
 size_t pso_walk_smem(const PsoParams& p) {
   const int P = p.P > 0 ? p.P : 1;
   const int Wd = 2 * p.R + 1;
-  const size_t per_warp = ((312 * 8 + 4 * (size_t)P * 8 + (size_t)((Wd * Wd + 31) / 32) * 4 + sizeof(Ctl)) + 15) & ~size_t(15);
-  return per_warp * kWarpsPerCta;
+  const size_t head = ((312 * 8 + 4 * (size_t)P * 8 + (size_t)((Wd * Wd + 31) / 32) * 4 + sizeof(Ctl)) + 15) & ~size_t(15);
+  return (head + (p.stage_surface ? (size_t)Wd * Wd * 8 : 0)) * kWarpsPerCta;
 }
 
 dicb200_status pso_walk_launch(PsoParams& p, cudaStream_t st) {
   if (p.n_records <= 0) return DICB200_OK;
+  p.stage_surface = 1;  // the surfaces in shared memory when they fit, else read through L1/L2
+  if (pso_walk_smem(p) > 200 * 1024) p.stage_surface = 0;
   const size_t smem = pso_walk_smem(p);
   if (smem > 200 * 1024) {
     set_error("particle_count / search window too large for the swarm walk kernel");

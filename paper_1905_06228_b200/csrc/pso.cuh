@@ -18,6 +18,7 @@ struct PsoParams {
   dicb200_poi_record* rec;
   int n_records;
   const double* surface;  // [n_records][2R+1][2R+1] ZNCC surface from the BFS kernel (NaN = no result)
+  int stage_surface;      // set by pso_walk_launch: copy each surface to shared memory first
 };
 
 size_t pso_walk_smem(const PsoParams& p);
