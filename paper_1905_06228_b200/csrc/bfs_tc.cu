@@ -906,7 +906,6 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p, int sp) {
         ++ahead_y;
       }
     }
-    int slot = 0;
     for (int idx = lane; idx < total; idx += 32) {
       {
         const int dx = fx_lo + rx, dy = fy_lo + ry;
@@ -920,7 +919,6 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p, int sp) {
           ahead_x -= fw;
           ++ahead_y;
         }
-        (void)slot;
         Cand c;
         if (tc_candidate_s(pv, n, sf, sfg_v, cx - M + dx, cy - M + dy, c)) {
           ++cnt;
