@@ -373,6 +373,58 @@ __device__ __forceinline__ f2x mul2(f2x a, f2x b) {
   return d;
 }
 
+// First IC-GN pass: the warp is the integer displacement with zero gradients,
+// so every sample sits exactly on a target node and the bilinear value is the
+// node itself (fma(a, 0, f00) == f00): one load per pixel, bit-identical sums
+// to icgn_pass_fast2 at these parameters.
+__device__ __forceinline__ void icgn_pass_node(const PassCtx& c, const Walk& w0, float* acc, float& gmin,
+                                               float& gmax) {
+  float s0 = 0.f, s1 = 0.f;
+  f2x a36 = pk2(0.f, 0.f), a47 = a36, a58 = a36;
+  gmin = 3.0e38f;
+  gmax = -3.0e38f;
+  const f2x step = pk2(w0.r32f, w0.q32f), wrap = pk2(-w0.sidef, 1.0f);
+  f2x dxy = pk2(w0.dxf, w0.dyf);
+  int roff = w0.roff;
+  const int side = (int)w0.sidef, q = (int)w0.q32f, r = (int)w0.r32f;
+  const int tstep = q * c.tP + r, twrap = c.tP - side;
+  const float* Tb = c.T + c.ioffy * c.tP + c.ioffx;
+  int toff = (int)w0.dyf * c.tP + (int)w0.dxf;
+  const int cnt = w0.npl - (w0.last_valid ? 0 : 1);
+#pragma unroll 2
+  for (int i = 0; i < cnt; ++i) {
+    float dx, dy;
+    up2(dxy, dx, dy);
+    const float gv = Tb[toff];
+    gmin = fminf(gmin, gv);
+    gmax = fmaxf(gmax, gv);
+    const float2 gg = c.Gs[roff];
+    const float gp = gv - c.fbar;
+    s0 += gp;
+    s1 = fmaf(gp, gp, s1);
+    const f2x txy = mul2(pk2(gg.x, gg.y), pk2(gp, gp));
+    a36 = add2(a36, txy);
+    a47 = fma2(txy, pk2(dx, dx), a47);
+    a58 = fma2(txy, pk2(dy, dy), a58);
+    dxy = add2(dxy, step);
+    roff += w0.roff_step;
+    toff += tstep;
+    float ndx, ndy;
+    up2(dxy, ndx, ndy);
+    if (ndx > w0.Mf) {
+      dxy = add2(dxy, wrap);
+      roff += w0.roff_wrap;
+      toff += twrap;
+    }
+  }
+  acc[0] = s0;
+  acc[1] = s1;
+  acc[2] = 0.f;
+  up2(a36, acc[3], acc[6]);
+  up2(a47, acc[4], acc[7]);
+  up2(a58, acc[5], acc[8]);
+}
+
 // Fast IC-GN pass with packed x/y arithmetic: same sums as pixel_pass<true, kIcgn>.
 __device__ __forceinline__ void icgn_pass_fast2(const PassCtx& c, const Walk& w0, float* acc, float& gmin,
                                                 float& gmax) {
@@ -846,7 +898,9 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
       else
         pixel_pass<false, kFinal, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
     } else if (METHOD == 1) {
-      if (fast)
+      if (fast && iter == 1)  // integer start: samples on the nodes
+        icgn_pass_node(pc, wk, acc, gmin, gmax);
+      else if (fast)
         icgn_pass_fast2(pc, wk, acc, gmin, gmax);
       else
         pixel_pass<false, kIcgn, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
