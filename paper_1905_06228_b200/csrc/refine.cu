@@ -482,7 +482,10 @@ __device__ __forceinline__ void icgn_pass_fast2(const PassCtx& c, const Walk& w0
   up2(a58, acc[5], acc[8]);
 }
 
-template <bool FAST, int KIND, typename Pix>
+// NODE: the integer start (u, v integral, zero gradients) — every sample and
+// its bilinear gradient sit on a node: value t[0], gradient half the central
+// differences, exactly what the weighted forms give with weights (1, 0, 0, 0).
+template <bool FAST, int KIND, typename Pix, bool NODE = false>
 __device__ __forceinline__ void pixel_pass(const PassCtx& c, const ImageView& tgt, const Walk& w0,
                                            float* acc, int& bad, float& gmin, float& gmax) {
   constexpr int NV = KIND == kNr ? 39 : 9;
@@ -500,7 +503,14 @@ __device__ __forceinline__ void pixel_pass(const PassCtx& c, const ImageView& tg
     const float xl = fmaf(c.uy, dy, fmaf(c.ux, dx, dx + c.ul));
     const float yl = fmaf(c.vy, dy, fmaf(c.vx, dx, dy + c.vl));
     float gv, gx = 0.f, gy = 0.f;
-    if (FAST) {
+    if (FAST && NODE) {
+      const float* t = Tb + (int)dy * c.tP + (int)dx;
+      gv = t[0];
+      if (KIND == kNr) {
+        gx = 0.5f * (t[1] - t[-1]);
+        gy = 0.5f * (t[c.tP] - t[-c.tP]);
+      }
+    } else if (FAST) {
       const float flx = floorf(xl), fly = floorf(yl);  // subset-local: exact frac
       const float fx = xl - flx, fy = yl - fly;
       const float* t = Tb + (int)fly * c.tP + (int)flx;
@@ -905,7 +915,9 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
       else
         pixel_pass<false, kIcgn, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
     } else {
-      if (fast)
+      if (fast && iter == 1)  // integer start: samples on the nodes
+        pixel_pass<true, kNr, Pix, true>(pc, p.tgt, wk, acc, bad, gmin, gmax);
+      else if (fast)
         pixel_pass<true, kNr, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
       else
         pixel_pass<false, kNr, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
