@@ -101,7 +101,7 @@ def describe(w, subsets_per_pair: int, n_pairs: int, world: int) -> dict:
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
@@ -116,7 +116,16 @@ class Clocks:
         except OSError:
             self.proc = None
 
-    def stop(self) -> dict:
+    @staticmethod
+    def _ts(line: str) -> float:
+        try:
+            return time.mktime(time.strptime(line.split(",")[0].strip().split(".")[0], "%Y/%m/%d %H:%M:%S"))
+        except ValueError:
+            return 0.0
+
+    def stop(self, t_from: float = 0.0) -> dict:
+        """Samples taken from host time t_from on (the timed region); the sampler
+        itself starts before the warm-up so the GPU never idles before timing."""
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.25)
@@ -124,16 +133,22 @@ class Clocks:
         out, _ = self.proc.communicate()
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
+        lines = out.strip().splitlines()
+        if t_from and not any(self._ts(ln) + 1.0 >= t_from for ln in lines):
+            t_from = 0.0  # a very short timed region between two samples: keep them all
+        for line in lines:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 6:
+            if len(parts) < 7:
                 continue
             try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
+                ts = time.mktime(time.strptime(parts[0].split(".")[0], "%Y/%m/%d %H:%M:%S"))
+                if ts + 1.0 < t_from:  # one-second timestamp resolution
+                    continue
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[2:6]):
+            for nm, v in zip(names, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
@@ -280,6 +295,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # the live pipe-rate microbenchmark runs in its own process before the warm-up,
     # so nothing it leaves behind (context switch, clocks) lands in the timed steps
     peaks = pipe_peaks() if rank == 0 else {}
+    # clock sampler from here on (no idle gap between the warm-up and the timed
+    # steps: an idle GPU drops its clocks and the first timed step pays for it)
+    clocks = Clocks(local_rank)
+    clocks.start()
     # warm-up (the last step with stage timing on, so the timing events are
     # created here and only recycled inside the timed region)
     with torch.cuda.stream(stream):
@@ -292,13 +311,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     L.dicb200_profile_enable(0)
 
     # timed region: K steps, CUDA events on the launch stream, stage events live
-    clocks = Clocks(local_rank)
     L.dicb200_profile_read((C.c_double * N_STAGES)(), (C.c_uint64 * N_STAGES)())  # clear
     barrier()
     torch.cuda.synchronize()
     L.dicb200_reset_launch_count()
-    clocks.start()
-    time.sleep(0.3)
+    t_timed = time.time()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     flush_ev = []
     L.dicb200_profile_enable(1)
@@ -319,7 +336,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     ev1.synchronize()
     L.dicb200_profile_enable(0)
     launches = int(L.dicb200_launch_count())
-    clk = clocks.stop()
+    clk = clocks.stop(t_timed)
     torch.cuda.synchronize()
     barrier()
     ms_total = ev0.elapsed_time(ev1)
