@@ -174,3 +174,24 @@ def test_block_sum_row_shards_and_degenerate(gpu):
     assert (exp["status"] != 0).any()
     for f in FIELDS:
         assert np.array_equal(got[f], exp[f], equal_nan=True), f
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_block_sum_randomized_against_cuda_core(gpu, seed):
+    """Randomised lattices matching the block-sum instantiations (spacing,
+    remainder, q) with random radii, sizes, bit depths, displacements and
+    flat patches: block-sum records == CUDA-core records, bit for bit."""
+    rng = np.random.default_rng(1000 + seed)
+    M, step = [(20, 10), (20, 5), (15, 10), (15, 8)][seed % 4]
+    R = int(rng.integers(3, 16))
+    w, h = int(rng.integers(420, 500)), int(rng.integers(420, 500))
+    maxv = int(rng.choice([1023, 4095]))
+    a, b = _frames(w, h, _abi.U16, maxv, 77 + seed, float(rng.uniform(-R + 1, R - 1)), float(rng.uniform(-R + 1, R - 1)))
+    if seed % 2:
+        b[rng.integers(0, h - 40):, : rng.integers(20, 80)] = maxv // 3  # a flat target patch
+    cfg = _cfg(M, R, step)
+    got = _run(a, b, cfg, legacy=False, path="bs")
+    exp = _run(a, b, cfg, legacy=True)
+    assert len(got) >= 1024
+    for f in FIELDS:
+        assert np.array_equal(got[f], exp[f], equal_nan=True), (seed, M, step, R, f)
