@@ -67,21 +67,12 @@ __device__ __forceinline__ bool bilinear(const Win& wn, const ImageView& im, int
   if (x0 > im.width - 2) x0 = im.width - 2;
   if (y0 > im.height - 2) y0 = im.height - 2;
   const float fx = xl - (float)(x0 - bx), fy = yl - (float)(y0 - by);
-  const int lx = x0 - wn.ox, ly = y0 - wn.oy;
-  float f00, f10, f01, f11;
-  if ((unsigned)lx < (unsigned)(wn.S - 1) && (unsigned)ly < (unsigned)(wn.S - 1)) {
-    const float* p = wn.w + ly * wn.P + lx;
-    f00 = p[0];
-    f10 = p[1];
-    f01 = p[wn.P];
-    f11 = p[wn.P + 1];
-  } else {
-    const int x1 = min(x0 + 1, im.width - 1), y1 = min(y0 + 1, im.height - 1);
-    f00 = gpx<Pix>(im, x0, y0);
-    f10 = gpx<Pix>(im, x1, y0);
-    f01 = gpx<Pix>(im, x0, y1);
-    f11 = gpx<Pix>(im, x1, y1);
-  }
+  // slow path: the four corners straight from global memory (L1), loads issued
+  // together (no window test per tap)
+  (void)wn;
+  const int x1 = min(x0 + 1, im.width - 1), y1 = min(y0 + 1, im.height - 1);
+  const float f00 = gpx<Pix>(im, x0, y0), f10 = gpx<Pix>(im, x1, y0);
+  const float f01 = gpx<Pix>(im, x0, y1), f11 = gpx<Pix>(im, x1, y1);
   const float a10 = f10 - f00, a01 = f01 - f00, a11 = (f00 + f11) - f10 - f01;
   const float v = fmaf(a11 * fx, fy, fmaf(a01, fy, fmaf(a10, fx, f00)));
   const float lo = fminf(fminf(f00, f10), fminf(f01, f11));
@@ -102,19 +93,30 @@ __device__ __forceinline__ bool grad_bilinear(const Win& wn, const ImageView& im
   const int x0 = bx + (int)flx, y0 = by + (int)fly;
   const float fx = xl - flx, fy = yl - fly;
   const float wx[2] = {1.0f - fx, fx}, wy[2] = {1.0f - fy, fy};
+  // the 12 taps of the four nodes' central differences, loaded together from
+  // global memory (coordinates clamped: a clamped tap only ever meets a zero
+  // weight, and fmaf(0, d, a) == a, so the sums equal the reference's
+  // zero-weight skipping exactly)
+  (void)wn;
+  const int W1 = im.width - 1, H1 = im.height - 1;
+  const int xm = max(x0 - 1, 0), xa = min(x0 + 1, W1), xb = min(x0 + 2, W1);
+  const int ym = max(y0 - 1, 0), ya = min(y0 + 1, H1), yb = min(y0 + 2, H1);
+  const float t_m0 = gpx<Pix>(im, xm, y0), t_a0 = gpx<Pix>(im, xa, y0), t_b0 = gpx<Pix>(im, xb, y0);
+  const float t_0m = gpx<Pix>(im, x0, ym), t_0a = gpx<Pix>(im, x0, ya), t_0b = gpx<Pix>(im, x0, yb);
+  const float t_am = gpx<Pix>(im, xa, ym), t_aa = gpx<Pix>(im, xa, ya), t_ab = gpx<Pix>(im, xa, yb);
+  const float t_ma = gpx<Pix>(im, xm, ya), t_ba = gpx<Pix>(im, xb, ya), t_00 = gpx<Pix>(im, x0, y0);
+  // node (x0 + a, y0 + b): d/dx = t(x+1) - t(x-1), d/dy = t(y+1) - t(y-1)
+  const float ddx[2][2] = {{t_a0 - t_m0, t_b0 - t_00}, {t_aa - t_ma, t_ba - t_0a}};
+  const float ddy[2][2] = {{t_0a - t_0m, t_aa - t_am}, {t_0b - t_00, t_ab - t_a0}};
   float ax = 0.f, ay = 0.f;
 #pragma unroll
-  for (int b = 0; b < 2; ++b) {
-    if (wy[b] == 0.0f) continue;
+  for (int b = 0; b < 2; ++b)
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
-      if (wx[a] == 0.0f) continue;
-      const int i = x0 + a, j = y0 + b;
       const float w = wx[a] * wy[b] * 0.5f;
-      ax = fmaf(w, tap<Pix>(wn, im, i + 1, j) - tap<Pix>(wn, im, i - 1, j), ax);
-      ay = fmaf(w, tap<Pix>(wn, im, i, j + 1) - tap<Pix>(wn, im, i, j - 1), ay);
+      ax = fmaf(w, ddx[b][a], ax);
+      ay = fmaf(w, ddy[b][a], ay);
     }
-  }
   gx = ax;
   gy = ay;
   return true;
