@@ -217,7 +217,7 @@ __device__ void assemble_hessian(const double* mo, double scale, double* H) {
 // symmetric). pd = all pivots > 0. Runs on all 32 lanes of one warp.
 __device__ void warp_cholesky_inverse(double (&h)[6], double (&hinv)[6], bool& pd) {
   const int lane = threadIdx.x & 31;
-  double L[6][6];
+  double L[6][6], rdiag[6];  // rdiag: 1 / L[j][j], one division per pivot
   bool ok = true;
 #pragma unroll
   for (int j = 0; j < 6; ++j) {
@@ -232,10 +232,11 @@ __device__ void warp_cholesky_inverse(double (&h)[6], double (&hinv)[6], bool& p
 #pragma unroll
     for (int k2 = 0; k2 < j; ++k2) L[j][k2] = __shfl_sync(0xffffffffu, h[k2], j);
     L[j][j] = ljj;
+    rdiag[j] = 1.0 / ljj;
     double v = h[j];
 #pragma unroll
     for (int k2 = 0; k2 < j; ++k2) v -= h[k2] * L[j][k2];
-    if (lane > j) h[j] = v / ljj;
+    if (lane > j) h[j] = v * rdiag[j];
     if (lane == j) h[j] = ljj;
   }
 #pragma unroll
@@ -249,14 +250,14 @@ __device__ void warp_cholesky_inverse(double (&h)[6], double (&hinv)[6], bool& p
     double v = (i == lane) ? 1.0 : 0.0;
 #pragma unroll
     for (int k2 = 0; k2 < i; ++k2) v -= L[i][k2] * y[k2];
-    y[i] = v / L[i][i];
+    y[i] = v * rdiag[i];
   }
 #pragma unroll
   for (int i = 5; i >= 0; --i) {
     double v = y[i];
 #pragma unroll
     for (int k2 = i + 1; k2 < 6; ++k2) v -= L[k2][i] * hinv[k2];
-    hinv[i] = v / L[i][i];
+    hinv[i] = v * rdiag[i];
   }
   pd = ok;
 }
