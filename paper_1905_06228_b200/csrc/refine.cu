@@ -227,12 +227,12 @@ __device__ void warp_cholesky_inverse(double (&h)[6], double (&hinv)[6], bool& p
     for (int k2 = 0; k2 < j; ++k2) d -= h[k2] * h[k2];
     d = __shfl_sync(0xffffffffu, d, j);
     ok = ok && d > 0.0;
-    const double ljj = sqrt(d > 0.0 ? d : 1.0);
+    const double dd = d > 0.0 ? d : 1.0, rj = rsqrt(dd), ljj = dd * rj;  // sqrt and its reciprocal, one MUFU
     // broadcast row j of L (k < j) and finish column j on lanes i > j
 #pragma unroll
     for (int k2 = 0; k2 < j; ++k2) L[j][k2] = __shfl_sync(0xffffffffu, h[k2], j);
     L[j][j] = ljj;
-    rdiag[j] = 1.0 / ljj;
+    rdiag[j] = rj;
     double v = h[j];
 #pragma unroll
     for (int k2 = 0; k2 < j; ++k2) v -= h[k2] * L[j][k2];
