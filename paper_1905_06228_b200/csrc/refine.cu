@@ -173,8 +173,9 @@ __device__ int compose_with_inverse(double* p, const double* inc) {
   const double a10 = inc[4], a11 = 1.0 + inc[5];
   const double det = __dsub_rn(__dmul_rn(a00, a11), __dmul_rn(a01, a10));
   if (fabs(det) < 1e-8) return DICB200_POI_INCREMENT_NOT_INVERTIBLE;
-  const double i00 = __ddiv_rn(a11, det), i01 = __ddiv_rn(-a01, det);
-  const double i10 = __ddiv_rn(-a10, det), i11 = __ddiv_rn(a00, det);
+  const double rdet = 1.0 / det;  // one division (the reference divides each cofactor)
+  const double i00 = a11 * rdet, i01 = -a01 * rdet;
+  const double i10 = -a10 * rdet, i11 = a00 * rdet;
   const double inv[9] = {i00, i01, -__dadd_rn(__dmul_rn(i00, inc[0]), __dmul_rn(i01, inc[3])),
                          i10, i11, -__dadd_rn(__dmul_rn(i10, inc[0]), __dmul_rn(i11, inc[3])),
                          0.0, 0.0, 1.0};
