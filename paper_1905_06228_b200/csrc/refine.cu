@@ -6,7 +6,7 @@
 // One WARP per POI; a CTA (8 warps) takes a strip of 8 neighbouring POIs of
 // one grid row, which share one staged fp32 reference region (subsets + 1 px
 // gradient border) and one staged fp32 target region (union of the 8
-// neighbourhoods of the integer estimates + kPad). After staging there are no
+// neighbourhoods of the integer estimates + pad_for(method)). After staging there are no
 // block barriers: every reduction is a warp shuffle and the 6x6 algebra runs
 // lane-parallel in fp64 on the same warp. Samples whose warped subset leaves
 // the staged region (or needs domain checks near the image border) take the
@@ -36,7 +36,9 @@ namespace {
 
 constexpr int kWarps = 8;        // POIs per CTA
 constexpr int kNT = 32 * kWarps;
-constexpr int kPad = 4;          // staged target margin around each neighbourhood (px)
+// staged target margin around each neighbourhood (px): NR's iterates wander
+// further (C3: drifting, non-converging POIs) than IC-GN's
+__host__ __device__ constexpr int pad_for(int method) { return method == 0 ? 8 : 4; }
 constexpr int kSpread = 12;      // max spread of integer estimates folded into one region
 
 template <typename Pix>
@@ -647,6 +649,7 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
     G.rY0 = cy - M - 1;
     G.rP = (cx1 - cx0) + side + 2;
     G.rH = side + 2;
+    constexpr int kPad = pad_for(METHOD);
     G.tX0 = cx0 + dxlo - M - kPad;
     G.tY0 = cy + dylo - M - kPad;
     G.tP = (cx1 - cx0) + (dxhi - dxlo) + side + 2 * kPad;
@@ -1045,6 +1048,7 @@ static size_t strip_smem(int M, int step, int spc, int method) {
   const int side = 2 * M + 1;
   const int span = step * (spc - 1);
   const size_t ref = (size_t)(side + 2) * (span + side + 2);
+  const int kPad = pad_for(method);
   const size_t tgt = (size_t)(side + 2 * kPad + 2 * kSpread) * (span + 2 * kSpread + side + 2 * kPad);
   return (size_t)4 * (((ref + tgt + 1) & ~(size_t)1) + (method == 1 ? 2 * ref : 0));
 }
