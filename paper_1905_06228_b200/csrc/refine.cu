@@ -38,7 +38,7 @@ constexpr int kWarps = 8;        // POIs per CTA
 constexpr int kNT = 32 * kWarps;
 // staged target margin around each neighbourhood (px): NR's iterates wander
 // further (C3: drifting, non-converging POIs) than IC-GN's
-__host__ __device__ constexpr int pad_for(int method) { return method == 0 ? 8 : 4; }
+__host__ __device__ constexpr int pad_for(int method) { return method == 0 ? 32 : 4; }
 constexpr int kSpread = 12;      // max spread of integer estimates folded into one region
 
 template <typename Pix>
