@@ -115,6 +115,18 @@ class Clocks:
                  "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+        self.first = ""
+
+    def wait_ready(self, timeout: float = 10.0):
+        """Blocks until the first sample is out: nvidia-smi's NVML start-up
+        (hundreds of ms of driver work) then lands before the warm-up, never
+        inside the timed steps."""
+        if not self.proc:
+            return
+        import select
+
+        if select.select([self.proc.stdout], [], [], timeout)[0]:
+            self.first = self.proc.stdout.readline()
 
     @staticmethod
     def _ts(line: str) -> float:
@@ -131,6 +143,7 @@ class Clocks:
         time.sleep(0.25)
         self.proc.terminate()
         out, _ = self.proc.communicate()
+        out = self.first + out
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         lines = out.strip().splitlines()
@@ -292,13 +305,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
             dist.barrier()
 
+    # clock sampler from here on (no idle gap between the warm-up and the timed
+    # steps: an idle GPU drops its clocks and the first timed step pays for it);
+    # started before the pipe-rate run so its NVML start-up is over by the warm-up
+    clocks = Clocks(local_rank)
+    clocks.start()
     # the live pipe-rate microbenchmark runs in its own process before the warm-up,
     # so nothing it leaves behind (context switch, clocks) lands in the timed steps
     peaks = pipe_peaks() if rank == 0 else {}
-    # clock sampler from here on (no idle gap between the warm-up and the timed
-    # steps: an idle GPU drops its clocks and the first timed step pays for it)
-    clocks = Clocks(local_rank)
-    clocks.start()
+    clocks.wait_ready()
     # warm-up (the last step with stage timing on, so the timing events are
     # created here and only recycled inside the timed region)
     with torch.cuda.stream(stream):
@@ -322,8 +337,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     with torch.cuda.stream(stream):
         ev0.record(stream)
         step_ev = []
+        enqueue_ms = []
         for _ in range(args.steps):
+            t_e = time.perf_counter()
             step()
+            enqueue_ms.append(round(1e3 * (time.perf_counter() - t_e), 3))
             step_ev.append(torch.cuda.Event(enable_timing=True))
             step_ev[-1].record(stream)
             if flush is not None:
@@ -573,6 +591,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "roofline": roof,
         "roofline_search": roof_search,
         "step_ms": step_ms,
+        "enqueue_ms": enqueue_ms,  # host time to enqueue each timed step (GPU starves when it exceeds step_ms)
         "stages_isolated": {k: {"avg_ms": v} for k, v in iso.items()},
         "clocks": clk,
         "parity_in_run": {"records": int(n_all), "status_ok": int(ok_all), "mean_iterations": iters_all / max(1, n_all)},

@@ -99,6 +99,14 @@ struct TcRefCache {
   void* pvf = nullptr;
   void* tail = nullptr;
   size_t strips_cap = 0, psf_cap = 0, pvf_cap = 0, tail_cap = 0;
+  // per-pair scratch (window sums, cross terms, tile list), reused by every pair
+  // on the cache's stream: no allocation per pair, so the memory pool never has
+  // to grow (map GBs of fresh pages) in the middle of a sequence
+  void* s1 = nullptr;
+  void* s2 = nullptr;
+  void* sfg = nullptr;
+  void* tiles = nullptr;
+  size_t s1_cap = 0, s2_cap = 0, sfg_cap = 0, tiles_cap = 0;
   long key = -1;
   const void* data = nullptr;
   int W = 0, H = 0, M = 0, x0 = 0, y0 = 0, step = 0, nx = 0, rb = 0, re = 0;

@@ -1131,7 +1131,7 @@ cudaError_t grow(void*& ptr, size_t& cap, size_t bytes, cudaStream_t st) {
 }  // namespace
 
 void tc_cache_free(TcRefCache& c, cudaStream_t st, bool async) {
-  for (void* q : {c.tail, c.strips, c.psf, c.pvf})
+  for (void* q : {c.tail, c.strips, c.psf, c.pvf, c.s1, c.s2, c.sfg, c.tiles})
     if (q) async ? cudaFreeAsync(q, st) : cudaFree(q);
   c = TcRefCache{};
 }
@@ -1178,20 +1178,33 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
     p.poi_sf = (int64_t*)psf;
     p.poi_sqrtvf = (double*)pvf;
   }
-  if (e == cudaSuccess) e = cudaMallocAsync(&s1, sbytes * 4, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&s2, sbytes * 12, st);  // SQ (double) + RSQ (float)
   const size_t EW = 2 * (size_t)p.R + 1;
-  if (e == cudaSuccess) e = cudaMallocAsync(&part, npoi * EW * EW * sizeof(int64_t), st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&tiles, (size_t)std::max(1, p.n_tiles) * 16, st);
+  const size_t s1_bytes = sbytes * 4, s2_bytes = sbytes * 12;  // S1 (u32); SQ (double) + RSQ (float)
+  const size_t sfg_bytes = npoi * EW * EW * sizeof(int64_t), tiles_bytes = (size_t)std::max(1, p.n_tiles) * 16;
+  void *S1 = nullptr, *S2 = nullptr, *SFG = nullptr, *TILES = nullptr;
+  if (cache) {
+    if (e == cudaSuccess) e = grow(cache->s1, cache->s1_cap, s1_bytes, st);
+    if (e == cudaSuccess) e = grow(cache->s2, cache->s2_cap, s2_bytes, st);
+    if (e == cudaSuccess) e = grow(cache->sfg, cache->sfg_cap, sfg_bytes, st);
+    if (e == cudaSuccess) e = grow(cache->tiles, cache->tiles_cap, tiles_bytes, st);
+    S1 = cache->s1, S2 = cache->s2, SFG = cache->sfg, TILES = cache->tiles;
+  } else {
+    if (e == cudaSuccess) e = cudaMallocAsync(&s1, s1_bytes, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&s2, s2_bytes, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&part, sfg_bytes, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&tiles, tiles_bytes, st);
+    S1 = s1, S2 = s2, SFG = part, TILES = tiles;
+  }
   if (e != cudaSuccess) {
     cleanup();
     return e;
   }
-  p.S1 = (uint32_t*)s1;
-  p.SQ = (double*)s2;
-  p.RSQ = (float*)((char*)s2 + sbytes * 8);
-  p.sfg = (int64_t*)part;
-  p.tiles = tiles;
+  host_trace("tc mallocs");
+  p.S1 = (uint32_t*)S1;
+  p.SQ = (double*)S2;
+  p.RSQ = (float*)((char*)S2 + sbytes * 8);
+  p.sfg = (int64_t*)SFG;
+  p.tiles = TILES;
   const bool u8 = p.planes == 1;
   // (a) window sums of the target
   if (e == cudaSuccess && p.n_tiles > 0) {
@@ -1207,6 +1220,7 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
   }
+  host_trace("tc stats");
   // (b) reference moments + strip images (skipped when cached; the block-sum
   //     kernel reads the reference directly and needs no strips)
   BsGeom bsg{};
@@ -1247,10 +1261,12 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
       cache->re = p.re;
     }
   }
+  host_trace("tc prep");
   // (c) tensor-core search
   if (e == cudaSuccess && use_bs) {
     StageTimer tm(6, st);
     e = bs_launch(p, bsg, st);
+    host_trace("bs");
   }
   if (e == cudaSuccess && p.n_tiles > 0 && !use_bs) {
     tc_tiles_kernel<<<(p.n_tiles + 255) / 256, 256, 0, st>>>(p);

@@ -85,4 +85,7 @@ struct StageTimer {
 namespace dicb200 {
 dicb200_status cuda_fail(cudaError_t e, const char* what, const char* file, int line);
 void set_error(const char* msg);
+// DICB200_HOST_TRACE=1: reports host-side gaps > 5 ms between consecutive
+// marks on this thread (enqueue stalls that would starve the GPU)
+void host_trace(const char* what, long i = 0);
 }  // namespace dicb200

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <chrono>
 #include <string>
 #include <thread>
 #include <vector>
@@ -107,6 +108,16 @@ static dicb200_status make_lattice(int w, int h, const dicb200_run_config* cfg, 
 
 // Keep stream-ordered allocations (PSO surfaces, per-call images/records) in
 // the device pool across calls instead of returning them at every sync.
+void host_trace(const char* what, long i) {
+  static const bool on = std::getenv("DICB200_HOST_TRACE") != nullptr;
+  if (!on) return;
+  thread_local auto t_last = std::chrono::steady_clock::now();
+  auto t = std::chrono::steady_clock::now();
+  const double ms = std::chrono::duration<double, std::milli>(t - t_last).count();
+  if (ms > 5.0) fprintf(stderr, "[dicb200 trace] %s %ld: %.1f ms\n", what, i, ms);
+  t_last = t;
+}
+
 static void retain_pool_memory() {
   static std::mutex mu;
   static std::vector<int> done;
@@ -313,6 +324,7 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
     if (s != DICB200_OK) return s;
   }
 refine:
+  host_trace("search enqueued");
   if (cfg->subpixel_method != DICB200_SUB_NONE) {
     RefineParams r{};
     r.ref = view(ref);
@@ -327,6 +339,7 @@ refine:
     r.rec = out_dev;
     StageTimer tm(r.method == 0 ? 2 : 3, st);
     DICB200_CUDA_TRY(refine_launch(r, ref->dtype == DICB200_U8, st, icache, ref_key));
+    host_trace("refine enqueued");
   }
   return DICB200_OK;
 }
@@ -818,6 +831,8 @@ dicb200_status dicb200_analyze_sequence_device(const dicb200_image* images, size
   // of the other's. Each stream owns its reference-side caches: nothing is
   // shared between concurrently running pairs.
   const bool fixed = cfg->reference_policy == DICB200_POLICY_FIXED_FIRST;
+  auto mark = [](const char* what, long i) { host_trace(what, i); };
+  host_trace("seq begin");
   const char* env = std::getenv("DICB200_SEQ_STREAMS");
   const int ns = std::max(1, std::min<int>(env ? std::atoi(env) : kSeqStreams, (int)(n_images - 1)));
   std::vector<cudaStream_t> ss(ns, st);
@@ -833,15 +848,18 @@ dicb200_status dicb200_analyze_sequence_device(const dicb200_image* images, size
     }
     if (e != cudaSuccess) s = cuda_fail(e, "sequence stream fork", __FILE__, __LINE__);
   }
+  mark("fork", 0);
   for (size_t i = 0; i + 1 < n_images && s == DICB200_OK; ++i) {
     const int k = (int)(i % ns);
     s = enqueue_pair(&images[pairs[2 * i]], &images[pairs[2 * i + 1]], cfg, first_pair_index + i, lat, rb, re,
                      out_dev + i * pair_stride, ss[k], &tc[k], (long)pairs[2 * i], fixed ? &ic[k] : nullptr);
+    mark("pair", (long)i);
   }
   for (int k = 0; k < ns; ++k) {
     tc_cache_free(tc[k], ss[k], true);
     icgn_cache_free(ic[k], ss[k], true);
   }
+  mark("free", 0);
   if (ns > 1) {  // join: the caller's stream waits for every internal stream
     for (int k = 0; k < ns; ++k) {
       if (ss[k] == st) continue;
