@@ -157,108 +157,126 @@ __host__ __device__ inline void tile_pois(const TcParams& p, int X0, int Y0, int
 }
 
 // ---- exact window sums of g and g^2 at every position of the domain ----
-// CTA = 64 x 32 positions. The target region is staged in shared memory by
-// rows; row sums over `side` columns go to shared memory, then column sums over
-// `side` rows slide down each output column, so the global stores of S1/S2 are
-// coalesced rows. Exact in integers (u32 sums, u64 sums of squares).
-constexpr int kStatsBX = 64, kStatsBY = 32;
+// CTA = 64 x ty positions (ty = 64, or 32/16 for large subsets). The target
+// region is staged in shared memory by rows (division-free, batched loads);
+// row sums over `side` columns go to shared memory (odd pitches: lanes walk
+// rows without bank conflicts), then column sums over `side` rows slide down
+// each output column, so the global stores of S1/SQ/RSQ are coalesced rows.
+// Exact in integers: u32 sums, squares summed in u32 along rows when
+// side * maxv^2 < 2^32 (H2 = uint32_t), else u64; u64 along columns.
+constexpr int kStatsBX = 64, kStatsSeg = 16, kStatsCh = 16, kStatsHP = kStatsBX + 1;
 
-__host__ __device__ inline size_t stats_smem_bytes(int side) {
-  const size_t RW = kStatsBX + side - 1, RH = kStatsBY + side - 1;
-  return ((RH * RW * 2 + 15) & ~size_t(15)) + ((RH * kStatsBX * 4 + 15) & ~size_t(15)) + RH * kStatsBX * 8;
+__host__ __device__ inline int stats_reg_pitch(int side) {  // u16 elements, odd number of 4-byte words
+  int rw = (kStatsBX + side - 1 + 1) & ~1;
+  if (((rw >> 1) & 1) == 0) rw += 2;
+  return rw;
+}
+__host__ __device__ inline size_t stats_smem_bytes(int side, int ty, bool sq32) {
+  const size_t RH = ty + side - 1;
+  return ((RH * stats_reg_pitch(side) * 2 + 15) & ~size_t(15)) + ((RH * kStatsHP * 4 + 15) & ~size_t(15)) +
+         RH * kStatsHP * (sq32 ? 4 : 8);
 }
 
-template <typename Pix>
-__global__ void __launch_bounds__(256) tc_stats_kernel(TcParams p) {
-  extern __shared__ __align__(1024) unsigned char stats_smem[];
-  const int side = p.side, RW = kStatsBX + side - 1, RH = kStatsBY + side - 1;
+template <typename Pix, typename H2>
+__global__ void __launch_bounds__(256) tc_stats_kernel(TcParams p, int ty) {
+  extern __shared__ __align__(16) unsigned char stats_smem[];
+  const int side = p.side, RWp = stats_reg_pitch(side), RW = kStatsBX + side - 1;
+  const int RH = ty + side - 1;
   uint16_t* reg = reinterpret_cast<uint16_t*>(stats_smem);
-  uint32_t* h1 = reinterpret_cast<uint32_t*>(stats_smem + (((size_t)RH * RW * 2 + 15) & ~size_t(15)));
-  uint64_t* h2 = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(h1) +
-                                             (((size_t)RH * kStatsBX * 4 + 15) & ~size_t(15)));
-  const int sx0 = blockIdx.x * kStatsBX, sy0 = blockIdx.y * kStatsBY;
-  const int rows = min(kStatsBY, p.SH - sy0), cols = min(kStatsBX, p.SW - sx0);
+  uint32_t* h1 = reinterpret_cast<uint32_t*>(stats_smem + (((size_t)RH * RWp * 2 + 15) & ~size_t(15)));
+  H2* h2 = reinterpret_cast<H2*>(reinterpret_cast<unsigned char*>(h1) + (((size_t)RH * kStatsHP * 4 + 15) & ~size_t(15)));
+  const int sx0 = blockIdx.x * kStatsBX, sy0 = blockIdx.y * ty;
+  const int rows = min(ty, p.SH - sy0), cols = min(kStatsBX, p.SW - sx0);
   const Pix* img = reinterpret_cast<const Pix*>(p.tgt.data);
   const int pitch = p.tgt.pitch, gx0 = p.qx_min + sx0, gy0 = p.qy_min + sy0;
   const int W = p.tgt.width, H = p.tgt.height;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rh = rows + side - 1;  // region rows this CTA needs
-  {
-    // batches of 8 independent loads per thread (memory-level parallelism)
-    const int E = rh * RW;
-    constexpr int U = 8;
-    for (int base = threadIdx.x; base < E; base += U * 256) {
-      uint16_t v[U];
+  // staging: one warp per region row, 4 independent loads per lane in flight
+  for (int r = warp; r < rh; r += 8) {
+    const int gy = gy0 + r;
+    const Pix* src = img + (size_t)min(gy, H - 1) * pitch;
+    uint16_t* dst = reg + r * RWp;
+    for (int c0 = 0; c0 < RW; c0 += 128) {
+      uint16_t v[4];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = base + u * 256, r = i / RW, c = i - r * RW, gy = gy0 + r, gx = gx0 + c;
-        v[u] = (i < E && gy < H && gx < W) ? (uint16_t)img[(size_t)gy * pitch + gx] : (uint16_t)0;
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * 32 + lane, gx = gx0 + c;
+        v[u] = (c < RW && gy < H && gx < W) ? (uint16_t)src[gx] : (uint16_t)0;
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (base + u * 256 < E) reg[base + u * 256] = v[u];
+      for (int u = 0; u < 4; ++u)
+        if (c0 + u * 32 + lane < RW) dst[c0 + u * 32 + lane] = v[u];
     }
   }
-  (void)warp;
-  (void)lane;
-  (void)nw;
   __syncthreads();
-  // row sums over `side` columns: h[r][x], 8 outputs per item
-  constexpr int SEG = 8;
-  for (int item = threadIdx.x; item < rh * (kStatsBX / SEG); item += blockDim.x) {
-    const int r = item / (kStatsBX / SEG), x0 = (item % (kStatsBX / SEG)) * SEG;
-    const uint16_t* row = reg + r * RW;
+  // row sums over `side` columns: h[r][x0 .. x0+15]; lanes take consecutive rows
+  constexpr int nseg = kStatsBX / kStatsSeg;
+  for (int item = threadIdx.x; item < rh * nseg; item += blockDim.x) {
+    const int seg = item / rh, r = item - seg * rh, x0 = seg * kStatsSeg;
+    const uint16_t* row = reg + r * RWp + x0;
     uint32_t s1 = 0;
-    uint64_t s2 = 0;
+    H2 s2 = 0;
 #pragma unroll 8
     for (int c = 0; c < side; ++c) {
-      const uint32_t v = row[x0 + c];
+      const uint32_t v = row[c];
       s1 += v;
-      s2 += (uint64_t)v * v;
+      s2 += (H2)v * v;
     }
-    h1[r * kStatsBX + x0] = s1;
-    h2[r * kStatsBX + x0] = s2;
+    uint32_t* o1 = h1 + r * kStatsHP + x0;
+    H2* o2 = h2 + r * kStatsHP + x0;
+    o1[0] = s1;
+    o2[0] = s2;
 #pragma unroll
-    for (int x = x0 + 1; x < x0 + SEG; ++x) {
+    for (int x = 1; x < kStatsSeg; ++x) {
       const uint32_t a = row[x + side - 1], b = row[x - 1];
       s1 += a - b;
-      s2 += (uint64_t)a * a - (uint64_t)b * b;
-      h1[r * kStatsBX + x] = s1;
-      h2[r * kStatsBX + x] = s2;
+      s2 += (H2)a * a - (H2)b * b;  // modular: the running sum itself fits H2
+      o1[x] = s1;
+      o2[x] = s2;
     }
   }
   __syncthreads();
-  // column sums over `side` rows, sliding down 16 outputs per item (coalesced stores)
-  constexpr int CH = 16;
-  for (int item = threadIdx.x; item < kStatsBX * (kStatsBY / CH); item += blockDim.x) {
-    const int x = item % kStatsBX, t0 = (item / kStatsBX) * CH;
-    if (t0 >= rows || x >= cols) continue;
+  // column sums over `side` rows, sliding down kStatsCh outputs per item
+  const int nch = (rows + kStatsCh - 1) / kStatsCh;
+  const int64_t nn = (int64_t)side * side;
+  for (int item = threadIdx.x; item < kStatsBX * nch; item += blockDim.x) {
+    const int x = item % kStatsBX, t0 = (item / kStatsBX) * kStatsCh;
+    if (x >= cols) continue;
     uint32_t s1 = 0;
     uint64_t s2 = 0;
 #pragma unroll 8
     for (int r = 0; r < side; ++r) {
-      s1 += h1[(t0 + r) * kStatsBX + x];
-      s2 += h2[(t0 + r) * kStatsBX + x];
+      s1 += h1[(t0 + r) * kStatsHP + x];
+      s2 += (uint64_t)h2[(t0 + r) * kStatsHP + x];
     }
     size_t o = (size_t)(sy0 + t0) * p.SW + sx0 + x;
-    const int64_t nn = (int64_t)side * side;
-    auto put = [&](size_t oo, uint32_t a1, uint64_t a2) {
+    const int t1 = min(t0 + kStatsCh, rows);
+    for (int t = t0;;) {
       // sqrt(vg) exactly as zncc_from_moments forms it (0 = degenerate window)
-      const int64_t vg = nn * (int64_t)a2 - (int64_t)a1 * (int64_t)a1;
+      const int64_t vg = nn * (int64_t)s2 - (int64_t)s1 * (int64_t)s1;
       const double sq = vg > 0 ? sqrt((double)vg) : 0.0;
-      p.S1[oo] = a1;
-      p.SQ[oo] = sq;
-      p.RSQ[oo] = vg > 0 ? (float)(1.0 / sq) : 0.0f;
-    };
-    put(o, s1, s2);
-    const int t1 = min(t0 + CH, rows);
-    for (int t = t0 + 1; t < t1; ++t) {
-      s1 += h1[(t + side - 1) * kStatsBX + x] - h1[(t - 1) * kStatsBX + x];
-      s2 += h2[(t + side - 1) * kStatsBX + x] - h2[(t - 1) * kStatsBX + x];
+      p.S1[o] = s1;
+      p.SQ[o] = sq;
+      p.RSQ[o] = vg > 0 ? (float)(1.0 / sq) : 0.0f;
+      if (++t >= t1) break;
+      s1 += h1[(t + side - 1) * kStatsHP + x] - h1[(t - 1) * kStatsHP + x];
+      s2 += (uint64_t)h2[(t + side - 1) * kStatsHP + x] - (uint64_t)h2[(t - 1) * kStatsHP + x];
       o += p.SW;
-      put(o, s1, s2);
     }
   }
+}
+
+// tile height and squares width of the stats kernel (largest tile within ~110 KB)
+static bool stats_sq32(const TcParams& p) {
+  const double maxv = p.maxv > 0 ? p.maxv : (p.planes == 1 ? 255.0 : 65535.0);
+  return (double)p.side * maxv * maxv < 4294967296.0;
+}
+static int stats_ty(const TcParams& p) {
+  const bool q = stats_sq32(p);
+  for (int ty : {64, 32})
+    if (stats_smem_bytes(p.side, ty, q) <= 110 * 1024) return ty;
+  return 16;
 }
 
 // ---- per POI: exact reference moments (separable window sums at the lattice) ----
@@ -1049,7 +1067,7 @@ bool tc_plan(TcParams& p) {
   p.side = 2 * p.M + 1;
   if (p.side > 129) return false;
   if ((size_t)p.ref.width * 12 + 16 > 200 * 1024) return false;  // tc_prep_kernel column sums
-  if (stats_smem_bytes(p.side) > 200 * 1024) return false;
+  if (stats_smem_bytes(p.side, 16, false) > 200 * 1024) return false;
   if (pos_smem_bytes(p, 1) > 200 * 1024) return false;
   const int side = p.side, W = p.tgt.width, H = p.tgt.height;
   const int rows = p.re - p.rb;
@@ -1208,15 +1226,18 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
   const bool u8 = p.planes == 1;
   // (a) window sums of the target
   if (e == cudaSuccess && p.n_tiles > 0) {
-    const size_t sm = stats_smem_bytes(p.side);
-    dim3 grid((p.SW + kStatsBX - 1) / kStatsBX, (p.SH + kStatsBY - 1) / kStatsBY);
-    if (u8) {
-      e = set_smem(tc_stats_kernel<uint8_t>, sm);
-      if (e == cudaSuccess) tc_stats_kernel<uint8_t><<<grid, 256, sm, st>>>(p);
-    } else {
-      e = set_smem(tc_stats_kernel<uint16_t>, sm);
-      if (e == cudaSuccess) tc_stats_kernel<uint16_t><<<grid, 256, sm, st>>>(p);
-    }
+    const bool q = stats_sq32(p);
+    const int ty = stats_ty(p);
+    const size_t sm = stats_smem_bytes(p.side, ty, q);
+    dim3 grid((p.SW + kStatsBX - 1) / kStatsBX, (p.SH + ty - 1) / ty);
+    auto go = [&](auto kern) {
+      e = set_smem(kern, sm);
+      if (e == cudaSuccess) kern<<<grid, 256, sm, st>>>(p, ty);
+    };
+    if (u8)
+      q ? go(tc_stats_kernel<uint8_t, uint32_t>) : go(tc_stats_kernel<uint8_t, uint64_t>);
+    else
+      q ? go(tc_stats_kernel<uint16_t, uint32_t>) : go(tc_stats_kernel<uint16_t, uint64_t>);
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
   }
