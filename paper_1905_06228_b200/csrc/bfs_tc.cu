@@ -807,10 +807,12 @@ struct Cand {
   float rsq;   // ~1 / sq (candidate filter only)
 };
 
-// Position data (Sg, sqrt(vg), ~1/sqrt(vg)) of the union of a strip's windows,
-// staged in shared memory once per CTA (neighbouring POIs share most positions).
+// Position data (Sg, ~1/sqrt(vg)) of the union of a strip's windows, staged in
+// shared memory once per CTA (neighbouring POIs share most positions); the
+// exact sqrt(vg) is read from global memory for the few near-maximal
+// candidates only (tc_argmax_kernel). The surface kernel views global memory.
 struct PosView {
-  const double* sq;
+  const double* sq;  // surface kernel only
   const uint32_t* s1;
   const float* rsq;
   int x0, y0, W;
@@ -818,7 +820,7 @@ struct PosView {
 
 __host__ __device__ inline size_t pos_smem_bytes(const TcParams& p, int sp) {
   const size_t W = (size_t)(sp - 1) * p.lat.step + 2 * p.R + 1, H = 2 * (size_t)p.R + 1;
-  return W * H * 16;
+  return W * H * 8;
 }
 
 __device__ __forceinline__ PosView stage_positions(const TcParams& p, int iy, int ix0, int ts, unsigned char* sm) {
@@ -830,19 +832,17 @@ __device__ __forceinline__ PosView stage_positions(const TcParams& p, int iy, in
   const int y1 = min(p.lat.cy(iy) - M + R, p.qy_max);
   v.W = max(0, x1 - v.x0 + 1);
   const int H = max(0, y1 - v.y0 + 1), N = v.W * H;
-  double* sq = reinterpret_cast<double*>(sm);
-  uint32_t* s1 = reinterpret_cast<uint32_t*>(sm + (size_t)N * 8);
-  float* rsq = reinterpret_cast<float*>(sm + (size_t)N * 12);
+  uint32_t* s1 = reinterpret_cast<uint32_t*>(sm);
+  float* rsq = reinterpret_cast<float*>(sm + (size_t)N * 4);
   for (int r = threadIdx.x >> 5; r < H; r += blockDim.x >> 5) {
     const size_t o = (size_t)(v.y0 + r - p.qy_min) * p.SW + (v.x0 - p.qx_min);
     for (int c = threadIdx.x & 31; c < v.W; c += 32) {
-      sq[r * v.W + c] = p.SQ[o + c];
       s1[r * v.W + c] = p.S1[o + c];
       rsq[r * v.W + c] = p.RSQ[o + c];
     }
   }
   __syncthreads();
-  v.sq = sq;
+  v.sq = nullptr;
   v.s1 = s1;
   v.rsq = rsq;
   return v;
@@ -858,6 +858,20 @@ __device__ __forceinline__ bool tc_candidate_s(const PosView& v, uint32_t n, uin
   c.rsq = v.rsq[o];
   c.num = (int64_t)((uint64_t)sfg * n - (uint64_t)sf * v.s1[o]);
   return true;
+}
+
+// Filter pass: rsq > 0 exactly when sqrt(vg) > 0 (tc_stats_kernel writes 0 for
+// both when vg <= 0, and 1/sqrt(vg) >= 2^-32 is a normal float otherwise).
+__device__ __forceinline__ bool tc_candidate_f(const PosView& v, uint32_t n, uint32_t sf, int64_t sfg, int qx, int qy,
+                                               int64_t& num, float& rsq) {
+  const int o = (qy - v.y0) * v.W + (qx - v.x0);
+  rsq = v.rsq[o];
+  if (!(rsq > 0.0f)) return false;  // constant target window: skipped, not counted
+  num = (int64_t)((uint64_t)sfg * n - (uint64_t)sf * v.s1[o]);
+  return true;
+}
+__device__ __forceinline__ double tc_sq(const TcParams& p, int qx, int qy) {
+  return p.SQ[(size_t)(qy - p.qy_min) * p.SW + (qx - p.qx_min)];
 }
 
 // ---- per POI: count, exact argmax in improves() order -> record ----
@@ -892,7 +906,7 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p, int sp) {
     // approximate quotient
     int cnt = 0;
     double a1 = -3.0, a2 = -3.0;
-    Cand c1{0, 1.0, 1.0f};
+    int64_t num1 = 0;
     int x1 = 0, y1 = 0;
     // flattened (dy, dx) walk: lane l takes candidates l, l + 32, ... in row-major order
     const int fw = fx_hi - fx_lo + 1, total = fw * (fy_hi - fy_lo + 1);
@@ -937,13 +951,14 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p, int sp) {
           ahead_x -= fw;
           ++ahead_y;
         }
-        Cand c;
-        if (tc_candidate_s(pv, n, sf, sfg_v, cx - M + dx, cy - M + dy, c)) {
+        int64_t num;
+        float rsq;
+        if (tc_candidate_f(pv, n, sf, sfg_v, cx - M + dx, cy - M + dy, num, rsq)) {
           ++cnt;
-          const double av = i64_to_f64(c.num) * rsvf * (double)c.rsq;
+          const double av = i64_to_f64(num) * rsvf * (double)rsq;
           if (av > a1) {  // a2: the lane's runner-up (only its value is needed)
             a2 = a1;
-            a1 = av, c1 = c, x1 = dx, y1 = dy;
+            a1 = av, num1 = num, x1 = dx, y1 = dy;
           } else if (av > a2) {
             a2 = av;
           }
@@ -966,7 +981,7 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p, int sp) {
     if (!__any_sync(0xffffffffu, a2 >= thr)) {
       // every near-maximal candidate is some lane's best: exact quotients for those
       if (a1 >= thr) {
-        const double z = i64_to_f64(c1.num) / (svf * c1.sq);  // exact (zncc_from_moments)
+        const double z = i64_to_f64(num1) / (svf * tc_sq(p, cx - M + x1, cy - M + y1));  // exact (zncc_from_moments)
         b.found = 1;
         b.c = z;
         b.dx = x1;
@@ -976,11 +991,12 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p, int sp) {
       // near-ties beyond two per lane: second pass over the window
       for (int dy = fy_lo; dy <= fy_hi; ++dy)
         for (int dx = fx_lo + lane; dx <= fx_hi; dx += 32) {
-          Cand c;
-          if (tc_candidate_s(pv, n, sf, buf[(dy + R) * EW + (dx + R)], cx - M + dx, cy - M + dy, c)) {
-            const double nd = i64_to_f64(c.num);
-            if (nd * rsvf * (double)c.rsq >= thr) {
-              const double z = nd / (svf * c.sq);
+          int64_t num;
+          float rsq;
+          if (tc_candidate_f(pv, n, sf, buf[(dy + R) * EW + (dx + R)], cx - M + dx, cy - M + dy, num, rsq)) {
+            const double nd = i64_to_f64(num);
+            if (nd * rsvf * (double)rsq >= thr) {
+              const double z = nd / (svf * tc_sq(p, cx - M + dx, cy - M + dy));
               if (!b.found || improves(z, dx, dy, b.c, b.dx, b.dy)) {
                 b.found = 1;
                 b.c = z;
