@@ -46,6 +46,31 @@ __device__ __forceinline__ float gpx(const ImageView& im, int x, int y) {
   return (float)__ldg(reinterpret_cast<const Pix*>(im.data) + (size_t)y * im.pitch + x);
 }
 
+// Region rows [0, H) x [0, P) of `im` at (X0, Y0) -> dst (fp32, pitch P), zero
+// outside the image; warp w takes rows w, w + kWarps, ...
+template <typename Pix>
+__device__ __forceinline__ void stage_rows(const ImageView& im, int X0, int Y0, int P, int H, float* dst, int warp,
+                                           int lane) {
+  const Pix* base = reinterpret_cast<const Pix*>(im.data);
+  for (int y = warp; y < H; y += kWarps) {
+    const int gy = Y0 + y;
+    const bool yin = gy >= 0 && gy < im.height;
+    const Pix* src = base + (size_t)(yin ? gy : 0) * im.pitch;
+    float* d = dst + y * P;
+    for (int c0 = 0; c0 < P; c0 += 128) {
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int x = c0 + u * 32 + lane, gx = X0 + x;
+        v[u] = (x < P && yin && gx >= 0 && gx < im.width) ? (float)__ldg(src + gx) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c0 + u * 32 + lane < P) d[c0 + u * 32 + lane] = v[u];
+    }
+  }
+}
+
 struct Win {
   const float* w;  // S x S fp32 copy of the target around (bx, by), row pitch P
   int S, P, ox, oy;  // ox, oy: global coords of w[0]
@@ -445,7 +470,7 @@ __device__ __forceinline__ void icgn_pass_fast2(const PassCtx& c, const Walk& w0
   int roff = w0.roff;
   const int cnt = w0.npl - (w0.last_valid ? 0 : 1);
   const float* Tb = c.T + c.ioffy * c.tP + c.ioffx;  // target-region origin in subset-local coordinates
-#pragma unroll 2
+#pragma unroll 4
   for (int i = 0; i < cnt; ++i) {
     float dx, dy;
     up2(dxy, dx, dy);
@@ -661,24 +686,20 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
   float* T = smem_f + g.rH * g.rP;      // target region [tH][tP]
   // IC-GN: gradient region (2 grad f) [rH][rP] as float2, 8-byte aligned
   float2* G2 = reinterpret_cast<float2*>(smem_f + ((g.rH * g.rP + g.tH * g.tP + 1) & ~1));
-  // ---- stage both regions (fp32), zero outside the images ----
-  for (int i = tid; i < g.rH * g.rP; i += kNT) {
-    const int y = i / g.rP, x = i - y * g.rP;
-    const int gx = g.rX0 + x, gy = g.rY0 + y;
-    R[i] = (gx >= 0 && gx < p.ref.width && gy >= 0 && gy < p.ref.height) ? gpx<Pix>(p.ref, gx, gy) : 0.f;
-  }
-  for (int i = tid; i < g.tH * g.tP; i += kNT) {
-    const int y = i / g.tP, x = i - y * g.tP;
-    const int gx = g.tX0 + x, gy = g.tY0 + y;
-    T[i] = (gx >= 0 && gx < p.tgt.width && gy >= 0 && gy < p.tgt.height) ? gpx<Pix>(p.tgt, gx, gy) : 0.f;
-  }
+  // ---- stage both regions (fp32), zero outside the images: one warp per
+  // region row, 4 independent loads per lane in flight, no index division ----
+  stage_rows<Pix>(p.ref, g.rX0, g.rY0, g.rP, g.rH, R, warp, lane);
+  stage_rows<Pix>(p.tgt, g.tX0, g.tY0, g.tP, g.tH, T, warp, lane);
   __syncthreads();
   if (METHOD == 1) {  // central differences of the reference (icgn_precompute, subpixel.cpp:207-208), x2
-    for (int i = tid; i < g.rH * g.rP; i += kNT) {
-      const int y = i / g.rP, x = i - y * g.rP;
-      float2 v = make_float2(0.f, 0.f);
-      if (x >= 1 && x < g.rP - 1 && y >= 1 && y < g.rH - 1) v = make_float2(R[i + 1] - R[i - 1], R[i + g.rP] - R[i - g.rP]);
-      G2[i] = v;
+    for (int y = warp; y < g.rH; y += kWarps) {
+      const bool yin = y >= 1 && y < g.rH - 1;
+      for (int x = lane; x < g.rP; x += 32) {
+        const int i = y * g.rP + x;
+        float2 v = make_float2(0.f, 0.f);
+        if (yin && x >= 1 && x < g.rP - 1) v = make_float2(R[i + 1] - R[i - 1], R[i + g.rP] - R[i - g.rP]);
+        G2[i] = v;
+      }
     }
     __syncthreads();
   }
