@@ -874,11 +874,19 @@ __device__ __forceinline__ double tc_sq(const TcParams& p, int qx, int qy) {
   return p.SQ[(size_t)(qy - p.qy_min) * p.SW + (qx - p.qx_min)];
 }
 
+// Filter value num / (sqrt(vf) sqrt(vg)) in fp32: five roundings of relative
+// 2^-24 each (num, 1/sqrt(vf), 1/sqrt(vg), two products) -> absolute error
+// < 5.1 * 2^-24 < 2^-21.6 for |zncc| <= 1. No overflow or denormals:
+// |num| <= n Sfg < 2^14.1 * 2^46.1, each reciprocal factor >= 2^-30.1.
+__device__ __forceinline__ float approx_zncc(int64_t num, float rsvf, float rsq) {
+  return __fmul_rn(__fmul_rn(__ll2float_rn(num), rsvf), rsq);
+}
+
 // ---- per POI: count, exact argmax in improves() order -> record ----
-// One pass finds the maximum of a cheap quotient num * (1/sqrt(vf)) * rsq with
-// rsq the fp32 reciprocal of sqrt(vg) (relative error < 2^-22, i.e. absolute as
-// |zncc| <= 1); the EXACT IEEE quotient num / (sqrt(vf) sqrt(vg)) is formed only
-// for candidates within 2^-20 of it (a second pass when more than one per lane
+// One pass finds the maximum of a cheap fp32 quotient num * (1/sqrt(vf)) * rsq
+// with rsq the fp32 reciprocal of sqrt(vg) (approx_zncc: absolute error
+// < 2^-21.6 as |zncc| <= 1); the EXACT IEEE quotient num / (sqrt(vf) sqrt(vg)) is
+// formed only for candidates within 2^-19 of it (a second pass when more than one per lane
 // qualifies), so the winner and its value are exactly those of the sequential
 // reference loop. Warp per POI, lanes across the window candidates.
 __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p, int sp) {
@@ -902,10 +910,11 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p, int sp) {
   if (fx_lo <= fx_hi && fy_lo <= fy_hi && svf > 0.0) {
     const int64_t* buf = p.sfg + (size_t)k * EW * EW;
     const double rsvf = 1.0 / svf;
+    const float rsvf_f = (float)rsvf;
     // one pass over memory: count, and each lane's two best candidates by the
     // approximate quotient
     int cnt = 0;
-    double a1 = -3.0, a2 = -3.0;
+    float a1 = -3.0f, a2 = -3.0f;
     int64_t num1 = 0;
     int x1 = 0, y1 = 0;
     // flattened (dy, dx) walk: lane l takes candidates l, l + 32, ... in row-major order
@@ -955,7 +964,7 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p, int sp) {
         float rsq;
         if (tc_candidate_f(pv, n, sf, sfg_v, cx - M + dx, cy - M + dy, num, rsq)) {
           ++cnt;
-          const double av = i64_to_f64(num) * rsvf * (double)rsq;
+          const float av = approx_zncc(num, rsvf_f, rsq);
           if (av > a1) {  // a2: the lane's runner-up (only its value is needed)
             a2 = a1;
             a1 = av, num1 = num, x1 = dx, y1 = dy;
@@ -971,13 +980,13 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p, int sp) {
         ++ry;
       }
     }
-    double amax = a1;
+    float amax = a1;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-      amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     }
-    const double thr = amax - 0x1p-20;  // the filter's error (fp32 1/sqrt(vg)) is < 2^-22
+    const float thr = amax - 0x1p-19f;  // twice the filter's error bound (< 2^-21.6), see approx_zncc
     if (!__any_sync(0xffffffffu, a2 >= thr)) {
       // every near-maximal candidate is some lane's best: exact quotients for those
       if (a1 >= thr) {
@@ -994,9 +1003,8 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p, int sp) {
           int64_t num;
           float rsq;
           if (tc_candidate_f(pv, n, sf, buf[(dy + R) * EW + (dx + R)], cx - M + dx, cy - M + dy, num, rsq)) {
-            const double nd = i64_to_f64(num);
-            if (nd * rsvf * (double)rsq >= thr) {
-              const double z = nd / (svf * tc_sq(p, cx - M + dx, cy - M + dy));
+            if (approx_zncc(num, rsvf_f, rsq) >= thr) {
+              const double z = i64_to_f64(num) / (svf * tc_sq(p, cx - M + dx, cy - M + dy));
               if (!b.found || improves(z, dx, dy, b.c, b.dx, b.dy)) {
                 b.found = 1;
                 b.c = z;
