@@ -513,6 +513,56 @@ __device__ __forceinline__ void icgn_pass_fast2(const PassCtx& c, const Walk& w0
   up2(a58, acc[5], acc[8]);
 }
 
+// Final ZNCC pass with the packed walk of icgn_pass_fast2: the same values as
+// pixel_pass<true, kFinal> (IEEE fma per lane, pixel_pass's bilinear rounding
+// order): acc = {sum g', sum g'^2, sum (f - fbar) g'}.
+__device__ __forceinline__ void final_pass_fast2(const PassCtx& c, const Walk& w0, float* acc, float& gmin,
+                                                 float& gmax) {
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+  gmin = 3.0e38f;
+  gmax = -3.0e38f;
+  const f2x uvl = pk2(c.ul, c.vl);
+  const f2x uxvx = pk2(c.ux, c.vx), uyvy = pk2(c.uy, c.vy);
+  const f2x step = pk2(w0.r32f, w0.q32f), wrap = pk2(-w0.sidef, 1.0f);
+  f2x dxy = pk2(w0.dxf, w0.dyf);
+  int roff = w0.roff;
+  const int cnt = w0.npl - (w0.last_valid ? 0 : 1);
+  const float* Tb = c.T + c.ioffy * c.tP + c.ioffx;
+#pragma unroll 2
+  for (int i = 0; i < cnt; ++i) {
+    float dx, dy;
+    up2(dxy, dx, dy);
+    f2x xy = add2(dxy, uvl);
+    xy = fma2(uxvx, pk2(dx, dx), xy);
+    xy = fma2(uyvy, pk2(dy, dy), xy);
+    float xl, yl;
+    up2(xy, xl, yl);
+    const float flx = floorf(xl), fly = floorf(yl);
+    const float fx = xl - flx, fy = yl - fly;
+    const float* t = Tb + (int)fly * c.tP + (int)flx;
+    const float f00 = t[0], f10 = t[1], f01 = t[c.tP], f11 = t[c.tP + 1];
+    const float a10 = f10 - f00, a01 = f01 - f00, a11 = (f00 + f11) - f10 - f01;
+    const float gv = fmaf(a11 * fx, fy, fmaf(a01, fy, fmaf(a10, fx, f00)));
+    gmin = fminf(gmin, gv);
+    gmax = fmaxf(gmax, gv);
+    const float gp = gv - c.fbar;
+    s0 += gp;
+    s1 = fmaf(gp, gp, s1);
+    s2 = fmaf(c.Rs[roff] - c.fbar, gp, s2);
+    dxy = add2(dxy, step);
+    roff += w0.roff_step;
+    float ndx, ndy;
+    up2(dxy, ndx, ndy);
+    if (ndx > w0.Mf) {
+      dxy = add2(dxy, wrap);
+      roff += w0.roff_wrap;
+    }
+  }
+  acc[0] = s0;
+  acc[1] = s1;
+  acc[2] = s2;
+}
+
 // NODE: the integer start (u, v integral, zero gradients) — every sample and
 // its bilinear gradient sit on a node: value t[0], gradient half the central
 // differences, exactly what the weighted forms give with weights (1, 0, 0, 0).
@@ -931,7 +981,9 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
     int bad = 0;
     float gmin, gmax;
     if (final_pass) {
-      if (fast)
+      if (fast && METHOD == 1)
+        final_pass_fast2(pc, wk, acc, gmin, gmax);
+      else if (fast)
         pixel_pass<true, kFinal, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
       else
         pixel_pass<false, kFinal, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
