@@ -177,9 +177,22 @@ def pipe_peaks() -> dict:
         return {"error": str(e)}
 
 
-def cpu_baseline(w, frames_host, n_sample_rows: int) -> dict:
+def sample_band(w, n_sample_rows: int) -> int:
+    """Frame rows holding exactly the first n_sample_rows grid rows, with every
+    search window of those rows inside the band (the full frame when the sample
+    is the whole grid)."""
+    cfg = w.cfg
+    margin = cfg.effective_margin()
+    h = w.frames[0].height
+    band = margin + cfg.grid.spacing * (n_sample_rows - 1) + margin + 1
+    return h if band >= h - cfg.grid.spacing else band
+
+
+def cpu_baseline(w, frames_host, n_sample_rows: int, pair_index: int = 0) -> tuple:
     """The reference's own analyze_pair (oracle/_ref) on all host cores, on a
-    bounded sample: the first n_sample_rows grid rows of pair (0, 1)."""
+    bounded sample: the first n_sample_rows grid rows of the first pair.
+    Returns (cpu_baseline dict, reference records, integer-only reference
+    records, the frame band) — the records feed the line's parity block."""
     import copy
 
     from oracle import Oracle, available
@@ -190,19 +203,92 @@ def cpu_baseline(w, frames_host, n_sample_rows: int) -> dict:
     cfg.mode = dic.ExecMode.subimage_parallel
     threads = os.cpu_count() or 1
     cfg.worker_count = threads
-    margin = cfg.effective_margin()
-    band = min(frames_host[0].shape[0], margin + cfg.grid.spacing * (n_sample_rows - 1) + margin + 1)
+    band = sample_band(w, n_sample_rows)
     a = frames_host[0][:band].astype(np.float64)
     b = frames_host[1][:band].astype(np.float64)
     if kind == "reference":
-        secs, n = orc.analyze_pair_timed(a, b, cfg, 0, 1)
+        secs, n, recs = orc.analyze_pair_timed(a, b, cfg, pair_index, 1, records=True)
     else:
         t0 = time.perf_counter()
-        n = len(orc.analyze_pair(a, b, cfg, 0, threads))
+        recs = orc.analyze_pair(a, b, cfg, pair_index, threads)
         secs = time.perf_counter() - t0
-    return {"value": n / secs, "unit": "subsets/s", "cores": threads, "kind": kind,
-            "sample": f"pair (0,1), first {n_sample_rows} grid rows ({n} POIs, frame band {band} px high), "
+        n = len(recs)
+    # the integer stage alone (untimed): the reference's records of a refined
+    # run carry only the refined u, v
+    icfg = copy.deepcopy(cfg)
+    icfg.subpixel_method = dic.SubpixelMethod.none
+    irecs = orc.analyze_pair(a, b, icfg, pair_index, threads)
+    base = {"value": n / secs, "unit": "subsets/s", "cores": threads, "kind": kind,
+            "sample": f"pair {pair_index}, first {n_sample_rows} grid rows ({n} POIs, frame band {band} px high), "
                       f"dic::analyze_pair subimage_parallel x{threads} threads, {secs:.2f} s"}
+    return base, recs, irecs, band
+
+
+def parity_block(got, exp, iexp) -> dict:
+    """Device records vs the reference's on the same inputs: integer stage
+    bit-exact (dx, dy, evaluations), convergence flags, and the sub-pixel
+    deviations on every POI the reference refined to convergence."""
+    out = {"pois": int(len(exp))}
+    if len(got) != len(exp):
+        out["error"] = f"record count {len(got)} vs {len(exp)}"
+        return out
+    same_xy = (got["x"] == exp["x"]) & (got["y"] == exp["y"])
+    found = iexp["evaluations"] > 0
+    int_mis = (~same_xy) | (got["evaluations"] != exp["evaluations"]) | \
+        (found & ((got["integer_dx"] != iexp["u"].astype(np.int64)) | (got["integer_dy"] != iexp["v"].astype(np.int64))))
+    ok = (exp["converged"] == 1) & found
+    du = np.abs(got["u"] - exp["u"])[ok]
+    dv = np.abs(got["v"] - exp["v"])[ok]
+    dz = np.abs(got["zncc"] - exp["zncc"])[ok]
+    out.update({
+        "integer_mismatches": int(int_mis.sum()),
+        "update_evaluation_mismatches": int((got["update_evaluations"] != exp["update_evaluations"]).sum()),
+        "converged_mismatches": int((got["converged"] != exp["converged"]).sum()),
+        "iteration_mismatches": int((got["iterations"][ok] != exp["iterations"][ok]).sum()),
+        "compared_subpixel": int(ok.sum()),
+        "max_du": float(du.max(initial=0.0)), "max_dv": float(dv.max(initial=0.0)),
+        "max_dzncc": float(dz.max(initial=0.0)),
+        "tolerances": {"uv_px": 1e-3, "zncc": 1e-5},
+    })
+    out["pass"] = bool(out["integer_mismatches"] == 0 and out["converged_mismatches"] == 0 and
+                       out["max_du"] < 1e-3 and out["max_dv"] < 1e-3 and out["max_dzncc"] < 1e-5)
+    return out
+
+
+SHIM_BIN = os.path.join(ROOT, "tools", "shim", "shim_bench")
+
+
+def run_shim_bench(frames, seq, cfg, esize: int, warmup: int, steps: int):
+    """e2e of the reference-facing C++ shim (tools/shim/shim_bench): the frames
+    as dic::GrayImage doubles, dic::b200::analyze_sequence with the reference's
+    image-parallel mode and one worker per host thread (as a reference caller
+    configures it), timed around the shim call only."""
+    import copy
+    import tempfile
+
+    if not os.path.exists(SHIM_BIN):
+        return {"unavailable": "tools/shim/shim_bench not built (needs the reference headers at build time)"}
+    f0 = frames[seq[0]]
+    h, w = f0.shape
+    c = copy.deepcopy(cfg)
+    c.mode = dic.ExecMode.image_parallel
+    c.worker_count = os.cpu_count() or 1
+    with tempfile.TemporaryDirectory() as td:
+        fpath, cpath = os.path.join(td, "frames.raw"), os.path.join(td, "config.bin")
+        with open(fpath, "wb") as fh:
+            fh.write(np.array([w, h, len(seq), esize], np.int32).tobytes())
+            for i in seq:
+                fh.write(frames[i].cpu().numpy().tobytes())
+        with open(cpath, "wb") as fh:
+            fh.write(bytes(c.to_c()))
+        r = subprocess.run([SHIM_BIN, fpath, cpath, str(warmup), str(steps)], capture_output=True, text=True,
+                           timeout=900)
+    if r.returncode != 0:
+        return {"unavailable": f"shim_bench rc={r.returncode}: {r.stderr.strip()[-300:]}"}
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    out["h2d_bytes_per_step"] = int(len(seq) * w * h * esize)
+    out["d2h_bytes_per_step"] = int(out["pois_per_step"] * C.sizeof(_abi.PoiRecordC))
+    return out
 
 
 # ------------------------------------------------------------ our arm
@@ -455,74 +541,24 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                "path": "dicb200_analyze_sequence (C-ABI), pinned host frames" if n_pairs > 1 else
                        "dicb200_analyze_pair (C-ABI), pinned host frames and records"}
 
+    # ---- e2e through the C++ drop-in shim (GrayImage doubles in) ----
+    e2e_shim = None
+    if not args.no_e2e and world == 1:
+        e2e_shim = run_shim_bench(frames, [needed[0]] + [b for _, b in my_pairs] if n_pairs > 1 else list(my_pairs[0]),
+                                  cfg, esize, max(1, min(args.warmup, 2)), max(1, min(args.steps, 3)))
+
     if rank != 0:
         return None
 
-    # ---- roofline of the dominant stage ----
+    # ---- rooflines: the search kernel and the refinement kernel; the line's
+    # `roofline` is the one with the longer isolated per-launch time (the
+    # dominant kernel of the step) ----
     names = ["bfs_zncc", "pso", "nr", "icgn", "tc_cross_terms", "tc_zncc", "bs_cross_terms"]
     stage = {names[i]: {"ms_total": float(stage_ms[i]), "launches": int(stage_n[i]),
                         "avg_ms": float(stage_ms[i]) / max(1, int(stage_n[i]))} for i in range(N_STAGES) if stage_n[i]}
-    top = {k: v for k, v in stage.items() if k in names[:4]}
-    dom = max(top, key=lambda k: top[k]["ms_total"]) if top else None
+    iso = {names[i]: float(iso_ms[i]) / int(iso_n[i]) for i in range(N_STAGES) if iso_n[i]}
     n_px = (2 * cfg.grid.half_width + 1) ** 2
     planes = 1 if u8 else 2
-    roof = None
-    if dom in ("bfs_zncc", "pso") and "tc_cross_terms" in stage:
-        # tensor-core search: algorithmic u8 x u8 MACs = sum(evaluations) x n x planes^2
-        # (a 16-bit product is 4 exact byte products), per launch of bfs_tc_kernel
-        st_tc = stage["tc_cross_terms"]
-        evals_launch = evals * args.steps / max(1, st_tc["launches"])  # evals: one step of my pairs
-        macs_per_launch = evals_launch * n_px * planes * planes
-        achieved = macs_per_launch / (st_tc["avg_ms"] * 1e-3) / 1e12
-        i8_peak = MEASURED_PEAKS.get("bf16_tflops", 0.0)  # dense i8 = 2x bf16 ops = bf16 TFLOP/s in TMAC/s
-        roof = {"kernel": "bfs_tc_kernel", "bound": "tensor", "pipe": "tcgen05.mma kind::i8 (u8 x u8 -> s32)",
-                "achieved": achieved, "peak": i8_peak, "unit": "TMAC/s (i8)",
-                "frac": achieved / i8_peak if i8_peak else None, "traffic": None,
-                "peak_source": MEASURED_PEAKS["source"] + " bf16_tflops (dense bf16 FLOP/s == dense i8 MAC/s on B200)",
-                "work_per_launch": f"sum(evaluations) x (2M+1)^2 x planes^2 = {macs_per_launch:.4g} i8 MACs",
-                "launch_ms": st_tc["avg_ms"]}
-    elif dom in ("bfs_zncc", "pso") and "bs_cross_terms" in stage:
-        roof = None  # block-sum search: reported below as roofline_search
-    elif dom == "bfs_zncc":
-        # algorithmic work per launch: (sum of evaluations over the launch's POIs) x n MACs
-        macs_per_launch = evals / max(1, len(my_pairs)) * n_px
-        achieved = macs_per_launch / (stage[dom]["avg_ms"] * 1e-3) / 1e12
-        if u8:
-            peak = 4 * peaks.get("idp4a_u8_Ginstr_per_s", 0) / 1e3
-            pipe = "IDP4A (u8 x4 MAC/instr)"
-        else:
-            peak = peaks.get("imad_Ginstr_per_s", 0) / 1e3
-            pipe = "IMAD (u16 exact u32 MAC/instr)"
-        roof = {"kernel": "bfs_tile_kernel", "bound": "alu", "pipe": pipe, "achieved": achieved,
-                "peak": peak, "unit": "TMAC/s", "frac": achieved / peak if peak else None,
-                "traffic": None,
-                "peak_source": "measured live by tools/microbench/pipes (dependent-free stream, CUDA events)",
-                "work_per_launch": f"sum(evaluations) x (2M+1)^2 = {macs_per_launch:.4g} MACs"}
-    elif dom in ("icgn", "nr"):
-        flop_px_it = 30.0 if dom == "icgn" else 100.0
-        flops = iters / max(1, len(my_pairs)) * n_px * flop_px_it
-        achieved = flops / (stage[dom]["avg_ms"] * 1e-3) / 1e12
-        peak = 2 * peaks.get("ffma_Ginstr_per_s", 0) / 1e3
-        roof = {"kernel": "refine_kernel", "bound": "alu", "pipe": "FFMA (fp32)", "achieved": achieved,
-                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": None,
-                "peak_source": "measured live by tools/microbench/pipes",
-                "work_per_launch": f"sum(iterations) x n x {flop_px_it:.0f} flop"}
-        # SURVEY 8(d) (ii): gathered-tap bytes against the staged tiles' shared-memory bandwidth
-        tap_b = 4 * 4 + (8 if dom == "icgn" else 8 * 4)  # 4 fp32 target taps (+ gradient / difference taps)
-        taps = iters / max(1, len(my_pairs)) * n_px * tap_b
-        tap_ach = taps / (stage[dom]["avg_ms"] * 1e-3) / 1e9
-        smem_peak = 128.0 * (torch.cuda.get_device_properties(dev).multi_processor_count) * 1.965e9 / 1e9
-        roof["taps"] = {"achieved": tap_ach, "peak": smem_peak, "unit": "GB/s", "frac": tap_ach / smem_peak,
-                        "work_per_launch": f"sum(iterations) x n x {tap_b} B gathered from shared memory",
-                        "peak_source": "128 B/clk/SM (32 banks x 4 B) x SMs x 1965 MHz max SM clock"}
-    elif dom == "pso":
-        macs_per_launch = evals / max(1, len(my_pairs)) * n_px
-        achieved = macs_per_launch / (stage[dom]["avg_ms"] * 1e-3) / 1e12
-        peak = 4 * peaks.get("idp4a_u8_Ginstr_per_s", 0) / 1e3
-        roof = {"kernel": "pso_kernel", "bound": "alu", "pipe": "IDP4A", "achieved": achieved, "peak": peak,
-                "unit": "TMAC/s", "frac": achieved / peak if peak else None, "traffic": None,
-                "peak_source": "measured live by tools/microbench/pipes",
-                "work_per_launch": f"sum(evaluations) x n = {macs_per_launch:.4g} MACs"}
     roof_search = None
     if "bs_cross_terms" in stage:
         # block-sum search (csrc/bfs_bs.cu): its algorithmic work is every
@@ -539,7 +575,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         achieved = macs_launch / (st_bs["avg_ms"] * 1e-3) / 1e12
         peak = peaks.get("imad_Ginstr_per_s", 0) / 1e3
         per_poi = evals * args.steps / max(1, st_bs["launches"]) * n_px / (st_bs["avg_ms"] * 1e-3) / 1e12
-        roof_search = {"kernel": "bs_kernel", "bound": "alu", "pipe": "IMAD (exact u32 products)",
+        roof_search = {"kernel": "bs_kernel", "stage": "bs_cross_terms", "bound": "alu",
+                       "pipe": "IMAD (exact u32 products)",
                        "achieved": achieved, "peak": peak, "unit": "TMAC/s", "frac": achieved / peak if peak else None,
                        "traffic": None, "launch_ms": st_bs["avg_ms"],
                        "peak_source": "measured live by tools/microbench/pipes (IMAD issue rate)",
@@ -547,25 +584,85 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                        "per_poi_equivalent_tmacs": per_poi,
                        "note": "the per-POI formulation (sum(evaluations) x n) would need per_poi_equivalent "
                                "TMAC/s of IMAD; the block partials are shared by the (L/s)^2 overlapping subsets"}
-        if roof is None:
-            roof = roof_search
-    iso = {names[i]: float(iso_ms[i]) / int(iso_n[i]) for i in range(N_STAGES) if iso_n[i]}
-    stage_of = {"bfs_tc_kernel": "tc_cross_terms", "bs_kernel": "bs_cross_terms", "refine_kernel": dom}
-    for rf in (roof, roof_search):
-        if rf and iso.get(stage_of.get(rf["kernel"])) and stage.get(stage_of.get(rf["kernel"])):
-            live = stage[stage_of[rf["kernel"]]]["avg_ms"]
+    elif "tc_cross_terms" in stage:
+        # tensor-core search: algorithmic u8 x u8 MACs = sum(evaluations) x n x planes^2
+        # (a 16-bit product is 4 exact byte products), per launch of bfs_tc_kernel
+        st_tc = stage["tc_cross_terms"]
+        evals_launch = evals * args.steps / max(1, st_tc["launches"])  # evals: one step of my pairs
+        macs_per_launch = evals_launch * n_px * planes * planes
+        achieved = macs_per_launch / (st_tc["avg_ms"] * 1e-3) / 1e12
+        i8_peak = MEASURED_PEAKS.get("bf16_tflops", 0.0)  # dense i8 = 2x bf16 ops = bf16 TFLOP/s in TMAC/s
+        roof_search = {"kernel": "bfs_tc_kernel", "stage": "tc_cross_terms", "bound": "tensor",
+                       "pipe": "tcgen05.mma kind::i8 (u8 x u8 -> s32)",
+                       "achieved": achieved, "peak": i8_peak, "unit": "TMAC/s (i8)",
+                       "frac": achieved / i8_peak if i8_peak else None, "traffic": None,
+                       "peak_source": MEASURED_PEAKS["source"] + " bf16_tflops (dense bf16 FLOP/s == dense i8 MAC/s on B200)",
+                       "work_per_launch": f"sum(evaluations) x (2M+1)^2 x planes^2 = {macs_per_launch:.4g} i8 MACs",
+                       "launch_ms": st_tc["avg_ms"]}
+    elif "bfs_zncc" in stage or "pso" in stage:
+        # CUDA-core tile kernel: (sum of evaluations over the launch's POIs) x n MACs
+        key = "bfs_zncc" if "bfs_zncc" in stage else "pso"
+        macs_per_launch = evals * args.steps / max(1, stage[key]["launches"]) * n_px
+        achieved = macs_per_launch / (stage[key]["avg_ms"] * 1e-3) / 1e12
+        if u8:
+            peak = 4 * peaks.get("idp4a_u8_Ginstr_per_s", 0) / 1e3
+            pipe = "IDP4A (u8 x4 MAC/instr)"
+        else:
+            peak = peaks.get("imad_Ginstr_per_s", 0) / 1e3
+            pipe = "IMAD (u16 exact u32 MAC/instr)"
+        roof_search = {"kernel": "bfs_tile_kernel", "stage": key, "bound": "alu", "pipe": pipe,
+                       "achieved": achieved, "peak": peak, "unit": "TMAC/s", "frac": achieved / peak if peak else None,
+                       "traffic": None, "launch_ms": stage[key]["avg_ms"],
+                       "peak_source": "measured live by tools/microbench/pipes (dependent-free stream, CUDA events)",
+                       "work_per_launch": f"sum(evaluations) x (2M+1)^2 = {macs_per_launch:.4g} MACs"}
+    roof_refine = None
+    ref_stage = "icgn" if "icgn" in stage else "nr" if "nr" in stage else None
+    if ref_stage:
+        st_r = stage[ref_stage]
+        flop_px_it = 30.0 if ref_stage == "icgn" else 100.0
+        iters_launch = iters * args.steps / max(1, st_r["launches"])
+        flops = iters_launch * n_px * flop_px_it
+        achieved = flops / (st_r["avg_ms"] * 1e-3) / 1e12
+        peak = 2 * peaks.get("ffma_Ginstr_per_s", 0) / 1e3
+        roof_refine = {"kernel": "refine_strip_kernel", "stage": ref_stage, "bound": "alu", "pipe": "FFMA (fp32)",
+                       "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+                       "traffic": None, "launch_ms": st_r["avg_ms"],
+                       "peak_source": "measured live by tools/microbench/pipes (2 flop per FFMA)",
+                       "work_per_launch": f"sum(iterations) x n x {flop_px_it:.0f} flop = {flops:.4g} flop "
+                                          f"({iters_launch:.0f} POI-iterations x {n_px} px)"}
+        # SURVEY 8(d) (ii): gathered-tap bytes against the staged tiles' shared-memory bandwidth
+        tap_b = 4 * 4 + (8 if ref_stage == "icgn" else 8 * 4)  # 4 fp32 target taps (+ gradient / difference taps)
+        taps = iters_launch * n_px * tap_b
+        tap_ach = taps / (st_r["avg_ms"] * 1e-3) / 1e9
+        smem_peak = 128.0 * (torch.cuda.get_device_properties(dev).multi_processor_count) * 1.965e9 / 1e9
+        roof_refine["taps"] = {"achieved": tap_ach, "peak": smem_peak, "unit": "GB/s", "frac": tap_ach / smem_peak,
+                               "work_per_launch": f"sum(iterations) x n x {tap_b} B gathered from shared memory",
+                               "peak_source": "128 B/clk/SM (32 banks x 4 B) x SMs x 1965 MHz max SM clock"}
+    for rf in (roof_search, roof_refine):
+        if rf and iso.get(rf["stage"]):
+            live = rf["launch_ms"]
             rf["launch_ms_live"] = live
-            rf["launch_ms_isolated"] = iso[stage_of[rf["kernel"]]]
+            rf["launch_ms_isolated"] = iso[rf["stage"]]
             rf["frac_isolated"] = rf["frac"] * live / rf["launch_ms_isolated"] if rf.get("frac") else None
+            rf["achieved_isolated"] = rf["achieved"] * live / rf["launch_ms_isolated"]
+
+    def launch_time(rf):
+        return rf.get("launch_ms_isolated", rf["launch_ms"]) if rf else -1.0
+
+    roof = max((r for r in (roof_search, roof_refine) if r), key=launch_time, default=None)
+    if roof is not None:
+        roof["selected_by"] = "longest isolated per-launch time of the search and refinement kernels"
     prof_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if roof and os.path.exists(prof_path):
+    if os.path.exists(prof_path):
         try:
-            tr = json.load(open(prof_path)).get(f"{args.config}:{roof['kernel']}")
-            if tr:
-                roof["traffic"] = tr["dram_bytes_per_launch"]
-                roof["traffic_source"] = tr.get("source")
+            traffic = json.load(open(prof_path))
         except Exception:  # noqa: BLE001
-            pass
+            traffic = {}
+        for rf in (roof_search, roof_refine):
+            tr = traffic.get(f"{args.config}:{rf['kernel']}") if rf else None
+            if tr:
+                rf["traffic"] = tr["dram_bytes_per_launch"]
+                rf["traffic_source"] = tr.get("source")
 
     total_subsets = (spp * n_pairs) if n_pairs > 1 else spp
     value = total_subsets * args.steps / (ms_max * 1e-3)
@@ -586,10 +683,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "data": "synthetic (seeded Gaussian-blob speckle, analytic re-render; BASELINE datasets absent)",
         "config": describe(w, spp, n_pairs, world),
         "e2e": e2e,
+        "e2e_shim": e2e_shim,
         "gpu_launches": launches,
         "stages": stage,
         "roofline": roof,
         "roofline_search": roof_search,
+        "roofline_refine": roof_refine,
         "step_ms": step_ms,
         "enqueue_ms": enqueue_ms,  # host time to enqueue each timed step (GPU starves when it exceeds step_ms)
         "stages_isolated": {k: {"avg_ms": v} for k, v in iso.items()},
@@ -600,7 +699,21 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if world == 1 and not args.no_cpu_baseline:
         host0 = [frames[my_pairs[0][0]].cpu().numpy().astype(np.uint16 if not u8 else np.uint8),
                  frames[my_pairs[0][1]].cpu().numpy().astype(np.uint16 if not u8 else np.uint8)]
-        line["cpu_baseline"] = cpu_baseline(w, host0, n_sample_rows=cpu_rows(args.config))
+        pidx = all_pairs.index(my_pairs[0])
+        base, exp, iexp, band = cpu_baseline(w, host0, cpu_rows(args.config), pidx)
+        line["cpu_baseline"] = base
+        # parity of the run: this library on the SAME inputs as the timed
+        # reference sample (the device-rendered frames, cropped to its band)
+        if band == f0.height and row_range[0] < 0:
+            got = recs[:recs_per_pair]  # the last timed step's own records of this pair
+            src = "records of the last timed step"
+        else:
+            got = dic.analyze_pair(dic.GrayImage(host0[0][:band]), dic.GrayImage(host0[1][:band], 1), cfg,
+                                   pidx).records
+            src = "dicb200_analyze_pair on the sample band"
+        line["parity"] = parity_block(got, exp, iexp)
+        line["parity"]["sample"] = base["sample"].split(", dic::")[0] + " (device-rendered frames, both sides)"
+        line["parity"]["device_records"] = src
     return line
 
 
@@ -611,13 +724,31 @@ def cpu_rows(name: str) -> int:
 
 # ------------------------------------------------------- reference arm
 
+def _loaded_libraries() -> list:
+    """Shared objects of this repository mapped into the process."""
+    libs = set()
+    try:
+        for ln in open("/proc/self/maps"):
+            path = ln.split()[-1] if ln.strip() else ""
+            if path.endswith(".so") and os.path.realpath(path).startswith(os.path.realpath(ROOT)):
+                libs.add(os.path.relpath(os.path.realpath(path), os.path.realpath(ROOT)))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
 def run_reference(args, rank: int, world: int):
-    """The reference's own CPU implementation (oracle/_ref) on host cores."""
+    """The reference's own CPU implementation (oracle/_ref: the reference's
+    sources compiled unmodified) on all host cores. This arm never loads the
+    product library: frames come from oracle/libdicsynth.so (the host
+    generator, bit-identical to the device renderer the other arm uses) and
+    the grid from the reference build itself."""
     if rank != 0:
         return None
     import copy
 
     from oracle import Oracle, available
+    from oracle.pyoracle import render_rows
 
     kind = "reference" if available("reference") else "port"
     orc = Oracle(kind)
@@ -627,28 +758,26 @@ def run_reference(args, rank: int, world: int):
     cfg.mode = dic.ExecMode.subimage_parallel
     threads = os.cpu_count() or 1
     cfg.worker_count = threads
-    rows = {"c1": 14, "c2": 24, "c3": 20, "c4": 12, "c5": 24}.get(args.config, 20)
-    margin = cfg.effective_margin()
-    band = min(w.frames[0].height, 2 * margin + cfg.grid.spacing * (rows - 1) + 1)
-    # frames rendered on the host for the reference (same generator, host build)
-    from dataclasses import replace
-
-    def render_band(spec):
-        return replace(spec, height=band).render()
-
-    ref0 = render_band(w.frames[0]).astype(np.float64)
-    targets = [w.frames[b] for _, b in w.pairs]
+    f0 = w.frames[0]
+    spp = len(orc.grid(f0.width, f0.height, cfg.grid.half_width, cfg.grid.spacing, cfg.effective_margin()))
+    rows = {"c1": 14, "c2": 46, "c3": 40, "c4": 40, "c5": 96}.get(args.config, 20)
+    band = sample_band(w, rows)
+    # the first `band` rows of the same frames the device arm renders (crop, not a re-render)
+    ref0 = render_rows(f0, 0, band).astype(np.float64)
     total_subsets, total_s = 0, 0.0
     for s in range(args.warmup + args.steps):
-        tgt = render_band(targets[s % len(targets)]).astype(np.float64)
-        secs, n = orc.analyze_pair_timed(ref0, tgt, cfg, s % max(1, n_pairs), 1)
+        a, b = w.pairs[s % n_pairs]
+        ra = ref0 if a == 0 else render_rows(w.frames[a], 0, band).astype(np.float64)
+        tgt = render_rows(w.frames[b], 0, band).astype(np.float64)
+        secs, n = orc.analyze_pair_timed(ra, tgt, cfg, s % n_pairs, 1)
         if s >= args.warmup:
             total_subsets += n
             total_s += secs
     value = total_subsets / total_s
-    spp = w.subsets_per_pair()
-    sample = (f"per step: pair (0,k) cropped to its first {rows} grid rows ({total_subsets // max(1, args.steps)} POIs), "
-              f"dic::analyze_pair subimage_parallel x{threads} threads (reference sources, Eigen stand-in)")
+    sample = (f"per step: pair k of the sequence cropped to its first {rows} grid rows "
+              f"({total_subsets // max(1, args.steps)} POIs, frame band {band} px), dic::analyze_pair "
+              f"subimage_parallel x{threads} threads (reference sources, Eigen stand-in); frames from "
+              f"oracle/libdicsynth.so (bit-identical to the device renderer)")
     return {
         "impl": "reference",
         "metric": "subsets/sec (search+refine) and frame pairs/sec at 1/2/4/8 B200 vs roofline",
@@ -667,6 +796,7 @@ def run_reference(args, rank: int, world: int):
         "config": describe(w, spp, n_pairs, world),
         "cpu_baseline": {"value": value, "unit": "subsets/s", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "subsets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "native_libs_loaded": _loaded_libraries(),
     }
 
 

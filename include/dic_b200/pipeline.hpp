@@ -12,12 +12,17 @@
 // per-POI failure semantics). Pair-level failures throw dic::Error with the
 // reference's message. GrayImage values must be integers in [0, 65535]
 // (every 8/16-bit camera frame is) or fractional levels in [0, 255], which are
-// carried as 8.8 fixed point (see detail::pack); anything else throws dic::Error.
+// carried as 8.8 fixed point (see detail::Frames); anything else throws dic::Error.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "dic/error.hpp"
@@ -53,60 +58,118 @@ inline dicb200_run_config to_c(const RunConfig& c) {
   return r;
 }
 
-// GrayImage (doubles) -> packed u8/u16 + descriptor. Integer gray levels in
-// [0, 65535] map losslessly. Non-integer levels in [0, 255] (e.g. the
-// reference's synth_speckle / synth_warped_pair frames) are carried with 8
-// fractional bits: u16 = round(256 v). ZNCC, the IC-GN / NR steps and every
-// decision derived from them are invariant to a positive gray-level scale, so
-// only the 2^-9 quantisation of each sample separates the result from the
-// reference's doubles. Anything else (negative, > 65535, fractional above
-// 255, non-finite) throws dic::Error.
-struct Packed {
-  std::vector<uint8_t> u8;
-  std::vector<uint16_t> u16;
-  dicb200_image img{};
+// Pinned host blocks reused across calls (cudaMallocHost is slow; frames are
+// uploaded asynchronously from pinned memory). Grow-only, process lifetime.
+class PinnedPool {
+ public:
+  static PinnedPool& get() {
+    static PinnedPool pool;
+    return pool;
+  }
+  // `count` blocks of at least `bytes` each, held until release()
+  std::vector<void*> take(size_t count, size_t bytes) {
+    std::lock_guard<std::mutex> lk(mu_);
+    std::vector<void*> out;
+    for (auto it = free_.begin(); it != free_.end() && out.size() < count;) {
+      if (it->second >= bytes) {
+        out.push_back(it->first);
+        cap_[it->first] = it->second;
+        it = free_.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    while (out.size() < count) {
+      void* p = dicb200_host_alloc(bytes);
+      if (!p) {
+        for (void* q : out) free_.emplace_back(q, cap_[q]);
+        throw std::runtime_error("dicb200: pinned host allocation failed");
+      }
+      cap_[p] = bytes;
+      out.push_back(p);
+    }
+    return out;
+  }
+  void release(const std::vector<void*>& blocks) {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (void* p : blocks) free_.emplace_back(p, cap_[p]);
+  }
+
+ private:
+  std::mutex mu_;
+  std::vector<std::pair<void*, size_t>> free_;
+  std::map<void*, size_t> cap_;
 };
 
-inline bool is_integral(const GrayImage& g) {
-  for (double v : g.pixels())
-    if (v != std::floor(v)) return false;
-  return true;
-}
+// GrayImages (doubles) -> device gray levels, one multithreaded pass per frame
+// (dicb200_pack_gray). Integer levels in [0, 65535] map losslessly; when every
+// level of every frame is <= 255 they travel as u8 (narrowed in place). A frame
+// with non-integral levels in [0, 255] (e.g. the reference's synth_speckle /
+// synth_warped_pair frames) is carried with 8 fractional bits, u16 = lround(256 v):
+// ZNCC, the IC-GN / NR steps and every decision derived from them are invariant
+// to a positive gray-level scale of either frame, so only the 2^-9 quantisation
+// of each sample separates the result from the reference's doubles. Anything
+// else (negative, > 65535, fractional above 255, non-finite) throws dic::Error.
+class Frames {
+ public:
+  explicit Frames(const std::vector<const GrayImage*>& images) : pool_(PinnedPool::get()) {
+    const size_t n = images.size();
+    size_t px = 0;
+    for (const GrayImage* g : images) px = std::max(px, static_cast<size_t>(g->width()) * g->height());
+    blocks_ = pool_.take(n, std::max<size_t>(px * 2, 16));
+    imgs_.resize(n);
+    int maxv = 0;
+    bool any_frac = false;
+    for (size_t i = 0; i < n; ++i) {
+      const GrayImage& g = *images[i];
+      dicb200_image& im = imgs_[i];
+      im.width = g.width();
+      im.height = g.height();
+      im.pitch = g.width();
+      im.id = g.id();
+      im.dtype = DICB200_U16;
+      im.data = blocks_[i];
+      uint16_t* dst = static_cast<uint16_t*>(blocks_[i]);
+      int32_t frac = 0, mx = 0;
+      dicb200_status st = dicb200_pack_gray(g.pixels().data(), g.width(), g.height(), g.width(), 1, dst, &frac,
+                                            &mx, 0);
+      if (st == DICB200_OK && frac)
+        st = dicb200_pack_gray(g.pixels().data(), g.width(), g.height(), g.width(), 256, dst, nullptr, &mx, 0);
+      if (st != DICB200_OK) {
+        pool_.release(blocks_);
+        throw Error(frac ? "dicb200: fractional gray levels must lie in [0, 255]" : dicb200_last_error_message());
+      }
+      any_frac = any_frac || frac;
+      im.bits = frac ? 16 : 1;
+      while (!frac && im.bits < 16 && (1 << im.bits) - 1 < mx) ++im.bits;
+      maxv = std::max(maxv, frac ? 65535 : mx);
+    }
+    if (!any_frac && maxv <= 255) {  // every frame 8-bit: u8 (one byte plane on the device)
+      for (dicb200_image& im : imgs_) {
+        const uint16_t* s16 = static_cast<const uint16_t*>(im.data);
+        uint8_t* d8 = static_cast<uint8_t*>(const_cast<void*>(im.data));
+        const size_t m = static_cast<size_t>(im.width) * im.height;
+        for (size_t k = 0; k < m; ++k) d8[k] = static_cast<uint8_t>(s16[k]);  // in place, front to back
+        im.dtype = DICB200_U8;
+        im.bits = 8;
+      }
+    } else {  // one dtype for all frames (the C-ABI's rule); bits = the widest frame's
+      int bits = 1;
+      for (const dicb200_image& im : imgs_) bits = std::max(bits, static_cast<int>(im.bits));
+      for (dicb200_image& im : imgs_) im.bits = bits;
+    }
+  }
+  ~Frames() { pool_.release(blocks_); }
+  Frames(const Frames&) = delete;
+  Frames& operator=(const Frames&) = delete;
+  const dicb200_image* data() const { return imgs_.data(); }
+  const dicb200_image& operator[](size_t i) const { return imgs_[i]; }
 
-inline void pack(const GrayImage& g, Packed& out, bool force16) {
-  const auto& px = g.pixels();
-  const bool frac = !is_integral(g);
-  double mx = 0.0;
-  for (double v : px) {
-    if (!(v >= 0.0) || v > (frac ? 255.0 : 65535.0))
-      throw Error(frac ? "dicb200: fractional gray levels must lie in [0, 255]"
-                       : "dicb200: gray levels must be integers in [0, 65535]");
-    mx = v > mx ? v : mx;
-  }
-  out.img.width = g.width();
-  out.img.height = g.height();
-  out.img.pitch = g.width();
-  out.img.id = g.id();
-  if (frac) {
-    out.u16.resize(px.size());
-    for (size_t i = 0; i < px.size(); ++i) out.u16[i] = static_cast<uint16_t>(std::lround(px[i] * 256.0));
-    out.img.dtype = DICB200_U16;
-    out.img.bits = 16;
-    out.img.data = out.u16.data();
-  } else if (mx <= 255.0 && !force16) {
-    out.u8.assign(px.begin(), px.end());
-    out.img.dtype = DICB200_U8;
-    out.img.bits = 8;
-    out.img.data = out.u8.data();
-  } else {
-    out.u16.assign(px.begin(), px.end());
-    out.img.dtype = DICB200_U16;
-    int bits = 1;
-    while (bits < 16 && (1 << bits) - 1 < mx) ++bits;
-    out.img.bits = bits;
-    out.img.data = out.u16.data();
-  }
-}
+ private:
+  PinnedPool& pool_;
+  std::vector<void*> blocks_;
+  std::vector<dicb200_image> imgs_;
+};
 
 inline PoiRecord to_record(const dicb200_poi_record& r) {
   PoiRecord o;
@@ -122,10 +185,9 @@ inline PoiRecord to_record(const dicb200_poi_record& r) {
   return o;
 }
 
-inline bool max_is_u8(const GrayImage& g) {
-  for (double v : g.pixels())
-    if (v > 255.0) return false;
-  return is_integral(g);  // fractional frames travel as 8.8 fixed point (u16)
+[[noreturn]] inline void raise(dicb200_status st) {
+  if (st == DICB200_ERR_INVALID) throw Error(dicb200_last_error_message());
+  throw std::runtime_error(dicb200_last_error_message());
 }
 
 }  // namespace detail
@@ -134,19 +196,14 @@ inline DisplacementField analyze_pair(const GrayImage& reference, const GrayImag
                                       const RunConfig& cfg, std::uint64_t pair_index = 0) {
   if (reference.width() != target.width() || reference.height() != target.height())
     throw Error("dimension mismatch");
-  const bool wide = !detail::max_is_u8(reference) || !detail::max_is_u8(target);
-  detail::Packed a, b;
-  detail::pack(reference, a, wide);
-  detail::pack(target, b, wide);
-  a.img.bits = b.img.bits = std::max(a.img.bits, b.img.bits);
   const dicb200_run_config c = detail::to_c(cfg);
   size_t n = 0;
   dicb200_status st = dicb200_grid_size(reference.width(), reference.height(), &c, &n);
-  if (st != DICB200_OK) throw Error(dicb200_last_error_message());
+  if (st != DICB200_OK) detail::raise(st);
+  const detail::Frames fr({&reference, &target});
   std::vector<dicb200_poi_record> recs(n);
-  st = dicb200_analyze_pair(&a.img, &b.img, &c, pair_index, recs.data(), recs.size(), &n);
-  if (st == DICB200_ERR_INVALID) throw Error(dicb200_last_error_message());
-  if (st != DICB200_OK) throw std::runtime_error(dicb200_last_error_message());
+  st = dicb200_analyze_pair(&fr[0], &fr[1], &c, pair_index, recs.data(), recs.size(), &n);
+  if (st != DICB200_OK) detail::raise(st);
   DisplacementField f;
   f.pair_index = static_cast<int>(pair_index);
   f.ref_id = reference.id();
@@ -156,21 +213,45 @@ inline DisplacementField analyze_pair(const GrayImage& reference, const GrayImag
   return f;
 }
 
-// pipeline.cpp:182-214 semantics: per-pair dic::Error -> field.error, fields in pair order.
+// pipeline.cpp:182-214 semantics: pairs from sequence_pairs(cfg.reference_policy),
+// one dicb200_analyze_sequence call (pipelined uploads / compute / read-back;
+// cfg.mode == image_parallel shards contiguous pair chunks over
+// min(worker_count, devices) devices, as the reference shards them over
+// worker threads). Per-pair dic::Error -> field.error, fields in pair order.
 inline std::vector<DisplacementField> analyze_sequence(const std::vector<GrayImage>& images,
                                                        const RunConfig& cfg) {
   const auto pairs = sequence_pairs(cfg.reference_policy, static_cast<int>(images.size()));
+  const dicb200_run_config c = detail::to_c(cfg);
+  // frames of one size pack together; a frame of another size fails its pairs
+  // with the reference's message (analyze_pair, pipeline.cpp:150-151)
+  std::vector<const GrayImage*> ptrs;
+  for (const GrayImage& g : images) ptrs.push_back(&g);
+  const detail::Frames fr(ptrs);
+  std::vector<std::vector<dicb200_poi_record>> recs(pairs.size());
+  std::vector<dicb200_field> cf(pairs.size());
+  for (size_t i = 0; i < pairs.size(); ++i) {
+    size_t n = 0;
+    const GrayImage& a = images[pairs[i].first];
+    if (dicb200_grid_size(a.width(), a.height(), &c, &n) != DICB200_OK) n = 0;
+    recs[i].resize(std::max<size_t>(n, 1));
+    cf[i] = dicb200_field{};
+    cf[i].records = recs[i].data();
+    cf[i].capacity = n;
+  }
+  const dicb200_status st = dicb200_analyze_sequence(fr.data(), images.size(), &c, cf.data(), cf.size());
+  if (st != DICB200_OK) detail::raise(st);
   std::vector<DisplacementField> fields(pairs.size());
   for (size_t i = 0; i < pairs.size(); ++i) {
-    const auto& [a, b] = pairs[i];
-    try {
-      fields[i] = b200::analyze_pair(images[a], images[b], cfg, i);
-    } catch (const Error& e) {
-      fields[i].pair_index = static_cast<int>(i);
-      fields[i].ref_id = images[a].id();
-      fields[i].tgt_id = images[b].id();
-      fields[i].error = e.what();
+    DisplacementField& f = fields[i];
+    f.pair_index = static_cast<int>(i);
+    f.ref_id = images[pairs[i].first].id();
+    f.tgt_id = images[pairs[i].second].id();
+    if (cf[i].status != DICB200_OK) {
+      f.error = cf[i].error;
+      continue;
     }
+    f.records.reserve(cf[i].count);
+    for (size_t k = 0; k < cf[i].count; ++k) f.records.push_back(detail::to_record(recs[i][k]));
   }
   return fields;
 }

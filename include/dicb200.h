@@ -243,6 +243,20 @@ dicb200_status dicb200_load_pgm(const char* path, int32_t flags, int32_t* width,
 dicb200_status dicb200_save_pgm(const char* path, const dicb200_image* img);
 dicb200_status dicb200_sequence_files(const char* dir, const char* pattern, char* buf, size_t cap, size_t* needed,
                                       size_t* count);
+/* GrayImage (row-major doubles, src_pitch elements per row; 0 = width) ->
+ * the device path's gray levels in dst (width*height u16, packed rows), one
+ * multithreaded pass (threads <= 0: all cores). Replaces the reference's
+ * image storage (image.hpp:14-31) at the drop-in boundary, used by the C++
+ * shim include/dic_b200/pipeline.hpp.
+ *   scale 1:   integral levels in [0, 65535], stored losslessly. A
+ *              non-integral level sets *fractional (dst is then not usable:
+ *              pack again with scale 256).
+ *   scale 256: levels in [0, 255] as 8.8 fixed point, lround(256 v).
+ * *max_level = largest stored value. Out-of-range or non-finite levels:
+ * DICB200_ERR_INVALID with the shim's dic::Error message. */
+dicb200_status dicb200_pack_gray(const double* src, int32_t width, int32_t height, int32_t src_pitch,
+                                 int32_t scale, uint16_t* dst, int32_t* fractional, int32_t* max_level,
+                                 int32_t threads);
 void* dicb200_host_alloc(size_t bytes); /* pinned host memory (NULL on failure) */
 void dicb200_host_free(void* p);
 

@@ -40,8 +40,14 @@ typedef struct {
 /* Renders one frame into out (pitch in elements). threads <= 0: all cores. */
 int dicb200_synth_render(const dicb200_synth_spec* spec, void* out, int32_t pitch, int32_t threads);
 
+/* Rows [row_begin, row_end) of the same frame into out (out's row 0 = frame
+ * row row_begin): identical pixels to the corresponding rows of a full render. */
+int dicb200_synth_render_rows(const dicb200_synth_spec* spec, void* out, int32_t pitch, int32_t row_begin,
+                              int32_t row_end, int32_t threads);
+
 /* Same frame rendered on the GPU into device memory (pitch in elements);
- * stream is a cudaStream_t (NULL = legacy default). Synchronous. */
+ * stream is a cudaStream_t (NULL = legacy default). Synchronous. Bit-identical
+ * to dicb200_synth_render (shared per-pixel code, synth_math.h). */
 int dicb200_synth_render_device(const dicb200_synth_spec* spec, void* out_dev, int32_t pitch, void* stream);
 
 /* Displacement d(y) at a reference-frame point (ground truth helper). */

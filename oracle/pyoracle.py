@@ -92,7 +92,7 @@ class Oracle:
             ]
             f("analyze_pair_timed").argtypes = [
                 C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(_abi.RunConfigC), C.c_uint64, C.c_int,
-                C.POINTER(C.c_double), C.POINTER(C.c_size_t), C.c_char_p, C.c_size_t,
+                C.POINTER(C.c_double), C.POINTER(C.c_size_t), C.c_void_p, C.c_size_t, C.c_char_p, C.c_size_t,
             ]
             f("analyze_sequence").argtypes = [
                 C.c_void_p, C.c_size_t, C.c_int, C.c_int, C.POINTER(_abi.RunConfigC), C.POINTER(_abi.FieldC),
@@ -151,17 +151,25 @@ class Oracle:
             raise OracleError(err.value.decode())
         return out[: n.value]
 
-    def analyze_pair_timed(self, ref, tgt, cfg, pair_index=0, repeats=1) -> Tuple[float, int]:
-        """Reference build only: seconds (best of repeats) of dic::analyze_pair alone."""
+    def analyze_pair_timed(self, ref, tgt, cfg, pair_index=0, repeats=1, records: bool = False):
+        """Reference build only: seconds (best of repeats) of dic::analyze_pair
+        alone, the POI count and (records=True) the last repeat's records."""
         a, b = _as_double(ref), _as_double(tgt)
         h, w = a.shape
         c = cfg.to_c()
         s = C.c_double(0)
         n = C.c_size_t(0)
         err = C.create_string_buffer(160)
+        out, cap = None, 0
+        if records:
+            cap = len(self.grid(w, h, cfg.grid.half_width, cfg.grid.spacing, cfg.effective_margin()))
+            out = np.zeros(cap, dtype=_abi.record_dtype())
         if self._f("analyze_pair_timed")(a.ctypes.data, b.ctypes.data, w, h, C.byref(c), pair_index, repeats,
-                                         C.byref(s), C.byref(n), err, 160):
+                                         C.byref(s), C.byref(n), out.ctypes.data if records else None, cap,
+                                         err, 160):
             raise OracleError(err.value.decode())
+        if records:
+            return s.value, n.value, out[: n.value]
         return s.value, n.value
 
     # -- per-subset pins ---------------------------------------------------
@@ -271,3 +279,23 @@ def ref_accuracy_sweep(combos, cfg):
                                         C.byref(el), err, 160):
         raise OracleError(err.value.decode())
     return list(out), wc.value, pc.value, el.value
+
+
+# -- synthetic frames without the product library (bench reference arm) -------
+PATHS_SYNTH = os.path.join(HERE, "libdicsynth.so")
+
+
+def render_rows(spec, row_begin: int = 0, row_end: Optional[int] = None, threads: int = 0) -> np.ndarray:
+    """Rows [row_begin, row_end) of a configs.FrameSpec frame rendered by
+    oracle/libdicsynth.so (the host generator synth.c built on its own): the
+    same pixels as FrameSpec.render() / the device renderer, without loading
+    libdicb200.so into the calling process."""
+    L = C.CDLL(PATHS_SYNTH)
+    L.dicb200_synth_render_rows.argtypes = [C.POINTER(_abi.SynthSpecC), C.c_void_p, C.c_int32, C.c_int32,
+                                            C.c_int32, C.c_int32]
+    if row_end is None:
+        row_end = spec.height
+    out = np.zeros((row_end - row_begin, spec.width), np.uint8 if spec.dtype == _abi.U8 else np.uint16)
+    if L.dicb200_synth_render_rows(C.byref(spec.to_c()), out.ctypes.data, spec.width, row_begin, row_end, threads):
+        raise OracleError("synth_render_rows failed")
+    return out

@@ -93,9 +93,12 @@ int dicref_analyze_pair(const double* ref, const double* tgt, int w, int h,
 
 // Timed variant for the CPU baseline: images are wrapped once; only
 // analyze_pair runs between the two steady_clock reads (bench.cpp:36-48 style).
+// `out` (optional, capacity `cap`) receives the last repeat's records, so the
+// bench can check its own device records against the timed reference run.
 int dicref_analyze_pair_timed(const double* ref, const double* tgt, int w, int h,
                               const dicb200_run_config* cfg, uint64_t pair_index, int repeats,
-                              double* seconds_out, size_t* count, char* err, size_t errcap) {
+                              double* seconds_out, size_t* count, dicb200_poi_record* out, size_t cap,
+                              char* err, size_t errcap) {
   try {
     const dic::GrayImage a = make_image(ref, w, h, 0), b = make_image(tgt, w, h, 1);
     const dic::RunConfig rc = to_run_config(*cfg);
@@ -107,6 +110,8 @@ int dicref_analyze_pair_timed(const double* ref, const double* tgt, int w, int h
       *count = f.records.size();
       const double s = std::chrono::duration<double>(t1 - t0).count();
       if (s < best) best = s;
+      if (out && r == repeats - 1)
+        for (size_t i = 0; i < f.records.size() && i < cap; ++i) to_record(f.records[i], out[i]);
     }
     *seconds_out = best;
     return 0;

@@ -97,6 +97,56 @@ int main() {
       bad += !ok;
     }
   }
+  // sequences: both reference policies, serial and image-parallel modes, one
+  // frame of the wrong size (its pairs fail with the reference's message, the
+  // sequence continues: pipeline.cpp:182-214)
+  {
+    std::vector<dic::GrayImage> seq;
+    for (int k = 0; k < 5; ++k) {
+      std::vector<uint8_t> px(W * H);
+      sp.field = k == 0 ? DICB200_FIELD_NONE : DICB200_FIELD_AFFINE;
+      sp.a[0] = 0.7 * k;
+      sp.a[3] = -0.45 * k;
+      sp.a[1] = 0.001 * k;
+      dicb200_synth_render(&sp, px.data(), W, 1);
+      seq.emplace_back(W, H, std::vector<double>(px.begin(), px.end()), k);
+    }
+    seq[3] = dic::GrayImage(W - 8, H, std::vector<double>((W - 8) * H, 7.0), 3);
+    for (int policy = 0; policy < 2; ++policy)
+      for (int mode = 0; mode < 2; ++mode) {
+        dic::RunConfig cfg;
+        cfg.integer_method = dic::IntegerMethod::bfs;
+        cfg.subpixel_method = dic::SubpixelMethod::icgn;
+        cfg.search.bfs_domain = dic::BfsDomain::window;
+        cfg.search.search_radius = 8;
+        cfg.grid.half_width = 10;
+        cfg.grid.spacing = 12;
+        cfg.refine.tol = 1e-4;
+        cfg.reference_policy = policy ? dic::ReferencePolicy::update_every_pair : dic::ReferencePolicy::fixed_first;
+        cfg.mode = mode ? dic::ExecMode::image_parallel : dic::ExecMode::serial;
+        cfg.worker_count = mode ? 2 : 1;
+        const auto ref = dic::analyze_sequence(seq, cfg);
+        const auto got = dic::b200::analyze_sequence(seq, cfg);
+        int mism = 0, errs = 0;
+        double du = 0.0;
+        bool ok = ref.size() == got.size();
+        for (size_t i = 0; ok && i < ref.size(); ++i) {
+          const auto &rf = ref[i], &gf = got[i];
+          ok = ok && rf.pair_index == gf.pair_index && rf.ref_id == gf.ref_id && rf.tgt_id == gf.tgt_id &&
+               rf.error == gf.error && rf.records.size() == gf.records.size();
+          errs += !rf.error.empty();
+          for (size_t k = 0; ok && k < rf.records.size(); ++k) {
+            const auto &r = rf.records[k], &g = gf.records[k];
+            if (r.x != g.x || r.y != g.y || r.evaluations != g.evaluations || r.converged != g.converged) ++mism;
+            if (r.converged) du = std::fmax(du, std::fmax(std::fabs(r.u - g.u), std::fabs(r.v - g.v)));
+          }
+        }
+        ok = ok && mism == 0 && du < 1e-3 && errs > 0;
+        std::printf("sequence policy %d mode %d: %zu fields (%d pair errors), integer mismatches %d, "
+                    "max |du|,|dv| %.3g -> %s\n", policy, mode, ref.size(), errs, mism, du, ok ? "ok" : "FAIL");
+        bad += !ok;
+      }
+  }
   try {
     dic::GrayImage small(W, H - 1, std::vector<double>(W * (H - 1), 0.0));
     dic::b200::analyze_pair(ga, small, dic::RunConfig{});

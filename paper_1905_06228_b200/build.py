@@ -43,7 +43,7 @@ def build_library(verbose: bool = False, force: bool = False) -> str:
         objs.append(obj)
     for src in C_SOURCES:
         obj = os.path.join(objdir, src + ".o")
-        cmd = ["gcc", "-std=c11", "-O2", "-fPIC", "-I", inc, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = ["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fPIC", "-I", inc, "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
         objs.append(obj)
     failed = False

@@ -110,6 +110,8 @@ struct TcRefCache {
   long key = -1;
   const void* data = nullptr;
   int W = 0, H = 0, M = 0, x0 = 0, y0 = 0, step = 0, nx = 0, rb = 0, re = 0;
+  int planes = 0;
+  bool use_bs = false;  // built for the block-sum kernel (no strip images)
   void reset() { key = -1; }
 };
 

@@ -887,8 +887,11 @@ __device__ __forceinline__ float approx_zncc(int64_t num, float rsvf, float rsq)
 // with rsq the fp32 reciprocal of sqrt(vg) (approx_zncc: absolute error
 // < 2^-21.6 as |zncc| <= 1); the EXACT IEEE quotient num / (sqrt(vf) sqrt(vg)) is
 // formed only for candidates within 2^-19 of it (a second pass when more than one per lane
-// qualifies), so the winner and its value are exactly those of the sequential
-// reference loop. Warp per POI, lanes across the window candidates.
+// qualifies): the exact argmax, in improves() order, of the correlation formed
+// from exact integer moments. The reference accumulates centred doubles with
+// rounding, so its values differ from these in the last bits and the two can
+// only disagree at ties closer than that (sub-ulp). Warp per POI, lanes across
+// the window candidates.
 __global__ void __launch_bounds__(256) tc_argmax_kernel(TcParams p, int sp) {
   extern __shared__ __align__(16) unsigned char pos_smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1192,12 +1195,19 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
   const size_t sbytes = (size_t)std::max(1, p.SW) * std::max(1, p.SH);
   p.strip_h = ((p.ref.height + 63) / 64) * 64;
   const size_t strip_bytes = (size_t)p.planes * 8 * p.ref.width * p.strip_h;
+  // Block-sum or tensor-core search: decided per pair from the pair's pixel range
+  // (p.maxv), so a reference frame cached for one kernel may be reused by the
+  // other — the cache key includes the choice (only the tensor kernel needs the
+  // strip images).
+  BsGeom bsg{};
+  const bool use_bs = bs_plan(p, bsg);
   // reference-side inputs: from the cache when this reference frame's were built already
   bool ref_ready = false;
   if (cache && ref_key >= 0) {
     ref_ready = cache->key == ref_key && cache->data == p.ref.data && cache->W == p.ref.width &&
                 cache->H == p.ref.height && cache->M == p.M && cache->x0 == p.lat.x0 && cache->y0 == p.lat.y0 &&
-                cache->step == p.lat.step && cache->nx == p.lat.nx && cache->rb == p.rb && cache->re == p.re;
+                cache->step == p.lat.step && cache->nx == p.lat.nx && cache->rb == p.rb && cache->re == p.re &&
+                cache->planes == p.planes && cache->use_bs == use_bs;
     if (!ref_ready) {
       cache->key = -1;
       e = grow(cache->strips, cache->strips_cap, strip_bytes, st);
@@ -1268,8 +1278,6 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
   host_trace("tc stats");
   // (b) reference moments + strip images (skipped when cached; the block-sum
   //     kernel reads the reference directly and needs no strips)
-  BsGeom bsg{};
-  const bool use_bs = bs_plan(p, bsg);
   if (e == cudaSuccess && !ref_ready) {
     if (!use_bs) {
       dim3 sg((p.ref.width + 31) / 32, p.strip_h / 64);
@@ -1304,6 +1312,8 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
       cache->nx = p.lat.nx;
       cache->rb = p.rb;
       cache->re = p.re;
+      cache->planes = p.planes;
+      cache->use_bs = use_bs;
     }
   }
   host_trace("tc prep");

@@ -888,7 +888,15 @@ dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_im
   dicb200_sequence_pairs(cfg->reference_policy, (int32_t)n_images, pairs.data());
   int ndev = dicb200_device_count();
   int workers = 1;
-  if (cfg->mode == DICB200_MODE_IMAGE) workers = cfg->worker_count <= 0 ? ndev : std::min(cfg->worker_count, ndev);
+  if (cfg->mode == DICB200_MODE_IMAGE) {
+    // the reference's worker threads (pipeline.cpp:201-209) become devices; each
+    // worker already keeps two pairs in flight on its device.
+    // DICB200_WORKERS_PER_DEVICE (default 1) lets several workers share a device
+    // (worker w runs on device w % ndev).
+    const char* wpd = std::getenv("DICB200_WORKERS_PER_DEVICE");
+    const int slots = ndev * std::max(1, wpd ? std::atoi(wpd) : 1);
+    workers = cfg->worker_count <= 0 ? slots : std::min(cfg->worker_count, slots);
+  }
   workers = std::max(1, std::min<int>(workers, (int)n_fields));
   std::vector<size_t> ranges(2 * workers);
   dicb200_partition_ranges(n_fields, workers, ranges.data());
@@ -905,7 +913,7 @@ dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_im
   // pair's frames are uploaded while the current pair computes, and the host
   // finalises pair i-1 while the device runs pair i.
   auto run = [&](int wk) {
-    const int dev = workers == 1 ? cur : wk;
+    const int dev = workers == 1 ? cur : wk % ndev;
     cudaSetDevice(dev);
     auto fail_field = [&](dicb200_field& f, dicb200_status s) {
       f.count = 0;
@@ -981,14 +989,20 @@ dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_im
         if (e == cudaSuccess) e = cudaStreamWaitEvent(cst, c->frames[sb].ready, 0);
         if (e != cudaSuccess) s = cuda_fail(e, "compute stream setup", __FILE__, __LINE__);
       }
+      const bool staged_ok = s == DICB200_OK;
       if (s == DICB200_OK)
         s = enqueue_pair(&c->frames[sa].im, &c->frames[sb].im, cfg, i, lat[i - lo], 0, lat[i - lo].ny,
                          (dicb200_poi_record*)r.dev.p, cst, k ? &c->tcache2 : &c->tcache, (long)pairs[2 * i],
                          cfg->reference_policy == DICB200_POLICY_FIXED_FIRST ? (k ? &c->icache2 : &c->icache)
                                                                              : nullptr);
-      if (s == DICB200_OK) {
+      if (staged_ok) {
+        // the frames' last reader is this stream, also when enqueue_pair failed
+        // after queueing some kernels: a later upload into either slot waits for them
         e = cudaEventRecord(k ? c->frames[sa].idle2 : c->frames[sa].idle, cst);
         if (e == cudaSuccess) e = cudaEventRecord(k ? c->frames[sb].idle2 : c->frames[sb].idle, cst);
+        if (e != cudaSuccess && s == DICB200_OK) s = cuda_fail(e, "frame idle event", __FILE__, __LINE__);
+      }
+      if (s == DICB200_OK) {
         r.staged = !is_pinned(f.records);
         void* dst = f.records;
         if (e == cudaSuccess && r.staged) {

@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -177,6 +178,70 @@ dicb200_status dicb200_sequence_files(const char* dir, const char* pattern, char
     std::memcpy(buf, s.c_str(), s.size() + 1);
     buf += s.size() + 1;
   }
+  return DICB200_OK;
+}
+
+// GrayImage doubles -> device gray levels (the C++ shim's one pass per frame).
+dicb200_status dicb200_pack_gray(const double* src, int32_t width, int32_t height, int32_t src_pitch,
+                                 int32_t scale, uint16_t* dst, int32_t* fractional, int32_t* max_level,
+                                 int32_t threads) {
+  if (!src || !dst || width < 1 || height < 1) return io_error("null argument");
+  if (scale != 1 && scale != 256) return io_error("pack scale must be 1 or 256");
+  const int pitch = src_pitch > 0 ? src_pitch : width;
+  if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  // below ~256 K pixels per thread the spawn costs more than the scan
+  threads = std::max(1, std::min<int>(threads, (int)(((size_t)width * height) >> 18)));
+  threads = std::min(threads, height);
+  struct Part {
+    int frac = 0, bad = 0, mx = 0;
+  };
+  std::vector<Part> part(threads);
+  const double lim = scale == 1 ? 65535.0 : 255.0;
+  auto work = [&](int t) {
+    Part& r = part[t];
+    const int y0 = (int)((long)height * t / threads), y1 = (int)((long)height * (t + 1) / threads);
+    int mx = 0, frac = 0, bad = 0;
+    for (int y = y0; y < y1; ++y) {
+      const double* s = src + (size_t)y * pitch;
+      uint16_t* d = dst + (size_t)y * width;
+      for (int x = 0; x < width; ++x) {
+        const double v = s[x];
+        const bool b = !(v >= 0.0 && v <= lim);  // also catches NaN
+        bad |= b;
+        if (scale == 1) {
+          const uint16_t q = (uint16_t)(b ? 0.0 : v);
+          frac |= (double)q != v;
+          d[x] = q;
+          mx = q > mx ? q : mx;
+        } else {
+          const uint16_t q = (uint16_t)(b ? 0 : std::lround(v * 256.0));  // 8.8 fixed point
+          d[x] = q;
+          mx = q > mx ? q : mx;
+        }
+      }
+    }
+    r.mx = mx;
+    r.frac = frac;
+    r.bad = bad;
+  };
+  if (threads == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) pool.emplace_back(work, t);
+    for (auto& th : pool) th.join();
+  }
+  int mx = 0, frac = 0, bad = 0;
+  for (const Part& r : part) {
+    mx = std::max(mx, r.mx);
+    frac |= r.frac;
+    bad |= r.bad;
+  }
+  if (fractional) *fractional = frac;
+  if (max_level) *max_level = mx;
+  if (bad)
+    return io_error(scale == 1 ? "dicb200: gray levels must be integers in [0, 65535]"
+                               : "dicb200: fractional gray levels must lie in [0, 255]");
   return DICB200_OK;
 }
 

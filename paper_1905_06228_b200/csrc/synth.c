@@ -16,6 +16,7 @@
 
 
 #include "synth_internal.h"
+#include "synth_math.h"
 
 static uint64_t splitmix_next(uint64_t* s) {
   uint64_t z = (*s += 0x9e3779b97f4a7c15ULL);
@@ -27,47 +28,12 @@ static double u01(uint64_t* s) { return (double)(splitmix_next(s) >> 11) * 0x1.0
 
 void dicb200_synth_displacement(const dicb200_synth_spec* sp, double yx, double yy, double* dx,
                                 double* dy) {
-  const double* a = sp->a;
-  if (sp->field == DICB200_FIELD_AFFINE) {
-    const double rx = yx - a[6], ry = yy - a[7];
-    *dx = a[0] + a[1] * rx + a[2] * ry;
-    *dy = a[3] + a[4] * rx + a[5] * ry;
-  } else if (sp->field == DICB200_FIELD_SINUSOID) {
-    *dx = a[0] * sin(2.0 * M_PI * yy / a[1]);
-    *dy = a[2] * cos(2.0 * M_PI * yx / a[3]);
-  } else {
-    *dx = 0.0;
-    *dy = 0.0;
-  }
+  sx_displacement(sp, yx, yy, dx, dy);
 }
 
 /* Preimage y of pixel x under x = y + d(y). */
 void dicb200_synth_preimage(const dicb200_synth_spec* sp, double x, double y, double* px, double* py) {
-  const double* a = sp->a;
-  if (sp->field == DICB200_FIELD_AFFINE) {
-    /* x - o = (I + A)(y - o) + t  =>  y = o + (I + A)^-1 (x - o - t) */
-    const double m00 = 1.0 + a[1], m01 = a[2], m10 = a[4], m11 = 1.0 + a[5];
-    const double det = m00 * m11 - m01 * m10;
-    const double bx = x - a[6] - a[0], by = y - a[7] - a[3];
-    *px = a[6] + (m11 * bx - m01 * by) / det;
-    *py = a[7] + (-m10 * bx + m00 * by) / det;
-  } else if (sp->field == DICB200_FIELD_SINUSOID) {
-    double yx = x, yy = y;
-    for (int it = 0; it < 60; ++it) {
-      double dx, dy;
-      dicb200_synth_displacement(sp, yx, yy, &dx, &dy);
-      const double nx = x - dx, ny = y - dy;
-      const double ch = fabs(nx - yx) + fabs(ny - yy);
-      yx = nx;
-      yy = ny;
-      if (ch < 1e-13) break;
-    }
-    *px = yx;
-    *py = yy;
-  } else {
-    *px = x;
-    *py = y;
-  }
+  sx_preimage(sp, x, y, px, py);
 }
 
 typedef struct {
@@ -78,40 +44,22 @@ typedef struct {
   int gx, gy;
   void* out;
   int pitch;
+  int row0;  /* frame row stored in out's first row */
   int y0, y1;
 } job_t;
 
 static void* render_rows(void* arg) {
   const job_t* j = (const job_t*)arg;
   const dicb200_synth_spec* sp = j->sp;
-  const double maxv = (double)sp->max_value;
   const int reach_cells = (int)ceil(5.0 * sp->sigma_max / CELL) + 1;
   for (int y = j->y0; y < j->y1; ++y)
     for (int x = 0; x < sp->width; ++x) {
-      double qx, qy;
-      dicb200_synth_preimage(sp, x, y, &qx, &qy);
-      double v = sp->background;
-      const int cx = (int)floor(qx / CELL), cy = (int)floor(qy / CELL);
-      for (int by = cy - reach_cells; by <= cy + reach_cells; ++by) {
-        if (by < 0 || by >= j->gy) continue;
-        for (int bx = cx - reach_cells; bx <= cx + reach_cells; ++bx) {
-          if (bx < 0 || bx >= j->gx) continue;
-          const int c = by * j->gx + bx;
-          for (int i = j->cell_start[c]; i < j->cell_start[c + 1]; ++i) {
-            const blob_t* b = &j->blobs[j->cell_items[i]];
-            const double ddx = qx - b->cx, ddy = qy - b->cy;
-            const double r2 = ddx * ddx + ddy * ddy;
-            if (r2 <= b->reach2) v += b->peak * exp(-r2 * b->inv2s2);
-          }
-        }
-      }
-      if (v < 0.0) v = 0.0;
-      if (v > maxv) v = maxv;
-      const double q = floor(v + 0.5);
+      const double q = sx_pixel(sp, j->blobs, j->cell_start, j->cell_items, j->gx, j->gy, reach_cells, x, y);
+      const size_t o = (size_t)(y - j->row0) * j->pitch + x;
       if (sp->dtype == DICB200_U8)
-        ((uint8_t*)j->out)[(size_t)y * j->pitch + x] = (uint8_t)q;
+        ((uint8_t*)j->out)[o] = (uint8_t)q;
       else
-        ((uint16_t*)j->out)[(size_t)y * j->pitch + x] = (uint16_t)q;
+        ((uint16_t*)j->out)[o] = (uint16_t)q;
     }
   return NULL;
 }
@@ -163,18 +111,21 @@ void dicb200_synth_blobs_free(synth_blobs_t* b) {
   free(b->items);
 }
 
-int dicb200_synth_render(const dicb200_synth_spec* sp, void* out, int32_t pitch, int32_t threads) {
+int dicb200_synth_render_rows(const dicb200_synth_spec* sp, void* out, int32_t pitch, int32_t row_begin,
+                              int32_t row_end, int32_t threads) {
   if (sp->width < 1 || sp->height < 1 || sp->blob_count < 0 || pitch < sp->width) return 1;
+  if (row_begin < 0 || row_end > sp->height || row_end <= row_begin) return 1;
   synth_blobs_t B;
   dicb200_synth_blobs(sp, &B);
+  const int rows = row_end - row_begin;
   if (threads <= 0) threads = (int)sysconf(_SC_NPROCESSORS_ONLN);
   if (threads < 1) threads = 1;
-  if (threads > sp->height) threads = sp->height;
+  if (threads > rows) threads = rows;
   job_t* jobs = (job_t*)calloc((size_t)threads, sizeof(job_t));
   pthread_t* tid = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
   for (int t = 0; t < threads; ++t) {
-    jobs[t] = (job_t){sp, B.blobs, B.cell_start, B.items, B.gx, B.gy, out, pitch,
-                      (int)((long)sp->height * t / threads), (int)((long)sp->height * (t + 1) / threads)};
+    jobs[t] = (job_t){sp, B.blobs, B.cell_start, B.items, B.gx, B.gy, out, pitch, row_begin,
+                      row_begin + (int)((long)rows * t / threads), row_begin + (int)((long)rows * (t + 1) / threads)};
     if (threads == 1)
       render_rows(&jobs[t]);
     else
@@ -186,4 +137,8 @@ int dicb200_synth_render(const dicb200_synth_spec* sp, void* out, int32_t pitch,
   free(tid);
   dicb200_synth_blobs_free(&B);
   return 0;
+}
+
+int dicb200_synth_render(const dicb200_synth_spec* sp, void* out, int32_t pitch, int32_t threads) {
+  return dicb200_synth_render_rows(sp, out, pitch, 0, sp->height, threads);
 }

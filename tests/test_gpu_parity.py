@@ -277,3 +277,24 @@ def test_failure_semantics_degenerate_target(gpu, port):
         stable = (exp["converged"] == 1) | (exp["iterations"] == 0)
         assert np.mean(got["status"][stable] == exp["status"][stable]) > 0.97
         assert (exp["status"] != 0).any()
+
+
+def test_sequence_mixed_bit_widths_reuse_reference_cache(gpu, port):
+    """A fixed-first sequence whose targets change the pair's pixel range: the
+    first pair (12-bit) runs the block-sum search, the second (13-bit target)
+    the tensor-core search on the SAME cached reference frame, which then needs
+    its strip images. Each field must equal an independent analyze_pair and the
+    oracle (the per-stream reference cache is keyed on the kernel choice)."""
+    w = configs.crop(configs.c5(4), 384, 384)
+    frames = [f.render() for f in w.frames]
+    for k in (3, 4):  # later targets: max 8190 -> 13 bits; pairs alternate over two compute streams
+        frames[k] = (frames[k].astype(np.uint32) * 2).astype(np.uint16)
+    imgs = [dic.GrayImage(f, i) for i, f in enumerate(frames)]
+    assert imgs[1].bits() == 12 and imgs[3].bits() == 13
+    fields = dic.analyze_sequence(imgs, w.cfg)
+    for f, tb in zip(fields, (1, 2, 3, 4)):
+        assert not f.failed()
+        exp = run_device(frames[0], frames[tb], w.cfg, pair_index=f.pair_index)
+        for k in exp.dtype.names:
+            assert np.array_equal(f.records[k], exp[k], equal_nan=True), (tb, k)
+        assert_parity(f.records, port.analyze_pair(frames[0], frames[tb], w.cfg, pair_index=f.pair_index))
