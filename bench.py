@@ -58,6 +58,12 @@ def _measured_peaks() -> dict:
 MEASURED_PEAKS = _measured_peaks()
 
 
+def _backend() -> str:
+    import torch.distributed as dist
+
+    return dist.get_backend() if dist.is_initialized() else ""
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -68,6 +74,8 @@ def parse():
     ap.add_argument("--pairs", type=int, default=64, help="C5 sequence length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dump-records", default=None,
+                    help="write this rank's records of the last timed step to DIR/rank<R>.npy (tests)")
     return ap.parse_args()
 
 
@@ -463,7 +471,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         L.dicb200_profile_read(iso_ms, iso_n)
     # flush time is not analysis work: subtract it (measured on the same stream)
     ms = ms_total - sum(a.elapsed_time(b) for a, b in flush_ev)
-    ms_tensor = torch.tensor([ms], dtype=torch.float64, device=dev)
+    red_dev = "cpu" if world > 1 and _backend() == "gloo" else dev
+    ms_tensor = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         import torch.distributed as dist
 
@@ -476,7 +485,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     iters = int(recs["iterations"].sum())
     status_ok = int((recs["status"] == 0).sum())
     n_local = len(my_pairs) * recs_per_pair
-    tot = torch.tensor([evals, iters, n_local, status_ok], dtype=torch.float64, device=dev)
+    tot = torch.tensor([evals, iters, n_local, status_ok], dtype=torch.float64, device=red_dev)
+    if args.dump_records:
+        os.makedirs(args.dump_records, exist_ok=True)
+        np.save(os.path.join(args.dump_records, f"rank{rank}.npy"), recs)
     if world > 1:
         import torch.distributed as dist
 
@@ -529,7 +541,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             e2e_step()
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
-        et = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        et = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
         if world > 1:
             import torch.distributed as dist
 
@@ -805,6 +817,13 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test knob: every rank on one device (the multi-rank code paths on a
+    # 1-GPU box; ranks never wait on each other's kernels — no data-path
+    # collective — so sharing the device only serialises them). NCCL refuses
+    # two ranks per device, so the host-side plumbing goes over gloo then.
+    one_device = os.environ.get("DICB200_BENCH_ONE_DEVICE") == "1"
+    if one_device:
+        local_rank = 0
     if args.impl == "reference":
         line = run_reference(args, rank, world)
     else:
@@ -813,7 +832,10 @@ def main():
             import torch.distributed as dist
 
             torch.cuda.set_device(local_rank)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            if one_device:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         line = run_ours(args, rank, world, local_rank)
         if world > 1:
             import torch.distributed as dist
