@@ -26,9 +26,12 @@
 // Convergence test, guard band M+2, domain checks, |det| < 1e-8, non-finite
 // steps and the final re-sample + ZNCC follow subpixel.cpp; failure semantics
 // follow pipeline.cpp:82-133 (status set, converged = 0, integer fields kept).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "linalg.cuh"
 #include "refine.cuh"
+#include "tma.cuh"
 
 namespace dicb200 {
 
@@ -563,6 +566,169 @@ __device__ __forceinline__ void final_pass_fast2(const PassCtx& c, const Walk& w
   acc[2] = s2;
 }
 
+// ---- fixed-geometry IC-GN passes (subset side and strip geometry known at
+// compile time: C4 / C5) ----
+// The subset is walked in two parts with a FIXED column per lane, so the
+// per-pixel walk is one row step and the dx-weighted sums factor out of the
+// pixel loop (sum txy dx = dx sum txy per lane):
+//   part A: NA blocks of 32 columns, lane = column, one subset row per trip;
+//   part B: the BW = side mod 32 remaining columns, RPT = 32 / BW rows per
+//           trip (lanes >= RPT * BW and rows past the subset carry weight 0).
+// The target region is staged as VERTICAL PAIRS T2[y][x] = (T[y][x], T[y+1][x]),
+// so a bilinear sample is two 8-byte loads (left / right column pairs) and one
+// packed lerp. floor / fraction / tap address come from the float bits of
+// (xy - 0.5) + 1.5 * 2^23 (round to nearest integer = floor(xy), or xy - 1 at an
+// exact integer, where the fraction is then 1 and the lerp gives the same node
+// value): no conversion instructions.
+template <int M>
+struct FixedMap {
+  static constexpr int SIDE = 2 * M + 1;
+  static constexpr int NA = SIDE / 32;
+  static constexpr int BW = SIDE % 32;
+  static constexpr int RPT = BW ? 32 / BW : 1;
+  static constexpr int NB = BW ? (SIDE + RPT - 1) / RPT : 0;
+};
+
+struct FixedCtx {
+  uint32_t t2;   // shared address: T2 pair of subset-local (0, 0) minus the magic bias (see fixed_tap)
+  uint32_t tn;   // shared address: T2 pair of subset-local (-M, -M) at the integer estimate (node pass)
+  uint32_t g2;   // shared address: G2 (2 grad f) at subset pixel (-M, -M)
+  uint32_t r;    // shared address: R (f) at subset pixel (-M, -M)
+  float fbar;
+  f2x o;         // (ul, vl) + kFixedK: warped origin, shifted to positive coordinates
+  f2x A, B;      // (1 + ux, vx), (uy, 1 + vy)
+};
+
+constexpr int kFixedK = 32;            // fixed passes sample at subset-local + kFixedK (> 0)
+constexpr uint32_t kMagicBits = 0x4B000000u;  // bit pattern of 2^23
+
+__device__ __forceinline__ uint32_t fbits(float v) { return __float_as_uint(v); }
+__device__ __forceinline__ float lds1(uint32_t a) {
+  float r;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ f2x lds2x(uint32_t a) {
+  f2x r;
+  asm("ld.shared.b64 %0, [%1];" : "=l"(r) : "r"(a));
+  return r;
+}
+
+// Bilinear sample at xk = subset-local position + kFixedK (packed x/y, >= 1 on
+// the fast path). xk + (2^23 - 0.5) lands in [2^23, 2^24), whose integers are
+// exactly the representable values: the sum rounds to 2^23 + round(xk - 0.5) =
+// 2^23 + floor(xk) (or floor(xk) - 1 at an exact integer, where the fraction
+// is then 1 and the lerp returns the same node value), and its bit pattern is
+// 0x4B000000 + that floor.
+template <int TP>
+__device__ __forceinline__ float fixed_tap(const FixedCtx& c, f2x xk) {
+  const f2x v = add2(xk, pk2(8388607.5f, 8388607.5f));
+  const f2x fr = fma2(add2(v, pk2(-8388608.0f, -8388608.0f)), pk2(-1.0f, -1.0f), xk);  // xk - floor: exact
+  float vx, vy, fx, fy;
+  up2(v, vx, vy);
+  up2(fr, fx, fy);
+  // c.t2 carries -(0x4B000000 (TP + 1)) * 8 (mod 2^32)
+  const uint32_t a = fbits(vy) * (uint32_t)(TP * 8) + (fbits(vx) * 8u + c.t2);
+  const f2x p0 = lds2x(a), p1 = lds2x(a + 8u);  // (f00, f01), (f10, f11)
+  const f2x d = fma2(p0, pk2(-1.0f, -1.0f), p1);
+  const f2x cc = fma2(d, pk2(fx, fx), p0);  // (top, bottom) at fx
+  float top, bot;
+  up2(cc, top, bot);
+  return fmaf(fy, bot - top, top);
+}
+
+// KIND 0: node pass (integer start), 1: IC-GN pass, 2: final ZNCC pass.
+// acc: {sum g', sum g'^2, sum f g' (final), sum g' 2gx {1,dx,dy}, sum g' 2gy {1,dx,dy}}
+template <int M, int TP, int RP, int KIND>
+__device__ __forceinline__ void fixed_pass(const FixedCtx& c, float* acc) {
+  using F = FixedMap<M>;
+  const int lane = threadIdx.x & 31;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+  f2x a36 = pk2(0.f, 0.f), a58 = a36, a47 = a36;
+  // ---- part A: lane = column, one row per trip ----
+#pragma unroll
+  for (int blk = 0; blk < F::NA; ++blk) {
+    const int col = 32 * blk + lane;
+    const float dxf = (float)(col - M);
+    const f2x base = fma2(c.A, pk2(dxf, dxf), c.o);
+    const uint32_t gcol = c.g2 + (uint32_t)col * 8u, rcol = c.r + (uint32_t)col * 4u;
+    const uint32_t ncol = c.tn + (uint32_t)col * 8u;
+    f2x bsum = pk2(0.f, 0.f);
+    float dyf = (float)-M;
+#pragma unroll 4
+    for (int t = 0; t < F::SIDE; ++t, dyf += 1.0f) {
+      const f2x dy2 = pk2(dyf, dyf);
+      float g;
+      if (KIND == 0)
+        g = lds1(ncol + (uint32_t)(t * TP * 8));
+      else
+        g = fixed_tap<TP>(c, fma2(c.B, dy2, base));
+      const float gp = g - c.fbar;
+      s0 += gp;
+      s1 = fmaf(gp, gp, s1);
+      if (KIND == 2) {
+        s2 = fmaf(lds1(rcol + (uint32_t)(t * RP * 4)) - c.fbar, gp, s2);
+      } else {
+        const f2x txy = mul2(lds2x(gcol + (uint32_t)(t * RP * 8)), pk2(gp, gp));
+        bsum = add2(bsum, txy);
+        a58 = fma2(txy, dy2, a58);
+      }
+    }
+    if (KIND != 2) {
+      a36 = add2(a36, bsum);
+      a47 = fma2(bsum, pk2(dxf, dxf), a47);
+    }
+  }
+  // ---- part B: the remaining BW columns, RPT rows per trip ----
+  if (F::BW) {
+    const int lc = lane % F::BW, lr = lane / F::BW;
+    const int col = 32 * F::NA + lc;
+    const float dxf = (float)(col - M);
+    const bool lane_ok = lane < F::RPT * F::BW;
+    const f2x base = fma2(c.A, pk2(dxf, dxf), c.o);
+    const uint32_t gcol = c.g2 + (uint32_t)(col + lr * RP) * 8u, rcol = c.r + (uint32_t)(col + lr * RP) * 4u;
+    const uint32_t ncol = c.tn + (uint32_t)(col + lr * TP) * 8u;
+    f2x bsum = pk2(0.f, 0.f);
+#pragma unroll 2
+    for (int t = 0; t < F::NB; ++t) {
+      const int row = t * F::RPT + lr;
+      const bool ok = lane_ok && row < F::SIDE;
+      const int rr = ok ? row : 0;  // weight 0: any valid pixel, contribution dropped
+      const float w = ok ? 1.0f : 0.0f;
+      const float dyf = (float)(rr - M);
+      const f2x dy2 = pk2(dyf, dyf);
+      const int roff = (ok ? t * F::RPT : -lr);
+      float g;
+      if (KIND == 0)
+        g = lds1(ncol + (uint32_t)(roff * TP * 8));
+      else
+        g = fixed_tap<TP>(c, fma2(c.B, dy2, base));
+      const float gp = fmaf(g, w, -c.fbar * w);
+      s0 += gp;
+      s1 = fmaf(gp, gp, s1);
+      if (KIND == 2) {
+        s2 = fmaf(lds1(rcol + (uint32_t)(roff * RP * 4)) - c.fbar, gp, s2);
+      } else {
+        const f2x txy = mul2(lds2x(gcol + (uint32_t)(roff * RP * 8)), pk2(gp, gp));
+        bsum = add2(bsum, txy);
+        a58 = fma2(txy, dy2, a58);
+      }
+    }
+    if (KIND != 2) {
+      a36 = add2(a36, bsum);
+      a47 = fma2(bsum, pk2(dxf, dxf), a47);
+    }
+  }
+  acc[0] = s0;
+  acc[1] = s1;
+  acc[2] = s2;
+  up2(a36, acc[3], acc[6]);
+  up2(a47, acc[4], acc[7]);
+  up2(a58, acc[5], acc[8]);
+}
+
 // NODE: the integer start (u, v integral, zero gradients) — every sample and
 // its bilinear gradient sit on a node: value t[0], gradient half the central
 // differences, exactly what the weighted forms give with weights (1, 0, 0, 0).
@@ -667,9 +833,74 @@ __device__ __forceinline__ void hessian_row(const double* mo, double scale, int 
   }
 }
 
-template <typename Pix, int METHOD>
-__global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
+// Fixed-geometry variant (FM > 0, IC-GN only): subset half-width FM and
+// lattice step FSTEP known at compile time, strip regions of static shape
+// (target staged as vertical pairs, around the median integer estimate +-
+// kFixedSpread), fixed_pass for every staged-region pass.
+constexpr int kFixedPad = 3, kFixedSpread = 3;
+template <int FM, int FSTEP>
+struct FixedGeom {
+  static constexpr int SIDE = 2 * FM + 1, SPAN = FSTEP * (kWarps - 1);
+  static constexpr int RP = SPAN + SIDE + 2, RH = SIDE + 2;
+  static constexpr int TP = SPAN + SIDE + 2 * kFixedPad + 2 * kFixedSpread;
+  static constexpr int TH = SIDE + 2 * kFixedPad + 2 * kFixedSpread;  // float rows; TH - 1 pair rows
+  static constexpr size_t G2_OFF = (((size_t)RH * RP + 3) & ~(size_t)3);  // floats (16-byte aligned)
+  static constexpr size_t T2_OFF = G2_OFF + 2 * (size_t)RH * RP;
+  static constexpr size_t SMEM = 4 * (T2_OFF + 2 * (size_t)(TH - 1) * TP);
+  // TMA boxes of the raw u8/u16 regions (inner extent a multiple of 16 bytes),
+  // landed inside the gradient area, which is only written after they are converted
+  template <int ES>
+  struct Raw {
+    // box starts are aligned down to 16 bytes (measured: an unaligned inner
+    // start coordinate faults, tools/microbench/tma_check.cu), so the boxes are
+    // up to 16 bytes wider than the regions
+    static constexpr int AE = 16 / ES;
+    static constexpr int RBW = ((RP + AE - 1 + AE - 1) / AE) * AE, TBW = ((TP + AE - 1 + AE - 1) / AE) * AE;
+    static constexpr size_t T_BYTES = (size_t)TH * TBW * ES, R_BYTES = (size_t)RH * RBW * ES;
+    static constexpr uint32_t BYTES = (uint32_t)(T_BYTES + R_BYTES);
+    // TMA destinations are 128-byte aligned (raw_dst); worst-case padding included
+    static_assert(SIDE <= 3 || 4 * G2_OFF + 127 + ((T_BYTES + 127) & ~(size_t)127) + R_BYTES <= 4 * T2_OFF,
+                  "raw TMA boxes must fit in the gradient area");
+  };
+};
+
+// 128-byte aligned TMA destinations of the raw target / reference boxes inside
+// the gradient area starting at `area`.
+template <typename RAW>
+__device__ __forceinline__ void raw_dst(float* area, unsigned char** t, unsigned char** r) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(area);
+  const uint32_t pt = (128u - (a & 127u)) & 127u;
+  unsigned char* b = reinterpret_cast<unsigned char*>(area);
+  *t = b + pt;
+  *r = b + pt + ((RAW::T_BYTES + 127) & ~(size_t)127);
+}
+
+// Rows [0, H-1) of vertical pairs (T[y][x], T[y+1][x]) of `im` at (X0, Y0), zero outside.
+template <typename Pix>
+__device__ __forceinline__ void stage_pairs(const ImageView& im, int X0, int Y0, int P, int H, float2* dst, int warp,
+                                            int lane) {
+  const Pix* base = reinterpret_cast<const Pix*>(im.data);
+  for (int y = warp; y < H - 1; y += kWarps) {
+    const int gy = Y0 + y;
+    const bool y0in = gy >= 0 && gy < im.height, y1in = gy + 1 >= 0 && gy + 1 < im.height;
+    const Pix* r0 = base + (size_t)(y0in ? gy : 0) * im.pitch;
+    const Pix* r1 = base + (size_t)(y1in ? gy + 1 : 0) * im.pitch;
+    float2* d = dst + y * P;
+    for (int x = lane; x < P; x += 32) {
+      const int gx = X0 + x;
+      const bool xin = gx >= 0 && gx < im.width;
+      d[x] = make_float2(xin && y0in ? (float)__ldg(r0 + gx) : 0.f, xin && y1in ? (float)__ldg(r1 + gx) : 0.f);
+    }
+  }
+}
+
+template <typename Pix, int METHOD, int FM = 0, int FSTEP = 0>
+__global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, const __grid_constant__ TmaPair tm) {
+  constexpr bool FIXED = FM > 0;
+  using FG = FixedGeom<FIXED ? FM : 1, FIXED ? FSTEP : 1>;
+  using RAW = typename FG::template Raw<(int)sizeof(Pix)>;
   extern __shared__ __align__(16) float smem_f[];
+  __shared__ uint64_t s_bar;  // TMA staging completion
   __shared__ int s_idx[kWarps], s_idy[kWarps], s_ok[kWarps];
   __shared__ WarpConst s_const[kWarps];
   __shared__ StripGeom G;
@@ -694,6 +925,7 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
     s_idx[tid] = dx;
     s_idy[tid] = dy;
   }
+  if (FIXED && p.use_tma && tid == 0) tma_mbar_init(&s_bar, 1);
   __syncthreads();
   if (tid == 0) {
     int first = -1;
@@ -718,17 +950,45 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
       dxhi = min(dxhi, s_idx[first] + kSpread);
       dylo = max(dylo, s_idy[first] - kSpread);
       dyhi = min(dyhi, s_idy[first] + kSpread);
+      if (FIXED) {  // static region: median estimate +- kFixedSpread
+        int vx[kWarps], vy[kWarps], nv = 0;
+        for (int s2 = 0; s2 < ts; ++s2)
+          if (s_ok[s2]) {
+            int j = nv++;
+            for (; j > 0 && vx[j - 1] > s_idx[s2]; --j) vx[j] = vx[j - 1];
+            vx[j] = s_idx[s2];
+            j = nv - 1;
+            for (; j > 0 && vy[j - 1] > s_idy[s2]; --j) vy[j] = vy[j - 1];
+            vy[j] = s_idy[s2];
+          }
+        dxlo = vx[nv / 2] - kFixedSpread;
+        dxhi = vx[nv / 2] + kFixedSpread;
+        dylo = vy[nv / 2] - kFixedSpread;
+        dyhi = vy[nv / 2] + kFixedSpread;
+      }
     }
     const int cx0 = p.lat.cx(ix0), cx1 = p.lat.cx(ix0 + ts - 1);
     G.rX0 = cx0 - M - 1;
     G.rY0 = cy - M - 1;
     G.rP = (cx1 - cx0) + side + 2;
     G.rH = side + 2;
-    constexpr int kPad = pad_for(METHOD);
+    constexpr int kPad = FIXED ? kFixedPad : pad_for(METHOD);
     G.tX0 = cx0 + dxlo - M - kPad;
     G.tY0 = cy + dylo - M - kPad;
     G.tP = (cx1 - cx0) + (dxhi - dxlo) + side + 2 * kPad;
     G.tH = (dyhi - dylo) + side + 2 * kPad;
+    if (FIXED) {
+      G.rP = FG::RP;
+      G.tP = FG::TP;
+      G.tH = FG::TH;
+      if (p.use_tma) {  // both raw regions in flight while the block syncs
+        unsigned char *rt, *rr;
+        raw_dst<RAW>(smem_f + FG::G2_OFF, &rt, &rr);
+        tma_mbar_expect_tx(&s_bar, RAW::BYTES);
+        tma_load_2d(rt, &tm.tgt, G.tX0 & ~(RAW::AE - 1), G.tY0, &s_bar);
+        tma_load_2d(rr, &tm.ref, G.rX0 & ~(RAW::AE - 1), G.rY0, &s_bar);
+      }
+    }
   }
   __syncthreads();
   const StripGeom g = G;
@@ -736,12 +996,63 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
   float* T = smem_f + g.rH * g.rP;      // target region [tH][tP]
   // IC-GN: gradient region (2 grad f) [rH][rP] as float2, 8-byte aligned
   float2* G2 = reinterpret_cast<float2*>(smem_f + ((g.rH * g.rP + g.tH * g.tP + 1) & ~1));
+  float2* T2 = nullptr;  // fixed geometry: target as vertical pairs [tH - 1][tP]
+  if (FIXED) {
+    G2 = reinterpret_cast<float2*>(smem_f + FG::G2_OFF);
+    T2 = reinterpret_cast<float2*>(smem_f + FG::T2_OFF);
+    T = nullptr;
+  }
   // ---- stage both regions (fp32), zero outside the images: one warp per
   // region row, 4 independent loads per lane in flight, no index division ----
-  stage_rows<Pix>(p.ref, g.rX0, g.rY0, g.rP, g.rH, R, warp, lane);
-  stage_rows<Pix>(p.tgt, g.tX0, g.tY0, g.tP, g.tH, T, warp, lane);
+  if (FIXED && p.use_tma) {
+    // raw u8/u16 boxes (TMA, zero outside the image) -> fp32 reference rows and
+    // target vertical pairs, shared memory to shared memory
+    tma_mbar_wait(&s_bar, 0);
+    unsigned char *rtb, *rrb;
+    raw_dst<RAW>(smem_f + FG::G2_OFF, &rtb, &rrb);
+    const Pix* rr = reinterpret_cast<const Pix*>(rrb);
+    const Pix* rt = reinterpret_cast<const Pix*>(rtb);
+    const int oxr = g.rX0 & (RAW::AE - 1), oxt = g.tX0 & (RAW::AE - 1);
+    for (int y = warp; y < FG::RH; y += kWarps) {
+      const Pix* src = rr + y * RAW::RBW + oxr;
+#pragma unroll
+      for (int x = lane; x < FG::RP; x += 32) R[y * FG::RP + x] = (float)src[x];
+    }
+    for (int y = warp; y < FG::TH - 1; y += kWarps) {
+      const Pix* s0 = rt + y * RAW::TBW + oxt;
+#pragma unroll
+      for (int x = lane; x < FG::TP; x += 32)
+        T2[y * FG::TP + x] = make_float2((float)s0[x], (float)s0[x + RAW::TBW]);
+    }
+  } else {
+    stage_rows<Pix>(p.ref, g.rX0, g.rY0, g.rP, g.rH, R, warp, lane);
+    if (FIXED)
+      stage_pairs<Pix>(p.tgt, g.tX0, g.tY0, g.tP, g.tH, T2, warp, lane);
+    else
+      stage_rows<Pix>(p.tgt, g.tX0, g.tY0, g.tP, g.tH, T, warp, lane);
+  }
   __syncthreads();
-  if (METHOD == 1) {  // central differences of the reference (icgn_precompute, subpixel.cpp:207-208), x2
+  if (FIXED) {  // static region shape: four independent columns per lane in flight
+    for (int y = warp; y < FG::RH; y += kWarps) {
+      const bool yin = y >= 1 && y < FG::RH - 1;
+      const float* r0 = R + y * FG::RP;
+#pragma unroll
+      for (int x0 = 0; x0 < FG::RP; x0 += 128) {
+        float2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int x = x0 + 32 * u + lane;
+          v[u] = make_float2(0.f, 0.f);
+          if (yin && x >= 1 && x < FG::RP - 1)
+            v[u] = make_float2(r0[x + 1] - r0[x - 1], r0[x + FG::RP] - r0[x - FG::RP]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (x0 + 32 * u + lane < FG::RP) G2[y * FG::RP + x0 + 32 * u + lane] = v[u];
+      }
+    }
+    __syncthreads();
+  } else if (METHOD == 1) {  // central differences of the reference (icgn_precompute, subpixel.cpp:207-208), x2
     for (int y = warp; y < g.rH; y += kWarps) {
       const bool yin = y >= 1 && y < g.rH - 1;
       for (int x = lane; x < g.rP; x += 32) {
@@ -947,8 +1258,19 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
   pc.wn.oy = g.tY0;
   pc.bx = bx;
   pc.by = by;
+  FixedCtx fc;
+  if (FIXED) {
+    const uint32_t t2b = smem_addr(T2);
+    fc.t2 = t2b + (uint32_t)(((pc.ioffy - kFixedK) * FG::TP + (pc.ioffx - kFixedK)) * 8) -
+            kMagicBits * (uint32_t)((FG::TP + 1) * 8);
+    fc.tn = t2b + (uint32_t)(((pc.ioffy - M) * FG::TP + (pc.ioffx - M)) * 8);
+    fc.g2 = smem_addr(Gs);
+    fc.r = smem_addr(Rs);
+    fc.fbar = fbarf;
+  }
   double zncc = 0.0;
   int status = DICB200_POI_OK;
+  bool force_slow = false;  // fixed passes: exact min == max recheck on the checked path
   for (int iter = 1;; ++iter) {
     const bool final_pass = iter > p.max_iter || done;
     {  // check_guard (subpixel.cpp:134-141)
@@ -980,7 +1302,28 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
     float acc[NV];
     int bad = 0;
     float gmin, gmax;
-    if (final_pass) {
+    // fixed passes also need the shifted sample coordinates >= 1 (fixed_tap)
+    const bool fixed_fast = FIXED && fast && !force_slow &&
+                            pc.ul - fabsf((float)M + (float)M * pc.ux) - fabsf((float)M * pc.uy) + (float)kFixedK >= 1.0f &&
+                            pc.vl - fabsf((float)M * pc.vx) - fabsf((float)M + (float)M * pc.vy) + (float)kFixedK >= 1.0f;
+    if (fixed_fast) {
+      fc.o = pk2(pc.ul + (float)kFixedK, pc.vl + (float)kFixedK);
+      fc.A = pk2(1.0f + pc.ux, pc.vx);
+      fc.B = pk2(pc.uy, 1.0f + pc.vy);
+      if (final_pass)
+        fixed_pass<FIXED ? FM : 1, FG::TP, FG::RP, 2>(fc, acc);
+      else if (iter == 1)
+        fixed_pass<FIXED ? FM : 1, FG::TP, FG::RP, 0>(fc, acc);
+      else
+        fixed_pass<FIXED ? FM : 1, FG::TP, FG::RP, 1>(fc, acc);
+      gmin = 0.f;  // no min / max in the fixed passes: see the ng2 test below
+      gmax = 1.f;
+    } else if (FIXED) {  // checked path (global memory) only
+      if (final_pass)
+        pixel_pass<false, kFinal, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
+      else
+        pixel_pass<false, kIcgn, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
+    } else if (final_pass) {
       if (fast && METHOD == 1)
         final_pass_fast2(pc, wk, acc, gmin, gmax);
       else if (fast)
@@ -1027,6 +1370,14 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p) {
     const double delta = t0 / n_d;                           // gbar - fbar
     const double ng2 = fmax(t1 - n_d * delta * delta, 0.0);  // sum (g - gbar)^2
     const double ng = sqrt(ng2);
+    if (fixed_fast && !(ng2 > 1e-4 * t1)) {
+      // (nearly) constant warped target: decide "degenerate target" exactly
+      // (min == max over the samples) on the checked path
+      force_slow = true;
+      --iter;
+      continue;
+    }
+    force_slow = false;
     if (bad) {
       status = DICB200_POI_DRIFTED;
       break;
@@ -1176,23 +1527,60 @@ cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st, Icgn
   }
   p.spc = kWarps;
   while (p.spc > 1 && strip_smem(p.M, p.lat.step, p.spc, p.method) > 110 * 1024) --p.spc;
-  const size_t smem = strip_smem(p.M, p.lat.step, p.spc, p.method);
+  size_t smem = strip_smem(p.M, p.lat.step, p.spc, p.method);
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   const int rows = p.n_records / p.lat.nx;
-  dim3 grid((p.lat.nx + p.spc - 1) / p.spc, rows);
   cudaError_t e;
+  // fixed-geometry IC-GN kernels for the BASELINE subset / lattice shapes
+  // (C4: 41 px subsets every 5 px, C5: every 10 px)
+  static const bool generic = std::getenv("DICB200_REFINE_GENERIC") != nullptr;
+  TmaPair tm{};
+  if (p.method == 1 && p.M == 20 && (p.lat.step == 10 || p.lat.step == 5) && !generic) {
+    p.spc = kWarps;
+    dim3 grid((p.lat.nx + p.spc - 1) / p.spc, rows);
+    // TMA staging of the raw regions (falls back to per-thread loads when the
+    // images do not meet the tensor-map layout rules)
+    static const bool no_tma = std::getenv("DICB200_NO_TMA") != nullptr;
+    const int es = u8 ? 1 : 2;
+    auto boxes = [&](int rp, int tp, int rh, int th) {
+      const int ae = 16 / es, rbw = ((rp + 2 * ae - 2) / ae) * ae, tbw = ((tp + 2 * ae - 2) / ae) * ae;
+      return !no_tma &&
+             tma_encode_2d(&tm.ref, p.ref.data, es, p.ref.width, p.ref.height, p.ref.pitch, rbw, rh) &&
+             tma_encode_2d(&tm.tgt, p.tgt.data, es, p.tgt.width, p.tgt.height, p.tgt.pitch, tbw, th);
+    };
+    p.use_tma = p.lat.step == 10 ? boxes(FixedGeom<20, 10>::RP, FixedGeom<20, 10>::TP, FixedGeom<20, 10>::RH,
+                                         FixedGeom<20, 10>::TH)
+                                 : boxes(FixedGeom<20, 5>::RP, FixedGeom<20, 5>::TP, FixedGeom<20, 5>::RH,
+                                         FixedGeom<20, 5>::TH);
+    auto go = [&](auto k, size_t sm) {
+      e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+      if (e == cudaSuccess) k<<<grid, kNT, sm, st>>>(p, tm);
+    };
+    if (p.lat.step == 10)
+      u8 ? go(refine_strip_kernel<uint8_t, 1, 20, 10>, FixedGeom<20, 10>::SMEM)
+         : go(refine_strip_kernel<uint16_t, 1, 20, 10>, FixedGeom<20, 10>::SMEM);
+    else
+      u8 ? go(refine_strip_kernel<uint8_t, 1, 20, 5>, FixedGeom<20, 5>::SMEM)
+         : go(refine_strip_kernel<uint16_t, 1, 20, 5>, FixedGeom<20, 5>::SMEM);
+    count_launch();
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
+  dim3 grid((p.lat.nx + p.spc - 1) / p.spc, rows);
   if (p.method == 0) {
     auto k = u8 ? refine_strip_kernel<uint8_t, 0> : refine_strip_kernel<uint16_t, 0>;
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    if (e == cudaSuccess) k<<<grid, kNT, smem, st>>>(p);
+    if (e == cudaSuccess) k<<<grid, kNT, smem, st>>>(p, tm);
   } else {
     auto k = u8 ? refine_strip_kernel<uint8_t, 1> : refine_strip_kernel<uint16_t, 1>;
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    if (e == cudaSuccess) k<<<grid, kNT, smem, st>>>(p);
+    if (e == cudaSuccess) k<<<grid, kNT, smem, st>>>(p, tm);
   }
   count_launch();
   if (e != cudaSuccess) return e;
