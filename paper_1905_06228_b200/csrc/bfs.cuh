@@ -127,6 +127,7 @@ struct BsGeom {
   int RWp, RHp, TWp, THp;                                                // staged regions (pixels)
   size_t off_tgt, off_blk, smem;
   int threads;
+  int minb;      // CTAs per SM the variant targets
   int async_ok;  // u16 images with 8-byte aligned rows: cp.async staging
 };
 bool bs_plan(const TcParams& p, BsGeom& g);

@@ -44,8 +44,8 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_by
                : "memory");
 }
 
-template <int S, int RR, int Q, int DXC, int NT, typename Pix>
-__global__ void __launch_bounds__(NT, 1) bs_kernel(TcParams p, BsGeom g) {
+template <int S, int RR, int Q, int DXC, int NT, int MINB, typename Pix>
+__global__ void __launch_bounds__(NT, MINB) bs_kernel(TcParams p, BsGeom g) {
   extern __shared__ __align__(16) unsigned char bs_smem[];
   // both images staged as u16 whatever the pixel type (u8 operands made the
   // compiler keep packed bytes live and spill)
@@ -222,24 +222,28 @@ __global__ void __launch_bounds__(NT, 1) bs_kernel(TcParams p, BsGeom g) {
 // Instantiations: (s, r, DXC, threads). A configuration runs on the block-sum
 // kernel when one of them matches its lattice spacing and remainder.
 struct BsVariant {
-  int S, RR, Q, DXC, NT;
+  int S, RR, Q, DXC, NT, MINB;  // MINB: CTAs per SM the variant is sized for (shared memory, registers)
 };
 constexpr BsVariant kVariants[] = {
-    {10, 1, 4, 25, 256},  // c5: L 41, s 10, R 12
-    {10, 1, 3, 31, 256},  // c2: L 31, s 10, R 15
-    {5, 1, 8, 11, 384},   // c4: L 41, s 5, R 5
-    {8, 7, 3, 41, 256},   // c3: L 31, s 8, R 20
+    {10, 1, 4, 25, 256, 1},  // c5: L 41, s 10, R 12
+    {10, 1, 3, 31, 256, 1},  // c2: L 31, s 10, R 15
+    {5, 1, 8, 11, 384, 1},   // c4: L 41, s 5, R 5
+    {8, 7, 3, 41, 256, 1},   // c3: L 31, s 8, R 20
 };
+// Measured and dropped (C5, B200): two CTAs per SM with dx chunks of 13 / 9
+// (127 registers, 16 x 4 POI tiles to fit 110 KB): 0.93 / 0.98 ms against
+// 0.57 ms for {10, 1, 4, 25, 256, 1} — the taller halo and the per-chunk
+// target reloads cost more than the second CTA's latency hiding recovers.
 
-template <int S, int RR, int Q, int DXC, int NT>
+template <int S, int RR, int Q, int DXC, int NT, int MINB>
 cudaError_t launch_variant(const TcParams& p, const BsGeom& g, dim3 grid, cudaStream_t st) {
   cudaError_t e;
   if (p.planes == 1) {
-    auto k = bs_kernel<S, RR, Q, DXC, NT, uint8_t>;
+    auto k = bs_kernel<S, RR, Q, DXC, NT, MINB, uint8_t>;
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
     if (e == cudaSuccess) k<<<grid, NT, g.smem, st>>>(p, g);
   } else {
-    auto k = bs_kernel<S, RR, Q, DXC, NT, uint16_t>;
+    auto k = bs_kernel<S, RR, Q, DXC, NT, MINB, uint16_t>;
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
     if (e == cudaSuccess) k<<<grid, NT, g.smem, st>>>(p, g);
   }
@@ -274,8 +278,11 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
   g.RR = L - g.q * s;
   g.EW = 2 * p.R + 1;
   int best = -1, waste = 1 << 30;
-  for (int v = 0; v < (int)(sizeof(kVariants) / sizeof(kVariants[0])); ++v) {
+  const char* force = std::getenv("DICB200_BS_VARIANT");
+  const int nvar = (int)(sizeof(kVariants) / sizeof(kVariants[0]));
+  for (int v = 0; v < nvar; ++v) {
     if (kVariants[v].S != s || kVariants[v].RR != g.RR || kVariants[v].Q != g.q) continue;
+    if (force ? v != std::atoi(force) : kVariants[v].MINB != 1) continue;
     const int nch = (g.EW + kVariants[v].DXC - 1) / kVariants[v].DXC;
     const int w = nch * kVariants[v].DXC - g.EW;
     if (w < waste) {
@@ -288,6 +295,8 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
                (p.ref.pitch % 4) == 0 && (p.tgt.pitch % 4) == 0;
   g.DXC = kVariants[best].DXC;
   g.threads = kVariants[best].NT;
+  g.minb = kVariants[best].MINB;
+  const size_t smem_cap = g.minb > 1 ? (size_t)(227 * 1024 / g.minb - 1024) : (size_t)220 * 1024;
   g.nchunk = (g.EW + g.DXC - 1) / g.DXC;
   const size_t pix = 2;  // staged as u16
   const int rows = p.re - p.rb;
@@ -314,7 +323,7 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
     g.off_tgt = al((size_t)g.RWp * g.RHp * pix);
     g.off_blk = al(g.off_tgt + (size_t)g.TWp * g.THp * pix);
     g.smem = g.off_blk + (size_t)g.nblk * (4 * g.EW + 1) * 4;
-    if (g.smem <= 220 * 1024) break;
+    if (g.smem <= smem_cap) break;
     if (g.PY > 2)
       g.PY /= 2;
     else if (g.PX > 4)
@@ -334,10 +343,10 @@ cudaError_t bs_launch(const TcParams& p, const BsGeom& g, cudaStream_t st) {
   const int rows = p.re - p.rb;
   dim3 grid((p.lat.nx + g.PX - 1) / g.PX, (rows + g.PY - 1) / g.PY, g.nsplit);
   cudaError_t e = cudaErrorInvalidValue;
-  if (g.S == 10 && g.RR == 1 && g.q == 4 && g.DXC == 25) e = launch_variant<10, 1, 4, 25, 256>(p, g, grid, st);
-  if (g.S == 10 && g.RR == 1 && g.q == 3 && g.DXC == 31) e = launch_variant<10, 1, 3, 31, 256>(p, g, grid, st);
-  if (g.S == 5 && g.RR == 1 && g.q == 8 && g.DXC == 11) e = launch_variant<5, 1, 8, 11, 384>(p, g, grid, st);
-  if (g.S == 8 && g.RR == 7 && g.q == 3 && g.DXC == 41) e = launch_variant<8, 7, 3, 41, 256>(p, g, grid, st);
+  if (g.S == 10 && g.RR == 1 && g.q == 4 && g.DXC == 25) e = launch_variant<10, 1, 4, 25, 256, 1>(p, g, grid, st);
+  if (g.S == 10 && g.RR == 1 && g.q == 3 && g.DXC == 31) e = launch_variant<10, 1, 3, 31, 256, 1>(p, g, grid, st);
+  if (g.S == 5 && g.RR == 1 && g.q == 8 && g.DXC == 11) e = launch_variant<5, 1, 8, 11, 384, 1>(p, g, grid, st);
+  if (g.S == 8 && g.RR == 7 && g.q == 3 && g.DXC == 41) e = launch_variant<8, 7, 3, 41, 256, 1>(p, g, grid, st);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
