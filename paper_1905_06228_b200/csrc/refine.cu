@@ -630,7 +630,13 @@ __device__ __forceinline__ float fixed_tap(const FixedCtx& c, f2x xk) {
   up2(v, vx, vy);
   up2(fr, fx, fy);
   // c.t2 carries -(0x4B000000 (TP + 1)) * 8 (mod 2^32)
-  const uint32_t a = fbits(vy) * (uint32_t)(TP * 8) + (fbits(vx) * 8u + c.t2);
+  uint32_t a;
+  if ((TP & (TP - 1)) == 0) {  // shifts (ALU pipe)
+    constexpr int LG = TP == 128 ? 10 : TP == 64 ? 9 : TP == 32 ? 8 : 0;
+    a = (fbits(vy) << LG) + (fbits(vx) << 3) + c.t2;
+  } else {
+    a = fbits(vy) * (uint32_t)(TP * 8) + (fbits(vx) * 8u + c.t2);
+  }
   const f2x p0 = lds2x(a), p1 = lds2x(a + 8u);  // (f00, f01), (f10, f11)
   const f2x d = fma2(p0, pk2(-1.0f, -1.0f), p1);
   const f2x cc = fma2(d, pk2(fx, fx), p0);  // (top, bottom) at fx
@@ -842,7 +848,10 @@ template <int FM, int FSTEP>
 struct FixedGeom {
   static constexpr int SIDE = 2 * FM + 1, SPAN = FSTEP * (kWarps - 1);
   static constexpr int RP = SPAN + SIDE + 2, RH = SIDE + 2;
-  static constexpr int TP = SPAN + SIDE + 2 * kFixedPad + 2 * kFixedSpread;
+  // target pitch padded to a power of two when that costs < 8 columns of pairs
+  // (the tap address is then two shifts on the ALU pipe instead of IMADs)
+  static constexpr int TP0 = SPAN + SIDE + 2 * kFixedPad + 2 * kFixedSpread;
+  static constexpr int TP = (TP0 <= 128 && TP0 > 120) ? 128 : (TP0 <= 64 && TP0 > 56) ? 64 : TP0;
   static constexpr int TH = SIDE + 2 * kFixedPad + 2 * kFixedSpread;  // float rows; TH - 1 pair rows
   static constexpr size_t G2_OFF = (((size_t)RH * RP + 3) & ~(size_t)3);  // floats (16-byte aligned)
   static constexpr size_t T2_OFF = G2_OFF + 2 * (size_t)RH * RP;
@@ -913,7 +922,7 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
   const size_t rec0 = (size_t)(iy - p.row_begin) * p.lat.nx + ix0;
 
   // ---- strip geometry from the integer estimates ----
-  if (tid < kWarps) {
+  if (!FIXED && tid < kWarps) {
     int ok = 0, dx = 0, dy = 0;
     if (tid < ts) {
       const dicb200_poi_record& r = p.rec[rec0 + tid];
@@ -925,9 +934,60 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
     s_idx[tid] = dx;
     s_idy[tid] = dy;
   }
-  if (FIXED && p.use_tma && tid == 0) tma_mbar_init(&s_bar, 1);
+  if (FIXED) {
+    // static region around the median integer estimate, computed by warp 0
+    // (lanes = the strip's POIs; ranks by shuffles), then lane 0 issues the TMA
+    // copies of both raw regions before the block syncs
+    if (warp == 0) {
+      int ok = 0, dx = 0, dy = 0;
+      if (lane < ts) {
+        const dicb200_poi_record& r = p.rec[rec0 + lane];
+        ok = r.status == DICB200_POI_OK;
+        dx = r.integer_dx;
+        dy = r.integer_dy;
+      }
+      if (lane < kWarps) {
+        s_ok[lane] = ok;
+        s_idx[lane] = dx;
+        s_idy[lane] = dy;
+      }
+      const unsigned valid = __ballot_sync(0xffffffffu, ok);
+      const int nv = __popc(valid);
+      int rx = 0, ry = 0;  // rank of this lane's estimate among the valid ones (ties by lane)
+#pragma unroll
+      for (int j = 0; j < kWarps; ++j) {
+        const int ox = __shfl_sync(0xffffffffu, dx, j), oy = __shfl_sync(0xffffffffu, dy, j);
+        const bool vj = (valid >> j) & 1u;
+        rx += vj && (ox < dx || (ox == dx && j < lane));
+        ry += vj && (oy < dy || (oy == dy && j < lane));
+      }
+      const unsigned mx = __ballot_sync(0xffffffffu, ok && rx == nv / 2);
+      const unsigned my = __ballot_sync(0xffffffffu, ok && ry == nv / 2);
+      const int dxc = nv ? __shfl_sync(0xffffffffu, dx, __ffs(mx) - 1) : 0;
+      const int dyc = nv ? __shfl_sync(0xffffffffu, dy, __ffs(my) - 1) : 0;
+      if (lane == 0) {
+        const int cx0 = p.lat.cx(ix0);
+        G.rX0 = cx0 - M - 1;
+        G.rY0 = cy - M - 1;
+        G.rP = FG::RP;
+        G.rH = FG::RH;
+        G.tX0 = cx0 + dxc - kFixedSpread - M - kFixedPad;
+        G.tY0 = cy + dyc - kFixedSpread - M - kFixedPad;
+        G.tP = FG::TP;
+        G.tH = FG::TH;
+        if (p.use_tma) {
+          tma_mbar_init(&s_bar, 1);
+          unsigned char *rt, *rr;
+          raw_dst<RAW>(smem_f + FG::G2_OFF, &rt, &rr);
+          tma_mbar_expect_tx(&s_bar, RAW::BYTES);
+          tma_load_2d(rt, &tm.tgt, G.tX0 & ~(RAW::AE - 1), G.tY0, &s_bar);
+          tma_load_2d(rr, &tm.ref, G.rX0 & ~(RAW::AE - 1), G.rY0, &s_bar);
+        }
+      }
+    }
+  }
   __syncthreads();
-  if (tid == 0) {
+  if (!FIXED && tid == 0) {
     int first = -1;
     for (int s = 0; s < ts; ++s)
       if (s_ok[s]) {
@@ -950,22 +1010,6 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
       dxhi = min(dxhi, s_idx[first] + kSpread);
       dylo = max(dylo, s_idy[first] - kSpread);
       dyhi = min(dyhi, s_idy[first] + kSpread);
-      if (FIXED) {  // static region: median estimate +- kFixedSpread
-        int vx[kWarps], vy[kWarps], nv = 0;
-        for (int s2 = 0; s2 < ts; ++s2)
-          if (s_ok[s2]) {
-            int j = nv++;
-            for (; j > 0 && vx[j - 1] > s_idx[s2]; --j) vx[j] = vx[j - 1];
-            vx[j] = s_idx[s2];
-            j = nv - 1;
-            for (; j > 0 && vy[j - 1] > s_idy[s2]; --j) vy[j] = vy[j - 1];
-            vy[j] = s_idy[s2];
-          }
-        dxlo = vx[nv / 2] - kFixedSpread;
-        dxhi = vx[nv / 2] + kFixedSpread;
-        dylo = vy[nv / 2] - kFixedSpread;
-        dyhi = vy[nv / 2] + kFixedSpread;
-      }
     }
     const int cx0 = p.lat.cx(ix0), cx1 = p.lat.cx(ix0 + ts - 1);
     G.rX0 = cx0 - M - 1;
@@ -977,20 +1021,8 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
     G.tY0 = cy + dylo - M - kPad;
     G.tP = (cx1 - cx0) + (dxhi - dxlo) + side + 2 * kPad;
     G.tH = (dyhi - dylo) + side + 2 * kPad;
-    if (FIXED) {
-      G.rP = FG::RP;
-      G.tP = FG::TP;
-      G.tH = FG::TH;
-      if (p.use_tma) {  // both raw regions in flight while the block syncs
-        unsigned char *rt, *rr;
-        raw_dst<RAW>(smem_f + FG::G2_OFF, &rt, &rr);
-        tma_mbar_expect_tx(&s_bar, RAW::BYTES);
-        tma_load_2d(rt, &tm.tgt, G.tX0 & ~(RAW::AE - 1), G.tY0, &s_bar);
-        tma_load_2d(rr, &tm.ref, G.rX0 & ~(RAW::AE - 1), G.rY0, &s_bar);
-      }
-    }
   }
-  __syncthreads();
+  if (!FIXED) __syncthreads();
   const StripGeom g = G;
   float* R = smem_f;                    // reference region [rH][rP]
   float* T = smem_f + g.rH * g.rP;      // target region [tH][tP]
@@ -1238,7 +1270,7 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
   // ---- iterations (all lanes hold the same warp parameters) ----
   double P[6] = {(double)idx, 0.0, 0.0, (double)idy, 0.0, 0.0};  // u, ux, uy, v, vx, vy
   int iterations = 0, converged = 0, done = 0;
-  const double n_d = (double)n;
+  const double n_d = (double)n, inv_n = 1.0 / n_d;
   const double lim = (double)(M + 2);
   PassCtx pc;
   pc.T = T;
@@ -1346,11 +1378,13 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
         pixel_pass<false, kNr, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
     }
     // ---- warp reductions ----
-    bad = __any_sync(0xffffffffu, bad);
+    if (!fixed_fast) {  // the fixed passes track no min / max (see the ng2 test below)
+      bad = __any_sync(0xffffffffu, bad);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      gmin = fminf(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
-      gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+      for (int o = 16; o; o >>= 1) {
+        gmin = fminf(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
+        gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+      }
     }
     double t0, t1, t2 = 0.0, G6[6] = {0, 0, 0, 0, 0, 0};
     if (METHOD == 1 && !final_pass) {
@@ -1367,9 +1401,10 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
       t1 = tget<4>(r, 1);
       t2 = tget<4>(r, 2);
     }
-    const double delta = t0 / n_d;                           // gbar - fbar
+    const double delta = t0 * inv_n;                         // gbar - fbar
     const double ng2 = fmax(t1 - n_d * delta * delta, 0.0);  // sum (g - gbar)^2
-    const double ng = sqrt(ng2);
+    const double rng = rsqrt(ng2);                           // one MUFU + refinement, no divisions
+    const double ng = ng2 * rng;
     if (fixed_fast && !(ng2 > 1e-4 * t1)) {
       // (nearly) constant warped target: decide "degenerate target" exactly
       // (min == max over the samples) on the checked path
@@ -1394,7 +1429,7 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
     bool finite;
     if (METHOD == 1) {
       // rhs = sum e_k sd_k (subpixel.cpp:328-333), expanded; step = H^-1 (-rhs)
-      const double ratio = C.nf / ng;
+      const double ratio = C.nf * rng;
       double rhs[6];
 #pragma unroll
       for (int j = 0; j < 6; ++j) rhs[j] = C.A[j] - ratio * (0.5 * G6[j] - delta * C.S[j]);
