@@ -70,7 +70,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c3x", "c4", "c5"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c2b", "c3", "c3x", "c4", "c5"])
     ap.add_argument("--pairs", type=int, default=64, help="C5 sequence length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -98,7 +98,7 @@ def describe(w, subsets_per_pair: int, n_pairs: int, world: int) -> dict:
         "search_radius": cfg.search.search_radius,
         "pairs": n_pairs,
         "subsets_per_pair": subsets_per_pair,
-        "interp": "bilinear (reference semantics)",
+        "interp": "bicubic (B200 extension, parity unpinned)" if int(cfg.interp) == 1 else "bilinear (reference semantics)",
         "parallelism": f"image-parallel: pairs sharded over {world} rank(s)" if n_pairs > 1 else
                        f"subset-parallel: grid rows sharded over {world} rank(s)",
         "l2": "inputs larger than L2 (no flush)" if n_pairs * f.width * f.height * (1 if f.dtype == _abi.U8 else 2) > 126e6
@@ -205,7 +205,9 @@ def cpu_baseline(w, frames_host, n_sample_rows: int, pair_index: int = 0) -> tup
 
     from oracle import Oracle, available
 
-    kind = "reference" if available("reference") else "port"
+    # the reference build has bilinear interpolation only: the bicubic variant's
+    # CPU baseline and parity are the builder's restatement (parity unpinned)
+    kind = "reference" if available("reference") and int(w.cfg.interp) == 0 else "port"
     orc = Oracle(kind)
     cfg = copy.deepcopy(w.cfg)
     cfg.mode = dic.ExecMode.subimage_parallel
@@ -731,7 +733,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
 def cpu_rows(name: str) -> int:
     # bounded samples of ~10-20 s of reference CPU work on a 16-core host
-    return {"c1": 14, "c2": 46, "c3": 40, "c4": 60, "c5": 199}.get(name, 40)
+    return {"c1": 14, "c2": 46, "c2b": 46, "c3": 40, "c4": 60, "c5": 199}.get(name, 40)
 
 
 # ------------------------------------------------------- reference arm
@@ -762,9 +764,9 @@ def run_reference(args, rank: int, world: int):
     from oracle import Oracle, available
     from oracle.pyoracle import render_rows
 
-    kind = "reference" if available("reference") else "port"
-    orc = Oracle(kind)
     w = workload(args.config, args.pairs)
+    kind = "reference" if available("reference") and int(w.cfg.interp) == 0 else "port"
+    orc = Oracle(kind)
     n_pairs = len(w.pairs)
     cfg = copy.deepcopy(w.cfg)
     cfg.mode = dic.ExecMode.subimage_parallel
@@ -781,7 +783,12 @@ def run_reference(args, rank: int, world: int):
         a, b = w.pairs[s % n_pairs]
         ra = ref0 if a == 0 else render_rows(w.frames[a], 0, band).astype(np.float64)
         tgt = render_rows(w.frames[b], 0, band).astype(np.float64)
-        secs, n = orc.analyze_pair_timed(ra, tgt, cfg, s % n_pairs, 1)
+        if kind == "reference":
+            secs, n = orc.analyze_pair_timed(ra, tgt, cfg, s % n_pairs, 1)
+        else:  # bicubic variant: the builder's restatement (the reference has no bicubic)
+            t0 = time.perf_counter()
+            n = len(orc.analyze_pair(ra, tgt, cfg, s % n_pairs, threads))
+            secs = time.perf_counter() - t0
         if s >= args.warmup:
             total_subsets += n
             total_s += secs

@@ -112,9 +112,18 @@ typedef struct {
   int32_t margin;           /* -1: auto = half_width + search_radius */
   /* B200 extensions */
   int32_t inertia_mode;     /* DICB200_INERTIA_REFERENCE */
-  int32_t pad1;
+  int32_t interp;           /* DICB200_INTERP_BILINEAR (reference, default) | DICB200_INTERP_BICUBIC */
   double inertia_constant;  /* used when inertia_mode == CONSTANT */
 } dicb200_run_config;
+
+/* Sub-pixel interpolation of the refiners. BILINEAR = the reference's
+ * interp_bilinear / grad_bilinear (subpixel.cpp:59-128), the parity default.
+ * BICUBIC = BASELINE.json's "bicubic interpolation": Keys cubic convolution
+ * (a = -0.5) over 4 x 4 taps with replicated borders and its analytic
+ * gradient — a B200 extension the reference does not have, so
+ * its parity is pinned only to the builder's CPU restatement
+ * (oracle/dic_oracle.c, "parity unpinned"). */
+enum { DICB200_INTERP_BILINEAR = 0, DICB200_INTERP_BICUBIC = 1 };
 
 /* Per-POI status: 0 = no dic::Error was raised; otherwise which reference
  * error aborted the chain (the reference swallows the message, pipeline.cpp:131-133,

@@ -38,6 +38,9 @@ int dco_refine(const double* ref, const double* tgt, int w, int h, int cx, int c
 int dco_icgn_hessian(const double* ref, int w, int h, int cx, int cy, int m, double* hess,
                      double* condition, char* err, size_t errcap);
 double dco_interp_bilinear(const double* img, int w, int h, double x, double y, int* ok);
+/* bicubic variant (B200 extension, parity unpinned): value / analytic gradient */
+double dco_interp_bicubic(const double* img, int w, int h, double x, double y, int* ok);
+int dco_grad_bicubic(const double* img, int w, int h, double x, double y, double* gx, double* gy);
 uint64_t dco_derive_stream_seed(uint64_t seed, uint64_t pair, uint64_t subset);
 void dco_mt64(uint64_t seed, size_t n, uint64_t* out);
 void dco_uniform01(uint64_t seed, size_t n, double* out);

@@ -220,6 +220,20 @@ class Oracle:
         v = self._f("interp_bilinear")(a.ctypes.data, a.shape[1], a.shape[0], x, y, C.byref(ok))
         return v if ok.value else None
 
+    def interp_bicubic(self, img, x, y):
+        """Port only: the bicubic variant (parity unpinned) -> (value or None, (gx, gy) or None)."""
+        a = _as_double(img)
+        L = self.L
+        L.dco_interp_bicubic.restype = C.c_double
+        L.dco_interp_bicubic.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double, C.POINTER(C.c_int)]
+        L.dco_grad_bicubic.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double,
+                                       C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        ok = C.c_int(0)
+        v = L.dco_interp_bicubic(a.ctypes.data, a.shape[1], a.shape[0], x, y, C.byref(ok))
+        gx, gy = C.c_double(), C.c_double()
+        gok = L.dco_grad_bicubic(a.ctypes.data, a.shape[1], a.shape[0], x, y, C.byref(gx), C.byref(gy))
+        return (v if ok.value else None), ((gx.value, gy.value) if gok else None)
+
     def derive_stream_seed(self, seed, pair, subset) -> int:
         return int(self._f("derive_stream_seed")(seed, pair, subset))
 

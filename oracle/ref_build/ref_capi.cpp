@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <stdexcept>
 #include <random>
 #include <string>
 #include <vector>
@@ -24,6 +25,8 @@
 namespace {
 
 dic::RunConfig to_run_config(const dicb200_run_config& c) {
+  // the reference has bilinear interpolation only (subpixel.cpp:59-128)
+  if (c.interp != DICB200_INTERP_BILINEAR) throw std::runtime_error("reference build: bilinear interpolation only");
   dic::RunConfig r;
   r.integer_method = static_cast<dic::IntegerMethod>(c.integer_method);
   r.subpixel_method = static_cast<dic::SubpixelMethod>(c.subpixel_method);

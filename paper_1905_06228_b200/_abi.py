@@ -68,9 +68,12 @@ class RunConfigC(C.Structure):
         ("spacing", C.c_int32),
         ("margin", C.c_int32),
         ("inertia_mode", C.c_int32),
-        ("pad1", C.c_int32),
+        ("interp", C.c_int32),
         ("inertia_constant", C.c_double),
     ]
+
+
+INTERP_BILINEAR, INTERP_BICUBIC = 0, 1  # dicb200_run_config.interp
 
 
 class PoiRecordC(C.Structure):

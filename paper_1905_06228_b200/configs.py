@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _abi
 from .dic import (
-    BfsDomain, GrayImage, GridParams, InertiaMode, IntegerMethod, RefineConfig, ReferencePolicy,
+    BfsDomain, GrayImage, GridParams, InertiaMode, IntegerMethod, Interp, RefineConfig, ReferencePolicy,
     RunConfig, SearchConfig, SubpixelMethod, lib,
 )
 
@@ -180,9 +180,19 @@ def c5(n_pairs: int = 64) -> Workload:
 ALL = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}
 
 
+def c2b() -> Workload:
+    """C2 with BASELINE's literal bicubic interpolation (B200 extension; the
+    reference, and so every parity run, uses bilinear)."""
+    w = c2()
+    w.cfg.interp = Interp.bicubic
+    return replace(w, name="c2b", description="BFS + NR (bicubic), 512^2 u8, M=15, step 10, R=15, (2.37,-1.62)")
+
+
 def get(name: str) -> Workload:
     if name == "c3x":
         return c3(inertia_constant=0.7)
+    if name == "c2b":
+        return c2b()
     return ALL[name]()
 
 

@@ -161,6 +161,8 @@ static dicb200_status validate_pair(const dicb200_image* a, const dicb200_image*
     return invalid("unsupported pixel type (u8, u16, f32 or f64, identical for both images)");
   if (cfg->integer_method < 0 || cfg->integer_method > 2) return invalid("unknown integer method");
   if (cfg->subpixel_method < 0 || cfg->subpixel_method > 2) return invalid("unknown subpixel method");
+  if (cfg->interp != DICB200_INTERP_BILINEAR && cfg->interp != DICB200_INTERP_BICUBIC)
+    return invalid("unknown interpolation");
   if (cfg->subpixel_method != DICB200_SUB_NONE) {
     int ppt, nt;
     if (!refine_plan(cfg->half_width, &ppt, &nt))
@@ -336,6 +338,7 @@ refine:
     r.method = cfg->subpixel_method == DICB200_SUB_NR ? 0 : 1;
     r.tol = cfg->tol;
     r.max_iter = cfg->max_iter;
+    r.interp = cfg->interp;
     r.rec = out_dev;
     StageTimer tm(r.method == 0 ? 2 : 3, st);
     DICB200_CUDA_TRY(refine_launch(r, ref->dtype == DICB200_U8, st, icache, ref_key));

@@ -152,6 +152,71 @@ __device__ __forceinline__ bool grad_bilinear(const Win& wn, const ImageView& im
   return true;
 }
 
+// ---- bicubic variant (dicb200_run_config.interp = DICB200_INTERP_BICUBIC) ----
+// Keys cubic convolution (a = -0.5) and its derivative; the CPU restatement is
+// oracle/dic_oracle.c (bicubic_eval), same tap order and row-first summation.
+__device__ __forceinline__ void keys_weights(float f, float (&w)[4], float (&d)[4]) {
+  w[0] = ((-0.5f * f + 1.0f) * f - 0.5f) * f;
+  w[1] = (1.5f * f - 2.5f) * f * f + 1.0f;
+  w[2] = ((-1.5f * f + 2.0f) * f + 0.5f) * f;
+  w[3] = (0.5f * f - 0.5f) * f * f;
+  d[0] = (-1.5f * f + 2.0f) * f - 0.5f;
+  d[1] = (4.5f * f - 5.0f) * f;
+  d[2] = (-4.5f * f + 4.0f) * f + 0.5f;
+  d[3] = (1.5f * f - 1.0f) * f;
+}
+
+// 4 x 4 taps at rows/columns (0..3) of `tap(i, j)`, weights in x / y.
+template <bool GRADS, typename TapF>
+__device__ __forceinline__ float bicubic_sum(const TapF& tap, float fx, float fy, float& gx, float& gy) {
+  float wx[4], dwx[4], wy[4], dwy[4];
+  keys_weights(fx, wx, dwx);
+  keys_weights(fy, wy, dwy);
+  float v = 0.f, vx = 0.f, vy = 0.f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float r = 0.f, rd = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float t = tap(i, j);
+      r = fmaf(wx[i], t, r);
+      if (GRADS) rd = fmaf(dwx[i], t, rd);
+    }
+    v = fmaf(wy[j], r, v);
+    if (GRADS) {
+      vx = fmaf(wy[j], rd, vx);
+      vy = fmaf(dwy[j], r, vy);
+    }
+  }
+  if (GRADS) {
+    gx = vx;
+    gy = vy;
+  }
+  return v;
+}
+
+// Checked path: global taps, domain checks and replicated borders as the oracle.
+template <typename Pix, bool GRADS>
+__device__ __forceinline__ bool bicubic_global(const ImageView& im, int bx, int by, float xl, float yl, float& g,
+                                               float& gx, float& gy) {
+  if (!(xl >= (float)(-bx) && xl <= (float)(im.width - 1 - bx) && yl >= (float)(-by) &&
+        yl <= (float)(im.height - 1 - by)))
+    return false;
+  if (GRADS && !(xl >= (float)(1 - bx) && xl <= (float)(im.width - 2 - bx) && yl >= (float)(1 - by) &&
+                 yl <= (float)(im.height - 2 - by)))
+    return false;
+  int x0 = bx + (int)floorf(xl), y0 = by + (int)floorf(yl);
+  if (x0 > im.width - 2) x0 = im.width - 2;
+  if (y0 > im.height - 2) y0 = im.height - 2;
+  const float fx = xl - (float)(x0 - bx), fy = yl - (float)(y0 - by);
+  auto tap = [&](int i, int j) {
+    const int x = min(max(x0 - 1 + i, 0), im.width - 1), y = min(max(y0 - 1 + j, 0), im.height - 1);
+    return gpx<Pix>(im, x, y);
+  };
+  g = bicubic_sum<GRADS>(tap, fx, fy, gx, gy);
+  return true;
+}
+
 __device__ __forceinline__ double warp_sum1(double v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -738,7 +803,7 @@ __device__ __forceinline__ void fixed_pass(const FixedCtx& c, float* acc) {
 // NODE: the integer start (u, v integral, zero gradients) — every sample and
 // its bilinear gradient sit on a node: value t[0], gradient half the central
 // differences, exactly what the weighted forms give with weights (1, 0, 0, 0).
-template <bool FAST, int KIND, typename Pix, bool NODE = false>
+template <bool FAST, int KIND, typename Pix, bool NODE = false, int INTERP = 0>
 __device__ __forceinline__ void pixel_pass(const PassCtx& c, const ImageView& tgt, const Walk& w0,
                                            float* acc, int& bad, float& gmin, float& gmax) {
   constexpr int NV = KIND == kNr ? 39 : 9;
@@ -763,6 +828,11 @@ __device__ __forceinline__ void pixel_pass(const PassCtx& c, const ImageView& tg
         gx = 0.5f * (t[1] - t[-1]);
         gy = 0.5f * (t[c.tP] - t[-c.tP]);
       }
+    } else if (FAST && INTERP == DICB200_INTERP_BICUBIC) {
+      const float flx = floorf(xl), fly = floorf(yl);
+      const float* t = Tb + ((int)fly - 1) * c.tP + (int)flx - 1;
+      const int tP = c.tP;
+      gv = bicubic_sum<KIND == kNr>([&](int i, int j) { return t[j * tP + i]; }, xl - flx, yl - fly, gx, gy);
     } else if (FAST) {
       const float flx = floorf(xl), fly = floorf(yl);  // subset-local: exact frac
       const float fx = xl - flx, fy = yl - fly;
@@ -778,6 +848,9 @@ __device__ __forceinline__ void pixel_pass(const PassCtx& c, const ImageView& tg
         gx = 0.5f * (w00 * dx00 + w10 * dx10 + w01 * dx01 + w11 * dx11);
         gy = 0.5f * (w00 * dy00 + w10 * dy10 + w01 * dy01 + w11 * dy11);
       }
+    } else if (INTERP == DICB200_INTERP_BICUBIC) {
+      gv = 0.f;
+      bad |= !bicubic_global<Pix, KIND == kNr>(tgt, c.bx, c.by, xl, yl, gv, gx, gy);
     } else {
       gv = 0.f;
       bool ok = bilinear<Pix>(c.wn, tgt, c.bx, c.by, xl, yl, gv);
@@ -903,7 +976,7 @@ __device__ __forceinline__ void stage_pairs(const ImageView& im, int X0, int Y0,
   }
 }
 
-template <typename Pix, int METHOD, int FM = 0, int FSTEP = 0>
+template <typename Pix, int METHOD, int FM = 0, int FSTEP = 0, int INTERP = 0>
 __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, const __grid_constant__ TmaPair tm) {
   constexpr bool FIXED = FM > 0;
   using FG = FixedGeom<FIXED ? FM : 1, FIXED ? FSTEP : 1>;
@@ -1324,7 +1397,8 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
       const float Mf = (float)M;
       const float ex = fabsf(Mf + Mf * pc.ux) + fabsf(Mf * pc.uy), ey = fabsf(Mf * pc.vx) + fabsf(Mf + Mf * pc.vy);
       const float lo_x = pc.ul - ex, hi_x = pc.ul + ex, lo_y = pc.vl - ey, hi_y = pc.vl + ey;
-      const float mg = grads ? 2.0f : 1.0f;
+      // taps beyond the sample's cell: bilinear +-1 (NR central differences +-2); bicubic -1 / +2
+      const float mg = (grads || INTERP == DICB200_INTERP_BICUBIC) ? 2.0f : 1.0f;
       fast = pc.offx + lo_x - mg >= 0.0f && pc.offx + hi_x + mg + 1.0f <= (float)(g.tP - 1) &&
              pc.offy + lo_y - mg >= 0.0f && pc.offy + hi_y + mg + 1.0f <= (float)(g.tH - 1) &&
              (float)bx + lo_x - mg >= 0.0f && (float)bx + hi_x + mg <= (float)(p.tgt.width - 1) &&
@@ -1356,26 +1430,30 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
       else
         pixel_pass<false, kIcgn, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
     } else if (final_pass) {
-      if (fast && METHOD == 1)
+      if (fast && METHOD == 1 && INTERP == DICB200_INTERP_BILINEAR)
         final_pass_fast2(pc, wk, acc, gmin, gmax);
       else if (fast)
-        pixel_pass<true, kFinal, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
+        pixel_pass<true, kFinal, Pix, false, INTERP>(pc, p.tgt, wk, acc, bad, gmin, gmax);
       else
-        pixel_pass<false, kFinal, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
+        pixel_pass<false, kFinal, Pix, false, INTERP>(pc, p.tgt, wk, acc, bad, gmin, gmax);
     } else if (METHOD == 1) {
-      if (fast && iter == 1)  // integer start: samples on the nodes
+      // the integer start samples on the nodes: value = node for either interpolant
+      if (fast && iter == 1)
         icgn_pass_node(pc, wk, acc, gmin, gmax);
-      else if (fast)
+      else if (fast && INTERP == DICB200_INTERP_BILINEAR)
         icgn_pass_fast2(pc, wk, acc, gmin, gmax);
+      else if (fast)
+        pixel_pass<true, kIcgn, Pix, false, INTERP>(pc, p.tgt, wk, acc, bad, gmin, gmax);
       else
-        pixel_pass<false, kIcgn, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
+        pixel_pass<false, kIcgn, Pix, false, INTERP>(pc, p.tgt, wk, acc, bad, gmin, gmax);
     } else {
-      if (fast && iter == 1)  // integer start: samples on the nodes
+      // nodes: bicubic's analytic gradient there is the central difference too
+      if (fast && iter == 1)
         pixel_pass<true, kNr, Pix, true>(pc, p.tgt, wk, acc, bad, gmin, gmax);
       else if (fast)
-        pixel_pass<true, kNr, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
+        pixel_pass<true, kNr, Pix, false, INTERP>(pc, p.tgt, wk, acc, bad, gmin, gmax);
       else
-        pixel_pass<false, kNr, Pix>(pc, p.tgt, wk, acc, bad, gmin, gmax);
+        pixel_pass<false, kNr, Pix, false, INTERP>(pc, p.tgt, wk, acc, bad, gmin, gmax);
     }
     // ---- warp reductions ----
     if (!fixed_fast) {  // the fixed passes track no min / max (see the ng2 test below)
@@ -1570,7 +1648,8 @@ cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st, Icgn
   // (C4: 41 px subsets every 5 px, C5: every 10 px)
   static const bool generic = std::getenv("DICB200_REFINE_GENERIC") != nullptr;
   TmaPair tm{};
-  if (p.method == 1 && p.M == 20 && (p.lat.step == 10 || p.lat.step == 5) && !generic) {
+  if (p.method == 1 && p.M == 20 && (p.lat.step == 10 || p.lat.step == 5) && !generic &&
+      p.interp == DICB200_INTERP_BILINEAR) {
     p.spc = kWarps;
     dim3 grid((p.lat.nx + p.spc - 1) / p.spc, rows);
     // TMA staging of the raw regions (falls back to per-thread loads when the
@@ -1604,18 +1683,23 @@ cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st, Icgn
     return cudaGetLastError();
   }
   dim3 grid((p.lat.nx + p.spc - 1) / p.spc, rows);
+  auto go = [&](auto k) {
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (e == cudaSuccess) k<<<grid, kNT, smem, st>>>(p, tm);
+  };
+  const bool cubic = p.interp == DICB200_INTERP_BICUBIC;
   if (p.method == 0) {
-    auto k = u8 ? refine_strip_kernel<uint8_t, 0> : refine_strip_kernel<uint16_t, 0>;
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    if (e == cudaSuccess) k<<<grid, kNT, smem, st>>>(p, tm);
+    if (cubic)
+      u8 ? go(refine_strip_kernel<uint8_t, 0, 0, 0, 1>) : go(refine_strip_kernel<uint16_t, 0, 0, 0, 1>);
+    else
+      u8 ? go(refine_strip_kernel<uint8_t, 0>) : go(refine_strip_kernel<uint16_t, 0>);
   } else {
-    auto k = u8 ? refine_strip_kernel<uint8_t, 1> : refine_strip_kernel<uint16_t, 1>;
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    if (e == cudaSuccess) k<<<grid, kNT, smem, st>>>(p, tm);
+    if (cubic)
+      u8 ? go(refine_strip_kernel<uint8_t, 1, 0, 0, 1>) : go(refine_strip_kernel<uint16_t, 1, 0, 0, 1>);
+    else
+      u8 ? go(refine_strip_kernel<uint8_t, 1>) : go(refine_strip_kernel<uint16_t, 1>);
   }
   count_launch();
   if (e != cudaSuccess) return e;

@@ -15,6 +15,7 @@ struct RefineParams {
   int max_iter;
   dicb200_poi_record* rec;
   int spc;  // POIs per CTA strip (<= 8), chosen by refine_launch to fit shared memory
+  int interp;   // DICB200_INTERP_BILINEAR | DICB200_INTERP_BICUBIC
   int use_tma;  // fixed-geometry kernels: regions staged by TMA (tensor maps passed beside the params)
   // IC-GN reference-side constants per POI (kIcgnCacheStride doubles, global
   // POI index), reused while the reference frame repeats (fixed_first

@@ -59,6 +59,11 @@ class InertiaMode(IntEnum):  # B200 extension (BASELINE asks for constant 0.7)
     constant = 1
 
 
+class Interp(IntEnum):  # B200 extension: BASELINE's "bicubic interpolation" (parity unpinned)
+    bilinear = 0  # the reference's interp_bilinear / grad_bilinear (subpixel.cpp:59-128)
+    bicubic = 1   # Keys cubic convolution a = -0.5, analytic gradient (include/dicb200.h)
+
+
 @dataclass
 class SearchConfig:  # integer_search.hpp:14-23
     search_radius: int = 25
@@ -96,6 +101,7 @@ class RunConfig:  # pipeline.hpp:33-49
     grid: GridParams = field(default_factory=GridParams)
     inertia_mode: InertiaMode = InertiaMode.reference_schedule
     inertia_constant: float = 0.7
+    interp: Interp = Interp.bilinear
 
     def effective_margin(self) -> int:
         return self.grid.margin if self.grid.margin >= 0 else self.grid.half_width + self.search.search_radius
@@ -125,6 +131,7 @@ class RunConfig:  # pipeline.hpp:33-49
         c.margin = int(self.grid.margin)
         c.inertia_mode = int(self.inertia_mode)
         c.inertia_constant = float(self.inertia_constant)
+        c.interp = int(self.interp)
         return c
 
 

@@ -171,3 +171,28 @@ def test_swarm_budgets_and_determinism(kind, request):
 def test_grid_matches_reference(port, reference):
     for (w, h, m, s, mg) in [(256, 256, 10, 16, 20), (100, 60, 15, 7, 0), (2048, 2048, 20, 5, 25), (31, 31, 15, 1, 15)]:
         assert np.array_equal(port.grid(w, h, m, s, mg), reference.grid(w, h, m, s, mg))
+
+
+def test_bicubic_restatement_known_answers(port):
+    """The bicubic variant (B200 extension, parity unpinned: the reference has
+    bilinear only): Keys cubic convolution reproduces polynomials of degree <= 2
+    exactly away from the border, returns the node value on nodes, and its
+    analytic gradient is exact on them too; out-of-domain samples fail like the
+    bilinear pair (value [0, w-1], gradient [1, w-2])."""
+    h, w = 24, 30
+    y, x = np.mgrid[0:h, 0:w].astype(np.float64)
+    cases = (
+        (lambda a, b: 3.0 * a - 2.0 * b + 7.0, lambda a, b: (3.0, -2.0)),
+        (lambda a, b: 0.5 * a * a + 0.25 * b * b + a * b, lambda a, b: (a + b, 0.5 * b + a)),
+    )
+    for f, grad in cases:
+        img = f(x, y)
+        for (sx, sy) in ((5.25, 7.5), (10.0, 11.0), (17.8, 3.3), (22.125, 16.9)):
+            v, g = port.interp_bicubic(img, sx, sy)
+            assert abs(v - f(sx, sy)) < 1e-9, (sx, sy, v)
+            assert np.allclose(g, grad(sx, sy), atol=1e-9), (sx, sy, g)
+    img = np.random.default_rng(3).integers(0, 4096, (h, w)).astype(np.float64)
+    assert port.interp_bicubic(img, 9.0, 4.0)[0] == img[4, 9]
+    assert port.interp_bicubic(img, -0.01, 4.0)[0] is None
+    assert port.interp_bicubic(img, w - 1.0, h - 1.0)[0] == img[h - 1, w - 1]
+    assert port.interp_bicubic(img, 0.5, 4.0)[1] is None  # gradient domain [1, w-2]
