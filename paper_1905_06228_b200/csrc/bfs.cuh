@@ -87,6 +87,7 @@ struct TcParams {
   int64_t* sfg;          // [poi][2R+1][2R+1] exact cross terms from the tensor cores
   void* tiles;           // [n_tiles] uint4: tx|ty<<16, ix_lo|iy_lo<<16, nix|niy<<16
   double* surface;       // optional [poi][2R+1][2R+1]
+  void* slices;          // fused block-sum search: per [poi][dy slice] filter winner (bfs_bs.cu) + flag list
   dicb200_poi_record* rec;
 };
 
@@ -106,7 +107,8 @@ struct TcRefCache {
   void* s2 = nullptr;
   void* sfg = nullptr;
   void* tiles = nullptr;
-  size_t s1_cap = 0, s2_cap = 0, sfg_cap = 0, tiles_cap = 0;
+  void* slices = nullptr;
+  size_t s1_cap = 0, s2_cap = 0, sfg_cap = 0, tiles_cap = 0, slices_cap = 0;
   long key = -1;
   const void* data = nullptr;
   int W = 0, H = 0, M = 0, x0 = 0, y0 = 0, step = 0, nx = 0, rb = 0, re = 0;
@@ -125,13 +127,17 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache = nullptr,
 struct BsGeom {
   int S, RR, q, PX, PY, nbx, nby, nblk, EW, DXC, nchunk, dy_per, nsplit;  // s, r, L / s, POI tile, blocks
   int RWp, RHp, TWp, THp;                                                // staged regions (pixels)
-  size_t off_tgt, off_blk, smem;
+  size_t off_tgt, off_blk, off_state, smem;
   int threads;
+  int fuse;      // exact argmax fused into the kernel (records via bs_merge_kernel), no cross-term buffer
   int minb;      // CTAs per SM the variant targets
   int async_ok;  // u16 images with 8-byte aligned rows: cp.async staging
 };
 bool bs_plan(const TcParams& p, BsGeom& g);
 cudaError_t bs_launch(const TcParams& p, const BsGeom& g, cudaStream_t st);
+// records from the fused kernel's per-slice results (p.slices)
+cudaError_t bs_merge_launch(const TcParams& p, const BsGeom& g, cudaStream_t st);
+size_t bs_slices_bytes(size_t npoi, const BsGeom& g);  // p.slices buffer of the fused search
 
 // async: stream-ordered release on `st` (device-resident callers); else cudaFree.
 void tc_cache_free(TcRefCache& c, cudaStream_t st = nullptr, bool async = false);

@@ -30,6 +30,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <numeric>
+#include <cstdio>
+#include <vector>
 
 #include "bfs.cuh"
 
@@ -44,7 +46,50 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_by
                : "memory");
 }
 
-template <int S, int RR, int Q, int DXC, int NT, int MINB, typename Pix>
+// ---- fused exact argmax (FUSE): the cross terms never leave the SM ----
+// Phase B maps one warp (or a 16-lane half for 2R+1 <= 16) to a POI column,
+// lanes = dx. For every Sfg it forms the candidate exactly as tc_argmax_kernel
+// does: the fp32 filter quotient num * (1/sqrt(vf)) * (1/sqrt(vg)) (absolute
+// error < 2^-21.6), a running per-POI maximum, and the EXACT IEEE quotient
+// num / (sqrt(vf) sqrt(vg)) only for candidates within 2^-19 of the running
+// maximum at their row — a superset of the candidates within 2^-19 of the
+// final maximum, which contains every possible winner. Each POI keeps its
+// exact best in improves() order (integer_search.cpp:43-48) and its count of
+// non-degenerate candidates in shared memory; a CTA covers one slice of the dy
+// range, and bs_merge_kernel combines the slices into the record.
+__device__ __forceinline__ uint32_t fkey(float a) {  // monotonic float -> u32 (0 = none)
+  const uint32_t b = __float_as_uint(a);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float funkey(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+__device__ __forceinline__ double bs_i64_to_f64(int64_t x) {  // exact for |x| < 2^51 without the XU unit
+  if (x >= -(1ll << 51) && x < (1ll << 51))
+    return __longlong_as_double(0x4338000000000000ll + x) - 6755399441055744.0;
+  return (double)x;
+}
+
+constexpr int kBsMaxPY = 8;
+
+// One dy slice's result for one POI (fused block-sum search).
+struct BsSlice {
+  long long num;  // exact numerator of the slice's best filter value
+  float a1, a2;   // best / runner-up filter values (-3 = none)
+  int cnt;        // non-degenerate candidates
+  short dx, dy;
+};  // POI rows per CTA tile (bs_plan starts at 8 and only shrinks)
+
+struct BsPoiState {
+  long long num;  // exact numerator n Sfg - Sf Sg of the slice's best filter value
+  float a1, a2;   // best and runner-up filter values of the slice (-3 = none)
+  int cnt;        // non-degenerate candidates of the slice
+  short dx, dy;   // the best candidate
+  float rsvf;     // POI constants: 1 / sqrt(vf), Sf (staged once per CTA)
+  uint32_t sf;
+};
+
+template <int S, int RR, int Q, int DXC, int NT, int MINB, typename Pix, bool FUSE = false>
 __global__ void __launch_bounds__(NT, MINB) bs_kernel(TcParams p, BsGeom g) {
   extern __shared__ __align__(16) unsigned char bs_smem[];
   // both images staged as u16 whatever the pixel type (u8 operands made the
@@ -110,6 +155,24 @@ __global__ void __launch_bounds__(NT, MINB) bs_kernel(TcParams p, BsGeom g) {
   }
   __syncthreads();
   const int nx_here = min(g.PX, p.lat.nx - ix0), ny_here = min(g.PY, p.re - iy0);
+  BsPoiState* st = reinterpret_cast<BsPoiState*>(bs_smem + g.off_state);  // FUSE: [PY][PX]
+  if (FUSE) {
+    for (int i = threadIdx.x; i < g.PX * g.PY; i += NT) {
+      const int pi = i % g.PX, pj = i / g.PX;
+      st[i].num = 0;
+      st[i].a1 = st[i].a2 = -3.0f;
+      st[i].cnt = 0;
+      st[i].dx = st[i].dy = 0;
+      st[i].rsvf = 0.0f;
+      st[i].sf = 0;
+      if (pi < nx_here && pj < ny_here) {
+        const size_t k = (size_t)(iy0 + pj - p.rb) * p.lat.nx + (ix0 + pi);
+        const double svf = p.poi_sqrtvf[k];
+        st[i].rsvf = svf > 0.0 ? (float)(1.0 / svf) : 0.0f;  // 0: degenerate reference subset, no candidates
+        st[i].sf = (uint32_t)p.poi_sf[k];
+      }
+    }
+  }
   const int nbx = g.nbx;  // block-record row stride
   const int nbx_here = nx_here + Q - (RR == 0 ? 1 : 0), nby = ny_here + Q - (RR == 0 ? 1 : 0);  // blocks needed
   const int BS = 4 * EW + 1;  // words per block record (odd: conflict-free stores across blocks)
@@ -172,6 +235,117 @@ __global__ void __launch_bounds__(NT, MINB) bs_kernel(TcParams p, BsGeom g) {
         }
     }
     __syncthreads();
+    if (FUSE) {
+      // ---- phase B + exact argmax: a warp segment per POI column, lanes = dx ----
+      // The candidates' window data (Sg, ~1/sqrt(vg)) of all the column's POI
+      // rows are loaded up front (independent loads, one latency), the block-row
+      // walk is unrolled so they stay in registers.
+      constexpr int PYM = kBsMaxPY;
+      const int seg = EW <= 16 ? 16 : 32, per_warp = 32 / seg;
+      const int sub = lane / seg, dxi = lane - sub * seg;
+      const unsigned segmask = seg == 32 ? 0xffffffffu : (0xffffu << (16 * sub));
+      const uint32_t n = (uint32_t)(p.side * p.side);
+      const int dy_ = dy;
+      for (int col0 = warp * per_warp; col0 < nx_here; col0 += (NT / 32) * per_warp) {
+        const int pi = col0 + sub;
+        const bool act = dxi < EW && pi < nx_here;
+        const int pic = act ? pi : 0;
+        const uint32_t* col = blk + pic * BS + (act ? dxi : 0);
+        const int cxp = p.lat.cx(ix0 + pic);
+        const int dx = dxi - R;
+        const bool xin = act && dx >= max(-R, M - cxp) && dx <= min(R, p.tgt.width - 1 - M - cxp);
+        float rsq[PYM];
+        uint32_t s1[PYM];
+#pragma unroll
+        for (int j = 0; j < PYM; ++j) {
+          rsq[j] = 0.0f;
+          s1[j] = 0;
+          if (j < ny_here) {
+            const int cyp = p.lat.cy(iy0 + j);
+            if (xin && st[j * g.PX + pic].rsvf > 0.0f && dy_ >= max(-R, M - cyp) &&
+                dy_ <= min(R, p.tgt.height - 1 - M - cyp)) {
+              const size_t o = (size_t)(cyp - M + dy_ - p.qy_min) * p.SW + (cxp - M + dx - p.qx_min);
+              rsq[j] = p.RSQ[o];
+              s1[j] = p.S1[o];
+            }
+          }
+        }
+        uint64_t ring[Q];
+#pragma unroll
+        for (int b = 0; b < Q; ++b) ring[b] = 0;
+#pragma unroll
+        for (int by = 0; by < PYM + Q; ++by) {
+          if (by >= nby) break;  // uniform
+          uint64_t h = 0, hw = 0;
+#pragma unroll
+          for (int a = 0; a < Q; ++a) {
+            h += col[a * BS];
+            if (RR > 0) hw += col[a * BS + 2 * EW];
+          }
+          if (RR > 0) {
+            h += col[Q * BS + EW];
+            hw += col[Q * BS + 3 * EW];
+          }
+          col += nbx * BS;
+          constexpr int sh = RR == 0 ? 1 : 0;
+          uint64_t sfg = 0;
+          if (RR > 0) {
+            sfg = hw;
+#pragma unroll
+            for (int b = 0; b < Q; ++b) sfg += ring[b];
+          }
+#pragma unroll
+          for (int b = 0; b < Q - 1; ++b) ring[b] = ring[b + 1];
+          ring[Q - 1] = h;
+          if (RR == 0) {
+            sfg = 0;
+#pragma unroll
+            for (int b = 0; b < Q; ++b) sfg += ring[b];
+          }
+          const int pj = by - Q + sh;  // the POI row whose box ends here (compile-time per unrolled step)
+          if (pj < 0 || pj >= PYM) continue;
+          if (pj >= ny_here) break;  // uniform
+          // ---- candidate (POI (ix0+pi, iy0+pj), displacement (dx, dy)) ----
+          BsPoiState& ps = st[pj * g.PX + pic];
+          const bool valid = rsq[pj] > 0.0f;  // outside the window / constant target window: skipped, not counted
+          const int64_t num = (int64_t)(sfg * n - (uint64_t)ps.sf * s1[pj]);
+          const float a = __fmul_rn(__fmul_rn(__ll2float_rn(num), ps.rsvf), rsq[pj]);
+          // the row's best (first lane on equal values) and runner-up filter values
+          const uint32_t key = valid ? fkey(a) : 0u;
+          uint32_t km = key;
+#pragma unroll
+          for (int o2 = 8; o2; o2 >>= 1) km = max(km, __shfl_xor_sync(0xffffffffu, km, o2));
+          if (seg == 32) km = max(km, __shfl_xor_sync(0xffffffffu, km, 16));
+          const unsigned top = __ballot_sync(0xffffffffu, key == km && km != 0u) & segmask;
+          const int wl = top ? __ffs(top) - 1 : -1;  // winning lane of the segment
+          uint32_t k2 = lane == wl ? 0u : key;
+#pragma unroll
+          for (int o2 = 8; o2; o2 >>= 1) k2 = max(k2, __shfl_xor_sync(0xffffffffu, k2, o2));
+          if (seg == 32) k2 = max(k2, __shfl_xor_sync(0xffffffffu, k2, 16));
+          const unsigned vb = __ballot_sync(0xffffffffu, valid) & segmask;
+          const float a1o = ps.a1, a2o = ps.a2;
+          __syncwarp();
+          if (km) {
+            const float r1 = funkey(km), r2 = k2 ? funkey(k2) : -3.0f;
+            if (r1 > a1o) {  // new best from this row (equal values: a near tie, see bs_merge_kernel)
+              if (lane == wl) {
+                ps.a2 = fmaxf(a1o, r2);
+                ps.a1 = r1;
+                ps.num = num;
+                ps.dx = (short)dx;
+                ps.dy = (short)dy_;
+              }
+            } else if (dxi == 0) {
+              ps.a2 = fmaxf(a2o, r1);
+            }
+          }
+          if (dxi == 0 && pi < nx_here) ps.cnt += __popc(vb);
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      continue;
+    }
     // ---- phase B: one (POI column, dx) per thread, sliding down the block rows:
     //   h(by)  = sum_{a<Q} F(i+a, by) + C(i+Q, by)    (the POI column's row of blocks)
     //   hw(by) = sum_{a<Q} W(i+a, by) + K(i+Q, by)    (its first-r-rows strip)
@@ -217,6 +391,171 @@ __global__ void __launch_bounds__(NT, MINB) bs_kernel(TcParams p, BsGeom g) {
     }
     __syncthreads();
   }
+  if (FUSE) {  // this dy slice's result per POI
+    for (int i = threadIdx.x; i < nx_here * ny_here; i += NT) {
+      const int pi = i % nx_here, pj = i / nx_here;
+      const BsPoiState& ps = st[pj * g.PX + pi];
+      BsSlice b;
+      b.num = ps.num;
+      b.a1 = ps.a1;
+      b.a2 = ps.a2;
+      b.cnt = ps.cnt;
+      b.dx = ps.dx;
+      b.dy = ps.dy;
+      const size_t k = (size_t)(iy0 + pj - p.rb) * p.lat.nx + (ix0 + pi);
+      reinterpret_cast<BsSlice*>(p.slices)[k * g.nsplit + blockIdx.z] = b;
+    }
+  }
+}
+
+// Per POI: the dy slices' filter winners -> the record (tc_argmax_kernel's
+// output, including "all positions degenerate"). Every candidate that can be
+// the exact maximum has a filter value within 2^-19 of the largest one (filter
+// error < 2^-21.6, approx_zncc): when those are exactly the slices' stored
+// winners, their exact quotients decide in improves() order; when a runner-up
+// also lies that close (a near tie the slices did not keep), the POI is
+// flagged and bs_exact_kernel searches it exactly.
+__global__ void __launch_bounds__(256) bs_merge_kernel(TcParams p, int nsplit, int* flagged, int* n_flagged) {
+  const size_t npoi = (size_t)(p.re - p.rb) * p.lat.nx;
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= npoi) return;
+  const int ix = (int)(k % p.lat.nx), iy = p.rb + (int)(k / p.lat.nx);
+  const int cx = p.lat.cx(ix), cy = p.lat.cy(iy), M = p.M, R = p.R;
+  const int fx_lo = max(-R, M - cx), fx_hi = min(R, p.tgt.width - 1 - M - cx);
+  const int fy_lo = max(-R, M - cy), fy_hi = min(R, p.tgt.height - 1 - M - cy);
+  BestPartial b;
+  b.c = -2.0;
+  b.dx = b.dy = 0;
+  b.count = 0;
+  b.found = 0;
+  const double svf = p.poi_sqrtvf[k];
+  if (fx_lo <= fx_hi && fy_lo <= fy_hi && svf > 0.0) {
+    const BsSlice* sl = reinterpret_cast<const BsSlice*>(p.slices) + k * nsplit;
+    float amax = -3.0f;
+    for (int s = 0; s < nsplit; ++s) {
+      b.count += sl[s].cnt;
+      amax = fmaxf(amax, sl[s].a1);
+    }
+    const float thr = amax - 0x1p-19f;
+    bool near_tie = false;
+    for (int s = 0; s < nsplit; ++s) {
+      if (sl[s].cnt == 0) continue;
+      near_tie |= sl[s].a2 >= thr;
+      if (sl[s].a1 >= thr) {
+        const int qx = cx - M + sl[s].dx, qy = cy - M + sl[s].dy;
+        const double z = bs_i64_to_f64(sl[s].num) /
+                         (svf * p.SQ[(size_t)(qy - p.qy_min) * p.SW + (qx - p.qx_min)]);  // exact
+        if (!b.found || improves(z, sl[s].dx, sl[s].dy, b.c, b.dx, b.dy)) {
+          b.found = 1;
+          b.c = z;
+          b.dx = sl[s].dx;
+          b.dy = sl[s].dy;
+        }
+      }
+    }
+    if (near_tie) {
+      flagged[atomicAdd(n_flagged, 1)] = (int)k;
+      return;  // bs_exact_kernel writes this record
+    }
+  }
+  write_integer_record(p.rec[k], cx, cy, b, p.subpixel_none);
+}
+
+// Flagged POIs (near ties of the filter): the reference's bfs_search over the
+// window, exactly — CTA per POI, the reference subset and the target window
+// staged in shared memory, exact u64 cross terms per candidate (thread per
+// candidate), exact quotients, block argmax in improves() order.
+constexpr int kExactMaxSide = 64, kExactMaxWin = 96;
+template <typename Pix>
+__global__ void __launch_bounds__(256) bs_exact_kernel(TcParams p, const int* flagged, const int* n_flagged) {
+  __shared__ uint16_t fs[kExactMaxSide * kExactMaxSide];
+  __shared__ uint16_t gs[kExactMaxWin * kExactMaxWin];
+  __shared__ double red_c[8];
+  __shared__ int red_d[8][3];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nf = *n_flagged;
+  for (int i = blockIdx.x; i < nf; i += gridDim.x) {
+    const size_t k = (size_t)flagged[i];
+    const int ix = (int)(k % p.lat.nx), iy = p.rb + (int)(k / p.lat.nx);
+    const int cx = p.lat.cx(ix), cy = p.lat.cy(iy), M = p.M, R = p.R, side = p.side;
+    const int fx_lo = max(-R, M - cx), fx_hi = min(R, p.tgt.width - 1 - M - cx);
+    const int fy_lo = max(-R, M - cy), fy_hi = min(R, p.tgt.height - 1 - M - cy);
+    const int fw = fx_hi - fx_lo + 1, fh = fy_hi - fy_lo + 1, ww = fw + side - 1, wh = fh + side - 1;
+    const Pix* f = static_cast<const Pix*>(p.ref.data);
+    const Pix* g = static_cast<const Pix*>(p.tgt.data);
+    __syncthreads();  // previous POI's reduction done
+    for (int t = tid; t < side * side; t += 256) {
+      const int r = t / side, c = t - r * side;
+      fs[t] = (uint16_t)f[(size_t)(cy - M + r) * p.ref.pitch + (cx - M + c)];
+    }
+    for (int t = tid; t < ww * wh; t += 256) {
+      const int r = t / ww, c = t - r * ww;
+      gs[t] = (uint16_t)g[(size_t)(cy - M + fy_lo + r) * p.tgt.pitch + (cx - M + fx_lo + c)];
+    }
+    __syncthreads();
+    const uint32_t n = (uint32_t)(side * side), sf = (uint32_t)p.poi_sf[k];
+    const double svf = p.poi_sqrtvf[k];
+    BestPartial b;
+    b.c = -2.0;
+    b.dx = b.dy = 0;
+    b.count = 0;
+    b.found = 0;
+    for (int t = tid; t < fw * fh; t += 256) {
+      const int ry = t / fw, rx = t - ry * fw, dx = fx_lo + rx, dy = fy_lo + ry;
+      const size_t o = (size_t)(cy - M + dy - p.qy_min) * p.SW + (cx - M + dx - p.qx_min);
+      const double sq = p.SQ[o];
+      if (!(sq > 0.0)) continue;  // constant target window: skipped, not counted
+      uint64_t sfg = 0;
+      for (int r = 0; r < side; ++r) {
+        const uint16_t* fr = fs + r * side;
+        const uint16_t* gr = gs + (ry + r) * ww + rx;
+        for (int c = 0; c < side; ++c) sfg += (uint64_t)((uint32_t)fr[c] * gr[c]);  // each product < 2^32
+      }
+      const int64_t num = (int64_t)(sfg * n - (uint64_t)sf * p.S1[o]);
+      const double z = bs_i64_to_f64(num) / (svf * sq);
+      ++b.count;
+      if (!b.found || improves(z, dx, dy, b.c, b.dx, b.dy)) {
+        b.found = 1;
+        b.c = z;
+        b.dx = dx;
+        b.dy = dy;
+      }
+    }
+#pragma unroll
+    for (int o2 = 16; o2; o2 >>= 1) {
+      BestPartial q;
+      q.c = __shfl_xor_sync(0xffffffffu, b.c, o2);
+      q.dx = __shfl_xor_sync(0xffffffffu, b.dx, o2);
+      q.dy = __shfl_xor_sync(0xffffffffu, b.dy, o2);
+      q.count = __shfl_xor_sync(0xffffffffu, b.count, o2);
+      q.found = __shfl_xor_sync(0xffffffffu, b.found, o2);
+      merge_best(b, q);
+    }
+    if (lane == 0) {
+      red_c[warp] = b.found ? b.c : -3.0;
+      red_d[warp][0] = b.found ? b.dx : 0x7fff;
+      red_d[warp][1] = b.found ? b.dy : 0x7fff;
+      red_d[warp][2] = b.count;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      BestPartial t;
+      t.c = -2.0;
+      t.dx = t.dy = 0;
+      t.count = 0;
+      t.found = 0;
+      for (int w2 = 0; w2 < 8; ++w2) {
+        BestPartial q;
+        q.c = red_c[w2];
+        q.dx = red_d[w2][0];
+        q.dy = red_d[w2][1];
+        q.count = red_d[w2][2];
+        q.found = red_d[w2][0] != 0x7fff;
+        merge_best(t, q);
+      }
+      write_integer_record(p.rec[k], cx, cy, t, p.subpixel_none);
+    }
+  }
 }
 
 // Instantiations: (s, r, DXC, threads). A configuration runs on the block-sum
@@ -237,16 +576,15 @@ constexpr BsVariant kVariants[] = {
 
 template <int S, int RR, int Q, int DXC, int NT, int MINB>
 cudaError_t launch_variant(const TcParams& p, const BsGeom& g, dim3 grid, cudaStream_t st) {
-  cudaError_t e;
-  if (p.planes == 1) {
-    auto k = bs_kernel<S, RR, Q, DXC, NT, MINB, uint8_t>;
+  cudaError_t e = cudaSuccess;
+  auto go = [&](auto k) {
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
     if (e == cudaSuccess) k<<<grid, NT, g.smem, st>>>(p, g);
-  } else {
-    auto k = bs_kernel<S, RR, Q, DXC, NT, MINB, uint16_t>;
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
-    if (e == cudaSuccess) k<<<grid, NT, g.smem, st>>>(p, g);
-  }
+  };
+  if (p.planes == 1)
+    g.fuse ? go(bs_kernel<S, RR, Q, DXC, NT, MINB, uint8_t, true>) : go(bs_kernel<S, RR, Q, DXC, NT, MINB, uint8_t>);
+  else
+    g.fuse ? go(bs_kernel<S, RR, Q, DXC, NT, MINB, uint16_t, true>) : go(bs_kernel<S, RR, Q, DXC, NT, MINB, uint16_t>);
   return e;
 }
 
@@ -293,6 +631,14 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
   if (best < 0) return false;
   g.async_ok = p.planes == 2 && ((uintptr_t)p.ref.data % 8) == 0 && ((uintptr_t)p.tgt.data % 8) == 0 &&
                (p.ref.pitch % 4) == 0 && (p.tgt.pitch % 4) == 0;
+  // fused argmax (opt-in, DICB200_BS_FUSE=1): record mode (not the swarm's
+  // surface), window of <= 32 dx. Bit-identical records without the cross-term
+  // buffer (DRAM traffic ~ the two frames), but measured slower on C5 (B200):
+  // 1.01 ms + 0.08 ms merge against 0.57 ms + 0.136 ms argmax — the warp-per-
+  // POI-column phase B with its per-row reductions costs more than the HBM
+  // round trip it removes (the unfused kernel writes the buffer while the IMAD
+  // pipe is busy, and the argmax pass runs at 70% issue).
+  g.fuse = !p.surface && g.EW <= 32 && L <= 64 && L + g.EW - 1 <= 96 && std::getenv("DICB200_BS_FUSE") != nullptr;
   g.DXC = kVariants[best].DXC;
   g.threads = kVariants[best].NT;
   g.minb = kVariants[best].MINB;
@@ -322,7 +668,8 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
     auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };
     g.off_tgt = al((size_t)g.RWp * g.RHp * pix);
     g.off_blk = al(g.off_tgt + (size_t)g.TWp * g.THp * pix);
-    g.smem = g.off_blk + (size_t)g.nblk * (4 * g.EW + 1) * 4;
+    g.off_state = al(g.off_blk + (size_t)g.nblk * (4 * g.EW + 1) * 4);
+    g.smem = g.off_state + (g.fuse ? (size_t)g.PX * g.PY * sizeof(BsPoiState) : 0);
     if (g.smem <= smem_cap) break;
     if (g.PY > 2)
       g.PY /= 2;
@@ -337,6 +684,39 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
   g.dy_per = (g.EW + g.nsplit - 1) / g.nsplit;
   g.nsplit = (g.EW + g.dy_per - 1) / g.dy_per;
   return tiles > 0;
+}
+
+cudaError_t bs_merge_launch(const TcParams& p, const BsGeom& g, cudaStream_t st) {
+  const size_t npoi = (size_t)(p.re - p.rb) * p.lat.nx;
+  // scratch after the slice records: [n_flagged][flagged POIs]
+  int* n_flagged = reinterpret_cast<int*>(reinterpret_cast<BsSlice*>(p.slices) + npoi * g.nsplit);
+  int* flagged = n_flagged + 1;
+  cudaError_t e = cudaMemsetAsync(n_flagged, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  bs_merge_kernel<<<(unsigned)((npoi + 255) / 256), 256, 0, st>>>(p, g.nsplit, flagged, n_flagged);
+  count_launch();
+  if (std::getenv("DICB200_BS_DEBUG")) {
+    int nf = 0;
+    cudaMemcpyAsync(&nf, n_flagged, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    std::vector<BsSlice> h(std::min<size_t>(npoi * g.nsplit, 64));
+    cudaMemcpy(h.data(), p.slices, h.size() * sizeof(BsSlice), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[bs debug] flagged %d of %zu POIs (nsplit %d)\n", nf, npoi, g.nsplit);
+    for (size_t i = 0; i < h.size() && i < 16; ++i)
+      fprintf(stderr, "  slice %zu: a1 %.9g a2 %.9g cnt %d d (%d,%d)\n", i, h[i].a1, h[i].a2, h[i].cnt, h[i].dx, h[i].dy);
+  }
+  // one CTA per flagged POI (grid-stride; near ties are rare, idle CTAs exit at once)
+  const unsigned ctas = (unsigned)std::min<size_t>(npoi, 148);
+  if (p.planes == 1)
+    bs_exact_kernel<uint8_t><<<ctas, 256, 0, st>>>(p, flagged, n_flagged);
+  else
+    bs_exact_kernel<uint16_t><<<ctas, 256, 0, st>>>(p, flagged, n_flagged);
+  count_launch();
+  return cudaGetLastError();
+}
+
+size_t bs_slices_bytes(size_t npoi, const BsGeom& g) {
+  return npoi * (size_t)g.nsplit * sizeof(BsSlice) + (npoi + 1) * sizeof(int);
 }
 
 cudaError_t bs_launch(const TcParams& p, const BsGeom& g, cudaStream_t st) {

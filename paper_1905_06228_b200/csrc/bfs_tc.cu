@@ -1232,7 +1232,11 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
   }
   const size_t EW = 2 * (size_t)p.R + 1;
   const size_t s1_bytes = sbytes * 4, s2_bytes = sbytes * 12;  // S1 (u32); SQ (double) + RSQ (float)
-  const size_t sfg_bytes = npoi * EW * EW * sizeof(int64_t), tiles_bytes = (size_t)std::max(1, p.n_tiles) * 16;
+  // the fused block-sum search keeps its cross terms on chip: per-slice
+  // results instead of the [poi][2R+1][2R+1] buffer
+  const bool fused = use_bs && bsg.fuse;
+  const size_t sfg_bytes = fused ? bs_slices_bytes(npoi, bsg) : npoi * EW * EW * sizeof(int64_t);
+  const size_t tiles_bytes = (size_t)std::max(1, p.n_tiles) * 16;
   void *S1 = nullptr, *S2 = nullptr, *SFG = nullptr, *TILES = nullptr;
   if (cache) {
     if (e == cudaSuccess) e = grow(cache->s1, cache->s1_cap, s1_bytes, st);
@@ -1255,7 +1259,8 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
   p.S1 = (uint32_t*)S1;
   p.SQ = (double*)S2;
   p.RSQ = (float*)((char*)S2 + sbytes * 8);
-  p.sfg = (int64_t*)SFG;
+  p.sfg = fused ? nullptr : (int64_t*)SFG;
+  p.slices = fused ? SFG : nullptr;
   p.tiles = TILES;
   const bool u8 = p.planes == 1;
   // (a) window sums of the target
@@ -1361,7 +1366,10 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
     }
   }
   // (d) per POI: exact ZNCC -> argmax record, or the full surface for the swarm walk
-  if (e == cudaSuccess) {
+  if (e == cudaSuccess && fused) {
+    StageTimer tm(5, st);
+    e = bs_merge_launch(p, bsg, st);
+  } else if (e == cudaSuccess) {
     int sp = 8;  // POIs per CTA strip (one warp each), sharing the staged position data
     while (sp > 1 && pos_smem_bytes(p, sp) > 96 * 1024) sp /= 2;
     const size_t sm = pos_smem_bytes(p, sp);

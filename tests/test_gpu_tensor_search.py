@@ -195,3 +195,27 @@ def test_block_sum_randomized_against_cuda_core(gpu, seed):
     assert len(got) >= 1024
     for f in FIELDS:
         assert np.array_equal(got[f], exp[f], equal_nan=True), (seed, M, step, R, f)
+
+
+def test_fused_block_sum_argmax_bit_identical(gpu):
+    """DICB200_BS_FUSE=1: the block-sum search with the exact argmax fused into
+    its second phase (no cross-term buffer; per-slice filter winners merged,
+    near ties searched exactly) returns bit-identical records to the default
+    two-kernel path, on a C5 crop and a C4 crop (16-lane segments)."""
+    import copy
+    import os
+
+    from paper_1905_06228_b200 import configs, dic
+
+    for w, k in ((configs.crop(configs.c5(8), 320, 288), 5), (configs.crop(configs.get("c4"), 256, 256), 1)):
+        a, b = w.frames[0].render(), w.frames[k].render()
+        cfg = copy.deepcopy(w.cfg)
+        cfg.subpixel_method = dic.SubpixelMethod.none
+        ref = dic.analyze_pair(dic.GrayImage(a), dic.GrayImage(b, 1), cfg).records
+        os.environ["DICB200_BS_FUSE"] = "1"
+        try:
+            got = dic.analyze_pair(dic.GrayImage(a), dic.GrayImage(b, 1), cfg).records
+        finally:
+            os.environ.pop("DICB200_BS_FUSE", None)
+        for f in ref.dtype.names:
+            assert np.array_equal(got[f], ref[f], equal_nan=True), f
