@@ -205,9 +205,12 @@ def cpu_baseline(w, frames_host, n_sample_rows: int, pair_index: int = 0) -> tup
 
     from oracle import Oracle, available
 
-    # the reference build has bilinear interpolation only: the bicubic variant's
-    # CPU baseline and parity are the builder's restatement (parity unpinned)
-    kind = "reference" if available("reference") and int(w.cfg.interp) == 0 else "port"
+    # the reference build has bilinear interpolation and the w(t) inertia
+    # schedule only: the bicubic (c2b) and constant-inertia (c3x) variants' CPU
+    # baseline and parity are the builder's C restatement, which has both
+    # (bicubic: parity unpinned)
+    kind = "reference" if (available("reference") and int(w.cfg.interp) == 0 and
+                           int(w.cfg.inertia_mode) == 0) else "port"
     orc = Oracle(kind)
     cfg = copy.deepcopy(w.cfg)
     cfg.mode = dic.ExecMode.subimage_parallel
@@ -728,6 +731,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         line["parity"] = parity_block(got, exp, iexp)
         line["parity"]["sample"] = base["sample"].split(", dic::")[0] + " (device-rendered frames, both sides)"
         line["parity"]["device_records"] = src
+        line["parity"]["against"] = ("oracle/_ref (reference sources)" if base["kind"] == "reference" else
+                                     "oracle/dic_oracle.c (C restatement: the reference build cannot express this variant)")
     return line
 
 

@@ -140,7 +140,12 @@ enum {
   DICB200_POI_BORDER_GRADIENTS = 8,       /* "subset too close to border for gradients" subpixel.cpp:193-195 */
   DICB200_POI_DEGENERATE_TEXTURE = 9,     /* "degenerate texture"                  subpixel.cpp:200,219,335 */
   DICB200_POI_WARP_NOT_INVERTIBLE = 10,   /* "warp not invertible"                 subpixel.cpp:279,339 */
-  DICB200_POI_INCREMENT_NOT_INVERTIBLE = 11 /* "non-invertible warp increment"     subpixel.cpp:30 */
+  DICB200_POI_INCREMENT_NOT_INVERTIBLE = 11, /* "non-invertible warp increment"    subpixel.cpp:30 */
+  /* B200 extension: a frame holds a pixel above its declared dicb200_image.bits
+   * (the exact u32 paths chosen from it would overflow); every record of the
+   * call carries it and the host entry points fail the pair with
+   * DICB200_ERR_INVALID. No reference counterpart (GrayImage has no width). */
+  DICB200_POI_BITS_EXCEEDED = 12
 };
 
 /* PoiRecord (pipeline.hpp:51-59) + status. */

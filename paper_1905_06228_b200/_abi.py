@@ -31,6 +31,7 @@ POI_STATUS = {
     9: "degenerate texture",
     10: "warp not invertible",
     11: "non-invertible warp increment",
+    12: "pixel values exceed the declared dicb200_image.bits",  # B200 extension
 }
 
 

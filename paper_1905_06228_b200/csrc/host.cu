@@ -178,6 +178,85 @@ static double pixel_max(const dicb200_image* a, const dicb200_image* b) {
   return (bits > 0 && bits < 16) ? (double)((1 << bits) - 1) : 65535.0;
 }
 
+// ---- declared-width guard --------------------------------------------------
+// dicb200_image.bits < the dtype's width selects exact u32 paths (block sums,
+// u32 IMAD row sums) that would overflow silently on wider data. When a caller
+// declares it, the frames are checked on the device (one read of each frame,
+// 16 B per thread-load) and, on a violation, every record of the call is
+// overwritten with DICB200_POI_BITS_EXCEEDED; the host entry points turn that
+// into a pair-level DICB200_ERR_INVALID.
+// (u8 data never takes a width-dependent path: pixel_max is 255 for it.)
+static bool declares_bits(const dicb200_image* im) {
+  return im->dtype == DICB200_U16 && im->bits > 0 && im->bits < 16;
+}
+
+template <typename Pix>
+__global__ void __launch_bounds__(256) bits_check_kernel(const Pix* data, int pitch, int w, int h, uint32_t limit,
+                                                         int* flag) {
+  const int per = 16 / sizeof(Pix);
+  const bool vec = ((uintptr_t)data % 16) == 0 && ((size_t)pitch * sizeof(Pix)) % 16 == 0;
+  uint32_t mx = 0;
+  const int chunks = (w + per - 1) / per;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < (long)chunks * h; i += (long)gridDim.x * blockDim.x) {
+    const int y = (int)(i / chunks), c = (int)(i - (long)y * chunks), x0 = c * per;
+    const Pix* row = data + (size_t)y * pitch;
+    if (vec && x0 + per <= w) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + x0));
+      const uint32_t v[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (sizeof(Pix) == 2)
+          mx = max(mx, max(v[k] & 0xffffu, v[k] >> 16));
+        else
+          mx = max(mx, max(max(v[k] & 0xffu, (v[k] >> 8) & 0xffu), max((v[k] >> 16) & 0xffu, v[k] >> 24)));
+      }
+    } else {
+      for (int x = x0; x < min(w, x0 + per); ++x) mx = max(mx, (uint32_t)row[x]);
+    }
+  }
+  if (__any_sync(0xffffffffu, mx > limit) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+__global__ void __launch_bounds__(256) bits_poison_kernel(const int* flag, dicb200_poi_record* rec, size_t n) {
+  if (!*flag) return;
+  for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) {
+    dicb200_poi_record& r = rec[k];
+    r.u = r.v = 0.0;
+    r.zncc = __longlong_as_double(0x7ff8000000000000ll);
+    r.converged = r.iterations = 0;
+    r.evaluations = r.update_evaluations = 0;
+    r.integer_dx = r.integer_dy = 0;
+    r.status = DICB200_POI_BITS_EXCEEDED;
+  }
+}
+
+static dicb200_status enqueue_bits_guard(const dicb200_image* ref, const dicb200_image* tgt, dicb200_poi_record* rec,
+                                         size_t n, cudaStream_t st) {
+  if (!declares_bits(ref) && !declares_bits(tgt)) return DICB200_OK;
+  int* flag = nullptr;
+  DICB200_CUDA_TRY(cudaMallocAsync((void**)&flag, sizeof(int), st));
+  DICB200_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  for (const dicb200_image* im : {ref, tgt}) {
+    if (!declares_bits(im)) continue;
+    const uint32_t limit = (1u << im->bits) - 1u;
+    const int pitch = im->pitch > 0 ? im->pitch : im->width;
+    if (im->dtype == DICB200_U8)
+      bits_check_kernel<uint8_t><<<2 * 148, 256, 0, st>>>(static_cast<const uint8_t*>(im->data), pitch, im->width,
+                                                           im->height, limit, flag);
+    else
+      bits_check_kernel<uint16_t><<<2 * 148, 256, 0, st>>>(static_cast<const uint16_t*>(im->data), pitch, im->width,
+                                                            im->height, limit, flag);
+    count_launch();
+  }
+  bits_poison_kernel<<<148, 256, 0, st>>>(flag, rec, n);
+  count_launch();
+  DICB200_CUDA_TRY(cudaGetLastError());
+  DICB200_CUDA_TRY(cudaFreeAsync(flag, st));
+  return DICB200_OK;
+}
+
+static const char kBitsMsg[] = "pixel values exceed the declared dicb200_image.bits";
+
 // Enqueue the whole per-pair chain for grid rows [rb, re) on `st`.
 static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image* tgt, const dicb200_run_config* cfg,
                                    uint64_t pair_index, const Lattice& lat, int rb, int re,
@@ -344,7 +423,7 @@ refine:
     DICB200_CUDA_TRY(refine_launch(r, ref->dtype == DICB200_U8, st, icache, ref_key));
     host_trace("refine enqueued");
   }
-  return DICB200_OK;
+  return enqueue_bits_guard(ref, tgt, out_dev, nrec, st);
 }
 
 static size_t elem_size(int dtype) {
@@ -755,6 +834,8 @@ dicb200_status dicb200_analyze_pair(const dicb200_image* ref, const dicb200_imag
     if (e != cudaSuccess) s = cuda_fail(e, "cudaMemcpyAsync(records)", __FILE__, __LINE__);
   }
   const dicb200_status rs = release_context(c);
+  if (s == DICB200_OK && rs == DICB200_OK && n > 0 && out[0].status == DICB200_POI_BITS_EXCEEDED)
+    return invalid(kBitsMsg);
   return s != DICB200_OK ? s : rs;
 }
 
@@ -966,6 +1047,10 @@ dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_im
         return;
       }
       if (r.staged) std::memcpy(f.records, r.stage, r.n * sizeof(dicb200_poi_record));
+      if (r.n > 0 && f.records[0].status == DICB200_POI_BITS_EXCEEDED) {
+        fail_field(f, invalid(kBitsMsg));
+        return;
+      }
       f.count = r.n;
       f.status = DICB200_OK;
     };

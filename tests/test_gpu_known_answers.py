@@ -79,3 +79,30 @@ def test_small_grid_tie_break_reference_case(gpu):
     k = np.nonzero((r["x"] == 16) & (r["y"] == 16))[0]
     assert len(k) == 1
     assert (r["integer_dx"][k[0]], r["integer_dy"][k[0]]) == (-8, -8)
+
+
+def test_understated_bits_fail_loudly(gpu):
+    """ADVICE r1 (host.cu bits trust): a caller declaring fewer significant bits
+    than the data holds must not get silently overflowed u32 sums — the host
+    entry point fails the pair, the device entry point marks every record."""
+    import ctypes as C
+
+    ref = _speckle(420, 400, 17, _abi.U16, 4095)
+    tgt = np.roll(ref, 3, axis=1)
+    cfg = _cfg(20, 12, 10)
+    good = dic.analyze_pair(dic.GrayImage(ref), dic.GrayImage(tgt, 1), cfg).records
+    assert np.all(good["status"] == 0)
+    a, b = dic.GrayImage(ref).as_c(), dic.GrayImage(tgt, 1).as_c()
+    a.bits = 8  # understated: the data holds 12 bits
+    c = cfg.to_c()
+    recs = np.zeros(len(good), dtype=_abi.record_dtype())
+    cnt = C.c_size_t(0)
+    st = dic.lib().dicb200_analyze_pair(C.byref(a), C.byref(b), C.byref(c), 0, recs.ctypes.data, len(recs), C.byref(cnt))
+    assert st == 1 and b"declared dicb200_image.bits" in dic.lib().dicb200_last_error_message()
+    assert np.all(recs["status"] == 12)
+    # a correct declaration (12 bits) passes the guard and keeps the records
+    a.bits = 12
+    st = dic.lib().dicb200_analyze_pair(C.byref(a), C.byref(b), C.byref(c), 0, recs.ctypes.data, len(recs), C.byref(cnt))
+    assert st == 0
+    for f in ("integer_dx", "integer_dy", "evaluations", "status"):
+        assert np.array_equal(recs[f], good[f]), f
