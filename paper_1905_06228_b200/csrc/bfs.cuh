@@ -132,6 +132,7 @@ struct BsGeom {
   int fuse;      // exact argmax fused into the kernel (records via bs_merge_kernel), no cross-term buffer
   int minb;      // CTAs per SM the variant targets
   int async_ok;  // u16 images with 8-byte aligned rows: cp.async staging
+  int ws, npw, ncw;  // warp-specialised kernel (bs_ws_kernel): producer / consumer warps
 };
 bool bs_plan(const TcParams& p, BsGeom& g);
 cudaError_t bs_launch(const TcParams& p, const BsGeom& g, cudaStream_t st);

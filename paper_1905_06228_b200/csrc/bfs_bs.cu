@@ -89,6 +89,65 @@ struct BsPoiState {
   uint32_t sf;
 };
 
+// Stage the CTA's reference blocks and the target rows of its dy slice as u16
+// (0 outside the images). u16 images: 8-byte cp.async from 4-pixel-aligned
+// global columns (zero-filled past the borders); the staged rows then start
+// `sh` pixels before the region. Phase A reads g.nchunk * dxc columns past
+// each block (dx past R: zero).
+template <typename Pix, int NT>
+__device__ __forceinline__ void bs_stage(const TcParams& p, const BsGeom& g, uint16_t* Rf, uint16_t* Tg, int RX0,
+                                         int RY0, int TX0, int TY0, int dy_lo, int dy_hi, int dxc, int& shR,
+                                         int& shT) {
+  const int R = p.R, RP = g.RWp, TP = g.TWp;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (sizeof(Pix) == 2 && g.async_ok) {
+    shR = RX0 & 3;
+    shT = TX0 & 3;
+    const int XR = RX0 - shR, XT = TX0 - shT;
+    const uint16_t* ref = static_cast<const uint16_t*>(p.ref.data);
+    const int cr = (shR + g.nbx * g.S + 3) / 4;  // 4-pixel chunks per staged row
+    for (int i = threadIdx.x; i < g.RHp * cr; i += NT) {
+      const int y = i / cr, c = i - y * cr, gy = RY0 + y, gx = XR + 4 * c;
+      const int valid = (gy >= 0 && gy < p.ref.height && gx >= 0) ? max(0, min(4, p.ref.width - gx)) : 0;
+      const uint16_t* src = valid ? ref + (size_t)gy * p.ref.pitch + gx : ref;
+      cp_async8(Rf + y * RP + 4 * c, src, 2 * valid);
+    }
+    const uint16_t* tgt = static_cast<const uint16_t*>(p.tgt.data);
+    const int ct = (shT + g.nbx * g.S + g.nchunk * dxc + 3) / 4;
+    const int y_lo = dy_lo + R, nrow = dy_hi - dy_lo + g.RHp;
+    for (int i = threadIdx.x; i < nrow * ct; i += NT) {
+      const int yy = i / ct, c = i - yy * ct, y = y_lo + yy, gy = TY0 + y, gx = XT + 4 * c;
+      const int valid = (gy >= 0 && gy < p.tgt.height && gx >= 0) ? max(0, min(4, p.tgt.width - gx)) : 0;
+      const uint16_t* src = valid ? tgt + (size_t)gy * p.tgt.pitch + gx : tgt;
+      cp_async8(Tg + y * TP + 4 * c, src, 2 * valid);
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+  } else {
+    const Pix* ref = static_cast<const Pix*>(p.ref.data);
+    const int w = g.nbx * g.S;
+    for (int y = warp; y < g.RHp; y += NT / 32) {
+      const int gy = RY0 + y;
+      const bool rowok = gy >= 0 && gy < p.ref.height;
+      const Pix* src = ref + (size_t)(rowok ? gy : 0) * p.ref.pitch;
+      for (int x = lane; x < w; x += 32) {
+        const int gx = RX0 + x;
+        Rf[y * RP + x] = (rowok && gx >= 0 && gx < p.ref.width) ? (uint16_t)src[gx] : (uint16_t)0;
+      }
+    }
+    const Pix* tgt = static_cast<const Pix*>(p.tgt.data);
+    const int tw = w + g.nchunk * dxc;  // columns read by phase A (dx past R: zero)
+    for (int y = dy_lo + R + warp; y < dy_hi + R + g.RHp; y += NT / 32) {
+      const int gy = TY0 + y;
+      const bool rowok = gy >= 0 && gy < p.tgt.height;
+      const Pix* src = tgt + (size_t)(rowok ? gy : 0) * p.tgt.pitch;
+      for (int x = lane; x < tw; x += 32) {
+        const int gx = TX0 + x;
+        Tg[y * TP + x] = (rowok && x < w + 2 * R && gx >= 0 && gx < p.tgt.width) ? (uint16_t)src[gx] : (uint16_t)0;
+      }
+    }
+  }
+}
+
 template <int S, int RR, int Q, int DXC, int NT, int MINB, typename Pix, bool FUSE = false>
 __global__ void __launch_bounds__(NT, MINB) bs_kernel(TcParams p, BsGeom g) {
   extern __shared__ __align__(16) unsigned char bs_smem[];
@@ -103,56 +162,9 @@ __global__ void __launch_bounds__(NT, MINB) bs_kernel(TcParams p, BsGeom g) {
   const int RX0 = p.lat.cx(ix0) - M, RY0 = p.lat.cy(iy0) - M;  // block (0, 0) origin
   const int TX0 = RX0 - R, TY0 = RY0 - R;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // ---- stage the reference blocks and the target rows of this dy slice (0 outside).
-  // u16 images: 8-byte cp.async from 4-pixel-aligned global columns (zero-filled
-  // past the borders); the staged rows then start `sh` pixels before the region.
+  // ---- stage the reference blocks and the target rows of this dy slice (0 outside)
   int shR = 0, shT = 0;
-  if (sizeof(Pix) == 2 && g.async_ok) {
-    shR = RX0 & 3;
-    shT = TX0 & 3;
-    const int XR = RX0 - shR, XT = TX0 - shT;
-    const uint16_t* ref = static_cast<const uint16_t*>(p.ref.data);
-    const int cr = (shR + g.nbx * S + 3) / 4;  // 4-pixel chunks per staged row
-    for (int i = threadIdx.x; i < g.RHp * cr; i += NT) {
-      const int y = i / cr, c = i - y * cr, gy = RY0 + y, gx = XR + 4 * c;
-      const int valid = (gy >= 0 && gy < p.ref.height && gx >= 0) ? max(0, min(4, p.ref.width - gx)) : 0;
-      const uint16_t* src = valid ? ref + (size_t)gy * p.ref.pitch + gx : ref;
-      cp_async8(Rf + y * RP + 4 * c, src, 2 * valid);
-    }
-    const uint16_t* tgt = static_cast<const uint16_t*>(p.tgt.data);
-    const int ct = (shT + g.nbx * S + g.nchunk * DXC + 3) / 4;
-    const int y_lo = dy_lo + R, nrow = dy_hi - dy_lo + g.RHp;
-    for (int i = threadIdx.x; i < nrow * ct; i += NT) {
-      const int yy = i / ct, c = i - yy * ct, y = y_lo + yy, gy = TY0 + y, gx = XT + 4 * c;
-      const int valid = (gy >= 0 && gy < p.tgt.height && gx >= 0) ? max(0, min(4, p.tgt.width - gx)) : 0;
-      const uint16_t* src = valid ? tgt + (size_t)gy * p.tgt.pitch + gx : tgt;
-      cp_async8(Tg + y * TP + 4 * c, src, 2 * valid);
-    }
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-  } else {
-    const Pix* ref = static_cast<const Pix*>(p.ref.data);
-    const int w = g.nbx * S;
-    for (int y = warp; y < g.RHp; y += NT / 32) {
-      const int gy = RY0 + y;
-      const bool rowok = gy >= 0 && gy < p.ref.height;
-      const Pix* src = ref + (size_t)(rowok ? gy : 0) * p.ref.pitch;
-      for (int x = lane; x < w; x += 32) {
-        const int gx = RX0 + x;
-        Rf[y * RP + x] = (rowok && gx >= 0 && gx < p.ref.width) ? (uint16_t)src[gx] : (uint16_t)0;
-      }
-    }
-    const Pix* tgt = static_cast<const Pix*>(p.tgt.data);
-    const int tw = w + g.nchunk * DXC;  // columns read by phase A (dx past R: zero)
-    for (int y = dy_lo + R + warp; y < dy_hi + R + g.RHp; y += NT / 32) {
-      const int gy = TY0 + y;
-      const bool rowok = gy >= 0 && gy < p.tgt.height;
-      const Pix* src = tgt + (size_t)(rowok ? gy : 0) * p.tgt.pitch;
-      for (int x = lane; x < tw; x += 32) {
-        const int gx = TX0 + x;
-        Tg[y * TP + x] = (rowok && x < w + 2 * R && gx >= 0 && gx < p.tgt.width) ? (uint16_t)src[gx] : (uint16_t)0;
-      }
-    }
-  }
+  bs_stage<Pix, NT>(p, g, Rf, Tg, RX0, RY0, TX0, TY0, dy_lo, dy_hi, DXC, shR, shT);
   __syncthreads();
   const int nx_here = min(g.PX, p.lat.nx - ix0), ny_here = min(g.PY, p.re - iy0);
   BsPoiState* st = reinterpret_cast<BsPoiState*>(bs_smem + g.off_state);  // FUSE: [PY][PX]
@@ -408,6 +420,156 @@ __global__ void __launch_bounds__(NT, MINB) bs_kernel(TcParams p, BsGeom g) {
   }
 }
 
+// ---- K1-BS-WS: the same block sums, warp-specialised ----
+// The single-role kernel above alternates phase A (IMAD-bound) and phase B
+// (loads and u64 adds) behind CTA barriers, so the IMAD pipe idles during
+// every phase B (ncu C5: fmaheavy 51 %, 8 warps/SM, 255 registers). Here the
+// dx range is cut into chunks of DXC (registers <= 128), phase A of item
+// (dy, chunk) runs on NPW producer warps while NCW consumer warps run phase B
+// of the previous item, over two block-partial buffers handed back and forth
+// with named barriers (FULL b: producers arrive, consumers wait; EMPTY b: the
+// reverse). Same partials, same u64 box sums, same cross-term buffer: the
+// records are bit-identical to bs_kernel's.
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int S, int RR, int Q, int DXC, int NPW, int NCW, typename Pix>
+__global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, BsGeom g) {
+  constexpr int NT = 32 * (NPW + NCW), NP = 32 * NPW, NC = 32 * NCW;
+  constexpr int BS = 4 * DXC + 1;  // words per block record (odd: conflict-free stores across blocks)
+  extern __shared__ __align__(16) unsigned char bs_smem[];
+  uint16_t* Rf = reinterpret_cast<uint16_t*>(bs_smem);              // [RHp][RP]
+  uint16_t* Tg = reinterpret_cast<uint16_t*>(bs_smem + g.off_tgt);  // [THp][TP]
+  uint32_t* blk0 = reinterpret_cast<uint32_t*>(bs_smem + g.off_blk);  // 2 x [nblk][F|C|W|K x DXC]
+  const int M = p.M, R = p.R, EW = g.EW, RP = g.RWp, TP = g.TWp;
+  const int ix0 = blockIdx.x * g.PX, iy0 = p.rb + blockIdx.y * g.PY;
+  const int dy_lo = -R + (int)blockIdx.z * g.dy_per, dy_hi = min(R, dy_lo + g.dy_per - 1);
+  const int RX0 = p.lat.cx(ix0) - M, RY0 = p.lat.cy(iy0) - M;  // block (0, 0) origin
+  const int TX0 = RX0 - R, TY0 = RY0 - R;
+  int shR = 0, shT = 0;
+  bs_stage<Pix, NT>(p, g, Rf, Tg, RX0, RY0, TX0, TY0, dy_lo, dy_hi, DXC, shR, shT);
+  __syncthreads();
+  const int nx_here = min(g.PX, p.lat.nx - ix0), ny_here = min(g.PY, p.re - iy0);
+  const int nbx = g.nbx;
+  const int nbx_here = nx_here + Q - (RR == 0 ? 1 : 0), nby = ny_here + Q - (RR == 0 ? 1 : 0);
+  const int nchunk = g.nchunk, n_items = (dy_hi - dy_lo + 1) * nchunk;
+  const size_t blk_words = (size_t)g.nblk * BS;
+  if (threadIdx.x < NP) {
+    // ---- producers: phase A of every item into buffer it & 1
+    for (int it = 0; it < n_items; ++it) {
+      const int b = it & 1;
+      if (it >= 2) named_bar_sync(3 + b, NT);  // consumers are done with item it - 2
+      const int dy = dy_lo + it / nchunk, dx0 = (it % nchunk) * DXC;
+      uint32_t* blk = blk0 + b * blk_words;
+      for (int task = threadIdx.x; task < nbx_here * nby; task += NP) {
+        const int by = task / nbx_here, bx = task - by * nbx_here, bi = by * nbx + bx;
+        const uint16_t* fr = Rf + (by * S) * RP + shR + bx * S;
+        const uint16_t* gr = Tg + (by * S + dy + R) * TP + shT + bx * S + dx0;
+        uint32_t* o = blk + bi * BS;
+        uint32_t F[DXC], Cc[DXC], Wr[DXC], Kc[DXC];
+#pragma unroll
+        for (int j = 0; j < DXC; ++j) F[j] = Cc[j] = Wr[j] = Kc[j] = 0u;
+#pragma unroll
+        for (int yy = 0; yy < S; ++yy) {
+          uint32_t f[S], gg[S + DXC - 1];
+#pragma unroll
+          for (int k = 0; k < S; ++k) f[k] = fr[yy * RP + k];
+#pragma unroll
+          for (int k = 0; k < S + DXC - 1; ++k) gg[k] = gr[yy * TP + k];
+          uint32_t part[DXC], full[DXC];
+#pragma unroll
+          for (int j = 0; j < DXC; ++j) part[j] = RR > 0 ? f[0] * gg[j] : 0u;
+#pragma unroll
+          for (int k = 1; k < RR; ++k)
+#pragma unroll
+            for (int j = 0; j < DXC; ++j) part[j] += f[k] * gg[k + j];
+#pragma unroll
+          for (int j = 0; j < DXC; ++j) full[j] = part[j];
+#pragma unroll
+          for (int k = RR; k < S; ++k)
+#pragma unroll
+            for (int j = 0; j < DXC; ++j) full[j] += f[k] * gg[k + j];
+#pragma unroll
+          for (int j = 0; j < DXC; ++j) {
+            F[j] += full[j];
+            if (RR > 0) {
+              Cc[j] += part[j];
+              if (yy < RR) {
+                Wr[j] += full[j];
+                Kc[j] += part[j];
+              }
+            }
+          }
+        }
+        // columns past the chunk's last dx hold products with zero padding or
+        // the next chunk's dx: stored anyway (never read)
+#pragma unroll
+        for (int j = 0; j < DXC; ++j) {
+          o[j] = F[j];
+          if (RR > 0) {
+            o[DXC + j] = Cc[j];
+            o[2 * DXC + j] = Wr[j];
+            o[3 * DXC + j] = Kc[j];
+          }
+        }
+      }
+      named_bar_arrive(1 + b, NT);
+    }
+  } else {
+    // ---- consumers: phase B, one (POI column, dx of the chunk) per thread
+    const int tc = threadIdx.x - NP;
+    const size_t ew2 = (size_t)EW * EW;
+    const size_t out_step = (size_t)p.lat.nx * ew2;
+    for (int it = 0; it < n_items; ++it) {
+      const int b = it & 1;
+      named_bar_sync(1 + b, NT);  // producers finished item it
+      const int dy = dy_lo + it / nchunk, dx0 = (it % nchunk) * DXC, nd = min(DXC, EW - dx0);
+      const uint32_t* blk = blk0 + b * blk_words;
+      for (int t = tc; t < nx_here * nd; t += NC) {
+        const int pi = t / nd, dxi = t - pi * nd;
+        const uint32_t* col = blk + pi * BS + dxi;
+        uint64_t ring[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) ring[q] = 0;
+        int64_t* out = p.sfg + ((size_t)(iy0 - p.rb) * p.lat.nx + (ix0 + pi)) * ew2 + (size_t)(dy + R) * EW + dx0 + dxi;
+        for (int by = 0; by < nby; ++by, col += nbx * BS) {
+          uint64_t h = 0, hw = 0;
+#pragma unroll
+          for (int a = 0; a < Q; ++a) {
+            h += col[a * BS];
+            if (RR > 0) hw += col[a * BS + 2 * DXC];
+          }
+          if (RR > 0) {
+            h += col[Q * BS + DXC];
+            hw += col[Q * BS + 3 * DXC];
+          }
+          const int pj = by - Q + (RR == 0 ? 1 : 0);  // the POI row whose box ends here
+          if (RR > 0 && pj >= 0) {
+            uint64_t s = hw;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) s += ring[q];
+            out[(size_t)pj * out_step] = (int64_t)s;
+          }
+#pragma unroll
+          for (int q = 0; q < Q - 1; ++q) ring[q] = ring[q + 1];
+          ring[Q - 1] = h;
+          if (RR == 0 && pj >= 0) {
+            uint64_t s = 0;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) s += ring[q];
+            out[(size_t)pj * out_step] = (int64_t)s;
+          }
+        }
+      }
+      if (it + 2 < n_items) named_bar_arrive(3 + b, NT);  // buffer b free for item it + 2
+    }
+  }
+}
+
 // Per POI: the dy slices' filter winners -> the record (tc_argmax_kernel's
 // output, including "all positions degenerate"). Every candidate that can be
 // the exact maximum has a filter value within 2^-19 of the largest one (filter
@@ -562,12 +724,15 @@ __global__ void __launch_bounds__(256) bs_exact_kernel(TcParams p, const int* fl
 // kernel when one of them matches its lattice spacing and remainder.
 struct BsVariant {
   int S, RR, Q, DXC, NT, MINB;  // MINB: CTAs per SM the variant is sized for (shared memory, registers)
+  int NPW, NCW;                 // warp-specialised (bs_ws_kernel): producer / consumer warps; 0 = bs_kernel
 };
 constexpr BsVariant kVariants[] = {
-    {10, 1, 4, 25, 256, 1},  // c5: L 41, s 10, R 12
-    {10, 1, 3, 31, 256, 1},  // c2: L 31, s 10, R 15
-    {5, 1, 8, 11, 384, 1},   // c4: L 41, s 5, R 5
-    {8, 7, 3, 41, 256, 1},   // c3: L 31, s 8, R 20
+    {10, 1, 4, 25, 256, 1, 0, 0},  // c5: L 41, s 10, R 12
+    {10, 1, 3, 31, 256, 1, 0, 0},  // c2: L 31, s 10, R 15
+    {5, 1, 8, 11, 384, 1, 0, 0},   // c4: L 41, s 5, R 5
+    {8, 7, 3, 41, 256, 1, 0, 0},   // c3: L 31, s 8, R 20
+    {10, 1, 4, 13, 512, 1, 8, 8},  // c5, warp-specialised (2 dx chunks)
+    {5, 1, 8, 11, 512, 1, 12, 4},  // c4, warp-specialised (384 blocks per tile: 12 producer warps)
 };
 // Measured and dropped (C5, B200): two CTAs per SM with dx chunks of 13 / 9
 // (127 registers, 16 x 4 POI tiles to fit 110 KB): 0.93 / 0.98 ms against
@@ -618,17 +783,24 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
   int best = -1, waste = 1 << 30;
   const char* force = std::getenv("DICB200_BS_VARIANT");
   const int nvar = (int)(sizeof(kVariants) / sizeof(kVariants[0]));
-  for (int v = 0; v < nvar; ++v) {
-    if (kVariants[v].S != s || kVariants[v].RR != g.RR || kVariants[v].Q != g.q) continue;
-    if (force ? v != std::atoi(force) : kVariants[v].MINB != 1) continue;
-    const int nch = (g.EW + kVariants[v].DXC - 1) / kVariants[v].DXC;
-    const int w = nch * kVariants[v].DXC - g.EW;
-    if (w < waste) {
-      waste = w;
-      best = v;
+  // warp-specialised variants first (DICB200_BS_CLASSIC=1: the single-role kernel)
+  for (int pass = std::getenv("DICB200_BS_CLASSIC") ? 1 : 0; pass < 2 && best < 0; ++pass) {
+    for (int v = 0; v < nvar; ++v) {
+      if (kVariants[v].S != s || kVariants[v].RR != g.RR || kVariants[v].Q != g.q) continue;
+      if (force ? v != std::atoi(force) : (kVariants[v].MINB != 1 || (kVariants[v].NPW > 0) != (pass == 0)))
+        continue;
+      const int nch = (g.EW + kVariants[v].DXC - 1) / kVariants[v].DXC;
+      const int w = nch * kVariants[v].DXC - g.EW;
+      if (w < waste) {
+        waste = w;
+        best = v;
+      }
     }
   }
   if (best < 0) return false;
+  g.ws = kVariants[best].NPW > 0;
+  g.npw = kVariants[best].NPW;
+  g.ncw = kVariants[best].NCW;
   g.async_ok = p.planes == 2 && ((uintptr_t)p.ref.data % 8) == 0 && ((uintptr_t)p.tgt.data % 8) == 0 &&
                (p.ref.pitch % 4) == 0 && (p.tgt.pitch % 4) == 0;
   // fused argmax (opt-in, DICB200_BS_FUSE=1): record mode (not the swarm's
@@ -638,7 +810,7 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
   // POI-column phase B with its per-row reductions costs more than the HBM
   // round trip it removes (the unfused kernel writes the buffer while the IMAD
   // pipe is busy, and the argmax pass runs at 70% issue).
-  g.fuse = !p.surface && g.EW <= 32 && L <= 64 && L + g.EW - 1 <= 96 && std::getenv("DICB200_BS_FUSE") != nullptr;
+  g.fuse = !g.ws && !p.surface && g.EW <= 32 && L <= 64 && L + g.EW - 1 <= 96 && std::getenv("DICB200_BS_FUSE") != nullptr;
   g.DXC = kVariants[best].DXC;
   g.threads = kVariants[best].NT;
   g.minb = kVariants[best].MINB;
@@ -668,7 +840,8 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
     auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };
     g.off_tgt = al((size_t)g.RWp * g.RHp * pix);
     g.off_blk = al(g.off_tgt + (size_t)g.TWp * g.THp * pix);
-    g.off_state = al(g.off_blk + (size_t)g.nblk * (4 * g.EW + 1) * 4);
+    g.off_state = g.ws ? al(g.off_blk + 2 * (size_t)g.nblk * (4 * g.DXC + 1) * 4)  // two chunk buffers
+                       : al(g.off_blk + (size_t)g.nblk * (4 * g.EW + 1) * 4);
     g.smem = g.off_state + (g.fuse ? (size_t)g.PX * g.PY * sizeof(BsPoiState) : 0);
     if (g.smem <= smem_cap) break;
     if (g.PY > 2)
@@ -681,6 +854,19 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
   // dy slices so that the grid covers the SMs several times (tail balance)
   const long tiles = (long)((p.lat.nx + g.PX - 1) / g.PX) * ((rows + g.PY - 1) / g.PY);
   g.nsplit = (int)std::min<long>(g.EW, std::max<long>(1, (4L * num_sms() + tiles - 1) / tiles));
+  if (g.ws) {
+    // whole waves: per CTA ~ (dy rows + staging) units, ceil(CTAs / SMs) waves
+    double best_cost = 1e30;
+    for (int ns = std::max(1, (int)((2L * num_sms() + tiles - 1) / tiles)); ns <= g.EW; ++ns) {
+      const int per = (g.EW + ns - 1) / ns, ns2 = (g.EW + per - 1) / per;
+      const double cost = (double)((tiles * ns2 + num_sms() - 1) / num_sms()) * (per + 0.7);
+      if (cost < best_cost - 1e-9) {
+        best_cost = cost;
+        g.nsplit = ns2;
+      }
+    }
+  }
+  if (const char* e = std::getenv("DICB200_BS_NSPLIT")) g.nsplit = std::max(1, std::min(g.EW, std::atoi(e)));
   g.dy_per = (g.EW + g.nsplit - 1) / g.nsplit;
   g.nsplit = (g.EW + g.dy_per - 1) / g.dy_per;
   return tiles > 0;
@@ -719,10 +905,33 @@ size_t bs_slices_bytes(size_t npoi, const BsGeom& g) {
   return npoi * (size_t)g.nsplit * sizeof(BsSlice) + (npoi + 1) * sizeof(int);
 }
 
+template <int S, int RR, int Q, int DXC, int NPW, int NCW>
+cudaError_t launch_ws(const TcParams& p, const BsGeom& g, dim3 grid, cudaStream_t st) {
+  cudaError_t e = cudaSuccess;
+  auto go = [&](auto k) {
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+    if (e == cudaSuccess) k<<<grid, 32 * (NPW + NCW), g.smem, st>>>(p, g);
+  };
+  if (p.planes == 1)
+    go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint8_t>);
+  else
+    go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint16_t>);
+  return e;
+}
+
 cudaError_t bs_launch(const TcParams& p, const BsGeom& g, cudaStream_t st) {
   const int rows = p.re - p.rb;
   dim3 grid((p.lat.nx + g.PX - 1) / g.PX, (rows + g.PY - 1) / g.PY, g.nsplit);
   cudaError_t e = cudaErrorInvalidValue;
+  if (g.ws) {
+    if (g.S == 10 && g.RR == 1 && g.q == 4 && g.DXC == 13 && g.npw == 8 && g.ncw == 8)
+      e = launch_ws<10, 1, 4, 13, 8, 8>(p, g, grid, st);
+    if (g.S == 5 && g.RR == 1 && g.q == 8 && g.DXC == 11 && g.npw == 12 && g.ncw == 4)
+      e = launch_ws<5, 1, 8, 11, 12, 4>(p, g, grid, st);
+    count_launch();
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
   if (g.S == 10 && g.RR == 1 && g.q == 4 && g.DXC == 25) e = launch_variant<10, 1, 4, 25, 256, 1>(p, g, grid, st);
   if (g.S == 10 && g.RR == 1 && g.q == 3 && g.DXC == 31) e = launch_variant<10, 1, 3, 31, 256, 1>(p, g, grid, st);
   if (g.S == 5 && g.RR == 1 && g.q == 8 && g.DXC == 11) e = launch_variant<5, 1, 8, 11, 384, 1>(p, g, grid, st);

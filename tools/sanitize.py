@@ -79,10 +79,11 @@ def main() -> None:
             cmd += [sys.executable, os.path.abspath(__file__), "--case", name]
             t0 = time.time()
             try:
-                p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1200)
+                p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=int(os.environ.get("SANITIZE_TIMEOUT", "600")))
                 text, rc = p.stdout + p.stderr, p.returncode
             except subprocess.TimeoutExpired as e:
-                text, rc = (e.stdout or b"").decode() + "\nTIMEOUT", -1
+                out_ = e.stdout or ""
+                text, rc = (out_.decode() if isinstance(out_, bytes) else out_) + "\nTIMEOUT", -1
             with open(log, "w") as f:
                 f.write(text)
             m = re.search(r"ERROR SUMMARY: (\d+) error", text)
