@@ -425,11 +425,13 @@ __global__ void __launch_bounds__(NT, MINB) bs_kernel(TcParams p, BsGeom g) {
 // (loads and u64 adds) behind CTA barriers, so the IMAD pipe idles during
 // every phase B (ncu C5: fmaheavy 51 %, 8 warps/SM, 255 registers). Here the
 // dx range is cut into chunks of DXC (registers <= 128), phase A of item
-// (dy, chunk) runs on NPW producer warps while NCW consumer warps run phase B
-// of the previous item, over two block-partial buffers handed back and forth
-// with named barriers (FULL b: producers arrive, consumers wait; EMPTY b: the
-// reverse). Same partials, same u64 box sums, same cross-term buffer: the
-// records are bit-identical to bs_kernel's.
+// (dy, chunk) runs on NPW producer warps (one block per thread, partials in
+// registers) while NCW consumer warps run phase B of the previous item; the
+// producers store into the single block-partial buffer once the consumers have
+// released it (named barriers: FULL = 1, producers arrive / consumers wait;
+// EMPTY = 2, the reverse), so the buffer costs one item of shared memory and
+// the tile can be taller (less halo). Same partials, same u64 box sums, same
+// cross-term buffer: the records are bit-identical to bs_kernel's.
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -444,7 +446,7 @@ __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, 
   extern __shared__ __align__(16) unsigned char bs_smem[];
   uint16_t* Rf = reinterpret_cast<uint16_t*>(bs_smem);              // [RHp][RP]
   uint16_t* Tg = reinterpret_cast<uint16_t*>(bs_smem + g.off_tgt);  // [THp][TP]
-  uint32_t* blk0 = reinterpret_cast<uint32_t*>(bs_smem + g.off_blk);  // 2 x [nblk][F|C|W|K x DXC]
+  uint32_t* blk0 = reinterpret_cast<uint32_t*>(bs_smem + g.off_blk);  // [nblk][F|C|W|K x DXC]
   const int M = p.M, R = p.R, EW = g.EW, RP = g.RWp, TP = g.TWp;
   const int ix0 = blockIdx.x * g.PX, iy0 = p.rb + blockIdx.y * g.PY;
   const int dy_lo = -R + (int)blockIdx.z * g.dy_per, dy_hi = min(R, dy_lo + g.dy_per - 1);
@@ -457,22 +459,24 @@ __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, 
   const int nbx = g.nbx;
   const int nbx_here = nx_here + Q - (RR == 0 ? 1 : 0), nby = ny_here + Q - (RR == 0 ? 1 : 0);
   const int nchunk = g.nchunk, n_items = (dy_hi - dy_lo + 1) * nchunk;
-  const size_t blk_words = (size_t)g.nblk * BS;
   if (threadIdx.x < NP) {
-    // ---- producers: phase A of every item into buffer it & 1
+    // ---- producers: phase A of item it in registers (one block per thread),
+    // then, once the consumers have released the buffer, the store
+    // blocks spread evenly over the four SM sub-partitions (warp w issues on
+    // SMSP w % 4): each takes a contiguous quarter of the block list
+    const int w = threadIdx.x >> 5, per_smsp = (nbx_here * nby + 3) / 4, slot = (w >> 2) * 32 + (threadIdx.x & 31);
+    const int task = (w & 3) * per_smsp + slot;
+    const bool active = slot < per_smsp && task < nbx_here * nby;
+    const int by = active ? task / nbx_here : 0, bx = active ? task - by * nbx_here : 0, bi = by * nbx + bx;
+    const uint16_t* fr = Rf + (by * S) * RP + shR + bx * S;
+    uint32_t* o = blk0 + bi * BS;
     for (int it = 0; it < n_items; ++it) {
-      const int b = it & 1;
-      if (it >= 2) named_bar_sync(3 + b, NT);  // consumers are done with item it - 2
       const int dy = dy_lo + it / nchunk, dx0 = (it % nchunk) * DXC;
-      uint32_t* blk = blk0 + b * blk_words;
-      for (int task = threadIdx.x; task < nbx_here * nby; task += NP) {
-        const int by = task / nbx_here, bx = task - by * nbx_here, bi = by * nbx + bx;
-        const uint16_t* fr = Rf + (by * S) * RP + shR + bx * S;
-        const uint16_t* gr = Tg + (by * S + dy + R) * TP + shT + bx * S + dx0;
-        uint32_t* o = blk + bi * BS;
-        uint32_t F[DXC], Cc[DXC], Wr[DXC], Kc[DXC];
+      const uint16_t* gr = Tg + (by * S + dy + R) * TP + shT + bx * S + dx0;
+      uint32_t F[DXC], Cc[DXC], Wr[DXC], Kc[DXC];
 #pragma unroll
-        for (int j = 0; j < DXC; ++j) F[j] = Cc[j] = Wr[j] = Kc[j] = 0u;
+      for (int j = 0; j < DXC; ++j) F[j] = Cc[j] = Wr[j] = Kc[j] = 0u;
+      if (active) {
 #pragma unroll
         for (int yy = 0; yy < S; ++yy) {
           uint32_t f[S], gg[S + DXC - 1];
@@ -505,8 +509,11 @@ __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, 
             }
           }
         }
-        // columns past the chunk's last dx hold products with zero padding or
-        // the next chunk's dx: stored anyway (never read)
+      }
+      if (it >= 1) named_bar_sync(2, NT);  // consumers are done with item it - 1
+      // columns past the chunk's last dx hold products with zero padding or
+      // the next chunk's dx: stored anyway (never read)
+      if (active) {
 #pragma unroll
         for (int j = 0; j < DXC; ++j) {
           o[j] = F[j];
@@ -517,7 +524,7 @@ __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, 
           }
         }
       }
-      named_bar_arrive(1 + b, NT);
+      named_bar_arrive(1, NT);
     }
   } else {
     // ---- consumers: phase B, one (POI column, dx of the chunk) per thread
@@ -525,10 +532,9 @@ __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, 
     const size_t ew2 = (size_t)EW * EW;
     const size_t out_step = (size_t)p.lat.nx * ew2;
     for (int it = 0; it < n_items; ++it) {
-      const int b = it & 1;
-      named_bar_sync(1 + b, NT);  // producers finished item it
+      named_bar_sync(1, NT);  // producers stored item it
       const int dy = dy_lo + it / nchunk, dx0 = (it % nchunk) * DXC, nd = min(DXC, EW - dx0);
-      const uint32_t* blk = blk0 + b * blk_words;
+      const uint32_t* blk = blk0;
       for (int t = tc; t < nx_here * nd; t += NC) {
         const int pi = t / nd, dxi = t - pi * nd;
         const uint32_t* col = blk + pi * BS + dxi;
@@ -565,7 +571,7 @@ __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, 
           }
         }
       }
-      if (it + 2 < n_items) named_bar_arrive(3 + b, NT);  // buffer b free for item it + 2
+      if (it + 1 < n_items) named_bar_arrive(2, NT);  // buffer free for item it + 1
     }
   }
 }
@@ -725,14 +731,16 @@ __global__ void __launch_bounds__(256) bs_exact_kernel(TcParams p, const int* fl
 struct BsVariant {
   int S, RR, Q, DXC, NT, MINB;  // MINB: CTAs per SM the variant is sized for (shared memory, registers)
   int NPW, NCW;                 // warp-specialised (bs_ws_kernel): producer / consumer warps; 0 = bs_kernel
+  int PX0, PY0;                 // POI tile tried first (bs_plan halves it until it fits)
 };
 constexpr BsVariant kVariants[] = {
-    {10, 1, 4, 25, 256, 1, 0, 0},  // c5: L 41, s 10, R 12
-    {10, 1, 3, 31, 256, 1, 0, 0},  // c2: L 31, s 10, R 15
-    {5, 1, 8, 11, 384, 1, 0, 0},   // c4: L 41, s 5, R 5
-    {8, 7, 3, 41, 256, 1, 0, 0},   // c3: L 31, s 8, R 20
-    {10, 1, 4, 13, 512, 1, 8, 8},  // c5, warp-specialised (2 dx chunks)
-    {5, 1, 8, 11, 512, 1, 12, 4},  // c4, warp-specialised (384 blocks per tile: 12 producer warps)
+    {10, 1, 4, 25, 256, 1, 0, 0, 16, 8},    // c5: L 41, s 10, R 12
+    {10, 1, 3, 31, 256, 1, 0, 0, 16, 8},    // c2: L 31, s 10, R 15
+    {5, 1, 8, 11, 384, 1, 0, 0, 16, 8},     // c4: L 41, s 5, R 5
+    {8, 7, 3, 41, 256, 1, 0, 0, 16, 8},     // c3: L 31, s 8, R 20
+    // warp-specialised: producer blocks fill whole warps on every SM sub-partition
+    {10, 1, 4, 13, 512, 1, 8, 8, 12, 12},   // c5: 2 dx chunks, 12 x 12 POI tiles = 16 x 16 blocks
+    {5, 1, 8, 11, 512, 1, 12, 4, 16, 8},    // c4: 16 x 8 POI tiles = 24 x 16 blocks
 };
 // Measured and dropped (C5, B200): two CTAs per SM with dx chunks of 13 / 9
 // (127 registers, 16 x 4 POI tiles to fit 110 KB): 0.93 / 0.98 ms against
@@ -818,7 +826,7 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
   g.nchunk = (g.EW + g.DXC - 1) / g.DXC;
   const size_t pix = 2;  // staged as u16
   const int rows = p.re - p.rb;
-  for (g.PX = 16, g.PY = 8;; ) {
+  for (g.PX = kVariants[best].PX0, g.PY = kVariants[best].PY0;; ) {
     g.nbx = g.PX + g.q - (g.RR == 0 ? 1 : 0);
     g.nby = g.PY + g.q - (g.RR == 0 ? 1 : 0);
     g.nblk = g.nbx * g.nby;
@@ -840,10 +848,11 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
     auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };
     g.off_tgt = al((size_t)g.RWp * g.RHp * pix);
     g.off_blk = al(g.off_tgt + (size_t)g.TWp * g.THp * pix);
-    g.off_state = g.ws ? al(g.off_blk + 2 * (size_t)g.nblk * (4 * g.DXC + 1) * 4)  // two chunk buffers
+    g.off_state = g.ws ? al(g.off_blk + (size_t)g.nblk * (4 * g.DXC + 1) * 4)  // one chunk buffer
                        : al(g.off_blk + (size_t)g.nblk * (4 * g.EW + 1) * 4);
     g.smem = g.off_state + (g.fuse ? (size_t)g.PX * g.PY * sizeof(BsPoiState) : 0);
-    if (g.smem <= smem_cap) break;
+    // ws: at most one block per producer thread on each SM sub-partition
+    if (g.smem <= smem_cap && (!g.ws || (g.nblk + 3) / 4 <= 8 * g.npw)) break;
     if (g.PY > 2)
       g.PY /= 2;
     else if (g.PX > 4)
