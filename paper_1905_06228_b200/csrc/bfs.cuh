@@ -127,7 +127,7 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache = nullptr,
 struct BsGeom {
   int S, RR, q, PX, PY, nbx, nby, nblk, EW, DXC, nchunk, dy_per, nsplit;  // s, r, L / s, POI tile, blocks
   int RWp, RHp, TWp, THp;                                                // staged regions (pixels)
-  size_t off_tgt, off_blk, off_state, smem;
+  size_t off_tgt, off_blk, off_state, off_pos, smem;
   int threads;
   int fuse;      // exact argmax fused into the kernel (records via bs_merge_kernel), no cross-term buffer
   int minb;      // CTAs per SM the variant targets

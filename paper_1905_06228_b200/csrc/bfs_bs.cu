@@ -439,7 +439,51 @@ __device__ __forceinline__ void named_bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int S, int RR, int Q, int DXC, int NPW, int NCW, typename Pix>
+// 4-byte global -> shared async copy.
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
+// Fused bs_ws_kernel: stage the window data (1/sqrt(vg) filter factor, Sg) of
+// every position the tile's candidates at displacement row dy can touch:
+// [PYM rows][XW] with XW = (PX-1) step + 2R + 1 (0 outside the position domain:
+// such candidates are outside their windows anyway). Issued by the consumers
+// one dy ahead (cp.async, one commit group per dy).
+__device__ __forceinline__ void bs_stage_positions(const TcParams& p, const BsGeom& g, int ix0, int iy0, int ny_here,
+                                                   int dy, int XW, int PYM, float* rsq, uint32_t* s1, int t, int nt) {
+  const int x0 = p.lat.cx(ix0) - p.M - p.R - p.qx_min;
+  for (int xo = t; xo < XW; xo += nt) {
+    const int qx = x0 + xo;
+    const bool xok = qx >= 0 && qx < p.SW;
+    for (int j = 0; j < ny_here; ++j) {
+      const int qy = p.lat.cy(iy0 + j) - p.M + dy - p.qy_min;
+      float* dr = rsq + j * XW + xo;
+      uint32_t* ds = s1 + j * XW + xo;
+      if (xok && qy >= 0 && qy < p.SH) {
+        const size_t o = (size_t)qy * p.SW + qx;
+        cp_async4(dr, p.RSQ + o);
+        cp_async4(ds, p.S1 + o);
+      } else {
+        *dr = 0.0f;
+        *ds = 0u;
+      }
+    }
+  }
+  (void)PYM;
+  (void)g;
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+// One dx lane's slice result for one POI (fused bs_ws_kernel, end-of-tile reduction).
+struct BsLane {
+  long long num;
+  float a1, a2;
+  uint32_t dc;
+  uint32_t pad;
+};
+
+template <int S, int RR, int Q, int DXC, int NPW, int NCW, typename Pix, bool FUSE = false, int PYM = 1>
 __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, BsGeom g) {
   constexpr int NT = 32 * (NPW + NCW), NP = 32 * NPW, NC = 32 * NCW;
   constexpr int BS = 4 * DXC + 1;  // words per block record (odd: conflict-free stores across blocks)
@@ -454,8 +498,25 @@ __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, 
   const int TX0 = RX0 - R, TY0 = RY0 - R;
   int shR = 0, shT = 0;
   bs_stage<Pix, NT>(p, g, Rf, Tg, RX0, RY0, TX0, TY0, dy_lo, dy_hi, DXC, shR, shT);
-  __syncthreads();
   const int nx_here = min(g.PX, p.lat.nx - ix0), ny_here = min(g.PY, p.re - iy0);
+  if (FUSE) {  // POI constants of the tile: 1 / sqrt(vf) (0: degenerate subset), Sf
+    float* prs = reinterpret_cast<float*>(bs_smem + g.off_state);
+    uint32_t* psf = reinterpret_cast<uint32_t*>(prs + g.PX * g.PY);
+    for (int i = threadIdx.x; i < g.PX * g.PY; i += NT) {
+      const int qi = i % g.PX, qj = i / g.PX;
+      float r = 0.0f;
+      uint32_t sf = 0;
+      if (qi < nx_here && qj < ny_here) {
+        const size_t k = (size_t)(iy0 + qj - p.rb) * p.lat.nx + (ix0 + qi);
+        const double svf = p.poi_sqrtvf[k];
+        r = svf > 0.0 ? (float)(1.0 / svf) : 0.0f;
+        sf = (uint32_t)p.poi_sf[k];
+      }
+      prs[i] = r;
+      psf[i] = sf;
+    }
+  }
+  __syncthreads();
   const int nbx = g.nbx;
   const int nbx_here = nx_here + Q - (RR == 0 ? 1 : 0), nby = ny_here + Q - (RR == 0 ? 1 : 0);
   const int nchunk = g.nchunk, n_items = (dy_hi - dy_lo + 1) * nchunk;
@@ -525,6 +586,150 @@ __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, 
         }
       }
       named_bar_arrive(1, NT);
+    }
+  } else if (FUSE) {
+    // ---- fused consumers: phase B and the exact-argmax filter. Thread
+    // (POI column pi, dx lane dxi) handles dx = c DXC + dxi of every chunk c and
+    // keeps, per POI row of the tile, its best filter value, runner-up, the
+    // best's exact numerator and dx/dy, and its candidate count in registers;
+    // the tile's slice result per POI is reduced over the dx lanes at the end
+    // (bs_merge_kernel then combines the dy slices exactly, near ties included).
+    const int tc = threadIdx.x - NP;
+    const bool act = tc < nx_here * DXC;
+    const int pi = act ? tc / DXC : 0, dxi = act ? tc - pi * DXC : 0;
+    const float* poi_rsvf = reinterpret_cast<const float*>(bs_smem + g.off_state);            // [PY][PX]
+    const uint32_t* poi_sf = reinterpret_cast<const uint32_t*>(poi_rsvf + g.PX * g.PY);        // [PY][PX]
+    const uint32_t n = (uint32_t)(p.side * p.side);
+    const int cxp = p.lat.cx(ix0 + pi);
+    const int fx_lo = max(-R, M - cxp), fx_hi = min(R, p.tgt.width - 1 - M - cxp);
+    float a1[PYM], a2[PYM];
+    long long num1[PYM];
+    uint32_t dc[PYM];  // count (bits 0-15) | dx index (16-23) | dy index (24-31) of the best
+#pragma unroll
+    for (int j = 0; j < PYM; ++j) {
+      a1[j] = a2[j] = -3.0f;
+      num1[j] = 0;
+      dc[j] = 0;
+    }
+    const int XW = (g.PX - 1) * p.lat.step + 2 * R + 1;
+    float* pos_rsq = reinterpret_cast<float*>(bs_smem + g.off_pos);  // [2][PYM][XW]
+    uint32_t* pos_s1 = reinterpret_cast<uint32_t*>(pos_rsq + 2 * PYM * XW);
+    bs_stage_positions(p, g, ix0, iy0, ny_here, dy_lo, XW, PYM, pos_rsq, pos_s1, tc, NC);
+    for (int it = 0; it < n_items; ++it) {
+      const int dy = dy_lo + it / nchunk, dxv = (it % nchunk) * DXC + dxi - R;
+      const int pb = (dy - dy_lo) & 1;
+      if (it % nchunk == 0) {  // new dy: its window data landed, the next dy's starts
+        named_bar_sync(3, NC);   // every consumer is done with dy - 1: its buffer is free
+        if (dy < dy_hi) {
+          bs_stage_positions(p, g, ix0, iy0, ny_here, dy + 1, XW, PYM, pos_rsq + (pb ^ 1) * PYM * XW,
+                             pos_s1 + (pb ^ 1) * PYM * XW, tc, NC);
+          asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        named_bar_sync(3, NC);
+      }
+      named_bar_sync(1, NT);  // producers stored item it
+      const bool xin = act && dxv <= R && dxv >= fx_lo && dxv <= fx_hi;
+      if (__any_sync(0xffffffffu, xin)) {
+        const uint32_t* col = blk0 + pi * BS + dxi;
+        const int xo = pi * p.lat.step + dxv + R;
+        const float* prow = pos_rsq + pb * PYM * XW + xo;
+        const uint32_t* srow = pos_s1 + pb * PYM * XW + xo;
+        uint64_t ring[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) ring[q] = 0;
+#pragma unroll
+        for (int by = 0; by < PYM + Q; ++by) {
+          if (by >= nby) break;  // uniform
+          uint64_t h = 0, hw = 0;
+#pragma unroll
+          for (int a = 0; a < Q; ++a) {
+            h += col[a * BS];
+            if (RR > 0) hw += col[a * BS + 2 * DXC];
+          }
+          if (RR > 0) {
+            h += col[Q * BS + DXC];
+            hw += col[Q * BS + 3 * DXC];
+          }
+          col += nbx * BS;
+          constexpr int sh = RR == 0 ? 1 : 0;
+          uint64_t sfg = 0;
+          if (RR > 0) {
+            sfg = hw;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) sfg += ring[q];
+          }
+#pragma unroll
+          for (int q = 0; q < Q - 1; ++q) ring[q] = ring[q + 1];
+          ring[Q - 1] = h;
+          if (RR == 0) {
+            sfg = 0;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) sfg += ring[q];
+          }
+          const int pj = by - Q + sh;  // the POI row whose box ends here (compile-time per step)
+          if (pj < 0 || pj >= PYM) continue;
+          const int cyp = p.lat.cy(iy0 + pj);
+          const float rsvf = poi_rsvf[pj * g.PX + pi];  // (pj >= ny_here: 0)
+          // integer_search.cpp:11-21 window; degenerate reference subset (rsvf 0): no candidates
+          // branch-free: an invalid candidate gets filter value -3 (never kept) and counts 0
+          const float rsq = prow[pj * XW];
+          // constant target window (rsq 0): skipped, not counted (tc_candidate_f)
+          const bool valid = xin && pj < ny_here && rsvf > 0.0f && rsq > 0.0f && dy >= max(-R, M - cyp) &&
+                             dy <= min(R, p.tgt.height - 1 - M - cyp);
+          const int64_t num = (int64_t)(sfg * n - (uint64_t)poi_sf[pj * g.PX + pi] * srow[pj * XW]);
+          const float a = valid ? __fmul_rn(__fmul_rn(__ll2float_rn(num), rsvf), rsq) : -3.0f;  // approx_zncc
+          const bool better = a > a1[pj];
+          a2[pj] = fmaxf(a2[pj], fminf(a, a1[pj]));  // runner-up (equal values: a near tie)
+          a1[pj] = fmaxf(a1[pj], a);
+          num1[pj] = better ? num : num1[pj];
+          dc[pj] = (better ? (((uint32_t)(dxv + R) << 16) | ((uint32_t)(dy + R) << 24)) : (dc[pj] & 0xffff0000u)) |
+                   ((dc[pj] & 0xffffu) + (valid ? 1u : 0u));
+        }
+      }
+      if (it + 1 < n_items) named_bar_arrive(2, NT);  // buffer free for item it + 1
+    }
+    // ---- slice result per POI: reduce the DXC dx lanes (through the free block buffer)
+    named_bar_sync(3, NC);  // every consumer is past its last read of the block buffer
+    BsLane* lanes = reinterpret_cast<BsLane*>(blk0);  // [PY][PX][DXC]
+    if (act) {
+#pragma unroll
+      for (int j = 0; j < PYM; ++j) {
+        if (j < ny_here) {
+          BsLane& l = lanes[(j * g.PX + pi) * DXC + dxi];
+          l.num = num1[j];
+          l.a1 = a1[j];
+          l.a2 = a2[j];
+          l.dc = dc[j];
+        }
+      }
+    }
+    named_bar_sync(3, NC);
+    for (int i = tc; i < nx_here * ny_here; i += NC) {
+      const int qi = i % nx_here, qj = i / nx_here;
+      const BsLane* l = lanes + (qj * g.PX + qi) * DXC;
+      BsSlice b;
+      b.num = 0;
+      b.a1 = b.a2 = -3.0f;
+      b.cnt = 0;
+      b.dx = b.dy = 0;
+      for (int d = 0; d < DXC; ++d) {
+        const BsLane v = l[d];
+        b.cnt += (int)(v.dc & 0xffffu);
+        if (v.a1 > b.a1) {
+          b.a2 = fmaxf(b.a1, v.a2);
+          b.a1 = v.a1;
+          b.num = v.num;
+          b.dx = (short)((int)((v.dc >> 16) & 0xffu) - R);
+          b.dy = (short)((int)(v.dc >> 24) - R);
+        } else {
+          b.a2 = fmaxf(b.a2, v.a1);  // equal values: a near tie, see bs_merge_kernel
+        }
+        b.a2 = fmaxf(b.a2, v.a2);
+      }
+      const size_t k = (size_t)(iy0 + qj - p.rb) * p.lat.nx + (ix0 + qi);
+      reinterpret_cast<BsSlice*>(p.slices)[k * g.nsplit + blockIdx.z] = b;
     }
   } else {
     // ---- consumers: phase B, one (POI column, dx of the chunk) per thread
@@ -818,8 +1023,11 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
   // POI-column phase B with its per-row reductions costs more than the HBM
   // round trip it removes (the unfused kernel writes the buffer while the IMAD
   // pipe is busy, and the argmax pass runs at 70% issue).
-  g.fuse = !g.ws && !p.surface && g.EW <= 32 && L <= 64 && L + g.EW - 1 <= 96 && std::getenv("DICB200_BS_FUSE") != nullptr;
+  g.fuse = g.ws ? (!p.surface && L <= 64 && L + g.EW - 1 <= 96 && std::getenv("DICB200_BS_UNFUSED") == nullptr)
+               : !p.surface && g.EW <= 32 && L <= 64 && L + g.EW - 1 <= 96 && std::getenv("DICB200_BS_FUSE") != nullptr;
   g.DXC = kVariants[best].DXC;
+  // fused ws: one consumer thread per (POI column, dx lane) of the widest tile
+  if (g.ws && g.fuse && kVariants[best].PX0 * g.DXC > 32 * g.ncw) g.fuse = 0;
   g.threads = kVariants[best].NT;
   g.minb = kVariants[best].MINB;
   const size_t smem_cap = g.minb > 1 ? (size_t)(227 * 1024 / g.minb - 1024) : (size_t)220 * 1024;
@@ -850,9 +1058,15 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
     g.off_blk = al(g.off_tgt + (size_t)g.TWp * g.THp * pix);
     g.off_state = g.ws ? al(g.off_blk + (size_t)g.nblk * (4 * g.DXC + 1) * 4)  // one chunk buffer
                        : al(g.off_blk + (size_t)g.nblk * (4 * g.EW + 1) * 4);
-    g.smem = g.off_state + (g.fuse ? (size_t)g.PX * g.PY * sizeof(BsPoiState) : 0);
+    g.smem = g.off_state + (g.fuse ? (size_t)g.PX * g.PY * (g.ws ? 8 : sizeof(BsPoiState)) : 0);
+    g.off_pos = al(g.smem);
+    if (g.ws && g.fuse)  // window data of two dy rows: [2][PY][XW] x (1/sqrt(vg), Sg)
+      g.smem = g.off_pos + 2 * (size_t)g.PY * ((g.PX - 1) * s + g.EW) * 8 + 4 * g.DXC;  // + the unused lanes' overrun
     // ws: at most one block per producer thread on each SM sub-partition
-    if (g.smem <= smem_cap && (!g.ws || (g.nblk + 3) / 4 <= 8 * g.npw)) break;
+    // fused ws: the end-of-tile lane reduction reuses the block buffer
+    const bool lanes_fit = !(g.ws && g.fuse) || (size_t)g.PX * g.PY * g.DXC * sizeof(BsLane) <=
+                                                     (size_t)g.nblk * (4 * g.DXC + 1) * 4;
+    if (g.smem <= smem_cap && lanes_fit && (!g.ws || (g.nblk + 3) / 4 <= 8 * g.npw)) break;
     if (g.PY > 2)
       g.PY /= 2;
     else if (g.PX > 4)
@@ -914,17 +1128,19 @@ size_t bs_slices_bytes(size_t npoi, const BsGeom& g) {
   return npoi * (size_t)g.nsplit * sizeof(BsSlice) + (npoi + 1) * sizeof(int);
 }
 
-template <int S, int RR, int Q, int DXC, int NPW, int NCW>
+template <int S, int RR, int Q, int DXC, int NPW, int NCW, int PYM>
 cudaError_t launch_ws(const TcParams& p, const BsGeom& g, dim3 grid, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
   auto go = [&](auto k) {
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
     if (e == cudaSuccess) k<<<grid, 32 * (NPW + NCW), g.smem, st>>>(p, g);
   };
+  if (g.PY > PYM) return cudaErrorInvalidValue;
   if (p.planes == 1)
-    go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint8_t>);
+    g.fuse ? go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint8_t, true, PYM>) : go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint8_t>);
   else
-    go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint16_t>);
+    g.fuse ? go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint16_t, true, PYM>)
+           : go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint16_t>);
   return e;
 }
 
@@ -934,9 +1150,9 @@ cudaError_t bs_launch(const TcParams& p, const BsGeom& g, cudaStream_t st) {
   cudaError_t e = cudaErrorInvalidValue;
   if (g.ws) {
     if (g.S == 10 && g.RR == 1 && g.q == 4 && g.DXC == 13 && g.npw == 8 && g.ncw == 8)
-      e = launch_ws<10, 1, 4, 13, 8, 8>(p, g, grid, st);
+      e = launch_ws<10, 1, 4, 13, 8, 8, 12>(p, g, grid, st);
     if (g.S == 5 && g.RR == 1 && g.q == 8 && g.DXC == 11 && g.npw == 12 && g.ncw == 4)
-      e = launch_ws<5, 1, 8, 11, 12, 4>(p, g, grid, st);
+      e = launch_ws<5, 1, 8, 11, 12, 4, 8>(p, g, grid, st);
     count_launch();
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
