@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(256) bits_check_kernel(const Pix* data, int pi
   const bool vec = ((uintptr_t)data % 16) == 0 && ((size_t)pitch * sizeof(Pix)) % 16 == 0;
   uint32_t mx = 0;
   const int chunks = (w + per - 1) / per;
+#pragma unroll 4
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < (long)chunks * h; i += (long)gridDim.x * blockDim.x) {
     const int y = (int)(i / chunks), c = (int)(i - (long)y * chunks), x0 = c * per;
     const Pix* row = data + (size_t)y * pitch;
@@ -241,10 +242,10 @@ static dicb200_status enqueue_bits_guard(const dicb200_image* ref, const dicb200
     const uint32_t limit = (1u << im->bits) - 1u;
     const int pitch = im->pitch > 0 ? im->pitch : im->width;
     if (im->dtype == DICB200_U8)
-      bits_check_kernel<uint8_t><<<2 * 148, 256, 0, st>>>(static_cast<const uint8_t*>(im->data), pitch, im->width,
+      bits_check_kernel<uint8_t><<<8 * 148, 256, 0, st>>>(static_cast<const uint8_t*>(im->data), pitch, im->width,
                                                            im->height, limit, flag);
     else
-      bits_check_kernel<uint16_t><<<2 * 148, 256, 0, st>>>(static_cast<const uint16_t*>(im->data), pitch, im->width,
+      bits_check_kernel<uint16_t><<<8 * 148, 256, 0, st>>>(static_cast<const uint16_t*>(im->data), pitch, im->width,
                                                             im->height, limit, flag);
     count_launch();
   }
