@@ -839,15 +839,136 @@ __global__ void __launch_bounds__(256) bs_merge_kernel(TcParams p, int nsplit, i
 // staged in shared memory, exact u64 cross terms per candidate (thread per
 // candidate), exact quotients, block argmax in improves() order.
 constexpr int kExactMaxSide = 64, kExactMaxWin = 96;
+// Flagged POIs, fast path: CTA (slot, candidate row) computes the exact cross
+// terms of one displacement row of one flagged POI — warp per dx, lanes across
+// the subset columns (u32 per lane: < 2 x side x 2^24 products, then u64 warp
+// sums) — and its row argmax / count; the last CTA of a POI (arrival counter)
+// merges the rows in improves() order and writes the record. A flagged POI is
+// 1 M exact MACs (C5): spread over 2R+1 CTAs instead of one (measured: the
+// single-CTA search cost ~70 us per pair with one or two flagged POIs; the
+// single-CTA bs_exact_kernel below takes the slots past kExactSlots).
+constexpr int kExactSlots = 256;
+constexpr int kExactRowWarps = 32;  // dx per CTA (2R+1 <= 32)
 template <typename Pix>
-__global__ void __launch_bounds__(256) bs_exact_kernel(TcParams p, const int* flagged, const int* n_flagged) {
+__global__ void __launch_bounds__(32 * kExactRowWarps) bs_exact_rows_kernel(TcParams p, const int* flagged,
+                                                                           const int* n_flagged, BestPartial* part,
+                                                                           int* arrivals) {
+  __shared__ uint16_t fs[kExactMaxSide * kExactMaxSide];
+  __shared__ uint16_t gs[kExactMaxSide * kExactMaxWin];
+  __shared__ double red_c[kExactRowWarps];
+  __shared__ int red_d[kExactRowWarps][3];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nf = min(*n_flagged, kExactSlots);
+  const int ry = blockIdx.y;
+  for (int i = blockIdx.x; i < nf; i += gridDim.x) {
+  const size_t k = (size_t)flagged[i];
+  const int ix = (int)(k % p.lat.nx), iy = p.rb + (int)(k / p.lat.nx);
+  const int cx = p.lat.cx(ix), cy = p.lat.cy(iy), M = p.M, R = p.R, side = p.side;
+  const int fx_lo = max(-R, M - cx), fx_hi = min(R, p.tgt.width - 1 - M - cx);
+  const int fy_lo = max(-R, M - cy), fy_hi = min(R, p.tgt.height - 1 - M - cy);
+  const int fw = fx_hi - fx_lo + 1, fh = fy_hi - fy_lo + 1, ww = fw + side - 1;
+  if (ry >= fh) continue;  // rows past the feasible window: no CTA work, no arrival (uniform)
+  const int dy = fy_lo + ry;
+  const Pix* f = static_cast<const Pix*>(p.ref.data);
+  const Pix* g = static_cast<const Pix*>(p.tgt.data);
+  __syncthreads();  // the previous slot's reduction is done with the staged data
+  for (int t = tid; t < side * side; t += blockDim.x) {
+    const int r = t / side, c = t - r * side;
+    fs[t] = (uint16_t)f[(size_t)(cy - M + r) * p.ref.pitch + (cx - M + c)];
+  }
+  for (int t = tid; t < ww * side; t += blockDim.x) {
+    const int r = t / ww, c = t - r * ww;
+    gs[t] = (uint16_t)g[(size_t)(cy - M + dy + r) * p.tgt.pitch + (cx - M + fx_lo + c)];
+  }
+  __syncthreads();
+  BestPartial b;
+  b.c = -2.0;
+  b.dx = b.dy = 0;
+  b.count = 0;
+  b.found = 0;
+  if (warp < fw) {
+    const int dx = fx_lo + warp;
+    const size_t o = (size_t)(cy - M + dy - p.qy_min) * p.SW + (cx - M + dx - p.qx_min);
+    const double sq = p.SQ[o];
+    if (sq > 0.0) {  // constant target window: skipped, not counted
+      uint64_t acc64 = 0;  // each product < 2^32 (16-bit pixels), sums exact in u64
+      for (int r = 0; r < side; ++r) {
+        const uint16_t* fr = fs + r * side;
+        const uint16_t* gr = gs + r * ww + warp;
+        for (int c = lane; c < side; c += 32) acc64 += (uint64_t)((uint32_t)fr[c] * gr[c]);
+      }
+#pragma unroll
+      for (int o2 = 16; o2; o2 >>= 1) acc64 += __shfl_xor_sync(0xffffffffu, acc64, o2);
+      const uint32_t n = (uint32_t)(side * side), sf = (uint32_t)p.poi_sf[k];
+      const int64_t num = (int64_t)(acc64 * n - (uint64_t)sf * p.S1[o]);
+      b.c = bs_i64_to_f64(num) / (p.poi_sqrtvf[k] * sq);
+      b.dx = dx;
+      b.dy = dy;
+      b.count = 1;
+      b.found = 1;
+    }
+  }
+  if (lane == 0) {
+    red_c[warp] = b.found ? b.c : -3.0;
+    red_d[warp][0] = b.found ? b.dx : 0x7fff;
+    red_d[warp][1] = b.found ? b.dy : 0x7fff;
+    red_d[warp][2] = b.count;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    BestPartial t;
+    t.c = -2.0;
+    t.dx = t.dy = 0;
+    t.count = 0;
+    t.found = 0;
+    for (int w2 = 0; w2 < kExactRowWarps; ++w2) {
+      BestPartial q;
+      q.c = red_c[w2];
+      q.dx = red_d[w2][0];
+      q.dy = red_d[w2][1];
+      q.count = red_d[w2][2];
+      q.found = red_d[w2][0] != 0x7fff;
+      merge_best(t, q);
+    }
+    part[(size_t)i * kExactMaxWin + ry] = t;
+    __threadfence();
+    s_last = atomicAdd(&arrivals[i], 1) == fh - 1;
+  }
+  __syncthreads();
+  if (s_last && tid == 0) {  // every row of this POI is in: merge (rows in dy order, improves() decides)
+    __threadfence();
+    BestPartial t;
+    t.c = -2.0;
+    t.dx = t.dy = 0;
+    t.count = 0;
+    t.found = 0;
+    for (int r = 0; r < fh; ++r) {
+      const BestPartial* src = part + (size_t)i * kExactMaxWin + r;  // written by other CTAs: read through L2
+      BestPartial q;
+      q.c = __ldcg(&src->c);
+      q.dx = __ldcg(&src->dx);
+      q.dy = __ldcg(&src->dy);
+      q.count = __ldcg(&src->count);
+      q.found = __ldcg(&src->found);
+      merge_best(t, q);
+    }
+    arrivals[i] = 0;
+    write_integer_record(p.rec[k], cx, cy, t, p.subpixel_none);
+  }
+  }
+}
+
+template <typename Pix>
+__global__ void __launch_bounds__(256) bs_exact_kernel(TcParams p, const int* flagged, const int* n_flagged,
+                                                       int first_slot) {
   __shared__ uint16_t fs[kExactMaxSide * kExactMaxSide];
   __shared__ uint16_t gs[kExactMaxWin * kExactMaxWin];
   __shared__ double red_c[8];
   __shared__ int red_d[8][3];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nf = *n_flagged;
-  for (int i = blockIdx.x; i < nf; i += gridDim.x) {
+  for (int i = first_slot + blockIdx.x; i < nf; i += gridDim.x) {  // earlier slots: bs_exact_rows_kernel
     const size_t k = (size_t)flagged[i];
     const int ix = (int)(k % p.lat.nx), iy = p.rb + (int)(k / p.lat.nx);
     const int cx = p.lat.cx(ix), cy = p.lat.cy(iy), M = p.M, R = p.R, side = p.side;
@@ -1097,10 +1218,15 @@ bool bs_plan(const TcParams& p, BsGeom& g) {
 
 cudaError_t bs_merge_launch(const TcParams& p, const BsGeom& g, cudaStream_t st) {
   const size_t npoi = (size_t)(p.re - p.rb) * p.lat.nx;
-  // scratch after the slice records: [n_flagged][flagged POIs]
+  // scratch after the slice records: [n_flagged][flagged POIs][row arrivals x
+  // kExactSlots][row partials x kExactSlots x kExactMaxWin] (bs_slices_bytes)
   int* n_flagged = reinterpret_cast<int*>(reinterpret_cast<BsSlice*>(p.slices) + npoi * g.nsplit);
   int* flagged = n_flagged + 1;
+  int* arrivals = flagged + npoi;
+  BestPartial* part = reinterpret_cast<BestPartial*>(
+      (reinterpret_cast<uintptr_t>(arrivals + kExactSlots) + 15) & ~(uintptr_t)15);
   cudaError_t e = cudaMemsetAsync(n_flagged, 0, sizeof(int), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(arrivals, 0, kExactSlots * sizeof(int), st);
   if (e != cudaSuccess) return e;
   bs_merge_kernel<<<(unsigned)((npoi + 255) / 256), 256, 0, st>>>(p, g.nsplit, flagged, n_flagged);
   count_launch();
@@ -1114,18 +1240,31 @@ cudaError_t bs_merge_launch(const TcParams& p, const BsGeom& g, cudaStream_t st)
     for (size_t i = 0; i < h.size() && i < 16; ++i)
       fprintf(stderr, "  slice %zu: a1 %.9g a2 %.9g cnt %d d (%d,%d)\n", i, h[i].a1, h[i].a2, h[i].cnt, h[i].dx, h[i].dy);
   }
-  // one CTA per flagged POI (grid-stride; near ties are rare, idle CTAs exit at once)
+  // flagged POIs (near ties are rare: idle CTAs exit at once): a CTA per
+  // (slot, displacement row), slots strided over 16 CTA columns; past
+  // kExactSlots, one CTA per POI
+  const int ew = 2 * p.R + 1;
+  const bool rows_ok = ew <= kExactRowWarps && p.side <= kExactMaxSide && p.side + ew - 1 <= kExactMaxWin;
+  if (rows_ok) {
+    const dim3 grid(16, ew);
+    if (p.planes == 1)
+      bs_exact_rows_kernel<uint8_t><<<grid, 32 * kExactRowWarps, 0, st>>>(p, flagged, n_flagged, part, arrivals);
+    else
+      bs_exact_rows_kernel<uint16_t><<<grid, 32 * kExactRowWarps, 0, st>>>(p, flagged, n_flagged, part, arrivals);
+    count_launch();
+  }
   const unsigned ctas = (unsigned)std::min<size_t>(npoi, 148);
   if (p.planes == 1)
-    bs_exact_kernel<uint8_t><<<ctas, 256, 0, st>>>(p, flagged, n_flagged);
+    bs_exact_kernel<uint8_t><<<ctas, 256, 0, st>>>(p, flagged, n_flagged, rows_ok ? kExactSlots : 0);
   else
-    bs_exact_kernel<uint16_t><<<ctas, 256, 0, st>>>(p, flagged, n_flagged);
+    bs_exact_kernel<uint16_t><<<ctas, 256, 0, st>>>(p, flagged, n_flagged, rows_ok ? kExactSlots : 0);
   count_launch();
   return cudaGetLastError();
 }
 
 size_t bs_slices_bytes(size_t npoi, const BsGeom& g) {
-  return npoi * (size_t)g.nsplit * sizeof(BsSlice) + (npoi + 1) * sizeof(int);
+  return npoi * (size_t)g.nsplit * sizeof(BsSlice) + (npoi + 1 + kExactSlots) * sizeof(int) + 16 +
+         (size_t)kExactSlots * kExactMaxWin * sizeof(BestPartial);
 }
 
 template <int S, int RR, int Q, int DXC, int NPW, int NCW, int PYM>

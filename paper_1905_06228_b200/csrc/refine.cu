@@ -920,14 +920,19 @@ constexpr int kFixedPad = 3, kFixedSpread = 3;
 template <int FM, int FSTEP>
 struct FixedGeom {
   static constexpr int SIDE = 2 * FM + 1, SPAN = FSTEP * (kWarps - 1);
-  static constexpr int RP = SPAN + SIDE + 2, RH = SIDE + 2;
-  // target pitch padded to a power of two when that costs < 8 columns of pairs
-  // (the tap address is then two shifts on the ALU pipe instead of IMADs)
-  static constexpr int TP0 = SPAN + SIDE + 2 * kFixedPad + 2 * kFixedSpread;
-  static constexpr int TP = (TP0 <= 128 && TP0 > 120) ? 128 : (TP0 <= 64 && TP0 > 56) ? 64 : TP0;
+  // reference pitch: the SPAN + SIDE + 2 region columns plus up to 3 columns of
+  // slack, a multiple of 4 (the pre-converted TMA boxes start 16-byte aligned)
+  static constexpr int RP = (SPAN + SIDE + 2 + 3 + 3) & ~3, RH = SIDE + 2;
+  // target pitch: the region plus one column of slack (even box start for the
+  // pre-converted pairs), padded to a power of two when that costs < 8 columns
+  // of pairs (the tap address is then two shifts on the ALU pipe instead of
+  // IMADs), else to an even width (16-byte box rows)
+  static constexpr int TP0 = SPAN + SIDE + 2 * kFixedPad + 2 * kFixedSpread + 1;
+  static constexpr int TP = (TP0 <= 128 && TP0 > 120) ? 128 : (TP0 <= 64 && TP0 > 56) ? 64 : (TP0 + 1) & ~1;
   static constexpr int TH = SIDE + 2 * kFixedPad + 2 * kFixedSpread;  // float rows; TH - 1 pair rows
-  static constexpr size_t G2_OFF = (((size_t)RH * RP + 3) & ~(size_t)3);  // floats (16-byte aligned)
-  static constexpr size_t T2_OFF = G2_OFF + 2 * (size_t)RH * RP;
+  // floats; 128-byte aligned (TMA destinations of the pre-converted staging)
+  static constexpr size_t G2_OFF = (((size_t)RH * RP + 31) & ~(size_t)31);
+  static constexpr size_t T2_OFF = ((G2_OFF + 2 * (size_t)RH * RP) + 31) & ~(size_t)31;
   static constexpr size_t SMEM = 4 * (T2_OFF + 2 * (size_t)(TH - 1) * TP);
   // TMA boxes of the raw u8/u16 regions (inner extent a multiple of 16 bytes),
   // landed inside the gradient area, which is only written after they are converted
@@ -981,15 +986,17 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
   constexpr bool FIXED = FM > 0;
   using FG = FixedGeom<FIXED ? FM : 1, FIXED ? FSTEP : 1>;
   using RAW = typename FG::template Raw<(int)sizeof(Pix)>;
-  extern __shared__ __align__(16) float smem_f[];
+  extern __shared__ __align__(128) float smem_f[];
   __shared__ uint64_t s_bar;  // TMA staging completion
   __shared__ int s_idx[kWarps], s_idy[kWarps], s_ok[kWarps];
   __shared__ WarpConst s_const[kWarps];
   __shared__ StripGeom G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int M = p.M, side = 2 * M + 1, n = side * side;
-  const int iy = p.row_begin + blockIdx.y;
-  const int ix0 = blockIdx.x * p.spc;
+  // strip of this CTA: launch order from p.order (NR: likely long walks first), else the grid
+  const int strip = p.order ? p.order[blockIdx.y * gridDim.x + blockIdx.x] : (int)(blockIdx.y * gridDim.x + blockIdx.x);
+  const int iy = p.row_begin + strip / (int)gridDim.x;
+  const int ix0 = (strip % (int)gridDim.x) * p.spc;
   const int ts = min(p.spc, p.lat.nx - ix0);
   const int cy = p.lat.cy(iy);
   const size_t rec0 = (size_t)(iy - p.row_begin) * p.lat.nx + ix0;
@@ -1048,7 +1055,18 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
         G.tY0 = cy + dyc - kFixedSpread - M - kFixedPad;
         G.tP = FG::TP;
         G.tH = FG::TH;
-        if (p.use_tma) {
+        if (p.use_tma == 2) {
+          // pre-converted images (fp32 reference, its 2 grad, target vertical
+          // pairs): the regions land in their final layout; the origins move to
+          // the aligned box starts (the pitches carry the slack)
+          G.rX0 &= ~3;
+          G.tX0 &= ~1;
+          tma_mbar_init(&s_bar, 1);
+          tma_mbar_expect_tx(&s_bar, (uint32_t)(4 * FG::RP * FG::RH + 8 * FG::RP * FG::RH + 8 * FG::TP * (FG::TH - 1)));
+          tma_load_2d(smem_f + FG::T2_OFF, &tm.tgt, G.tX0, G.tY0, &s_bar);
+          tma_load_2d(smem_f, &tm.ref, G.rX0, G.rY0, &s_bar);
+          tma_load_2d(smem_f + FG::G2_OFF, &tm.aux, G.rX0, G.rY0, &s_bar);
+        } else if (p.use_tma) {
           tma_mbar_init(&s_bar, 1);
           unsigned char *rt, *rr;
           raw_dst<RAW>(smem_f + FG::G2_OFF, &rt, &rr);
@@ -1109,7 +1127,9 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
   }
   // ---- stage both regions (fp32), zero outside the images: one warp per
   // region row, 4 independent loads per lane in flight, no index division ----
-  if (FIXED && p.use_tma) {
+  if (FIXED && p.use_tma == 2) {
+    tma_mbar_wait(&s_bar, 0);  // R, G2 and T2 in place: no conversion, no barrier
+  } else if (FIXED && p.use_tma) {
     // raw u8/u16 boxes (TMA, zero outside the image) -> fp32 reference rows and
     // target vertical pairs, shared memory to shared memory
     tma_mbar_wait(&s_bar, 0);
@@ -1136,8 +1156,10 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
     else
       stage_rows<Pix>(p.tgt, g.tX0, g.tY0, g.tP, g.tH, T, warp, lane);
   }
-  __syncthreads();
-  if (FIXED) {  // static region shape: four independent columns per lane in flight
+  const bool preconv = FIXED && p.use_tma == 2;  // the gradients came with the pre-converted images
+  if (!preconv) __syncthreads();
+  if (preconv) {
+  } else if (FIXED) {  // static region shape: four independent columns per lane in flight
     for (int y = warp; y < FG::RH; y += kWarps) {
       const bool yin = y >= 1 && y < FG::RH - 1;
       const float* r0 = R + y * FG::RP;
@@ -1189,8 +1211,8 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
   }
   Walk wk;
   wk.init(M, lane, g.rP);
-  const float* Rs = R + g.rP + (cx - p.lat.cx(ix0)) + 1;  // reference pixel (0,0) of this subset
-  const float2* Gs = G2 + g.rP + (cx - p.lat.cx(ix0)) + 1;
+  const float* Rs = R + g.rP + (cx - M - g.rX0);  // reference pixel (0,0) of this subset
+  const float2* Gs = G2 + g.rP + (cx - M - g.rX0);
 
   double* crec = (METHOD == 1 && p.cache)
                      ? p.cache + ((size_t)iy * p.lat.nx + ix0 + warp) * kIcgnCacheStride
@@ -1597,8 +1619,72 @@ bool refine_plan(int M, int* ppt_out, int* nt_out) {
 }
 
 void icgn_cache_free(IcgnRefCache& c, cudaStream_t st, bool async) {
-  if (c.data) async ? cudaFreeAsync(c.data, st) : cudaFree(c.data);
+  for (void* b : {(void*)c.data, c.rimg, c.gimg, c.timg})
+    if (b) async ? cudaFreeAsync(b, st) : cudaFree(b);
   c = IcgnRefCache{};
+}
+
+// ---- pre-converted staging images of the fixed-geometry IC-GN kernels ----
+// The strips' TMA boxes then land in their final layout (no shared-memory
+// conversion pass, no gradient pass, no block barriers): the reference as fp32
+// and its central differences (2 grad f, zero outside the image — exactly the
+// values the strip staging computed from its zero-filled region), and the
+// target as vertical pairs (T[y][x], T[y+1][x]). Dense rows of `wp` elements.
+template <typename Pix>
+__device__ __forceinline__ float img_at(const ImageView& im, int x, int y) {
+  return (x >= 0 && x < im.width && y >= 0 && y < im.height) ? gpx<Pix>(im, x, y) : 0.f;
+}
+
+template <typename Pix>
+__global__ void __launch_bounds__(256) ref_images_kernel(ImageView im, int wp, float* R, float2* G) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (x >= wp) return;
+  const size_t o = (size_t)y * wp + x;
+  R[o] = img_at<Pix>(im, x, y);
+  G[o] = make_float2(img_at<Pix>(im, x + 1, y) - img_at<Pix>(im, x - 1, y),
+                     img_at<Pix>(im, x, y + 1) - img_at<Pix>(im, x, y - 1));
+}
+
+template <typename Pix>
+__global__ void __launch_bounds__(256) pair_image_kernel(ImageView im, int wp, float2* T2) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (x >= wp) return;
+  T2[(size_t)y * wp + x] = make_float2(img_at<Pix>(im, x, y), img_at<Pix>(im, x, y + 1));
+}
+
+// NR launch order (bit-identical results: only the order in which strips start
+// changes). A POI whose integer estimate correlates poorly is the one whose
+// Newton walk runs long (C3: ~2 % of the POIs take 14-50 iterations against ~4
+// for the rest, and a CTA lasts as long as its slowest warp), so strips are
+// started in four buckets of their worst integer ZNCC, worst first: the long
+// walks overlap the bulk instead of trailing it. One CTA: counts, offsets,
+// scatter (order within a bucket is arbitrary).
+__global__ void __launch_bounds__(1024) strip_order_kernel(const dicb200_poi_record* rec, int nx, int rows, int spc,
+                                                           int* order) {
+  __shared__ int cnt[4], off[4];
+  const int nsx = (nx + spc - 1) / spc, ns = nsx * rows;
+  auto bucket = [&](int st) {
+    const int iy = st / nsx, ix0 = (st % nsx) * spc;
+    float worst = 1.0f;
+    for (int j = 0; j < spc && ix0 + j < nx; ++j) {
+      const dicb200_poi_record& r = rec[(size_t)iy * nx + ix0 + j];
+      if (r.status == DICB200_POI_OK && r.zncc == r.zncc) worst = fminf(worst, (float)r.zncc);
+    }
+    return worst < 0.5f ? 0 : worst < 0.8f ? 1 : worst < 0.95f ? 2 : 3;
+  };
+  if (threadIdx.x < 4) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (int st = threadIdx.x; st < ns; st += blockDim.x) atomicAdd(&cnt[bucket(st)], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int a = 0;
+    for (int b = 0; b < 4; ++b) {
+      off[b] = a;
+      a += cnt[b];
+    }
+  }
+  __syncthreads();
+  for (int st = threadIdx.x; st < ns; st += blockDim.x) order[atomicAdd(&off[bucket(st)], 1)] = st;
 }
 
 cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st, IcgnRefCache* cache, long ref_key) {
@@ -1666,6 +1752,65 @@ cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st, Icgn
                                          FixedGeom<20, 10>::TH)
                                  : boxes(FixedGeom<20, 5>::RP, FixedGeom<20, 5>::TP, FixedGeom<20, 5>::RH,
                                          FixedGeom<20, 5>::TH);
+    // pre-converted staging images (default; DICB200_REFINE_RAW_TMA=1: the raw
+    // boxes converted in shared memory)
+    static const bool raw_tma = std::getenv("DICB200_REFINE_RAW_TMA") != nullptr;
+    void* own[3] = {nullptr, nullptr, nullptr};
+    if (!no_tma && !raw_tma) {
+      const int W = p.ref.width, H = p.ref.height, wp = (W + 3) & ~3;
+      const size_t px = (size_t)wp * H;
+      void *rimg = nullptr, *gimg = nullptr, *timg = nullptr;
+      bool ref_ready = false;
+      e = cudaSuccess;
+      if (cache) {
+        if (cache->img_cap < px) {
+          for (void** b : {&cache->rimg, &cache->gimg, &cache->timg})
+            if (*b) {
+              cudaFreeAsync(*b, st);
+              *b = nullptr;
+            }
+          cache->img_cap = 0;
+          cache->img_key = -1;
+          e = cudaMallocAsync(&cache->rimg, px * 4, st);
+          if (e == cudaSuccess) e = cudaMallocAsync(&cache->gimg, px * 8, st);
+          if (e == cudaSuccess) e = cudaMallocAsync(&cache->timg, px * 8, st);
+          if (e != cudaSuccess) return e;
+          cache->img_cap = px;
+        }
+        rimg = cache->rimg, gimg = cache->gimg, timg = cache->timg;
+        ref_ready = ref_key >= 0 && cache->img_key == ref_key && cache->img_ref == p.ref.data;
+      } else {
+        e = cudaMallocAsync(&own[0], px * 4, st);
+        if (e == cudaSuccess) e = cudaMallocAsync(&own[1], px * 8, st);
+        if (e == cudaSuccess) e = cudaMallocAsync(&own[2], px * 8, st);
+        if (e != cudaSuccess) return e;
+        rimg = own[0], gimg = own[1], timg = own[2];
+      }
+      TmaPair pm{};
+      const int rp = p.lat.step == 10 ? FixedGeom<20, 10>::RP : FixedGeom<20, 5>::RP;
+      const int tp = p.lat.step == 10 ? FixedGeom<20, 10>::TP : FixedGeom<20, 5>::TP;
+      const int rh = FixedGeom<20, 10>::RH, th = FixedGeom<20, 10>::TH;
+      if (tma_encode_2d_f(&pm.ref, rimg, 4, W, H, wp, rp, rh) && tma_encode_2d_f(&pm.aux, gimg, 8, W, H, wp, rp, rh) &&
+          tma_encode_2d_f(&pm.tgt, timg, 8, W, H, wp, tp, th - 1)) {
+        const dim3 ig((wp + 255) / 256, H);
+        if (!ref_ready) {
+          u8 ? ref_images_kernel<uint8_t><<<ig, 256, 0, st>>>(p.ref, wp, (float*)rimg, (float2*)gimg)
+             : ref_images_kernel<uint16_t><<<ig, 256, 0, st>>>(p.ref, wp, (float*)rimg, (float2*)gimg);
+          count_launch();
+          if (cache) {
+            cache->img_key = ref_key;
+            cache->img_ref = p.ref.data;
+          }
+        }
+        u8 ? pair_image_kernel<uint8_t><<<ig, 256, 0, st>>>(p.tgt, wp, (float2*)timg)
+           : pair_image_kernel<uint16_t><<<ig, 256, 0, st>>>(p.tgt, wp, (float2*)timg);
+        count_launch();
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        tm = pm;
+        p.use_tma = 2;
+      }
+    }
     auto go = [&](auto k, size_t sm) {
       e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (e == cudaSuccess)
@@ -1679,6 +1824,8 @@ cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st, Icgn
       u8 ? go(refine_strip_kernel<uint8_t, 1, 20, 5>, FixedGeom<20, 5>::SMEM)
          : go(refine_strip_kernel<uint16_t, 1, 20, 5>, FixedGeom<20, 5>::SMEM);
     count_launch();
+    for (void* b : own)
+      if (b) cudaFreeAsync(b, st);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
   }
@@ -1690,6 +1837,14 @@ cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st, Icgn
     if (e == cudaSuccess) k<<<grid, kNT, smem, st>>>(p, tm);
   };
   const bool cubic = p.interp == DICB200_INTERP_BICUBIC;
+  int* order = nullptr;
+  if (p.method == 0 && grid.x * grid.y > 1 && std::getenv("DICB200_NR_GRID_ORDER") == nullptr) {
+    e = cudaMallocAsync((void**)&order, (size_t)grid.x * grid.y * sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    strip_order_kernel<<<1, 1024, 0, st>>>(p.rec, p.lat.nx, rows, p.spc, order);
+    count_launch();
+    p.order = order;
+  }
   if (p.method == 0) {
     if (cubic)
       u8 ? go(refine_strip_kernel<uint8_t, 0, 0, 0, 1>) : go(refine_strip_kernel<uint16_t, 0, 0, 0, 1>);
@@ -1702,6 +1857,7 @@ cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st, Icgn
       u8 ? go(refine_strip_kernel<uint8_t, 1>) : go(refine_strip_kernel<uint16_t, 1>);
   }
   count_launch();
+  if (order) cudaFreeAsync(order, st);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

@@ -22,6 +22,8 @@ struct RefineParams {
   // sequences): [0] tag (0 = not computed, 1 = ok, 1 + status = failed),
   // [1] fbar, [2] nf, [3] scf, [4..9] A, [10..15] S, [16..51] H^-1 rows.
   double* cache;
+  // launch order of the strips (CTA b runs strip order[b]; nullptr = grid order)
+  const int* order;
 };
 
 constexpr int kIcgnCacheStride = 52;
@@ -33,7 +35,19 @@ struct IcgnRefCache {
   long key = -1;
   const void* ref = nullptr;
   int W = 0, H = 0, M = 0, x0 = 0, y0 = 0, step = 0, nx = 0, ny = 0;
-  void reset() { key = -1; }
+  // pre-converted staging images of the fixed-geometry IC-GN kernels: the
+  // reference as fp32 and its 2 grad (kept while `img_key` repeats), the
+  // target as vertical pairs (rebuilt per pair); row pitch `img_pitch` elements
+  void* rimg = nullptr;
+  void* gimg = nullptr;
+  void* timg = nullptr;
+  size_t img_cap = 0;
+  long img_key = -1;
+  const void* img_ref = nullptr;
+  void reset() {
+    key = -1;
+    img_key = -1;
+  }
 };
 
 bool refine_plan(int M, int* ppt, int* nt);

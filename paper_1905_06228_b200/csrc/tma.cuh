@@ -17,7 +17,34 @@ namespace dicb200 {
 struct alignas(64) TmaPair {
   CUtensorMap ref;
   CUtensorMap tgt;
+  CUtensorMap aux;  // pre-converted refinement staging: the reference's 2 grad image
 };
+
+// 2D tiled map over a dense fp32 (elem 4) or 8-byte (float2, elem 8) image
+// with box box_w x box_h; zero fill outside. false: layout rules not met.
+inline bool tma_encode_2d_f(CUtensorMap* map, const void* base, int elem_bytes, int width, int height, int pitch,
+                            int box_w, int box_h) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return false;
+  const uint64_t stride = (uint64_t)pitch * elem_bytes;
+  if (((uintptr_t)base & 15) || (stride & 15) || ((box_w * elem_bytes) & 15) || box_w > 256 || box_h > 256)
+    return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)width, (cuuint64_t)height};
+  const cuuint64_t strides[1] = {stride};
+  const cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)box_h};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64, 2,
+                const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 // 2D tiled map over a u8/u16 image (width x height, pitch in elements) with box
 // box_w x box_h. false: the image does not meet TMA's layout rules (16-byte

@@ -1,5 +1,6 @@
 """Per-CUDA-source-line totals of an ncu report (instructions executed and
-warp-stall samples), top lines first:  ncu_src_top.py report.ncu-rep [file.cu] [N]"""
+warp-stall samples), top lines first:  ncu_src_top.py report.ncu-rep [file.cu] [N]
+(NCU_KERNEL=regex:<name> selects one kernel of a multi-kernel report)"""
 import csv
 import subprocess
 import sys
@@ -7,7 +8,10 @@ import sys
 rep = sys.argv[1]
 want = sys.argv[2] if len(sys.argv) > 2 else ""
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+import os
+
+kf = ["--kernel-name", os.environ["NCU_KERNEL"]] if os.environ.get("NCU_KERNEL") else []  # multi-kernel reports
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", *kf],
                      capture_output=True, text=True).stdout.splitlines()
 rows = list(csv.reader(out))
 h = next(r for r in rows[:10] if "Instructions Executed" in r)
