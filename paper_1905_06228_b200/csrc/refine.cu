@@ -1645,11 +1645,20 @@ __global__ void __launch_bounds__(256) ref_images_kernel(ImageView im, int wp, f
                      img_at<Pix>(im, x, y + 1) - img_at<Pix>(im, x, y - 1));
 }
 
+// four pairs per thread (wp is a multiple of 4): 16-byte stores
 template <typename Pix>
 __global__ void __launch_bounds__(256) pair_image_kernel(ImageView im, int wp, float2* T2) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  const int x = 4 * (blockIdx.x * blockDim.x + threadIdx.x), y = blockIdx.y;
   if (x >= wp) return;
-  T2[(size_t)y * wp + x] = make_float2(img_at<Pix>(im, x, y), img_at<Pix>(im, x, y + 1));
+  float a[4], b[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    a[j] = img_at<Pix>(im, x + j, y);
+    b[j] = img_at<Pix>(im, x + j, y + 1);
+  }
+  float4* d = reinterpret_cast<float4*>(T2 + (size_t)y * wp + x);
+  d[0] = make_float4(a[0], b[0], a[1], b[1]);
+  d[1] = make_float4(a[2], b[2], a[3], b[3]);
 }
 
 // NR launch order (bit-identical results: only the order in which strips start
@@ -1802,8 +1811,9 @@ cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st, Icgn
             cache->img_ref = p.ref.data;
           }
         }
-        u8 ? pair_image_kernel<uint8_t><<<ig, 256, 0, st>>>(p.tgt, wp, (float2*)timg)
-           : pair_image_kernel<uint16_t><<<ig, 256, 0, st>>>(p.tgt, wp, (float2*)timg);
+        const dim3 pg((wp / 4 + 255) / 256, H);
+        u8 ? pair_image_kernel<uint8_t><<<pg, 256, 0, st>>>(p.tgt, wp, (float2*)timg)
+           : pair_image_kernel<uint16_t><<<pg, 256, 0, st>>>(p.tgt, wp, (float2*)timg);
         count_launch();
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
