@@ -848,7 +848,7 @@ constexpr int kExactMaxSide = 64, kExactMaxWin = 96;
 // single-CTA search cost ~70 us per pair with one or two flagged POIs; the
 // single-CTA bs_exact_kernel below takes the slots past kExactSlots).
 constexpr int kExactSlots = 256;
-constexpr int kExactRowWarps = 32;  // dx per CTA (2R+1 <= 32)
+constexpr int kExactRowWarps = 8;  // warps per CTA, dx strided over them (2R+1 <= 32)
 template <typename Pix>
 __global__ void __launch_bounds__(32 * kExactRowWarps) bs_exact_rows_kernel(TcParams p, const int* flagged,
                                                                            const int* n_flagged, BestPartial* part,
@@ -887,26 +887,28 @@ __global__ void __launch_bounds__(32 * kExactRowWarps) bs_exact_rows_kernel(TcPa
   b.dx = b.dy = 0;
   b.count = 0;
   b.found = 0;
-  if (warp < fw) {
-    const int dx = fx_lo + warp;
+  for (int wx = warp; wx < fw; wx += kExactRowWarps) {
+    const int dx = fx_lo + wx;
     const size_t o = (size_t)(cy - M + dy - p.qy_min) * p.SW + (cx - M + dx - p.qx_min);
     const double sq = p.SQ[o];
     if (sq > 0.0) {  // constant target window: skipped, not counted
       uint64_t acc64 = 0;  // each product < 2^32 (16-bit pixels), sums exact in u64
       for (int r = 0; r < side; ++r) {
         const uint16_t* fr = fs + r * side;
-        const uint16_t* gr = gs + r * ww + warp;
+        const uint16_t* gr = gs + r * ww + wx;
         for (int c = lane; c < side; c += 32) acc64 += (uint64_t)((uint32_t)fr[c] * gr[c]);
       }
 #pragma unroll
       for (int o2 = 16; o2; o2 >>= 1) acc64 += __shfl_xor_sync(0xffffffffu, acc64, o2);
       const uint32_t n = (uint32_t)(side * side), sf = (uint32_t)p.poi_sf[k];
       const int64_t num = (int64_t)(acc64 * n - (uint64_t)sf * p.S1[o]);
-      b.c = bs_i64_to_f64(num) / (p.poi_sqrtvf[k] * sq);
-      b.dx = dx;
-      b.dy = dy;
-      b.count = 1;
-      b.found = 1;
+      BestPartial q;
+      q.c = bs_i64_to_f64(num) / (p.poi_sqrtvf[k] * sq);
+      q.dx = dx;
+      q.dy = dy;
+      q.count = 1;
+      q.found = 1;
+      merge_best(b, q);  // dx ascending within the warp
     }
   }
   if (lane == 0) {
@@ -1237,16 +1239,28 @@ cudaError_t bs_merge_launch(const TcParams& p, const BsGeom& g, cudaStream_t st)
     std::vector<BsSlice> h(std::min<size_t>(npoi * g.nsplit, 64));
     cudaMemcpy(h.data(), p.slices, h.size() * sizeof(BsSlice), cudaMemcpyDeviceToHost);
     fprintf(stderr, "[bs debug] flagged %d of %zu POIs (nsplit %d)\n", nf, npoi, g.nsplit);
+    if (nf > 0) {  // the first flagged POIs' slices
+      std::vector<int> fl(std::min(nf, 4));
+      cudaMemcpy(fl.data(), flagged, fl.size() * sizeof(int), cudaMemcpyDeviceToHost);
+      for (int k : fl) {
+        std::vector<BsSlice> sl(g.nsplit);
+        cudaMemcpy(sl.data(), reinterpret_cast<BsSlice*>(p.slices) + (size_t)k * g.nsplit, g.nsplit * sizeof(BsSlice),
+                   cudaMemcpyDeviceToHost);
+        for (int q = 0; q < g.nsplit; ++q)
+          fprintf(stderr, "  flagged poi %d slice %d: a1 %.9g a2 %.9g cnt %d d (%d,%d)\n", k, q, sl[q].a1, sl[q].a2,
+                  sl[q].cnt, sl[q].dx, sl[q].dy);
+      }
+    }
     for (size_t i = 0; i < h.size() && i < 16; ++i)
       fprintf(stderr, "  slice %zu: a1 %.9g a2 %.9g cnt %d d (%d,%d)\n", i, h[i].a1, h[i].a2, h[i].cnt, h[i].dx, h[i].dy);
   }
   // flagged POIs (near ties are rare: idle CTAs exit at once): a CTA per
-  // (slot, displacement row), slots strided over 16 CTA columns; past
+  // (slot, displacement row), slots strided over 64 CTA columns; past
   // kExactSlots, one CTA per POI
   const int ew = 2 * p.R + 1;
   const bool rows_ok = ew <= kExactRowWarps && p.side <= kExactMaxSide && p.side + ew - 1 <= kExactMaxWin;
   if (rows_ok) {
-    const dim3 grid(16, ew);
+    const dim3 grid(64, ew);
     if (p.planes == 1)
       bs_exact_rows_kernel<uint8_t><<<grid, 32 * kExactRowWarps, 0, st>>>(p, flagged, n_flagged, part, arrivals);
     else

@@ -20,6 +20,8 @@
 // probes (atomicOr returns whether the bit was new). Particle arithmetic is
 // fp64 with explicit _rn intrinsics (no FMA), rounding is llround (half away
 // from zero) as std::lround, clamps are std::clamp.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "pso.cuh"
 
@@ -199,7 +201,8 @@ struct GBest {
   int dx, dy, has;
 };
 
-__global__ void __launch_bounds__(32 * kWarpsPerCta) pso_walk_kernel(PsoParams p) {
+template <int MINB>
+__global__ void __launch_bounds__(32 * kWarpsPerCta, MINB) pso_walk_kernel(PsoParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k = blockIdx.x * kWarpsPerCta + warp;
@@ -459,11 +462,20 @@ dicb200_status pso_walk_launch(PsoParams& p, cudaStream_t st) {
     set_error("particle_count / search window too large for the swarm walk kernel");
     return DICB200_ERR_INVALID;
   }
-  cudaError_t e = cudaFuncSetAttribute(pso_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess) {
-    pso_walk_kernel<<<(p.n_records + kWarpsPerCta - 1) / kWarpsPerCta, 32 * kWarpsPerCta, smem, st>>>(p);
-    e = cudaGetLastError();
-  }
+  cudaError_t e;
+  auto go = [&](auto k) {
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) {
+      k<<<(p.n_records + kWarpsPerCta - 1) / kWarpsPerCta, 32 * kWarpsPerCta, smem, st>>>(p);
+      e = cudaGetLastError();
+    }
+  };
+  // 3 CTAs/SM (C3: <= 170 registers without spills, 3 x 67 KB of staged
+  // surfaces). Measured and dropped: 128 registers for 4 CTAs/SM with the
+  // surfaces read through L1/L2 (spills; no gain), and the row chunks' walks
+  // and refinements forked onto a second stream (C3 7.43 -> 7.46 M subsets/s:
+  // within noise, the per-chunk search setup eats the overlap)
+  go(pso_walk_kernel<3>);
   count_launch();
   if (e != cudaSuccess) return cuda_fail(e, "pso_walk_kernel", __FILE__, __LINE__);
   return DICB200_OK;
