@@ -10,9 +10,10 @@
 //
 // Semantics: identical records to dic::analyze_pair (same grid order, same
 // per-POI failure semantics). Pair-level failures throw dic::Error with the
-// reference's message. GrayImage values must be integers in [0, 65535]
-// (every 8/16-bit camera frame is) or fractional levels in [0, 255], which are
-// carried as 8.8 fixed point (see detail::Frames); anything else throws dic::Error.
+// reference's message. Integer GrayImage levels in [0, 65535] (every 8/16-bit
+// camera frame) travel as u8/u16 to the exact-integer kernels; any other levels
+// (e.g. the reference's fractional synthetic frames) are passed as the
+// GrayImage's own doubles to the exact fp64 path (see detail::Frames).
 #pragma once
 
 #include <algorithm>
@@ -103,13 +104,12 @@ class PinnedPool {
 
 // GrayImages (doubles) -> device gray levels, one multithreaded pass per frame
 // (dicb200_pack_gray). Integer levels in [0, 65535] map losslessly; when every
-// level of every frame is <= 255 they travel as u8 (narrowed in place). A frame
-// with non-integral levels in [0, 255] (e.g. the reference's synth_speckle /
-// synth_warped_pair frames) is carried with 8 fractional bits, u16 = lround(256 v):
-// ZNCC, the IC-GN / NR steps and every decision derived from them are invariant
-// to a positive gray-level scale of either frame, so only the 2^-9 quantisation
-// of each sample separates the result from the reference's doubles. Anything
-// else (negative, > 65535, fractional above 255, non-finite) throws dic::Error.
+// level of every frame is <= 255 they travel as u8 (narrowed in place). When a
+// frame has any other level (non-integral, e.g. the reference's synth_speckle /
+// synth_warped_pair frames, or outside [0, 65535]) every frame of the call is
+// handed over as its GrayImage's doubles (DICB200_F64): the integer search then
+// evaluates the reference's zncc in its own order (bit-identical values) and
+// the refiners gather fp32 samples of the fp64 images.
 class Frames {
  public:
   explicit Frames(const std::vector<const GrayImage*>& images) : pool_(PinnedPool::get()) {
@@ -119,8 +119,8 @@ class Frames {
     blocks_ = pool_.take(n, std::max<size_t>(px * 2, 16));
     imgs_.resize(n);
     int maxv = 0;
-    bool any_frac = false;
-    for (size_t i = 0; i < n; ++i) {
+    bool fp = false;  // some frame is not integral in [0, 65535]: all frames as doubles
+    for (size_t i = 0; i < n && !fp; ++i) {
       const GrayImage& g = *images[i];
       dicb200_image& im = imgs_[i];
       im.width = g.width();
@@ -131,20 +131,29 @@ class Frames {
       im.data = blocks_[i];
       uint16_t* dst = static_cast<uint16_t*>(blocks_[i]);
       int32_t frac = 0, mx = 0;
-      dicb200_status st = dicb200_pack_gray(g.pixels().data(), g.width(), g.height(), g.width(), 1, dst, &frac,
-                                            &mx, 0);
-      if (st == DICB200_OK && frac)
-        st = dicb200_pack_gray(g.pixels().data(), g.width(), g.height(), g.width(), 256, dst, nullptr, &mx, 0);
-      if (st != DICB200_OK) {
-        pool_.release(blocks_);
-        throw Error(frac ? "dicb200: fractional gray levels must lie in [0, 255]" : dicb200_last_error_message());
+      const dicb200_status st = dicb200_pack_gray(g.pixels().data(), g.width(), g.height(), g.width(), 1, dst, &frac,
+                                                  &mx, 0);
+      if (st != DICB200_OK || frac) {
+        fp = true;
+        break;
       }
-      any_frac = any_frac || frac;
-      im.bits = frac ? 16 : 1;
-      while (!frac && im.bits < 16 && (1 << im.bits) - 1 < mx) ++im.bits;
-      maxv = std::max(maxv, frac ? 65535 : mx);
+      im.bits = 1;
+      while (im.bits < 16 && (1 << im.bits) - 1 < mx) ++im.bits;
+      maxv = std::max(maxv, (int)mx);
     }
-    if (!any_frac && maxv <= 255) {  // every frame 8-bit: u8 (one byte plane on the device)
+    if (fp) {  // the GrayImages' own doubles (read-only for the call); non-finite levels fail the pair
+      for (size_t i = 0; i < n; ++i) {
+        const GrayImage& g = *images[i];
+        dicb200_image& im = imgs_[i];
+        im.width = g.width();
+        im.height = g.height();
+        im.pitch = g.width();
+        im.id = g.id();
+        im.dtype = DICB200_F64;
+        im.bits = 0;
+        im.data = g.pixels().data();
+      }
+    } else if (maxv <= 255) {  // every frame 8-bit: u8 (one byte plane on the device)
       for (dicb200_image& im : imgs_) {
         const uint16_t* s16 = static_cast<const uint16_t*>(im.data);
         uint8_t* d8 = static_cast<uint8_t*>(const_cast<void*>(im.data));

@@ -22,7 +22,8 @@
  *
  * Plain pointers and sizes only. Images are 8- or 16-bit unsigned gray levels
  * (the reference stores doubles; integer gray levels map losslessly, which is
- * what every BASELINE configuration uses). Errors: pair-level failures that the
+ * what every BASELINE configuration uses) or f32/f64 levels (the exact fp64
+ * path for fractional frames). Errors: pair-level failures that the
  * reference raises as dic::Error return DICB200_ERR_INVALID with the reference's
  * message in dicb200_last_error_message(); per-POI failures never fail the call
  * — they are reported in dicb200_poi_record.status with the reference's
@@ -54,11 +55,11 @@ typedef enum {
 } dicb200_status;
 
 /* Pixel storage. U8/U16: integer gray levels, used as they are (exact
- * integer search). F32/F64: gray levels in [0, 255] with fractions (e.g. the
- * reference's synthetic doubles), carried as 8.8 fixed point round(256 v) in
- * u16 — ZNCC and the refinement steps are invariant to that scale, so only the
- * 2^-9 quantisation differs from computing on the doubles. Host entry points
- * reject levels outside [0, 255]; device entry points saturate them. */
+ * integer search kernels). F32/F64: any finite gray levels (e.g. the
+ * reference's fractional synthetic frames) on the fp64 path: F32 is widened
+ * exactly, the integer search evaluates the reference's zncc in its own order
+ * (bit-identical correlation values and decisions), the refiners gather fp32
+ * samples of the fp64 image. Host entry points reject non-finite levels. */
 enum { DICB200_U8 = 0, DICB200_U16 = 1, DICB200_F32 = 2, DICB200_F64 = 3 };
 
 /* Enum values follow the declaration order of the reference enums. */
@@ -77,7 +78,7 @@ typedef struct {
   int32_t width;
   int32_t height;
   int32_t pitch;
-  int32_t dtype;  /* DICB200_U8 | DICB200_U16 */
+  int32_t dtype;  /* DICB200_U8 | DICB200_U16 | DICB200_F32 | DICB200_F64 */
   int32_t id;     /* GrayImage::id(), copied into field ref_id/tgt_id */
   int32_t bits;     /* significant bits per pixel (0 = full dtype width); lets u16
                     * data of <= 12 bits use the exact u32 IMAD path */

@@ -7,7 +7,7 @@ from __future__ import annotations
 
 import ctypes as C
 
-U8, U16, F32, F64 = 0, 1, 2, 3  # dicb200_image.dtype (F32/F64: fractional levels in [0, 255], 8.8 fixed point)
+U8, U16, F32, F64 = 0, 1, 2, 3  # dicb200_image.dtype (F32/F64: fractional levels, exact fp64 path)
 
 INT_BFS, INT_PSO, INT_MPSO = 0, 1, 2
 SUB_NR, SUB_ICGN, SUB_NONE = 0, 1, 2

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "bfs.cuh"
+#include "bfs_fp.cuh"
 #include "common.cuh"
 #include "pso.cuh"
 #include "refine.cuh"
@@ -266,6 +267,27 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
   const int rows = re - rb;
   if (rows <= 0) return DICB200_OK;
   const size_t nrec = (size_t)rows * lat.nx;
+  const bool fp = ref->dtype == DICB200_F64;  // fractional gray levels: the exact fp64 path (bfs_fp.cu)
+  auto fp_params = [&](int r0, dicb200_poi_record* rec, double* surface) {
+    FpParams f{};
+    f.ref = view(ref);
+    f.tgt = view(tgt);
+    f.lat = lat;
+    f.row_begin = r0;
+    f.M = cfg->half_width;
+    f.R = cfg->search_radius;
+    f.whole = surface ? 0 : cfg->bfs_domain == DICB200_BFS_WHOLE_IMAGE;
+    f.subpixel_none = cfg->subpixel_method == DICB200_SUB_NONE;
+    f.rec = rec;
+    f.surface = surface;
+    return f;
+  };
+  if (fp && cfg->integer_method == DICB200_INT_BFS) {
+    if (cfg->bfs_domain != DICB200_BFS_WHOLE_IMAGE && cfg->search_radius < 0) return invalid("search radius must be >= 0");
+    StageTimer tm(0, st);
+    DICB200_CUDA_TRY(bfs_fp_launch(fp_params(rb, out_dev, nullptr), rows, st));
+    goto refine;
+  }
   if (cfg->integer_method == DICB200_INT_BFS) {
     BfsParams p{};
     p.ref = view(ref);
@@ -358,13 +380,13 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
       t.subpixel_none = 1;
       t.maxv = pixel_max(ref, tgt);
       t.surface = surface;
-      const bool use_tc = tc_plan(t);
-      if (!use_tc && !bfs_plan(b, 72 * 1024) && !bfs_plan(b, 200 * 1024)) {
+      const bool use_tc = !fp && tc_plan(t);
+      if (!fp && !use_tc && !bfs_plan(b, 72 * 1024) && !bfs_plan(b, 200 * 1024)) {
         s = invalid("subset too large for the BFS tile (shared memory)");
         break;
       }
       BestPartial* partial = nullptr;
-      if (!use_tc && b.n_chunks > 1) {
+      if (!fp && !use_tc && b.n_chunks > 1) {
         cudaError_t e = cudaMallocAsync((void**)&partial, (size_t)(r1 - r0) * lat.nx * b.n_chunks * sizeof(BestPartial), st);
         if (e != cudaSuccess) {
           s = cuda_fail(e, "cudaMallocAsync(partial)", __FILE__, __LINE__);
@@ -396,7 +418,9 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
       p.surface = surface;
       {
         StageTimer tm(1, st);
-        cudaError_t e = use_tc ? tc_launch(t, st, tcache, ref_key) : bfs_launch(b, r1 - r0, st);
+        cudaError_t e = fp       ? bfs_fp_launch(fp_params(r0, out_chunk, surface), r1 - r0, st)
+                        : use_tc ? tc_launch(t, st, tcache, ref_key)
+                                 : bfs_launch(b, r1 - r0, st);
         if (e != cudaSuccess) s = cuda_fail(e, "bfs_launch(surface)", __FILE__, __LINE__);
         if (s == DICB200_OK) s = pso_walk_launch(p, st);
       }
@@ -421,7 +445,7 @@ refine:
     r.interp = cfg->interp;
     r.rec = out_dev;
     StageTimer tm(r.method == 0 ? 2 : 3, st);
-    DICB200_CUDA_TRY(refine_launch(r, ref->dtype == DICB200_U8, st, icache, ref_key));
+    DICB200_CUDA_TRY(refine_launch(r, ref->dtype, st, icache, ref_key));
     host_trace("refine enqueued");
   }
   return enqueue_bits_guard(ref, tgt, out_dev, nrec, st);
@@ -432,45 +456,33 @@ static size_t elem_size(int dtype) {
 }
 static bool is_float(int dtype) { return dtype == DICB200_F32 || dtype == DICB200_F64; }
 
-// Fractional gray levels -> 8.8 fixed point (see DICB200_F32 in dicb200.h).
-template <typename T>
-__global__ void fixed88_kernel(const T* src, int pitch, uint16_t* dst, int w, int h) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
-  if (x >= w) return;
-  const double v = (double)src[(size_t)y * pitch + x] * 256.0;
-  dst[(size_t)y * w + x] = (uint16_t)fmin(fmax(round(v), 0.0), 65535.0);  // half away from zero, as lround; NaN -> 0
-}
-
-// Device image `im` (f32/f64) converted into `buf` (w*h u16, stream-ordered).
-static dicb200_status to_fixed88_device(const dicb200_image* im, uint16_t** buf, dicb200_image* out,
-                                        cudaStream_t st) {
-  const int pitch = im->pitch > 0 ? im->pitch : im->width;
-  DICB200_CUDA_TRY(cudaMallocAsync((void**)buf, (size_t)im->width * im->height * 2, st));
-  const dim3 g((im->width + 255) / 256, im->height);
-  if (im->dtype == DICB200_F32)
-    fixed88_kernel<float><<<g, 256, 0, st>>>(static_cast<const float*>(im->data), pitch, *buf, im->width, im->height);
-  else
-    fixed88_kernel<double><<<g, 256, 0, st>>>(static_cast<const double*>(im->data), pitch, *buf, im->width, im->height);
-  count_launch();
-  DICB200_CUDA_TRY(cudaGetLastError());
+// Fractional gray levels run on the exact fp64 path (bfs_fp.cu, the refiners'
+// fp64 images): an F32 device image is widened (exactly) into `buf` for this
+// call; F64 images are used as they are.
+static dicb200_status widen_device(const dicb200_image* im, double** buf, dicb200_image* out, cudaStream_t st) {
   *out = *im;
-  out->dtype = DICB200_U16;
-  out->bits = 16;
+  if (im->dtype == DICB200_F64) return DICB200_OK;
+  const int pitch = im->pitch > 0 ? im->pitch : im->width;
+  DICB200_CUDA_TRY(cudaMallocAsync((void**)buf, (size_t)im->width * im->height * 8, st));
+  DICB200_CUDA_TRY(widen_f32_to_f64(static_cast<const float*>(im->data), pitch, *buf, im->width, im->height, st));
+  out->dtype = DICB200_F64;
+  out->bits = 0;
   out->pitch = im->width;
   out->data = *buf;
   return DICB200_OK;
 }
 
-// Host image (f32/f64) -> 8.8 fixed point on the host; levels outside [0, 255] are an error.
-static dicb200_status to_fixed88_host(const dicb200_image* im, std::vector<uint16_t>& v) {
+// Host image (f32/f64) -> dense fp64 on the host; non-finite levels are an
+// error (GrayImage's constructor rejects them, image.cpp:14-22).
+static dicb200_status to_f64_host(const dicb200_image* im, std::vector<double>& v) {
   const int pitch = im->pitch > 0 ? im->pitch : im->width;
   v.resize((size_t)im->width * im->height);
   for (int y = 0; y < im->height; ++y)
     for (int x = 0; x < im->width; ++x) {
       const double g = im->dtype == DICB200_F32 ? (double)static_cast<const float*>(im->data)[(size_t)y * pitch + x]
                                                 : static_cast<const double*>(im->data)[(size_t)y * pitch + x];
-      if (!(g >= 0.0 && g <= 255.0)) return invalid("fractional gray levels must lie in [0, 255]");
-      v[(size_t)y * im->width + x] = (uint16_t)std::lround(g * 256.0);
+      if (!std::isfinite(g)) return invalid("non-finite gray level");
+      v[(size_t)y * im->width + x] = g;
     }
   return DICB200_OK;
 }
@@ -637,16 +649,16 @@ static dicb200_status release_context(DeviceContext* c) {
 
 // H2D of a host image (any pitch) into `buf` on `st`; `dev` describes the copy.
 static dicb200_status upload(const dicb200_image* host, DevBuf& buf, dicb200_image* dev, cudaStream_t st) {
-  if (is_float(host->dtype)) {  // converted on the host, then uploaded as u16
-    std::vector<uint16_t> v;
-    dicb200_status s = to_fixed88_host(host, v);
+  if (is_float(host->dtype)) {  // checked and widened on the host, uploaded as fp64
+    std::vector<double> v;
+    dicb200_status s = to_f64_host(host, v);
     if (s != DICB200_OK) return s;
-    DICB200_CUDA_TRY(ensure(buf, v.size() * 2, st));
-    DICB200_CUDA_TRY(cudaMemcpyAsync(buf.p, v.data(), v.size() * 2, cudaMemcpyHostToDevice, st));
+    DICB200_CUDA_TRY(ensure(buf, v.size() * 8, st));
+    DICB200_CUDA_TRY(cudaMemcpyAsync(buf.p, v.data(), v.size() * 8, cudaMemcpyHostToDevice, st));
     DICB200_CUDA_TRY(cudaStreamSynchronize(st));  // v is a temporary
     *dev = *host;
-    dev->dtype = DICB200_U16;
-    dev->bits = 16;
+    dev->dtype = DICB200_F64;
+    dev->bits = 0;
     dev->pitch = host->width;
     dev->data = buf.p;
     return DICB200_OK;
@@ -859,12 +871,12 @@ dicb200_status dicb200_analyze_pair_device(const dicb200_image* ref, const dicb2
     set_error("output capacity smaller than the grid rows");
     return DICB200_ERR_CAPACITY;
   }
-  if (is_float(ref->dtype)) {  // fractional levels: 8.8 fixed-point copies for this call
+  if (ref->dtype == DICB200_F32) {  // fractional levels: fp64 copies for this call
     const cudaStream_t st = (cudaStream_t)stream;
-    uint16_t *ba = nullptr, *bb = nullptr;
+    double *ba = nullptr, *bb = nullptr;
     dicb200_image ra, rt;
-    s = to_fixed88_device(ref, &ba, &ra, st);
-    if (s == DICB200_OK) s = to_fixed88_device(tgt, &bb, &rt, st);
+    s = widen_device(ref, &ba, &ra, st);
+    if (s == DICB200_OK) s = widen_device(tgt, &bb, &rt, st);
     if (s == DICB200_OK) s = enqueue_pair(&ra, &rt, cfg, pair_index, lat, rb, re, out_dev, st);
     if (ba) cudaFreeAsync(ba, st);
     if (bb) cudaFreeAsync(bb, st);
@@ -903,12 +915,12 @@ dicb200_status dicb200_analyze_sequence_device(const dicb200_image* images, size
   // Reference-side inputs (tensor-core strips/moments, IC-GN constants) live for
   // this call only and are rebuilt whenever the pair's reference frame changes.
   const cudaStream_t st = (cudaStream_t)stream;
-  std::vector<dicb200_image> conv;  // fractional levels: 8.8 fixed-point copies for this call
-  std::vector<uint16_t*> conv_buf;
-  if (is_float(images[0].dtype)) {
+  std::vector<dicb200_image> conv;  // fractional f32 levels: fp64 copies for this call
+  std::vector<double*> conv_buf;
+  if (images[0].dtype == DICB200_F32) {
     conv.resize(n_images);
     conv_buf.assign(n_images, nullptr);
-    for (size_t i = 0; i < n_images && s == DICB200_OK; ++i) s = to_fixed88_device(&images[i], &conv_buf[i], &conv[i], st);
+    for (size_t i = 0; i < n_images && s == DICB200_OK; ++i) s = widen_device(&images[i], &conv_buf[i], &conv[i], st);
     if (s == DICB200_OK) images = conv.data();
   }
   // Pairs alternate over kSeqStreams internal streams forked from (and joined
@@ -958,7 +970,7 @@ dicb200_status dicb200_analyze_sequence_device(const dicb200_image* images, size
     }
     if (fork) cudaEventDestroy(fork);
   }
-  for (uint16_t* b : conv_buf)
+  for (double* b : conv_buf)
     if (b) cudaFreeAsync(b, st);
   return s;
 }

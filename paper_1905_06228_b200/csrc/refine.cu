@@ -30,6 +30,8 @@
 
 #include "common.cuh"
 #include "linalg.cuh"
+#include <type_traits>
+
 #include "refine.cuh"
 #include "tma.cuh"
 
@@ -1285,14 +1287,31 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
     }
     sf = warp_sum1(sf);
     sff = warp_sum1(sff);
-    const int64_t vf = (int64_t)n * (int64_t)sff - (int64_t)sf * (int64_t)sf;
-    if (vf <= 0) {  // constant subset (exact test)
+    double vfn;  // sum of squared centred values (subset_stats' norm^2, correlation.cpp:27-36)
+    if (std::is_floating_point<Pix>::value) {
+      // fractional levels: the sums are not exact, so the norm takes the
+      // reference's second pass over the centred values
+      const double mean = sf / (double)n;
+      double s2 = 0.0;
+      Walk w2 = wk;
+      for (int i = 0; i < w2.npl; ++i) {
+        if (i < w2.npl - 1 || w2.last_valid) {
+          const double c = (double)Rs[w2.roff] - mean;
+          s2 = fma(c, c, s2);
+        }
+        w2.advance();
+      }
+      vfn = warp_sum1(s2);
+    } else {  // integer levels: n sum f^2 - (sum f)^2 is exact
+      vfn = (double)((int64_t)n * (int64_t)sff - (int64_t)sf * (int64_t)sf) / (double)n;
+    }
+    if (!(vfn > 0.0)) {  // constant subset (exact test for integer levels)
       fail(METHOD == 1 ? DICB200_POI_DEGENERATE_TEXTURE : DICB200_POI_DEGENERATE_SUBSET);
       store_fail(DICB200_POI_DEGENERATE_TEXTURE);
       return;
     }
     fbar = sf / (double)n;  // correlation.cpp:25: exact sum / n
-    nf = sqrt((double)vf / (double)n);
+    nf = sqrt(vfn);
     if (lane == 0) {
       C.scf = sf - (double)n * fbar;  // sum of centred values
       C.nf = nf;
@@ -1696,7 +1715,8 @@ __global__ void __launch_bounds__(1024) strip_order_kernel(const dicb200_poi_rec
   for (int st = threadIdx.x; st < ns; st += blockDim.x) order[atomicAdd(&off[bucket(st)], 1)] = st;
 }
 
-cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st, IcgnRefCache* cache, long ref_key) {
+cudaError_t refine_launch(const RefineParams& p0, int dtype, cudaStream_t st, IcgnRefCache* cache, long ref_key) {
+  const bool u8 = dtype == DICB200_U8, f64 = dtype == DICB200_F64;
   if (p0.n_records <= 0) return cudaSuccess;
   RefineParams p = p0;
   p.cache = nullptr;
@@ -1743,7 +1763,7 @@ cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st, Icgn
   // (C4: 41 px subsets every 5 px, C5: every 10 px)
   static const bool generic = std::getenv("DICB200_REFINE_GENERIC") != nullptr;
   TmaPair tm{};
-  if (p.method == 1 && p.M == 20 && (p.lat.step == 10 || p.lat.step == 5) && !generic &&
+  if (p.method == 1 && p.M == 20 && (p.lat.step == 10 || p.lat.step == 5) && !generic && !f64 &&
       p.interp == DICB200_INTERP_BILINEAR) {
     p.spc = kWarps;
     dim3 grid((p.lat.nx + p.spc - 1) / p.spc, rows);
@@ -1855,7 +1875,12 @@ cudaError_t refine_launch(const RefineParams& p0, bool u8, cudaStream_t st, Icgn
     count_launch();
     p.order = order;
   }
-  if (p.method == 0) {
+  if (f64) {  // fractional gray levels: fp32 gathers of the fp64 images, fp64 sums
+    if (p.method == 0)
+      cubic ? go(refine_strip_kernel<double, 0, 0, 0, 1>) : go(refine_strip_kernel<double, 0>);
+    else
+      cubic ? go(refine_strip_kernel<double, 1, 0, 0, 1>) : go(refine_strip_kernel<double, 1>);
+  } else if (p.method == 0) {
     if (cubic)
       u8 ? go(refine_strip_kernel<uint8_t, 0, 0, 0, 1>) : go(refine_strip_kernel<uint16_t, 0, 0, 0, 1>);
     else

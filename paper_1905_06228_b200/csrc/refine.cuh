@@ -53,7 +53,8 @@ struct IcgnRefCache {
 bool refine_plan(int M, int* ppt, int* nt);
 // cache/ref_key: reuse the IC-GN reference-side constants across calls with
 // the same reference frame (ref_key >= 0, same device pointer, lattice and M).
-cudaError_t refine_launch(const RefineParams& p, bool u8, cudaStream_t st, IcgnRefCache* cache = nullptr,
+// dtype: DICB200_U8 | DICB200_U16 | DICB200_F64 (fractional levels, generic kernels)
+cudaError_t refine_launch(const RefineParams& p, int dtype, cudaStream_t st, IcgnRefCache* cache = nullptr,
                           long ref_key = -1);
 void icgn_cache_free(IcgnRefCache& c, cudaStream_t st = nullptr, bool async = false);
 

@@ -138,35 +138,30 @@ class RunConfig:  # pipeline.hpp:33-49
 class GrayImage:
     """Immutable single-channel image (image.hpp:14-31).
 
-    The reference stores doubles; the device path stores the integer gray
-    levels losslessly as uint8 / uint16. Fractional levels in [0, 255] (the
-    reference's synthetic frames) are carried as 8.8 fixed point, round(256 v)
-    in uint16 — ZNCC and the refinement steps are invariant to a positive
-    gray-level scale, so only the 2^-9 quantisation differs from the doubles
-    (`scale` = 256; `at()` returns the level in the caller's units). Anything
-    else raises DicError, as the C++ shim (include/dic_b200/pipeline.hpp) does.
+    The reference stores doubles; the device path stores integer gray levels
+    in [0, 65535] losslessly as uint8 / uint16 (the exact-integer search
+    kernels). Any other finite levels — e.g. the reference's fractional
+    synthetic frames — stay doubles and run on the exact fp64 path (the
+    integer search evaluates the reference's zncc in its own order, bit for
+    bit; the refiners gather fp32 from the fp64 image), as the C++ shim
+    (include/dic_b200/pipeline.hpp) does. Non-finite levels raise DicError
+    (image.cpp:14-22).
     """
 
     def __init__(self, pixels: np.ndarray, id: int = 0):
         a = np.asarray(pixels)
         if a.ndim != 2 or a.shape[0] < 1 or a.shape[1] < 1:
             raise DicError("zero-dimension image")
-        self.scale = 1
         if a.dtype == np.uint8 or a.dtype == np.uint16:
             px = np.ascontiguousarray(a)
         else:
             f = a.astype(np.float64)
             if not np.all(np.isfinite(f)):
                 raise DicError("non-finite gray level")
-            if np.all(f == np.round(f)):
-                if f.min() < 0 or f.max() > 65535:
-                    raise DicError("device path requires integer gray levels in [0, 65535]")
+            if np.all(f == np.round(f)) and f.min() >= 0 and f.max() <= 65535:
                 px = np.ascontiguousarray(f.astype(np.uint8 if f.max() <= 255 else np.uint16))
             else:
-                if f.min() < 0 or f.max() > 255:
-                    raise DicError("fractional gray levels must lie in [0, 255]")
-                px = np.ascontiguousarray(np.floor(f * 256.0 + 0.5).astype(np.uint16))  # half away from zero, as lround
-                self.scale = 256
+                px = np.ascontiguousarray(f)  # fractional (or out-of-range) levels: fp64 path
         px.setflags(write=False)
         self._px = px
         self._id = int(id)
@@ -184,16 +179,16 @@ class GrayImage:
         return self._px
 
     def at(self, x: int, y: int) -> float:
-        return float(self._px[y, x]) / self.scale
+        return float(self._px[y, x])
 
     def as_c(self) -> _abi.Image:
         im = _abi.Image()
         im.width = self.width()
         im.height = self.height()
         im.pitch = self.width()
-        im.dtype = _abi.U8 if self._px.dtype == np.uint8 else _abi.U16
+        im.dtype = {np.dtype(np.uint8): _abi.U8, np.dtype(np.uint16): _abi.U16}.get(self._px.dtype, _abi.F64)
         im.id = self._id
-        im.bits = self.bits()
+        im.bits = self.bits() if im.dtype != _abi.F64 else 0
         im.data = self._px.ctypes.data
         return im
 

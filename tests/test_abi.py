@@ -102,15 +102,17 @@ def test_dimension_mismatch_and_no_cpu_fallback():
 
 
 def test_grayimage_gray_level_mapping():
-    """Integer levels map losslessly; fractional levels in [0, 255] become 8.8
-    fixed point (as the C++ shim packs them); anything else is rejected."""
+    """Integer levels in [0, 65535] map losslessly to u8 / u16 (the exact
+    integer kernels); any other finite levels stay doubles (the fp64 path, as
+    the C++ shim passes them); non-finite levels are rejected (image.cpp:14-22)."""
     g = dic.GrayImage(np.full((8, 8), 300.0))
-    assert g.pixels().dtype == np.uint16 and g.scale == 1 and g.at(0, 0) == 300.0
+    assert g.pixels().dtype == np.uint16 and g.at(0, 0) == 300.0 and g.as_c().dtype == _abi.U16
     f = dic.GrayImage(np.array([[1.5, 0.0], [254.99609375, 17.25]]))
-    assert f.scale == 256 and f.pixels().tolist() == [[384, 0], [65279, 4416]] and f.at(0, 1) == 254.99609375
-    for bad in (np.full((8, 8), 300.5), np.full((8, 8), -0.5), np.full((8, 8), np.nan), np.full((8, 8), 70000.0)):
-        with pytest.raises(dic.DicError):
-            dic.GrayImage(bad)
+    assert f.pixels().dtype == np.float64 and f.at(0, 1) == 254.99609375 and f.as_c().dtype == _abi.F64
+    for frac in (np.full((8, 8), 300.5), np.full((8, 8), -0.5), np.full((8, 8), 70000.0)):
+        assert dic.GrayImage(frac).as_c().dtype == _abi.F64
+    with pytest.raises(dic.DicError):
+        dic.GrayImage(np.full((8, 8), np.nan))
 
 
 def test_synth_generator_is_deterministic_and_in_range():
