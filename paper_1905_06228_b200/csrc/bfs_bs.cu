@@ -860,8 +860,8 @@ __global__ void __launch_bounds__(32 * kExactRowWarps) bs_exact_rows_kernel(TcPa
   __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nf = min(*n_flagged, kExactSlots);
-  const int ry = blockIdx.y;
-  for (int i = blockIdx.x; i < nf; i += gridDim.x) {
+  const int ry = blockIdx.x;  // rows fastest: the CTAs of the first slots come first in launch order
+  for (int i = blockIdx.y; i < nf; i += gridDim.y) {
   const size_t k = (size_t)flagged[i];
   const int ix = (int)(k % p.lat.nx), iy = p.rb + (int)(k / p.lat.nx);
   const int cx = p.lat.cx(ix), cy = p.lat.cy(iy), M = p.M, R = p.R, side = p.side;
@@ -869,17 +869,20 @@ __global__ void __launch_bounds__(32 * kExactRowWarps) bs_exact_rows_kernel(TcPa
   const int fy_lo = max(-R, M - cy), fy_hi = min(R, p.tgt.height - 1 - M - cy);
   const int fw = fx_hi - fx_lo + 1, fh = fy_hi - fy_lo + 1, ww = fw + side - 1;
   if (ry >= fh) continue;  // rows past the feasible window: no CTA work, no arrival (uniform)
+  // u32 partial sums of at most flush_every products (< 2^32 for the pair's pixel range)
+  // (2R+1 <= kExactRowWarps * kExactDx dx lanes per CTA: rows_ok)
+  const double mv = p.maxv > 0 ? p.maxv : 65535.0;
+  const int flush_every = (int)fmax(1.0, fmin(64.0, floor(4294967295.0 / fmax(1.0, mv * mv))));
   const int dy = fy_lo + ry;
   const Pix* f = static_cast<const Pix*>(p.ref.data);
   const Pix* g = static_cast<const Pix*>(p.tgt.data);
   __syncthreads();  // the previous slot's reduction is done with the staged data
-  for (int t = tid; t < side * side; t += blockDim.x) {
-    const int r = t / side, c = t - r * side;
-    fs[t] = (uint16_t)f[(size_t)(cy - M + r) * p.ref.pitch + (cx - M + c)];
-  }
-  for (int t = tid; t < ww * side; t += blockDim.x) {
-    const int r = t / ww, c = t - r * ww;
-    gs[t] = (uint16_t)g[(size_t)(cy - M + dy + r) * p.tgt.pitch + (cx - M + fx_lo + c)];
+  // warp per row, lanes across columns: the loads of a warp's rows are independent
+  for (int r = warp; r < side; r += kExactRowWarps) {
+    const Pix* fr = f + (size_t)(cy - M + r) * p.ref.pitch + (cx - M);
+    const Pix* gr = g + (size_t)(cy - M + dy + r) * p.tgt.pitch + (cx - M + fx_lo);
+    for (int c = lane; c < side; c += 32) fs[r * side + c] = (uint16_t)fr[c];
+    for (int c = lane; c < ww; c += 32) gs[r * ww + c] = (uint16_t)gr[c];
   }
   __syncthreads();
   BestPartial b;
@@ -887,29 +890,65 @@ __global__ void __launch_bounds__(32 * kExactRowWarps) bs_exact_rows_kernel(TcPa
   b.dx = b.dy = 0;
   b.count = 0;
   b.found = 0;
-  for (int wx = warp; wx < fw; wx += kExactRowWarps) {
+  // warp w takes dx lanes w, w + 8, w + 16, w + 24 (kExactDx per warp, all
+  // at once: one reference load per pixel feeds them all); lanes across the
+  // subset columns (c and c + 32), rows in order; u32 runs of at most
+  // flush_every rows' products, flushed to u64 (exact)
+  constexpr int kExactDx = 4;
+  uint64_t acc64[kExactDx] = {0, 0, 0, 0};
+  uint32_t acc[kExactDx] = {0, 0, 0, 0};
+  const int c0 = lane, c1 = lane + 32;
+  const bool two = c1 < side;
+  int run = 0;
+  const bool wide = flush_every < 2;
+  const int rows_per_flush = max(1, flush_every / 2);
+  for (int r = 0; r < side; ++r) {
+    const uint16_t* fr = fs + r * side;
+    const uint16_t* gr = gs + r * ww + warp;
+    const uint32_t fa = c0 < side ? fr[c0] : 0u, fb = two ? fr[c1] : 0u;
+#pragma unroll
+    for (int j = 0; j < kExactDx; ++j) {
+      const int wx = j * kExactRowWarps;  // + warp (in gr)
+      if (warp + wx < fw) {
+        const uint32_t va = c0 < side ? fa * gr[wx + c0] : 0u, vb = two ? fb * gr[wx + c1] : 0u;
+        if (wide)  // products near 2^32 (16-bit pixels): straight into u64
+          acc64[j] += (uint64_t)va + vb;
+        else
+          acc[j] += va + vb;
+      }
+    }
+    if (++run == rows_per_flush) {
+#pragma unroll
+      for (int j = 0; j < kExactDx; ++j) {
+        acc64[j] += acc[j];
+        acc[j] = 0;
+      }
+      run = 0;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kExactDx; ++j) {
+    acc64[j] += acc[j];
+#pragma unroll
+    for (int o2 = 16; o2; o2 >>= 1) acc64[j] += __shfl_xor_sync(0xffffffffu, acc64[j], o2);
+  }
+  const uint32_t n = (uint32_t)(side * side), sf = (uint32_t)p.poi_sf[k];
+#pragma unroll
+  for (int j = 0; j < kExactDx; ++j) {  // dx ascending within the warp
+    const int wx = warp + j * kExactRowWarps;
+    if (wx >= fw) continue;
     const int dx = fx_lo + wx;
     const size_t o = (size_t)(cy - M + dy - p.qy_min) * p.SW + (cx - M + dx - p.qx_min);
     const double sq = p.SQ[o];
-    if (sq > 0.0) {  // constant target window: skipped, not counted
-      uint64_t acc64 = 0;  // each product < 2^32 (16-bit pixels), sums exact in u64
-      for (int r = 0; r < side; ++r) {
-        const uint16_t* fr = fs + r * side;
-        const uint16_t* gr = gs + r * ww + wx;
-        for (int c = lane; c < side; c += 32) acc64 += (uint64_t)((uint32_t)fr[c] * gr[c]);
-      }
-#pragma unroll
-      for (int o2 = 16; o2; o2 >>= 1) acc64 += __shfl_xor_sync(0xffffffffu, acc64, o2);
-      const uint32_t n = (uint32_t)(side * side), sf = (uint32_t)p.poi_sf[k];
-      const int64_t num = (int64_t)(acc64 * n - (uint64_t)sf * p.S1[o]);
-      BestPartial q;
-      q.c = bs_i64_to_f64(num) / (p.poi_sqrtvf[k] * sq);
-      q.dx = dx;
-      q.dy = dy;
-      q.count = 1;
-      q.found = 1;
-      merge_best(b, q);  // dx ascending within the warp
-    }
+    if (!(sq > 0.0)) continue;  // constant target window: skipped, not counted
+    const int64_t num = (int64_t)(acc64[j] * n - (uint64_t)sf * p.S1[o]);
+    BestPartial q;
+    q.c = bs_i64_to_f64(num) / (p.poi_sqrtvf[k] * sq);
+    q.dx = dx;
+    q.dy = dy;
+    q.count = 1;
+    q.found = 1;
+    merge_best(b, q);
   }
   if (lane == 0) {
     red_c[warp] = b.found ? b.c : -3.0;
@@ -938,14 +977,14 @@ __global__ void __launch_bounds__(32 * kExactRowWarps) bs_exact_rows_kernel(TcPa
     s_last = atomicAdd(&arrivals[i], 1) == fh - 1;
   }
   __syncthreads();
-  if (s_last && tid == 0) {  // every row of this POI is in: merge (rows in dy order, improves() decides)
+  if (s_last && warp == 0) {  // every row of this POI is in: merge (improves() decides, any order)
     __threadfence();
     BestPartial t;
     t.c = -2.0;
     t.dx = t.dy = 0;
     t.count = 0;
     t.found = 0;
-    for (int r = 0; r < fh; ++r) {
+    for (int r = lane; r < fh; r += 32) {  // rows loaded together, one per lane
       const BestPartial* src = part + (size_t)i * kExactMaxWin + r;  // written by other CTAs: read through L2
       BestPartial q;
       q.c = __ldcg(&src->c);
@@ -955,8 +994,20 @@ __global__ void __launch_bounds__(32 * kExactRowWarps) bs_exact_rows_kernel(TcPa
       q.found = __ldcg(&src->found);
       merge_best(t, q);
     }
-    arrivals[i] = 0;
-    write_integer_record(p.rec[k], cx, cy, t, p.subpixel_none);
+#pragma unroll
+    for (int o2 = 16; o2; o2 >>= 1) {
+      BestPartial q;
+      q.c = __shfl_xor_sync(0xffffffffu, t.c, o2);
+      q.dx = __shfl_xor_sync(0xffffffffu, t.dx, o2);
+      q.dy = __shfl_xor_sync(0xffffffffu, t.dy, o2);
+      q.count = __shfl_xor_sync(0xffffffffu, t.count, o2);
+      q.found = __shfl_xor_sync(0xffffffffu, t.found, o2);
+      merge_best(t, q);
+    }
+    if (lane == 0) {
+      arrivals[i] = 0;
+      write_integer_record(p.rec[k], cx, cy, t, p.subpixel_none);
+    }
   }
   }
 }
@@ -1255,12 +1306,12 @@ cudaError_t bs_merge_launch(const TcParams& p, const BsGeom& g, cudaStream_t st)
       fprintf(stderr, "  slice %zu: a1 %.9g a2 %.9g cnt %d d (%d,%d)\n", i, h[i].a1, h[i].a2, h[i].cnt, h[i].dx, h[i].dy);
   }
   // flagged POIs (near ties are rare: idle CTAs exit at once): a CTA per
-  // (slot, displacement row), slots strided over 64 CTA columns; past
+  // (slot, displacement row), slots strided over 16 CTA rows; past
   // kExactSlots, one CTA per POI
   const int ew = 2 * p.R + 1;
-  const bool rows_ok = ew <= kExactRowWarps && p.side <= kExactMaxSide && p.side + ew - 1 <= kExactMaxWin;
+  const bool rows_ok = ew <= 32 && p.side <= kExactMaxSide && p.side + ew - 1 <= kExactMaxWin;
   if (rows_ok) {
-    const dim3 grid(64, ew);
+    const dim3 grid(ew, 16);
     if (p.planes == 1)
       bs_exact_rows_kernel<uint8_t><<<grid, 32 * kExactRowWarps, 0, st>>>(p, flagged, n_flagged, part, arrivals);
     else

@@ -1841,7 +1841,10 @@ cudaError_t refine_launch(const RefineParams& p0, int dtype, cudaStream_t st, Ic
         p.use_tma = 2;
       }
     }
+    // DICB200_REFINE_SMEM_PAD (experiments): extra dynamic shared memory per CTA (occupancy study)
+    static const size_t smem_pad = std::getenv("DICB200_REFINE_SMEM_PAD") ? std::atoi(std::getenv("DICB200_REFINE_SMEM_PAD")) : 0;
     auto go = [&](auto k, size_t sm) {
+      sm += smem_pad;
       e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
