@@ -13,5 +13,5 @@ timeout 900 python bench.py > $O/bench_c5.json 2> $O/bench_c5.err
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref_c5.json 2> $O/bench_ref_c5.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_bench_c5.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_bench.log 2>&1
-OUT=$O/prof bash tools/r02_prof.sh
+OUT=$O/prof bash tools/prof_steady.sh
 ls -la $O
