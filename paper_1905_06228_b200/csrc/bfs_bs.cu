@@ -483,7 +483,13 @@ struct BsLane {
   uint32_t pad;
 };
 
-template <int S, int RR, int Q, int DXC, int NPW, int NCW, typename Pix, bool FUSE = false, int PYM = 1>
+// Cycle counters of one interior CTA (DICB200_BS_PROF=1, PROF instantiation):
+// [0..3] producer warp 0: compute, wait for the buffer, store, items;
+// [4..7] consumer warp 0: wait for the partials, phase B, window staging, items.
+__device__ unsigned long long g_bs_prof[8];
+
+template <int S, int RR, int Q, int DXC, int NPW, int NCW, typename Pix, bool FUSE = false, int PYM = 1, int PV = 0,
+          bool PROF = false>
 __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, BsGeom g) {
   constexpr int NT = 32 * (NPW + NCW), NP = 32 * NPW, NC = 32 * NCW;
   constexpr int BS = 4 * DXC + 1;  // words per block record (odd: conflict-free stores across blocks)
@@ -520,6 +526,12 @@ __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, 
   const int nbx = g.nbx;
   const int nbx_here = nx_here + Q - (RR == 0 ? 1 : 0), nby = ny_here + Q - (RR == 0 ? 1 : 0);
   const int nchunk = g.nchunk, n_items = (dy_hi - dy_lo + 1) * nchunk;
+  // PV 1, fused: the consumer warps past the (POI column, dx lane) threads of
+  // phase B are dedicated stagers of the window data (see below) and stay out of
+  // the item barriers
+  const int nbw = (g.PX * DXC + 31) >> 5;
+  const bool ded = FUSE && PV == 1 && nbw < NCW;
+  const int NTB = ded ? NP + 32 * nbw : NT;
   if (threadIdx.x < NP) {
     // ---- producers: phase A of item it in registers (one block per thread),
     // then, once the consumers have released the buffer, the store
@@ -531,13 +543,56 @@ __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, 
     const int by = active ? task / nbx_here : 0, bx = active ? task - by * nbx_here : 0, bi = by * nbx + bx;
     const uint16_t* fr = Rf + (by * S) * RP + shR + bx * S;
     uint32_t* o = blk0 + bi * BS;
+    const bool prof = PROF && blockIdx.x == 1 && blockIdx.y == 1 && blockIdx.z == 0 && threadIdx.x == 0;
+    unsigned long long pc0 = 0, pc1 = 0, pc2 = 0;
     for (int it = 0; it < n_items; ++it) {
       const int dy = dy_lo + it / nchunk, dx0 = (it % nchunk) * DXC;
       const uint16_t* gr = Tg + (by * S + dy + R) * TP + shT + bx * S + dx0;
+      long long t0 = 0, t1 = 0, t2 = 0;
+      if (PROF) t0 = clock64();
       uint32_t F[DXC], Cc[DXC], Wr[DXC], Kc[DXC];
 #pragma unroll
       for (int j = 0; j < DXC; ++j) F[j] = Cc[j] = Wr[j] = Kc[j] = 0u;
-      if (active) {
+      if (PV == 1) {
+        // rows >= RR accumulate straight into F (columns >= RR) and Cc (columns
+        // < RR), the first RR rows — walked last, so their accumulators are
+        // short-lived — into Wr / Kc; the four stored partials are sums of those
+        if (active) {
+#pragma unroll
+          for (int y2 = 0; y2 < S; ++y2) {
+            const int yy = y2 < S - RR ? y2 + RR : y2 - (S - RR);  // RR .. S-1, then 0 .. RR-1
+            uint32_t f[S], gg[S + DXC - 1];
+#pragma unroll
+            for (int k = 0; k < S; ++k) f[k] = fr[yy * RP + k];
+#pragma unroll
+            for (int k = 0; k < S + DXC - 1; ++k) gg[k] = gr[yy * TP + k];
+#pragma unroll
+            for (int k = 0; k < S; ++k)
+#pragma unroll
+              for (int j = 0; j < DXC; ++j) {
+                if (yy >= RR) {
+                  if (k >= RR)
+                    F[j] += f[k] * gg[k + j];
+                  else
+                    Cc[j] += f[k] * gg[k + j];
+                } else {
+                  if (k >= RR)
+                    Wr[j] += f[k] * gg[k + j];
+                  else
+                    Kc[j] += f[k] * gg[k + j];
+                }
+              }
+          }
+#pragma unroll
+          for (int j = 0; j < DXC; ++j) {
+            if (RR > 0) {
+              F[j] += Cc[j] + Wr[j] + Kc[j];
+              Cc[j] += Kc[j];
+              Wr[j] += Kc[j];
+            }
+          }
+        }
+      } else if (active) {
 #pragma unroll
         for (int yy = 0; yy < S; ++yy) {
           uint32_t f[S], gg[S + DXC - 1];
@@ -571,7 +626,9 @@ __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, 
           }
         }
       }
-      if (it >= 1) named_bar_sync(2, NT);  // consumers are done with item it - 1
+      if (PROF) t1 = clock64();
+      if (it >= 1) named_bar_sync(2, NTB);  // consumers are done with item it - 1
+      if (PROF) t2 = clock64();
       // columns past the chunk's last dx hold products with zero padding or
       // the next chunk's dx: stored anyway (never read)
       if (active) {
@@ -585,7 +642,19 @@ __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, 
           }
         }
       }
-      named_bar_arrive(1, NT);
+      named_bar_arrive(1, NTB);
+      if (PROF) {
+        const long long t3 = clock64();
+        pc0 += (unsigned long long)(t1 - t0);
+        pc1 += (unsigned long long)(t2 - t1);
+        pc2 += (unsigned long long)(t3 - t2);
+      }
+    }
+    if (prof) {
+      g_bs_prof[0] = pc0;
+      g_bs_prof[1] = pc1;
+      g_bs_prof[2] = pc2;
+      g_bs_prof[3] = (unsigned long long)n_items;
     }
   } else if (FUSE) {
     // ---- fused consumers: phase B and the exact-argmax filter. Thread
@@ -614,11 +683,34 @@ __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, 
     const int XW = (g.PX - 1) * p.lat.step + 2 * R + 1;
     float* pos_rsq = reinterpret_cast<float*>(bs_smem + g.off_pos);  // [2][PYM][XW]
     uint32_t* pos_s1 = reinterpret_cast<uint32_t*>(pos_rsq + 2 * PYM * XW);
-    bs_stage_positions(p, g, ix0, iy0, ny_here, dy_lo, XW, PYM, pos_rsq, pos_s1, tc, NC);
+    const bool cprof = PROF && blockIdx.x == 1 && blockIdx.y == 1 && blockIdx.z == 0 && tc == 0;
+    unsigned long long cc0 = 0, cc1 = 0, cc2 = 0;
+    if (ded && tc >= 32 * nbw) {
+      // ---- dedicated stagers: the window data of dy go into buffer (dy - dy_lo) & 1
+      // once the phase-B warps have released it (they were done with dy - 2),
+      // a whole displacement row ahead of its use. Named barriers by buffer
+      // parity: 3 / 4 = data landed (stagers arrive, phase B waits), 5 / 6 =
+      // buffer released (the reverse); a generation of either can only start
+      // after the previous one of the same parity completed.
+      const int ts = tc - 32 * nbw, ns = NC - 32 * nbw;
+      for (int dy = dy_lo; dy <= dy_hi; ++dy) {
+        const int pb = (dy - dy_lo) & 1;
+        if (dy >= dy_lo + 2) named_bar_sync(5 + pb, NC);
+        bs_stage_positions(p, g, ix0, iy0, ny_here, dy, XW, PYM, pos_rsq + pb * PYM * XW, pos_s1 + pb * PYM * XW, ts,
+                           ns);
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        named_bar_arrive(3 + pb, NC);
+      }
+    } else {
+    if (!ded) bs_stage_positions(p, g, ix0, iy0, ny_here, dy_lo, XW, PYM, pos_rsq, pos_s1, tc, NC);
     for (int it = 0; it < n_items; ++it) {
       const int dy = dy_lo + it / nchunk, dxv = (it % nchunk) * DXC + dxi - R;
       const int pb = (dy - dy_lo) & 1;
-      if (it % nchunk == 0) {  // new dy: its window data landed, the next dy's starts
+      long long c0 = 0, c1 = 0, c2 = 0;
+      if (PROF) c0 = clock64();
+      if (ded) {
+        if (it % nchunk == 0) named_bar_sync(3 + pb, NC);  // the stagers' data of dy landed
+      } else if (it % nchunk == 0) {  // new dy: its window data landed, the next dy's starts
         named_bar_sync(3, NC);   // every consumer is done with dy - 1: its buffer is free
         if (dy < dy_hi) {
           bs_stage_positions(p, g, ix0, iy0, ny_here, dy + 1, XW, PYM, pos_rsq + (pb ^ 1) * PYM * XW,
@@ -629,7 +721,9 @@ __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, 
         }
         named_bar_sync(3, NC);
       }
-      named_bar_sync(1, NT);  // producers stored item it
+      if (PROF) c1 = clock64();
+      named_bar_sync(1, NTB);  // producers stored item it
+      if (PROF) c2 = clock64();
       const bool xin = act && dxv <= R && dxv >= fx_lo && dxv <= fx_hi;
       if (__any_sync(0xffffffffu, xin)) {
         const uint32_t* col = blk0 + pi * BS + dxi;
@@ -688,10 +782,24 @@ __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, 
                    ((dc[pj] & 0xffffu) + (valid ? 1u : 0u));
         }
       }
-      if (it + 1 < n_items) named_bar_arrive(2, NT);  // buffer free for item it + 1
+      if (it + 1 < n_items) named_bar_arrive(2, NTB);  // buffer free for item it + 1
+      if (ded && it % nchunk == nchunk - 1 && dy + 2 <= dy_hi) named_bar_arrive(5 + pb, NC);  // done with dy
+      if (PROF) {
+        const long long c3 = clock64();
+        cc0 += (unsigned long long)(c2 - c1);
+        cc1 += (unsigned long long)(c3 - c2);
+        cc2 += (unsigned long long)(c1 - c0);
+      }
+    }
+    }
+    if (cprof) {
+      g_bs_prof[4] = cc0;
+      g_bs_prof[5] = cc1;
+      g_bs_prof[6] = cc2;
+      g_bs_prof[7] = (unsigned long long)n_items;
     }
     // ---- slice result per POI: reduce the DXC dx lanes (through the free block buffer)
-    named_bar_sync(3, NC);  // every consumer is past its last read of the block buffer
+    named_bar_sync(7, NC);  // every consumer is past its last read of the block buffer
     BsLane* lanes = reinterpret_cast<BsLane*>(blk0);  // [PY][PX][DXC]
     if (act) {
 #pragma unroll
@@ -705,7 +813,7 @@ __global__ void __launch_bounds__(32 * (NPW + NCW), 1) bs_ws_kernel(TcParams p, 
         }
       }
     }
-    named_bar_sync(3, NC);
+    named_bar_sync(7, NC);
     for (int i = tc; i < nx_here * ny_here; i += NC) {
       const int qi = i % nx_here, qj = i / nx_here;
       const BsLane* l = lanes + (qj * g.PX + qi) * DXC;
@@ -1340,11 +1448,25 @@ cudaError_t launch_ws(const TcParams& p, const BsGeom& g, dim3 grid, cudaStream_
     if (e == cudaSuccess) k<<<grid, 32 * (NPW + NCW), g.smem, st>>>(p, g);
   };
   if (g.PY > PYM) return cudaErrorInvalidValue;
+  static const int pv = std::getenv("DICB200_BS_PV") ? std::atoi(std::getenv("DICB200_BS_PV")) : 0;
+  static const bool prof = std::getenv("DICB200_BS_PROF") != nullptr;
   if (p.planes == 1)
     g.fuse ? go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint8_t, true, PYM>) : go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint8_t>);
-  else
-    g.fuse ? go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint16_t, true, PYM>)
-           : go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint16_t>);
+  else if (!g.fuse)
+    go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint16_t>);
+  else if (prof) {
+    pv == 1 ? go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint16_t, true, PYM, 1, true>)
+            : go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint16_t, true, PYM, 0, true>);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    unsigned long long h[8] = {0};
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(h, g_bs_prof, sizeof(h));
+    fprintf(stderr,
+            "[bs prof] pv %d items %llu producer: compute %llu wait %llu store %llu | consumer: wait %llu phaseB %llu "
+            "staging %llu (cycles, CTA (1,1,0))\n",
+            pv, h[3], h[0], h[1], h[2], h[4], h[5], h[6]);
+  } else
+    pv == 1 ? go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint16_t, true, PYM, 1>)
+            : go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint16_t, true, PYM>);
   return e;
 }
 
