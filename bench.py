@@ -299,6 +299,9 @@ def run_shim_bench(frames, seq, cfg, esize: int, warmup: int, steps: int):
     if r.returncode != 0:
         return {"unavailable": f"shim_bench rc={r.returncode}: {r.stderr.strip()[-300:]}"}
     out = json.loads(r.stdout.strip().splitlines()[-1])
+    tr = [ln for ln in r.stderr.splitlines() if ln.startswith("[dicb200 shim]")]
+    if tr:  # DICB200_SHIM_TRACE=1: host phase times of the last call
+        out["trace"] = tr[-1]
     out["h2d_bytes_per_step"] = int(len(seq) * w * h * esize)
     out["d2h_bytes_per_step"] = int(out["pois_per_step"] * C.sizeof(_abi.PoiRecordC))
     return out

@@ -17,12 +17,16 @@
 #pragma once
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <map>
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -120,7 +124,33 @@ class Frames {
     imgs_.resize(n);
     int maxv = 0;
     bool fp = false;  // some frame is not integral in [0, 65535]: all frames as doubles
+    bool same = true;  // frames of one size pack in one batched call
+    for (const GrayImage* g : images)
+      same = same && g->width() == images[0]->width() && g->height() == images[0]->height();
+    std::vector<int32_t> frac(n, 0), mx(n, 0);
+    if (same && n > 0) {
+      std::vector<const double*> src(n);
+      std::vector<uint16_t*> dst(n);
+      for (size_t i = 0; i < n; ++i) {
+        src[i] = images[i]->pixels().data();
+        dst[i] = static_cast<uint16_t*>(blocks_[i]);
+      }
+      const dicb200_status st = dicb200_pack_gray_batch(src.data(), static_cast<int32_t>(n), images[0]->width(),
+                                                        images[0]->height(), images[0]->width(), dst.data(),
+                                                        frac.data(), mx.data(), 0);
+      fp = st != DICB200_OK;
+    } else {
+      for (size_t i = 0; i < n && !fp; ++i) {
+        const GrayImage& g = *images[i];
+        fp = dicb200_pack_gray(g.pixels().data(), g.width(), g.height(), g.width(), 1,
+                               static_cast<uint16_t*>(blocks_[i]), &frac[i], &mx[i], 0) != DICB200_OK;
+      }
+    }
     for (size_t i = 0; i < n && !fp; ++i) {
+      if (frac[i]) {
+        fp = true;
+        break;
+      }
       const GrayImage& g = *images[i];
       dicb200_image& im = imgs_[i];
       im.width = g.width();
@@ -129,17 +159,9 @@ class Frames {
       im.id = g.id();
       im.dtype = DICB200_U16;
       im.data = blocks_[i];
-      uint16_t* dst = static_cast<uint16_t*>(blocks_[i]);
-      int32_t frac = 0, mx = 0;
-      const dicb200_status st = dicb200_pack_gray(g.pixels().data(), g.width(), g.height(), g.width(), 1, dst, &frac,
-                                                  &mx, 0);
-      if (st != DICB200_OK || frac) {
-        fp = true;
-        break;
-      }
       im.bits = 1;
-      while (im.bits < 16 && (1 << im.bits) - 1 < mx) ++im.bits;
-      maxv = std::max(maxv, (int)mx);
+      while (im.bits < 16 && (1 << im.bits) - 1 < mx[i]) ++im.bits;
+      maxv = std::max(maxv, (int)mx[i]);
     }
     if (fp) {  // the GrayImages' own doubles (read-only for the call); non-finite levels fail the pair
       for (size_t i = 0; i < n; ++i) {
@@ -154,13 +176,24 @@ class Frames {
         im.data = g.pixels().data();
       }
     } else if (maxv <= 255) {  // every frame 8-bit: u8 (one byte plane on the device)
-      for (dicb200_image& im : imgs_) {
-        const uint16_t* s16 = static_cast<const uint16_t*>(im.data);
-        uint8_t* d8 = static_cast<uint8_t*>(const_cast<void*>(im.data));
-        const size_t m = static_cast<size_t>(im.width) * im.height;
-        for (size_t k = 0; k < m; ++k) d8[k] = static_cast<uint8_t>(s16[k]);  // in place, front to back
-        im.dtype = DICB200_U8;
-        im.bits = 8;
+      auto narrow = [this](size_t lo, size_t hi) {
+        for (size_t i = lo; i < hi; ++i) {
+          dicb200_image& im = imgs_[i];
+          const uint16_t* s16 = static_cast<const uint16_t*>(im.data);
+          uint8_t* d8 = static_cast<uint8_t*>(const_cast<void*>(im.data));
+          const size_t m = static_cast<size_t>(im.width) * im.height;
+          for (size_t k = 0; k < m; ++k) d8[k] = static_cast<uint8_t>(s16[k]);  // in place, front to back
+          im.dtype = DICB200_U8;
+          im.bits = 8;
+        }
+      };
+      const size_t nt = std::min<size_t>(n, std::max(1u, std::thread::hardware_concurrency()));
+      if (nt <= 1 || px < (size_t(1) << 18)) {
+        narrow(0, n);
+      } else {  // whole frames per thread
+        std::vector<std::thread> pool;
+        for (size_t t = 0; t < nt; ++t) pool.emplace_back(narrow, n * t / nt, n * (t + 1) / nt);
+        for (auto& th : pool) th.join();
       }
     } else {  // one dtype for all frames (the C-ABI's rule); bits = the widest frame's
       int bits = 1;
@@ -235,34 +268,66 @@ inline std::vector<DisplacementField> analyze_sequence(const std::vector<GrayIma
   // with the reference's message (analyze_pair, pipeline.cpp:150-151)
   std::vector<const GrayImage*> ptrs;
   for (const GrayImage& g : images) ptrs.push_back(&g);
+  const bool trace = std::getenv("DICB200_SHIM_TRACE") != nullptr;  // phase times on stderr
+  const auto t0 = std::chrono::steady_clock::now();
   const detail::Frames fr(ptrs);
-  std::vector<std::vector<dicb200_poi_record>> recs(pairs.size());
-  std::vector<dicb200_field> cf(pairs.size());
+  const auto t1 = std::chrono::steady_clock::now();
+  // records are read back straight into pinned blocks (no staging copy, no
+  // zero fill) and each field is converted as soon as it is final, on the
+  // library's worker thread, while the device runs the following pairs
+  struct Ctx {
+    const std::vector<GrayImage>* images;
+    const std::vector<std::pair<int, int>>* pairs;
+    std::vector<dicb200_field> cf;
+    std::vector<DisplacementField> fields;
+  } ctx;
+  ctx.images = &images;
+  ctx.pairs = &pairs;
+  ctx.cf.resize(pairs.size());
+  ctx.fields.resize(pairs.size());
+  size_t cap = 0;
+  std::vector<size_t> counts(pairs.size(), 0);
   for (size_t i = 0; i < pairs.size(); ++i) {
-    size_t n = 0;
     const GrayImage& a = images[pairs[i].first];
-    if (dicb200_grid_size(a.width(), a.height(), &c, &n) != DICB200_OK) n = 0;
-    recs[i].resize(std::max<size_t>(n, 1));
-    cf[i] = dicb200_field{};
-    cf[i].records = recs[i].data();
-    cf[i].capacity = n;
+    if (dicb200_grid_size(a.width(), a.height(), &c, &counts[i]) != DICB200_OK) counts[i] = 0;
+    cap = std::max(cap, counts[i]);
   }
-  const dicb200_status st = dicb200_analyze_sequence(fr.data(), images.size(), &c, cf.data(), cf.size());
-  if (st != DICB200_OK) detail::raise(st);
-  std::vector<DisplacementField> fields(pairs.size());
+  detail::PinnedPool& pool = detail::PinnedPool::get();
+  const std::vector<void*> blocks = pool.take(pairs.size(), std::max<size_t>(cap, 1) * sizeof(dicb200_poi_record));
+  struct Release {
+    detail::PinnedPool& pool;
+    const std::vector<void*>& blocks;
+    ~Release() { pool.release(blocks); }
+  } release{pool, blocks};
   for (size_t i = 0; i < pairs.size(); ++i) {
-    DisplacementField& f = fields[i];
-    f.pair_index = static_cast<int>(i);
-    f.ref_id = images[pairs[i].first].id();
-    f.tgt_id = images[pairs[i].second].id();
-    if (cf[i].status != DICB200_OK) {
-      f.error = cf[i].error;
-      continue;
-    }
-    f.records.reserve(cf[i].count);
-    for (size_t k = 0; k < cf[i].count; ++k) f.records.push_back(detail::to_record(recs[i][k]));
+    ctx.cf[i] = dicb200_field{};
+    ctx.cf[i].records = static_cast<dicb200_poi_record*>(blocks[i]);
+    ctx.cf[i].capacity = counts[i];
   }
-  return fields;
+  auto ready = [](void* user, size_t i) {
+    Ctx& x = *static_cast<Ctx*>(user);
+    DisplacementField& f = x.fields[i];
+    const dicb200_field& cf = x.cf[i];
+    f.pair_index = static_cast<int>(i);
+    f.ref_id = (*x.images)[(*x.pairs)[i].first].id();
+    f.tgt_id = (*x.images)[(*x.pairs)[i].second].id();
+    if (cf.status != DICB200_OK) {
+      f.error = cf.error;
+      return;
+    }
+    f.records.reserve(cf.count);
+    for (size_t k = 0; k < cf.count; ++k) f.records.push_back(detail::to_record(cf.records[k]));
+  };
+  const dicb200_status st =
+      dicb200_analyze_sequence_cb(fr.data(), images.size(), &c, ctx.cf.data(), ctx.cf.size(), ready, &ctx);
+  if (trace) {
+    const auto t2 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[dicb200 shim] pack %.1f ms, device pipeline + records %.1f ms\n",
+                 std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                 std::chrono::duration<double, std::milli>(t2 - t1).count());
+  }
+  if (st != DICB200_OK) detail::raise(st);
+  return std::move(ctx.fields);
 }
 
 }  // namespace b200

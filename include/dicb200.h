@@ -201,6 +201,17 @@ dicb200_status dicb200_analyze_pair(const dicb200_image* reference, const dicb20
 dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_images,
                                         const dicb200_run_config* cfg, dicb200_field* fields,
                                         size_t n_fields);
+/* The same, calling field_ready(user, i) on the host as soon as fields[i] is
+ * final (records read back, or its pair-level error stored), while the device
+ * runs the following pairs: the caller converts / consumes field i there
+ * instead of after the whole sequence (the C++ shim builds the reference's
+ * DisplacementField records in it). Called once per field, from the worker
+ * thread of the field's device (concurrently for mode == IMAGE over several
+ * devices); it must not call back into the library. NULL = none. */
+typedef void (*dicb200_field_ready_fn)(void* user, size_t field_index);
+dicb200_status dicb200_analyze_sequence_cb(const dicb200_image* images, size_t n_images,
+                                           const dicb200_run_config* cfg, dicb200_field* fields,
+                                           size_t n_fields, dicb200_field_ready_fn field_ready, void* user);
 
 /* Device-resident entry point: images hold device pointers, records are
  * written to device memory `out_dev`, everything is enqueued on `stream`
@@ -272,6 +283,12 @@ dicb200_status dicb200_sequence_files(const char* dir, const char* pattern, char
 dicb200_status dicb200_pack_gray(const double* src, int32_t width, int32_t height, int32_t src_pitch,
                                  int32_t scale, uint16_t* dst, int32_t* fractional, int32_t* max_level,
                                  int32_t threads);
+/* The same for every frame of a sequence in one call (scale 1): the row bands
+ * of all frames are dealt to one set of threads; fractional[k] / max_level[k]
+ * per frame. */
+dicb200_status dicb200_pack_gray_batch(const double* const* src, int32_t count, int32_t width, int32_t height,
+                                       int32_t src_pitch, uint16_t* const* dst, int32_t* fractional,
+                                       int32_t* max_level, int32_t threads);
 void* dicb200_host_alloc(size_t bytes); /* pinned host memory (NULL on failure) */
 void dicb200_host_free(void* p);
 

@@ -15,7 +15,7 @@ LIB = os.path.join(HERE, "libdicb200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 CU_SOURCES = ["host.cu", "bfs.cu", "bfs_tc.cu", "bfs_bs.cu", "bfs_fp.cu", "io.cu", "accuracy.cu", "bench_matrix.cu", "refine.cu", "pso.cu", "synth_device.cu"]
-C_SOURCES = ["synth.c"]
+C_SOURCES = ["synth.c", "pack.c"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -1448,7 +1448,8 @@ cudaError_t launch_ws(const TcParams& p, const BsGeom& g, dim3 grid, cudaStream_
     if (e == cudaSuccess) k<<<grid, 32 * (NPW + NCW), g.smem, st>>>(p, g);
   };
   if (g.PY > PYM) return cudaErrorInvalidValue;
-  static const int pv = std::getenv("DICB200_BS_PV") ? std::atoi(std::getenv("DICB200_BS_PV")) : 0;
+  // producer / staging variant: 1 (default) = direct accumulation + dedicated stager warps, 0 = round-2a kernel (A/B)
+  static const int pv = std::getenv("DICB200_BS_PV") ? std::atoi(std::getenv("DICB200_BS_PV")) : 1;
   static const bool prof = std::getenv("DICB200_BS_PROF") != nullptr;
   if (p.planes == 1)
     g.fuse ? go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint8_t, true, PYM>) : go(bs_ws_kernel<S, RR, Q, DXC, NPW, NCW, uint8_t>);

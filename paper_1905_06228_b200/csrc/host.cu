@@ -977,6 +977,12 @@ dicb200_status dicb200_analyze_sequence_device(const dicb200_image* images, size
 
 dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_images, const dicb200_run_config* cfg,
                                         dicb200_field* fields, size_t n_fields) {
+  return dicb200_analyze_sequence_cb(images, n_images, cfg, fields, n_fields, nullptr, nullptr);
+}
+
+dicb200_status dicb200_analyze_sequence_cb(const dicb200_image* images, size_t n_images,
+                                           const dicb200_run_config* cfg, dicb200_field* fields, size_t n_fields,
+                                           dicb200_field_ready_fn field_ready, void* user) {
   if (!has_device()) return no_device();
   if (!images || !cfg || !fields) return invalid("null argument");
   if (n_images < 2) return invalid("insufficient images");
@@ -1021,6 +1027,7 @@ dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_im
         result[wk] = s;
         errs[wk] = g_last_error;
       }
+      if (field_ready) field_ready(user, (size_t)(&f - fields));
     };
     const size_t lo = ranges[2 * wk], hi = ranges[2 * wk + 1];
     std::vector<Lattice> lat(hi - lo);
@@ -1066,6 +1073,7 @@ dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_im
       }
       f.count = r.n;
       f.status = DICB200_OK;
+      if (field_ready) field_ready(user, (size_t)(&f - fields));
     };
     auto next_valid = [&](size_t i) {
       while (i < hi && pre[i - lo] != DICB200_OK) ++i;

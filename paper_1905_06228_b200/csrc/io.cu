@@ -12,6 +12,7 @@
 #include <sys/stat.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cctype>
 #include <cmath>
 #include <cstdio>
@@ -25,6 +26,8 @@
 #include "common.cuh"
 
 using namespace dicb200;
+
+extern "C" void dicb200_pack_span(const double* s, size_t n, uint16_t* d, int* frac, int* bad, int* mx);  // csrc/pack.c
 
 namespace {
 
@@ -204,20 +207,17 @@ dicb200_status dicb200_pack_gray(const double* src, int32_t width, int32_t heigh
     for (int y = y0; y < y1; ++y) {
       const double* s = src + (size_t)y * pitch;
       uint16_t* d = dst + (size_t)y * width;
+      if (scale == 1) {
+        dicb200_pack_span(s, (size_t)width, d, &frac, &bad, &mx);  // csrc/pack.c (AVX2 when present)
+        continue;
+      }
       for (int x = 0; x < width; ++x) {
         const double v = s[x];
         const bool b = !(v >= 0.0 && v <= lim);  // also catches NaN
         bad |= b;
-        if (scale == 1) {
-          const uint16_t q = (uint16_t)(b ? 0.0 : v);
-          frac |= (double)q != v;
-          d[x] = q;
-          mx = q > mx ? q : mx;
-        } else {
-          const uint16_t q = (uint16_t)(b ? 0 : std::lround(v * 256.0));  // 8.8 fixed point
-          d[x] = q;
-          mx = q > mx ? q : mx;
-        }
+        const uint16_t q = (uint16_t)(b ? 0 : std::lround(v * 256.0));  // 8.8 fixed point
+        d[x] = q;
+        mx = q > mx ? q : mx;
       }
     }
     r.mx = mx;
@@ -242,6 +242,60 @@ dicb200_status dicb200_pack_gray(const double* src, int32_t width, int32_t heigh
   if (bad)
     return io_error(scale == 1 ? "dicb200: gray levels must be integers in [0, 65535]"
                                : "dicb200: fractional gray levels must lie in [0, 255]");
+  return DICB200_OK;
+}
+
+// Every frame of a sequence in one call: row bands of all frames are dealt to
+// one set of threads (no per-frame thread start-up), per-frame flags out.
+dicb200_status dicb200_pack_gray_batch(const double* const* src, int32_t count, int32_t width, int32_t height,
+                                       int32_t src_pitch, uint16_t* const* dst, int32_t* fractional,
+                                       int32_t* max_level, int32_t threads) {
+  if (!src || !dst || count < 1 || width < 1 || height < 1) return io_error("null argument");
+  for (int k = 0; k < count; ++k)
+    if (!src[k] || !dst[k]) return io_error("null argument");
+  const int pitch = src_pitch > 0 ? src_pitch : width;
+  if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  const int band = std::max(1, std::min(height, (1 << 17) / std::max(1, width)));  // ~128 K pixels per task
+  const int bands = (height + band - 1) / band;
+  const long tasks = (long)count * bands;
+  threads = (int)std::max<long>(1, std::min<long>(threads, tasks / 2));
+  struct Flags {
+    std::atomic<int> frac{0}, bad{0}, mx{0};
+  };
+  std::vector<Flags> fl(count);
+  std::atomic<long> next{0};
+  auto work = [&]() {
+    for (long t = next.fetch_add(1); t < tasks; t = next.fetch_add(1)) {
+      const int k = (int)(t / bands), y0 = (int)(t % bands) * band, y1 = std::min(height, y0 + band);
+      int frac = 0, bad = 0, mx = 0;
+      if (pitch == width) {
+        dicb200_pack_span(src[k] + (size_t)y0 * width, (size_t)(y1 - y0) * width, dst[k] + (size_t)y0 * width, &frac,
+                          &bad, &mx);
+      } else {
+        for (int y = y0; y < y1; ++y)
+          dicb200_pack_span(src[k] + (size_t)y * pitch, (size_t)width, dst[k] + (size_t)y * width, &frac, &bad, &mx);
+      }
+      if (frac) fl[k].frac.store(1, std::memory_order_relaxed);
+      if (bad) fl[k].bad.store(1, std::memory_order_relaxed);
+      int cur = fl[k].mx.load(std::memory_order_relaxed);
+      while (mx > cur && !fl[k].mx.compare_exchange_weak(cur, mx, std::memory_order_relaxed)) {
+      }
+    }
+  };
+  if (threads == 1) {
+    work();
+  } else {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) pool.emplace_back(work);
+    for (auto& th : pool) th.join();
+  }
+  int any_bad = 0;
+  for (int k = 0; k < count; ++k) {
+    if (fractional) fractional[k] = fl[k].frac.load();
+    if (max_level) max_level[k] = fl[k].mx.load();
+    any_bad |= fl[k].bad.load();
+  }
+  if (any_bad) return io_error("dicb200: gray levels must be integers in [0, 65535]");
   return DICB200_OK;
 }
 

@@ -115,6 +115,51 @@ def test_grayimage_gray_level_mapping():
         dic.GrayImage(np.full((8, 8), np.nan))
 
 
+def test_pack_gray_single_and_batch():
+    """dicb200_pack_gray / _batch (the shim's GrayImage doubles -> u16 pass, AVX2
+    when the host has it): lossless integers, per-frame maximum, fractional and
+    out-of-range / NaN detection, odd widths (vector tail), row pitch."""
+    L = dic.lib()
+    L.dicb200_pack_gray.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                    C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int32]
+    L.dicb200_pack_gray_batch.argtypes = [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                          C.POINTER(C.c_void_p), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                          C.c_int32]
+    rng = np.random.default_rng(7)
+    w, h, n = 203, 157, 5
+    frames = [rng.integers(0, 65536 if k else 256, (h, w)).astype(np.float64) for k in range(n)]
+    frames[2][11, 17] = 65535.0
+    outs = [np.zeros((h, w), np.uint16) for _ in range(n)]
+    src = (C.c_void_p * n)(*[f.ctypes.data for f in frames])
+    dst = (C.c_void_p * n)(*[o.ctypes.data for o in outs])
+    frac = (C.c_int32 * n)()
+    mx = (C.c_int32 * n)()
+    for threads in (1, 4):
+        assert L.dicb200_pack_gray_batch(src, n, w, h, 0, dst, frac, mx, threads) == 0
+        for k in range(n):
+            assert np.array_equal(outs[k], frames[k].astype(np.uint16)) and frac[k] == 0
+            assert mx[k] == int(frames[k].max())
+    # single-frame entry, with a source pitch wider than the row
+    wide = np.zeros((h, w + 9))
+    wide[:, :w] = frames[1]
+    one = np.zeros((h, w), np.uint16)
+    f1, m1 = C.c_int32(0), C.c_int32(0)
+    assert L.dicb200_pack_gray(wide.ctypes.data, w, h, w + 9, 1, one.ctypes.data, C.byref(f1), C.byref(m1), 2) == 0
+    assert np.array_equal(one, outs[1]) and f1.value == 0 and m1.value == mx[1]
+    # a fractional level in the vector body and one in the scalar tail
+    for (y, x) in ((3, 8), (h - 1, w - 1)):
+        g = [f.copy() for f in frames]
+        g[3][y, x] += 0.25
+        src2 = (C.c_void_p * n)(*[f.ctypes.data for f in g])
+        assert L.dicb200_pack_gray_batch(src2, n, w, h, 0, dst, frac, mx, 3) == 0
+        assert [frac[k] for k in range(n)] == [0, 0, 0, 1, 0]
+    for badv in (-1.0, 65536.0, np.nan, np.inf):
+        g = [f.copy() for f in frames]
+        g[4][5, 5] = badv
+        src2 = (C.c_void_p * n)(*[f.ctypes.data for f in g])
+        assert L.dicb200_pack_gray_batch(src2, n, w, h, 0, dst, frac, mx, 2) != 0
+
+
 def test_synth_generator_is_deterministic_and_in_range():
     f = configs.crop(configs.get("c4"), 96, 96).frames[1]
     a, b = f.render(threads=1), f.render(threads=3)
