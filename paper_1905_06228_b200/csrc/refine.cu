@@ -729,10 +729,9 @@ __device__ __forceinline__ void fixed_pass(const FixedCtx& c, float* acc) {
     const uint32_t gcol = c.g2 + (uint32_t)col * 8u, rcol = c.r + (uint32_t)col * 4u;
     const uint32_t ncol = c.tn + (uint32_t)col * 8u;
     f2x bsum = pk2(0.f, 0.f);
-    float dyf = (float)-M;
+    f2x dy2 = pk2((float)-M, (float)-M);  // (dy, dy), stepped as a pair: one packed add per row
 #pragma unroll 4
-    for (int t = 0; t < F::SIDE; ++t, dyf += 1.0f) {
-      const f2x dy2 = pk2(dyf, dyf);
+    for (int t = 0; t < F::SIDE; ++t, dy2 = add2(dy2, pk2(1.0f, 1.0f))) {
       float g;
       if (KIND == 0)
         g = lds1(ncol + (uint32_t)(t * TP * 8));
@@ -757,15 +756,38 @@ __device__ __forceinline__ void fixed_pass(const FixedCtx& c, float* acc) {
   // ---- part B: the remaining BW columns, RPT rows per trip ----
   if (F::BW) {
     const int lc = lane % F::BW, lr = lane / F::BW;
+    const bool lane_ok = lane < F::RPT * F::BW;
     const int col = 32 * F::NA + lc;
     const float dxf = (float)(col - M);
-    const bool lane_ok = lane < F::RPT * F::BW;
     const f2x base = fma2(c.A, pk2(dxf, dxf), c.o);
     const uint32_t gcol = c.g2 + (uint32_t)(col + lr * RP) * 8u, rcol = c.r + (uint32_t)(col + lr * RP) * 4u;
     const uint32_t ncol = c.tn + (uint32_t)(col + lr * TP) * 8u;
     f2x bsum = pk2(0.f, 0.f);
+    // trips 0 .. NB-2: every lane's row is inside the subset (also the idle
+    // lanes', whose weight is 0), so weight, row offsets and dy need no selects
+    {
+      const float w = lane_ok ? 1.0f : 0.0f, nfw = -c.fbar * w;
+      f2x dy2 = pk2((float)(lr - M), (float)(lr - M));
 #pragma unroll 2
-    for (int t = 0; t < F::NB; ++t) {
+      for (int t = 0; t < F::NB - 1; ++t, dy2 = add2(dy2, pk2((float)F::RPT, (float)F::RPT))) {
+        float g;
+        if (KIND == 0)
+          g = lds1(ncol + (uint32_t)(t * F::RPT * TP * 8));
+        else
+          g = fixed_tap<TP>(c, fma2(c.B, dy2, base));
+        const float gp = fmaf(g, w, nfw);
+        s0 += gp;
+        s1 = fmaf(gp, gp, s1);
+        if (KIND == 2) {
+          s2 = fmaf(lds1(rcol + (uint32_t)(t * F::RPT * RP * 4)) - c.fbar, gp, s2);
+        } else {
+          const f2x txy = mul2(lds2x(gcol + (uint32_t)(t * F::RPT * RP * 8)), pk2(gp, gp));
+          bsum = add2(bsum, txy);
+          a58 = fma2(txy, dy2, a58);
+        }
+      }
+    }
+    for (int t = F::NB - 1; t < F::NB; ++t) {  // last trip: rows past the subset carry weight 0
       const int row = t * F::RPT + lr;
       const bool ok = lane_ok && row < F::SIDE;
       const int rr = ok ? row : 0;  // weight 0: any valid pixel, contribution dropped

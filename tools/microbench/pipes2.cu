@@ -27,6 +27,10 @@ __global__ void kern(uint32_t* out, int iters, uint32_t seed) {
         if (OP == 5) { a[i] = a[i] * b + c; f[i] = fmaf(f[i], fc, fb); d[i] = fma(d[i], dc, db); }
         if (OP == 6) { f[i] = fmaf(f[i], fc, fb); }
         if (OP == 7) { q[i] = fma2(q[i], qb, qc); }
+        if (OP == 8) { q[i] = fma2(q[i], qb, qc); f[i] = fmaf(f[i], fc, fb); }
+        if (OP == 9) { q[i] = fma2(q[i], qb, qc); f[i] = fmaf(f[i], fc, fb); f[i] = fmaf(f[i], fb, fc); }
+        if (OP == 10) { q[i] = fma2(q[i], qb, qc); a[i] = (a[i] ^ b) + c; }
+        if (OP == 11) { f[i] = fmaf(f[i], fc, fb); a[i] = (a[i] ^ b) + c; }
       }
     }
   }
@@ -38,9 +42,9 @@ __global__ void kern(uint32_t* out, int iters, uint32_t seed) {
 int main() {
   cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
   uint32_t* out; cudaMalloc(&out, 4);
-  const char* names[] = {"imad", "dfma", "imad+dfma(pairs)", "imad+ffma(pairs)", "i2f64+dadd", "imad+ffma+dfma(triples)", "ffma", "ffma2(instr)"};
+  const char* names[] = {"imad", "dfma", "imad+dfma(pairs)", "imad+ffma(pairs)", "i2f64+dadd", "imad+ffma+dfma(triples)", "ffma", "ffma2(instr)", "ffma2+ffma(pairs)", "ffma2+2ffma(triples)", "ffma2+alu(pairs)", "ffma+alu(pairs)"};
   printf("{");
-  for (int op = 0; op < 8; ++op) {
+  for (int op = 0; op < 12; ++op) {
     int grid = p.multiProcessorCount * 8, block = 256, iters = 2048;
     auto launch = [&]() {
       switch (op) {
@@ -52,6 +56,10 @@ int main() {
         case 5: kern<5><<<grid, block>>>(out, iters, 1); break;
         case 6: kern<6><<<grid, block>>>(out, iters, 1); break;
         case 7: kern<7><<<grid, block>>>(out, iters, 1); break;
+        case 8: kern<8><<<grid, block>>>(out, iters, 1); break;
+        case 9: kern<9><<<grid, block>>>(out, iters, 1); break;
+        case 10: kern<10><<<grid, block>>>(out, iters, 1); break;
+        case 11: kern<11><<<grid, block>>>(out, iters, 1); break;
       }
     };
     launch(); cudaDeviceSynchronize();
