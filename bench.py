@@ -74,6 +74,8 @@ def parse():
     ap.add_argument("--pairs", type=int, default=64, help="C5 sequence length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="default C5 run: skip the short C1-C4 runs reported under other_configs")
     ap.add_argument("--dump-records", default=None,
                     help="write this rank's records of the last timed step to DIR/rank<R>.npy (tests)")
     return ap.parse_args()
@@ -860,8 +862,39 @@ def main():
 
             dist.barrier()
             dist.destroy_process_group()
+    if (line is not None and args.impl == "ours" and world == 1 and args.config == "c5" and
+            not args.no_other_configs and not args.no_cpu_baseline):
+        line["other_configs"] = other_configs()
     if line is not None:
         print(json.dumps(line), flush=True)
+
+
+def other_configs() -> dict:
+    """BASELINE's other configurations (parity-test cases, not the bench line),
+    each measured by a short run of this script in its own process after the
+    timed C5 run: value, e2e, the dominant kernel's roofline, the reference CPU
+    sample and the parity block of that run — so every config's number and its
+    parity against the reference build are observed in the same bench call."""
+    out = {}
+    for c in ("c1", "c2", "c3", "c4"):
+        try:
+            r = subprocess.run([sys.executable, os.path.abspath(__file__), "--config", c, "--steps", "10", "--warmup",
+                                "3", "--no-other-configs"], capture_output=True, text=True, timeout=600,
+                               env={k: v for k, v in os.environ.items()
+                                    if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")})
+            d = json.loads(r.stdout.strip().splitlines()[-1])
+            rf = d.get("roofline") or {}
+            out[c] = {
+                "workload": d["config"]["workload"], "value": d["value"], "unit": d["unit"],
+                "ms_per_step": d["ms_per_step"], "steps": d["steps"], "warmup": d["warmup"],
+                "e2e": d["e2e"]["value"] if d.get("e2e") else None,
+                "roofline": {k: rf.get(k) for k in ("kernel", "bound", "pipe", "frac", "frac_isolated", "unit")},
+                "cpu_baseline": d.get("cpu_baseline"), "parity": d.get("parity"), "clocks": d.get("clocks"),
+                "gpu_launches": d.get("gpu_launches"),
+            }
+        except Exception as e:  # a secondary config never fails the bench line
+            out[c] = {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+    return out
 
 
 if __name__ == "__main__":

@@ -21,6 +21,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <future>
+#include <memory>
 #include <cstdint>
 #include <map>
 #include <mutex>
@@ -256,61 +258,61 @@ inline DisplacementField analyze_pair(const GrayImage& reference, const GrayImag
 }
 
 // pipeline.cpp:182-214 semantics: pairs from sequence_pairs(cfg.reference_policy),
-// one dicb200_analyze_sequence call (pipelined uploads / compute / read-back;
+// fields in pair order, per-pair dic::Error -> field.error. The sequence goes
+// to dicb200_analyze_sequence_cb (pipelined uploads / compute / read-back;
 // cfg.mode == image_parallel shards contiguous pair chunks over
-// min(worker_count, devices) devices, as the reference shards them over
-// worker threads). Per-pair dic::Error -> field.error, fields in pair order.
+// min(worker_count, devices) devices, as the reference shards them over worker
+// threads) in chunks of pairs: while the device works on one chunk, the host
+// packs the next chunk's GrayImage doubles (all cores), so for long sequences
+// of large frames only the first chunk's packing is exposed. Each chunk call
+// carries its first pair index, so RNG keys and results are those of one call.
+// DICB200_SHIM_CHUNK=<pairs> overrides the chunk length (0 = one call).
 inline std::vector<DisplacementField> analyze_sequence(const std::vector<GrayImage>& images,
                                                        const RunConfig& cfg) {
   const auto pairs = sequence_pairs(cfg.reference_policy, static_cast<int>(images.size()));
   const dicb200_run_config c = detail::to_c(cfg);
-  // frames of one size pack together; a frame of another size fails its pairs
-  // with the reference's message (analyze_pair, pipeline.cpp:150-151)
-  std::vector<const GrayImage*> ptrs;
-  for (const GrayImage& g : images) ptrs.push_back(&g);
   const bool trace = std::getenv("DICB200_SHIM_TRACE") != nullptr;  // phase times on stderr
-  const auto t0 = std::chrono::steady_clock::now();
-  const detail::Frames fr(ptrs);
-  const auto t1 = std::chrono::steady_clock::now();
-  // records are read back straight into pinned blocks (no staging copy, no
-  // zero fill) and each field is converted as soon as it is final, on the
-  // library's worker thread, while the device runs the following pairs
+  const size_t np = pairs.size();
+  // chunking pays when packing a chunk takes long enough to be worth hiding
+  size_t px = 0;
+  for (const GrayImage& g : images) px = std::max(px, static_cast<size_t>(g.width()) * g.height());
+  size_t chunk = (np >= 16 && px >= (size_t(1) << 20)) ? std::max<size_t>(8, np / 4) : np;
+  if (const char* e = std::getenv("DICB200_SHIM_CHUNK")) chunk = std::atoi(e) > 0 ? std::atoi(e) : np;
+  chunk = std::max<size_t>(1, std::min(chunk, std::max<size_t>(np, 1)));
+
   struct Ctx {
     const std::vector<GrayImage>* images;
     const std::vector<std::pair<int, int>>* pairs;
+    size_t first;  // global index of the chunk's first pair
     std::vector<dicb200_field> cf;
-    std::vector<DisplacementField> fields;
-  } ctx;
-  ctx.images = &images;
-  ctx.pairs = &pairs;
-  ctx.cf.resize(pairs.size());
-  ctx.fields.resize(pairs.size());
+    std::vector<DisplacementField>* fields;
+  };
+  std::vector<DisplacementField> fields(np);
   size_t cap = 0;
-  std::vector<size_t> counts(pairs.size(), 0);
-  for (size_t i = 0; i < pairs.size(); ++i) {
+  std::vector<size_t> counts(np, 0);
+  for (size_t i = 0; i < np; ++i) {
     const GrayImage& a = images[pairs[i].first];
     if (dicb200_grid_size(a.width(), a.height(), &c, &counts[i]) != DICB200_OK) counts[i] = 0;
     cap = std::max(cap, counts[i]);
   }
+  // records are read back straight into pinned blocks (no staging copy, no
+  // zero fill) and each field is converted as soon as it is final, on the
+  // library's worker thread, while the device runs the following pairs
   detail::PinnedPool& pool = detail::PinnedPool::get();
-  const std::vector<void*> blocks = pool.take(pairs.size(), std::max<size_t>(cap, 1) * sizeof(dicb200_poi_record));
+  const std::vector<void*> blocks = pool.take(chunk, std::max<size_t>(cap, 1) * sizeof(dicb200_poi_record));
   struct Release {
     detail::PinnedPool& pool;
     const std::vector<void*>& blocks;
     ~Release() { pool.release(blocks); }
   } release{pool, blocks};
-  for (size_t i = 0; i < pairs.size(); ++i) {
-    ctx.cf[i] = dicb200_field{};
-    ctx.cf[i].records = static_cast<dicb200_poi_record*>(blocks[i]);
-    ctx.cf[i].capacity = counts[i];
-  }
   auto ready = [](void* user, size_t i) {
     Ctx& x = *static_cast<Ctx*>(user);
-    DisplacementField& f = x.fields[i];
+    const size_t gi = x.first + i;
+    DisplacementField& f = (*x.fields)[gi];
     const dicb200_field& cf = x.cf[i];
-    f.pair_index = static_cast<int>(i);
-    f.ref_id = (*x.images)[(*x.pairs)[i].first].id();
-    f.tgt_id = (*x.images)[(*x.pairs)[i].second].id();
+    f.pair_index = static_cast<int>(gi);
+    f.ref_id = (*x.images)[(*x.pairs)[gi].first].id();
+    f.tgt_id = (*x.images)[(*x.pairs)[gi].second].id();
     if (cf.status != DICB200_OK) {
       f.error = cf.error;
       return;
@@ -318,16 +320,60 @@ inline std::vector<DisplacementField> analyze_sequence(const std::vector<GrayIma
     f.records.reserve(cf.count);
     for (size_t k = 0; k < cf.count; ++k) f.records.push_back(detail::to_record(cf.records[k]));
   };
-  const dicb200_status st =
-      dicb200_analyze_sequence_cb(fr.data(), images.size(), &c, ctx.cf.data(), ctx.cf.size(), ready, &ctx);
-  if (trace) {
-    const auto t2 = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[dicb200 shim] pack %.1f ms, device pipeline + records %.1f ms\n",
-                 std::chrono::duration<double, std::milli>(t1 - t0).count(),
-                 std::chrono::duration<double, std::milli>(t2 - t1).count());
+  // frames of pairs [a, b): the library derives the same pairs from them
+  // (fixed_first: frame 0 then the targets; update_every_pair: frames a .. b)
+  auto frames_of = [&](size_t a, size_t b) {
+    std::vector<const GrayImage*> ptrs;
+    ptrs.push_back(&images[pairs[a].first]);
+    for (size_t i = a; i < b; ++i) ptrs.push_back(&images[pairs[i].second]);
+    return std::unique_ptr<detail::Frames>(new detail::Frames(ptrs));
+  };
+  double pack_ms = 0.0, wait_ms = 0.0, run_ms = 0.0;
+  auto ms_since = [](std::chrono::steady_clock::time_point t) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+  };
+  std::future<std::unique_ptr<detail::Frames>> next;
+  std::unique_ptr<detail::Frames> cur;
+  if (np > 0) {
+    const auto t0 = std::chrono::steady_clock::now();
+    cur = frames_of(0, std::min(np, chunk));
+    pack_ms = ms_since(t0);
   }
-  if (st != DICB200_OK) detail::raise(st);
-  return std::move(ctx.fields);
+  size_t nchunk = 0;
+  for (size_t a = 0; a < np; a += chunk, ++nchunk) {
+    const size_t b = std::min(np, a + chunk);
+    if (b < np) next = std::async(std::launch::async, frames_of, b, std::min(np, b + chunk));
+    Ctx ctx;
+    ctx.images = &images;
+    ctx.pairs = &pairs;
+    ctx.first = a;
+    ctx.fields = &fields;
+    ctx.cf.resize(b - a);
+    for (size_t i = a; i < b; ++i) {
+      ctx.cf[i - a] = dicb200_field{};
+      ctx.cf[i - a].records = static_cast<dicb200_poi_record*>(blocks[i - a]);  // converted before the call returns
+      ctx.cf[i - a].capacity = counts[i];
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    const dicb200_status st = dicb200_analyze_sequence_cb(cur->data(), b - a + 1, &c, ctx.cf.data(), ctx.cf.size(),
+                                                          static_cast<uint64_t>(a), ready, &ctx);
+    run_ms += ms_since(t1);
+    if (st != DICB200_OK) {
+      if (next.valid()) next.wait();
+      detail::raise(st);
+    }
+    if (b < np) {
+      const auto t2 = std::chrono::steady_clock::now();
+      cur = next.get();
+      wait_ms += ms_since(t2);
+    }
+  }
+  if (trace)
+    std::fprintf(stderr,
+                 "[dicb200 shim] %zu pairs in %zu call(s): first chunk packed in %.1f ms, device pipeline + records "
+                 "%.1f ms, waiting for the packer %.1f ms\n",
+                 np, nchunk, pack_ms, run_ms, wait_ms);
+  return fields;
 }
 
 }  // namespace b200

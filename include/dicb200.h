@@ -201,17 +201,23 @@ dicb200_status dicb200_analyze_pair(const dicb200_image* reference, const dicb20
 dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_images,
                                         const dicb200_run_config* cfg, dicb200_field* fields,
                                         size_t n_fields);
-/* The same, calling field_ready(user, i) on the host as soon as fields[i] is
- * final (records read back, or its pair-level error stored), while the device
- * runs the following pairs: the caller converts / consumes field i there
- * instead of after the whole sequence (the C++ shim builds the reference's
- * DisplacementField records in it). Called once per field, from the worker
- * thread of the field's device (concurrently for mode == IMAGE over several
- * devices); it must not call back into the library. NULL = none. */
+/* The same for a contiguous part of a longer sequence, with a completion hook:
+ * pair i of this call uses pair index first_pair_index + i (the RNG key of
+ * derive_stream_seed, rng.hpp:20-55, and fields[i].pair_index), so a caller can
+ * hand a long sequence over in chunks — packing / loading the next chunk's
+ * frames while this one runs — and get the records of one whole call.
+ * field_ready(user, i) is called on the host as soon as fields[i] is final
+ * (records read back, or its pair-level error stored), while the device runs
+ * the following pairs: the caller converts / consumes field i there instead of
+ * after the whole call (the C++ shim builds the reference's DisplacementField
+ * records in it). Called once per field, from the worker thread of the field's
+ * device (concurrently for mode == IMAGE over several devices); it must not
+ * call back into the library. NULL = none. */
 typedef void (*dicb200_field_ready_fn)(void* user, size_t field_index);
 dicb200_status dicb200_analyze_sequence_cb(const dicb200_image* images, size_t n_images,
                                            const dicb200_run_config* cfg, dicb200_field* fields,
-                                           size_t n_fields, dicb200_field_ready_fn field_ready, void* user);
+                                           size_t n_fields, uint64_t first_pair_index,
+                                           dicb200_field_ready_fn field_ready, void* user);
 
 /* Device-resident entry point: images hold device pointers, records are
  * written to device memory `out_dev`, everything is enqueued on `stream`

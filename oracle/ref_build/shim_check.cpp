@@ -115,19 +115,22 @@ int main() {
       seq.emplace_back(W, H, std::vector<double>(px.begin(), px.end()), k);
     }
     seq[3] = dic::GrayImage(W - 8, H, std::vector<double>((W - 8) * H, 7.0), 3);
+    // mode 2: serial again with the swarm search (mPSO + NR), whose RNG streams
+    // are keyed by the pair index: with DICB200_SHIM_CHUNK set, the shim hands
+    // the sequence over in several calls and the keys must still be the global ones
     for (int policy = 0; policy < 2; ++policy)
-      for (int mode = 0; mode < 2; ++mode) {
+      for (int mode = 0; mode < 3; ++mode) {
         dic::RunConfig cfg;
-        cfg.integer_method = dic::IntegerMethod::bfs;
-        cfg.subpixel_method = dic::SubpixelMethod::icgn;
+        cfg.integer_method = mode == 2 ? dic::IntegerMethod::mpso : dic::IntegerMethod::bfs;
+        cfg.subpixel_method = mode == 2 ? dic::SubpixelMethod::nr : dic::SubpixelMethod::icgn;
         cfg.search.bfs_domain = dic::BfsDomain::window;
         cfg.search.search_radius = 8;
         cfg.grid.half_width = 10;
         cfg.grid.spacing = 12;
         cfg.refine.tol = 1e-4;
         cfg.reference_policy = policy ? dic::ReferencePolicy::update_every_pair : dic::ReferencePolicy::fixed_first;
-        cfg.mode = mode ? dic::ExecMode::image_parallel : dic::ExecMode::serial;
-        cfg.worker_count = mode ? 2 : 1;
+        cfg.mode = mode == 1 ? dic::ExecMode::image_parallel : dic::ExecMode::serial;
+        cfg.worker_count = mode == 1 ? 2 : 1;
         const auto ref = dic::analyze_sequence(seq, cfg);
         const auto got = dic::b200::analyze_sequence(seq, cfg);
         int mism = 0, errs = 0;

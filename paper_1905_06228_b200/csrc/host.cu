@@ -977,12 +977,13 @@ dicb200_status dicb200_analyze_sequence_device(const dicb200_image* images, size
 
 dicb200_status dicb200_analyze_sequence(const dicb200_image* images, size_t n_images, const dicb200_run_config* cfg,
                                         dicb200_field* fields, size_t n_fields) {
-  return dicb200_analyze_sequence_cb(images, n_images, cfg, fields, n_fields, nullptr, nullptr);
+  return dicb200_analyze_sequence_cb(images, n_images, cfg, fields, n_fields, 0, nullptr, nullptr);
 }
 
 dicb200_status dicb200_analyze_sequence_cb(const dicb200_image* images, size_t n_images,
                                            const dicb200_run_config* cfg, dicb200_field* fields, size_t n_fields,
-                                           dicb200_field_ready_fn field_ready, void* user) {
+                                           uint64_t first_pair_index, dicb200_field_ready_fn field_ready,
+                                           void* user) {
   if (!has_device()) return no_device();
   if (!images || !cfg || !fields) return invalid("null argument");
   if (n_images < 2) return invalid("insufficient images");
@@ -1035,7 +1036,7 @@ dicb200_status dicb200_analyze_sequence_cb(const dicb200_image* images, size_t n
     std::vector<dicb200_status> pre(hi - lo);
     for (size_t i = lo; i < hi; ++i) {
       dicb200_field& f = fields[i];
-      f.pair_index = (int32_t)i;
+      f.pair_index = (int32_t)(first_pair_index + i);
       f.ref_id = images[pairs[2 * i]].id;
       f.tgt_id = images[pairs[2 * i + 1]].id;
       f.count = 0;
@@ -1100,7 +1101,8 @@ dicb200_status dicb200_analyze_sequence_cb(const dicb200_image* images, size_t n
       }
       const bool staged_ok = s == DICB200_OK;
       if (s == DICB200_OK)
-        s = enqueue_pair(&c->frames[sa].im, &c->frames[sb].im, cfg, i, lat[i - lo], 0, lat[i - lo].ny,
+        s = enqueue_pair(&c->frames[sa].im, &c->frames[sb].im, cfg, first_pair_index + i, lat[i - lo], 0,
+                         lat[i - lo].ny,
                          (dicb200_poi_record*)r.dev.p, cst, k ? &c->tcache2 : &c->tcache, (long)pairs[2 * i],
                          cfg->reference_policy == DICB200_POLICY_FIXED_FIRST ? (k ? &c->icache2 : &c->icache)
                                                                              : nullptr);
