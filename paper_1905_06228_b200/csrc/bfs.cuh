@@ -114,7 +114,13 @@ struct TcRefCache {
   int W = 0, H = 0, M = 0, x0 = 0, y0 = 0, step = 0, nx = 0, rb = 0, re = 0;
   int planes = 0;
   bool use_bs = false;  // built for the block-sum kernel (no strip images)
-  void reset() { key = -1; }
+  // declared-width guard (host.cu): device flags {reference, target} and the
+  // reference frame flags[0] was computed for (checked once while it repeats)
+  int* guard = nullptr;
+  long guard_key = -1;
+  const void* guard_data = nullptr;
+  int guard_bits = -1;
+  void reset() { key = -1; guard_key = -1; }
 };
 
 // Plans the tensor-core search for POI rows [rb, re); false = not applicable

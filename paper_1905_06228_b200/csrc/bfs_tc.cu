@@ -1176,7 +1176,7 @@ cudaError_t grow(void*& ptr, size_t& cap, size_t bytes, cudaStream_t st) {
 }  // namespace
 
 void tc_cache_free(TcRefCache& c, cudaStream_t st, bool async) {
-  for (void* q : {c.tail, c.strips, c.psf, c.pvf, c.s1, c.s2, c.sfg, c.tiles})
+  for (void* q : {c.tail, c.strips, c.psf, c.pvf, c.s1, c.s2, c.sfg, c.tiles, (void*)c.guard})
     if (q) async ? cudaFreeAsync(q, st) : cudaFree(q);
   c = TcRefCache{};
 }

@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(256) bits_check_kernel(const Pix* data, int pi
 }
 
 __global__ void __launch_bounds__(256) bits_poison_kernel(const int* flag, dicb200_poi_record* rec, size_t n) {
-  if (!*flag) return;
+  if (!(flag[0] | flag[1])) return;  // {reference, target}
   for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) {
     dicb200_poi_record& r = rec[k];
     r.u = r.v = 0.0;
@@ -232,28 +232,49 @@ __global__ void __launch_bounds__(256) bits_poison_kernel(const int* flag, dicb2
   }
 }
 
+// `cache` (the stream's reference-side cache, optional): the flags live there
+// and the reference frame is checked once while it repeats along a sequence
+// (fixed_first), not once per pair.
 static dicb200_status enqueue_bits_guard(const dicb200_image* ref, const dicb200_image* tgt, dicb200_poi_record* rec,
-                                         size_t n, cudaStream_t st) {
+                                         size_t n, cudaStream_t st, TcRefCache* cache, long ref_key) {
   if (!declares_bits(ref) && !declares_bits(tgt)) return DICB200_OK;
   int* flag = nullptr;
-  DICB200_CUDA_TRY(cudaMallocAsync((void**)&flag, sizeof(int), st));
-  DICB200_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  bool ref_known = false;
+  if (cache) {
+    if (!cache->guard) {
+      DICB200_CUDA_TRY(cudaMallocAsync((void**)&cache->guard, 2 * sizeof(int), st));
+      cache->guard_key = -1;
+    }
+    flag = cache->guard;
+    ref_known = ref_key >= 0 && cache->guard_key == ref_key && cache->guard_data == ref->data &&
+                cache->guard_bits == (declares_bits(ref) ? (int)ref->bits : 0);
+  } else {
+    DICB200_CUDA_TRY(cudaMallocAsync((void**)&flag, 2 * sizeof(int), st));
+  }
+  DICB200_CUDA_TRY(cudaMemsetAsync(flag + (ref_known ? 1 : 0), 0, (ref_known ? 1 : 2) * sizeof(int), st));
+  int slot = 0;
   for (const dicb200_image* im : {ref, tgt}) {
-    if (!declares_bits(im)) continue;
+    const int s = slot++;
+    if (!declares_bits(im) || (s == 0 && ref_known)) continue;
     const uint32_t limit = (1u << im->bits) - 1u;
     const int pitch = im->pitch > 0 ? im->pitch : im->width;
     if (im->dtype == DICB200_U8)
       bits_check_kernel<uint8_t><<<8 * 148, 256, 0, st>>>(static_cast<const uint8_t*>(im->data), pitch, im->width,
-                                                           im->height, limit, flag);
+                                                           im->height, limit, flag + s);
     else
       bits_check_kernel<uint16_t><<<8 * 148, 256, 0, st>>>(static_cast<const uint16_t*>(im->data), pitch, im->width,
-                                                            im->height, limit, flag);
+                                                            im->height, limit, flag + s);
     count_launch();
+  }
+  if (cache) {
+    cache->guard_key = ref_key;
+    cache->guard_data = ref->data;
+    cache->guard_bits = declares_bits(ref) ? (int)ref->bits : 0;
   }
   bits_poison_kernel<<<148, 256, 0, st>>>(flag, rec, n);
   count_launch();
   DICB200_CUDA_TRY(cudaGetLastError());
-  DICB200_CUDA_TRY(cudaFreeAsync(flag, st));
+  if (!cache) DICB200_CUDA_TRY(cudaFreeAsync(flag, st));
   return DICB200_OK;
 }
 
@@ -448,7 +469,7 @@ refine:
     DICB200_CUDA_TRY(refine_launch(r, ref->dtype, st, icache, ref_key));
     host_trace("refine enqueued");
   }
-  return enqueue_bits_guard(ref, tgt, out_dev, nrec, st);
+  return enqueue_bits_guard(ref, tgt, out_dev, nrec, st, tcache, ref_key);
 }
 
 static size_t elem_size(int dtype) {

@@ -106,3 +106,48 @@ def test_understated_bits_fail_loudly(gpu):
     assert st == 0
     for f in ("integer_dx", "integer_dy", "evaluations", "status"):
         assert np.array_equal(recs[f], good[f]), f
+
+
+def test_bits_guard_along_a_sequence(gpu):
+    """The declared-width guard checks a repeated reference frame once per
+    stream (cached flag) and every target: with a fixed-first sequence on the
+    two compute streams, an understated target fails only its own pair, an
+    understated reference fails every pair, and correct declarations pass."""
+    import ctypes as C
+
+    ref = _speckle(420, 400, 23, _abi.U16, 4095)
+    frames = [ref] + [np.roll(ref, k, axis=1) for k in (1, 2, 3, 4, 5)]
+    cfg = _cfg(20, 12, 10)
+    cfg.reference_policy = dic.ReferencePolicy.fixed_first
+    gi = [dic.GrayImage(f, i) for i, f in enumerate(frames)]
+    good = dic.analyze_sequence(gi, cfg)
+    assert all(not f.error and np.all(f.records["status"] == 0) for f in good)
+    n = len(good[0].records)
+
+    def run(bits):
+        imgs = (_abi.Image * len(gi))()
+        for i, g in enumerate(gi):
+            imgs[i] = g.as_c()
+            imgs[i].bits = bits[i]
+        c = cfg.to_c()
+        fields = (_abi.FieldC * (len(gi) - 1))()
+        bufs = []
+        for i in range(len(gi) - 1):
+            b = np.zeros(n, dtype=_abi.record_dtype())
+            bufs.append(b)
+            fields[i].records = C.cast(b.ctypes.data, C.POINTER(_abi.PoiRecordC))
+            fields[i].capacity = n
+        st = dic.lib().dicb200_analyze_sequence(imgs, len(gi), C.byref(c), fields, len(gi) - 1)
+        return st, [fields[i].status for i in range(len(gi) - 1)], bufs
+
+    st, status, bufs = run([12] * 6)
+    assert st == 0 and status == [0] * 5
+    for i in range(5):
+        for f in ("integer_dx", "integer_dy", "evaluations", "status"):
+            assert np.array_equal(bufs[i][f], good[i].records[f]), (i, f)
+    st, status, bufs = run([12, 12, 12, 8, 12, 12])  # frame 3 (pair 2) understated
+    assert st == 0 and status == [0, 0, 1, 0, 0], status
+    for i in (0, 1, 3, 4):
+        assert np.array_equal(bufs[i]["integer_dx"], good[i].records["integer_dx"])
+    st, status, _ = run([8, 12, 12, 12, 12, 12])  # the reference understated: every pair fails
+    assert st == 0 and status == [1] * 5, status

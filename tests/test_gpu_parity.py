@@ -298,3 +298,42 @@ def test_sequence_mixed_bit_widths_reuse_reference_cache(gpu, port):
         for k in exp.dtype.names:
             assert np.array_equal(f.records[k], exp[k], equal_nan=True), (tb, k)
         assert_parity(f.records, port.analyze_pair(frames[0], frames[tb], w.cfg, pair_index=f.pair_index))
+
+
+def test_sequence_cb_chunks_equal_one_call(gpu):
+    """dicb200_analyze_sequence_cb: a sequence handed over in two calls (first
+    pair index 0 and 2) returns the fields of one call — pair indices, mPSO RNG
+    keys (evaluations), every record — and calls field_ready once per field."""
+    import ctypes as C
+
+    w = configs.crop(configs.get("c3"), 192, 176)
+    f0 = w.frames[0].render()
+    frames = [f0] + [np.roll(f0, (k % 3 - 1, k), axis=(0, 1)) for k in (1, 2, 3, 4)]
+    imgs = [dic.GrayImage(f, i) for i, f in enumerate(frames)]
+    cfg = copy.deepcopy(w.cfg)
+    cfg.reference_policy = dic.ReferencePolicy.fixed_first
+    one = dic.analyze_sequence(imgs, cfg)
+    n = len(one[0].records)
+    L = dic.lib()
+    CB = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t)
+    L.dicb200_analyze_sequence_cb.argtypes = [C.POINTER(_abi.Image), C.c_size_t, C.POINTER(_abi.RunConfigC),
+                                              C.POINTER(_abi.FieldC), C.c_size_t, C.c_uint64, CB, C.c_void_p]
+    c = cfg.to_c()
+    got, seen = {}, []
+    for first, idx in ((0, [0, 1, 2]), (2, [0, 3, 4])):
+        ims = (_abi.Image * 3)(*[imgs[i].as_c() for i in idx])
+        fields = (_abi.FieldC * 2)()
+        bufs = [np.zeros(n, dtype=_abi.record_dtype()) for _ in range(2)]
+        for i in range(2):
+            fields[i].records = C.cast(bufs[i].ctypes.data, C.POINTER(_abi.PoiRecordC))
+            fields[i].capacity = n
+        cb = CB(lambda user, i, first=first: seen.append(first + i))
+        assert L.dicb200_analyze_sequence_cb(ims, 3, C.byref(c), fields, 2, first, cb, None) == 0
+        for i in range(2):
+            assert fields[i].status == 0 and fields[i].pair_index == first + i and fields[i].count == n
+            got[first + i] = bufs[i]
+    assert sorted(seen) == [0, 1, 2, 3]
+    for k in range(4):
+        for f in _abi.record_dtype().names:
+            a, b = got[k][f], one[k].records[f]
+            assert np.array_equal(a, b, equal_nan=True) if a.dtype.kind == "f" else np.array_equal(a, b), (k, f)
