@@ -698,9 +698,15 @@ __device__ __forceinline__ float fixed_tap(const FixedCtx& c, f2x xk) {
   up2(fr, fx, fy);
   // c.t2 carries -(0x4B000000 (TP + 1)) * 8 (mod 2^32)
   uint32_t a;
-  if ((TP & (TP - 1)) == 0) {  // shifts (ALU pipe)
+  if ((TP & (TP - 1)) == 0) {
+    // shifts and a three-input add, kept on the ALU pipe (funnel shifts: ptxas
+    // turns shl + add into IMAD, and the fixed passes are bound by the FMA pipe,
+    // where packed FP32x2 instructions take two issue cycles each)
     constexpr int LG = TP == 128 ? 10 : TP == 64 ? 9 : TP == 32 ? 8 : 0;
-    a = (fbits(vy) << LG) + (fbits(vx) << 3) + c.t2;
+    uint32_t sy, sx;
+    asm("shf.l.clamp.b32 %0, 0, %1, %2;" : "=r"(sy) : "r"(fbits(vy)), "n"(LG));  // high word of {v : 0} << LG
+    asm("shf.l.clamp.b32 %0, 0, %1, 3;" : "=r"(sx) : "r"(fbits(vx)));
+    a = sy + sx + c.t2;
   } else {
     a = fbits(vy) * (uint32_t)(TP * 8) + (fbits(vx) * 8u + c.t2);
   }
