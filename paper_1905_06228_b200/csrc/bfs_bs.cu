@@ -1227,7 +1227,7 @@ constexpr BsVariant kVariants[] = {
     {8, 7, 3, 41, 256, 1, 0, 0, 16, 8},     // c3: L 31, s 8, R 20
     // warp-specialised: producer blocks fill whole warps on every SM sub-partition
     {10, 1, 4, 13, 512, 1, 8, 8, 12, 12},   // c5: 2 dx chunks, 12 x 12 POI tiles = 16 x 16 blocks
-    {5, 1, 8, 11, 512, 1, 12, 4, 16, 8},    // c4: 16 x 8 POI tiles = 24 x 16 blocks
+    {5, 1, 8, 11, 512, 1, 12, 4, 11, 8},    // c4: 11 x 8 POI tiles = 19 x 16 blocks; 121 (POI column, dx) consumer threads: fused argmax
 };
 // Measured and dropped (C5, B200): two CTAs per SM with dx chunks of 13 / 9
 // (127 registers, 16 x 4 POI tiles to fit 110 KB): 0.93 / 0.98 ms against

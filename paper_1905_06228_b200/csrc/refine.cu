@@ -958,7 +958,7 @@ struct FixedGeom {
   // of pairs (the tap address is then two shifts on the ALU pipe instead of
   // IMADs), else to an even width (16-byte box rows)
   static constexpr int TP0 = SPAN + SIDE + 2 * kFixedPad + 2 * kFixedSpread + 1;
-  static constexpr int TP = (TP0 <= 128 && TP0 > 120) ? 128 : (TP0 <= 64 && TP0 > 56) ? 64 : (TP0 + 1) & ~1;
+  static constexpr int TP = (TP0 <= 128 && TP0 > 80) ? 128 : (TP0 <= 64 && TP0 > 56) ? 64 : (TP0 + 1) & ~1;
   static constexpr int TH = SIDE + 2 * kFixedPad + 2 * kFixedSpread;  // float rows; TH - 1 pair rows
   // floats; 128-byte aligned (TMA destinations of the pre-converted staging)
   static constexpr size_t G2_OFF = (((size_t)RH * RP + 31) & ~(size_t)31);
