@@ -670,16 +670,21 @@ constexpr int kFixedK = 32;            // fixed passes sample at subset-local + 
 constexpr uint32_t kMagicBits = 0x4B000000u;  // bit pattern of 2^23
 
 __device__ __forceinline__ uint32_t fbits(float v) { return __float_as_uint(v); }
+// Shared-memory loads by address. `volatile`: a plain asm counts as a pure
+// function of its inputs, so the compiler may hoist it above the branch that
+// makes the address valid (it did: the node pass's loads moved out of the
+// iteration loop and faulted for a POI whose integer estimate lies outside the
+// strip's staged target window — the POI itself runs the checked path).
 __device__ __forceinline__ float lds1(uint32_t a) {
   float r;
-  asm("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(a));
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(a));
   return r;
 }
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ f2x lds2x(uint32_t a) {
   f2x r;
-  asm("ld.shared.b64 %0, [%1];" : "=l"(r) : "r"(a));
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(r) : "r"(a));
   return r;
 }
 
@@ -1437,7 +1442,11 @@ __global__ void __launch_bounds__(kNT, 2) refine_strip_kernel(RefineParams p, co
     const uint32_t t2b = smem_addr(T2);
     fc.t2 = t2b + (uint32_t)(((pc.ioffy - kFixedK) * FG::TP + (pc.ioffx - kFixedK)) * 8) -
             kMagicBits * (uint32_t)((FG::TP + 1) * 8);
-    fc.tn = t2b + (uint32_t)(((pc.ioffy - M) * FG::TP + (pc.ioffx - M)) * 8);
+    // the node pass's window [ioff - M, ioff + M]^2 lies inside the staged pairs
+    // whenever the first iteration is `fast`; otherwise (an integer estimate far
+    // from the strip's median) the address is parked on the region's origin
+    const bool tn_in = pc.ioffx - M >= 0 && pc.ioffx + M < FG::TP && pc.ioffy - M >= 0 && pc.ioffy + M <= FG::TH - 2;
+    fc.tn = t2b + (tn_in ? (uint32_t)(((pc.ioffy - M) * FG::TP + (pc.ioffx - M)) * 8) : 0u);
     fc.g2 = smem_addr(Gs);
     fc.r = smem_addr(Rs);
     fc.fbar = fbarf;
