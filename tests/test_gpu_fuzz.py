@@ -157,3 +157,59 @@ def test_random_geometry_parity(gpu, port, seed):
     except AssertionError as e:
         raise AssertionError(f"seed {seed}: {tag}: {e}") from None
     print(f"seed {seed}: {tag}: max|du,dv| {worst:.2e} flips at max_iter {flips}")
+
+
+N_SEQ = int(os.environ.get("FUZZ_SEQ_CASES", "12"))
+
+
+@pytest.mark.parametrize("seed", range(SEED0, SEED0 + N_SEQ))
+def test_random_sequence_equals_pairwise(gpu, seed):
+    """The pipelined analyze_sequence (frame slots, reference-side caches per compute stream, uploads
+    and read-back overlapped) against independent analyze_pair calls on the same frames: every record
+    field bit-identical, for random geometries, both reference policies, 3-7 frames whose fields and
+    (for 16-bit data) significant bit counts differ along the sequence."""
+    ref, _, cfg, _ = make_case(seed)
+    r = np.random.default_rng(50000 + seed)
+    cfg.reference_policy = [dic.ReferencePolicy.fixed_first, dic.ReferencePolicy.update_every_pair][int(r.integers(0, 2))]
+    lim = min(cfg.search.search_radius - 0.6, 5.0)
+    frames = [ref.render()]
+    for k in range(int(r.integers(2, 7))):
+        a = (float(r.uniform(-lim, lim)), float(r.uniform(-0.003, 0.003)), float(r.uniform(-0.003, 0.003)),
+             float(r.uniform(-lim, lim)), float(r.uniform(-0.003, 0.003)), float(r.uniform(-0.003, 0.003)),
+             (ref.width - 1) / 2.0, (ref.height - 1) / 2.0)
+        f = configs.replace(ref, field=_abi.FIELD_AFFINE, a=a).render()
+        if f.dtype == np.uint16 and r.random() < 0.4:  # fewer significant bits than its neighbours
+            f = (f >> int(r.integers(1, 4))).astype(np.uint16)
+        frames.append(f)
+    imgs = [dic.GrayImage(f, i) for i, f in enumerate(frames)]
+    fields = dic.analyze_sequence(imgs, cfg)
+    pairs = dic.sequence_pairs(cfg.reference_policy, len(imgs))
+    assert len(fields) == len(pairs)
+    for f, (ra, tb) in zip(fields, pairs):
+        assert not f.failed(), f.error
+        exp = run_device(frames[ra], frames[tb], cfg, pair_index=f.pair_index)
+        for k in exp.dtype.names:
+            assert np.array_equal(f.records[k], exp[k], equal_nan=True), (seed, cfg.reference_policy.name, f.pair_index, k)
+
+
+N_FP = int(os.environ.get("FUZZ_FP_CASES", "12"))
+
+
+@pytest.mark.parametrize("seed", range(SEED0, SEED0 + N_FP))
+def test_random_geometry_parity_fractional_frames(gpu, port, seed):
+    """The same sweep on fractional gray levels (GrayImage doubles that are not integers: the exact
+    fp64 search path, which evaluates the reference's zncc in its own order, and the refiners on the
+    fp64 images)."""
+    ref, tgt, cfg, pair_index = make_case(seed)
+    r = np.random.default_rng(70000 + seed)
+    gain, off = float(r.uniform(0.31, 1.9)), float(r.uniform(0.0, 3.0))
+    a = ref.render().astype(np.float64) * gain + off
+    b = tgt.render().astype(np.float64) * gain + off
+    exp = port.analyze_pair(a, b, cfg, pair_index=pair_index)
+    got = dic.analyze_pair(dic.GrayImage(a), dic.GrayImage(b, 1), cfg, pair_index).records
+    try:
+        check(got, exp, cfg.refine.max_iter, cfg.refine.tol)
+    except AssertionError as e:
+        raise AssertionError(f"seed {seed}: {ref.width}x{ref.height} M{cfg.grid.half_width} s{cfg.grid.spacing} "
+                             f"R{cfg.search.search_radius} {cfg.integer_method.name}/{cfg.subpixel_method.name}/"
+                             f"{cfg.interp.name}: {e}") from None
