@@ -176,6 +176,12 @@ __global__ void widen_f32_kernel(const float* src, int pitch, double* dst, int w
   if (x < w) dst[(size_t)y * w + x] = (double)src[(size_t)y * pitch + x];
 }
 
+template <typename Pix>
+__global__ void widen_int_kernel(const Pix* src, int pitch, double* dst, int w, int h) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (x < w) dst[(size_t)y * w + x] = (double)src[(size_t)y * pitch + x];
+}
+
 }  // namespace
 
 cudaError_t bfs_fp_launch(FpParams p, int rows, cudaStream_t st) {
@@ -197,6 +203,16 @@ cudaError_t bfs_fp_launch(FpParams p, int rows, cudaStream_t st) {
 
 cudaError_t widen_f32_to_f64(const float* src, int pitch, double* dst, int w, int h, cudaStream_t st) {
   widen_f32_kernel<<<dim3((w + 255) / 256, h), 256, 0, st>>>(src, pitch, dst, w, h);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t widen_int_to_f64(const void* src, int elem_size, int pitch, double* dst, int w, int h, cudaStream_t st) {
+  const dim3 grid((w + 255) / 256, h);
+  if (elem_size == 1)
+    widen_int_kernel<uint8_t><<<grid, 256, 0, st>>>(static_cast<const uint8_t*>(src), pitch, dst, w, h);
+  else
+    widen_int_kernel<uint16_t><<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(src), pitch, dst, w, h);
   count_launch();
   return cudaGetLastError();
 }

@@ -20,5 +20,7 @@ struct FpParams {
 cudaError_t bfs_fp_launch(FpParams p, int rows, cudaStream_t st);
 // f32 image (pitch in elements) -> dense fp64 copy (exact)
 cudaError_t widen_f32_to_f64(const float* src, int pitch, double* dst, int w, int h, cudaStream_t st);
+// u8 / u16 image (pitch in elements) -> dense fp64 copy (exact)
+cudaError_t widen_int_to_f64(const void* src, int elem_size, int pitch, double* dst, int w, int h, cudaStream_t st);
 
 }  // namespace dicb200

@@ -281,10 +281,10 @@ static dicb200_status enqueue_bits_guard(const dicb200_image* ref, const dicb200
 static const char kBitsMsg[] = "pixel values exceed the declared dicb200_image.bits";
 
 // Enqueue the whole per-pair chain for grid rows [rb, re) on `st`.
-static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image* tgt, const dicb200_run_config* cfg,
-                                   uint64_t pair_index, const Lattice& lat, int rb, int re,
-                                   dicb200_poi_record* out_dev, cudaStream_t st, TcRefCache* tcache = nullptr,
-                                   long ref_key = -1, IcgnRefCache* icache = nullptr) {
+static dicb200_status enqueue_pair_impl(const dicb200_image* ref, const dicb200_image* tgt, const dicb200_run_config* cfg,
+                                        uint64_t pair_index, const Lattice& lat, int rb, int re,
+                                        dicb200_poi_record* out_dev, cudaStream_t st, TcRefCache* tcache,
+                                        long ref_key, IcgnRefCache* icache) {
   const int rows = re - rb;
   if (rows <= 0) return DICB200_OK;
   const size_t nrec = (size_t)rows * lat.nx;
@@ -470,6 +470,45 @@ refine:
     host_trace("refine enqueued");
   }
   return enqueue_bits_guard(ref, tgt, out_dev, nrec, st, tcache, ref_key);
+}
+
+// Subsets below this half-width (under 17 x 17 px) hold so little texture that
+// distinct candidates reach mathematically tied ZNCC values; the reference orders
+// those by the rounding of its sequential fp64 sums, which the exact-integer
+// kernels (they compare exact moments) cannot reproduce. Such grids run on the
+// fp64 path instead, which evaluates zncc in the reference's own order (bit
+// for bit): integer frames are widened for the call. The work per POI is tiny
+// at these sizes; no BASELINE configuration is affected (M >= 10).
+constexpr int kRefOrderBelowM = 8;
+
+static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image* tgt, const dicb200_run_config* cfg,
+                                   uint64_t pair_index, const Lattice& lat, int rb, int re,
+                                   dicb200_poi_record* out_dev, cudaStream_t st, TcRefCache* tcache = nullptr,
+                                   long ref_key = -1, IcgnRefCache* icache = nullptr) {
+  const bool integer_frames = ref->dtype == DICB200_U8 || ref->dtype == DICB200_U16;
+  if (!integer_frames || cfg->half_width >= kRefOrderBelowM || re <= rb)
+    return enqueue_pair_impl(ref, tgt, cfg, pair_index, lat, rb, re, out_dev, st, tcache, ref_key, icache);
+  double* buf[2] = {nullptr, nullptr};
+  dicb200_image wide[2] = {*ref, *tgt};
+  dicb200_status s = DICB200_OK;
+  for (int k = 0; k < 2 && s == DICB200_OK; ++k) {
+    const dicb200_image* im = k ? tgt : ref;
+    const int pitch = im->pitch > 0 ? im->pitch : im->width;
+    cudaError_t e = cudaMallocAsync((void**)&buf[k], (size_t)im->width * im->height * 8, st);
+    if (e == cudaSuccess)
+      e = widen_int_to_f64(im->data, im->dtype == DICB200_U8 ? 1 : 2, pitch, buf[k], im->width, im->height, st);
+    if (e != cudaSuccess) s = cuda_fail(e, "widen integer frame", __FILE__, __LINE__);
+    wide[k].dtype = DICB200_F64;
+    wide[k].bits = 0;
+    wide[k].pitch = im->width;
+    wide[k].data = buf[k];
+  }
+  // the widened copies live for this call only: no reference-side caches
+  if (s == DICB200_OK)
+    s = enqueue_pair_impl(&wide[0], &wide[1], cfg, pair_index, lat, rb, re, out_dev, st, nullptr, -1, nullptr);
+  for (double* b : buf)
+    if (b) cudaFreeAsync(b, st);
+  return s;
 }
 
 static size_t elem_size(int dtype) {
