@@ -215,3 +215,57 @@ def test_random_geometry_parity_fractional_frames(gpu, port, seed):
         raise AssertionError(f"seed {seed}: {ref.width}x{ref.height} M{cfg.grid.half_width} s{cfg.grid.spacing} "
                              f"R{cfg.search.search_radius} {cfg.integer_method.name}/{cfg.subpixel_method.name}/"
                              f"{cfg.interp.name}: {e}") from None
+
+
+N_DEV = int(os.environ.get("FUZZ_DEV_CASES", "12"))
+
+
+@pytest.mark.parametrize("seed", range(SEED0, SEED0 + N_DEV))
+def test_random_row_shards_and_pitches_on_device(gpu, seed):
+    """dicb200_analyze_pair_device on device images with a random row pitch (>= width, any
+    alignment: the TMA paths must decline what they cannot describe) over a random split of the grid
+    rows, against the host-image call on dense frames: every record field bit-identical, subset
+    indices (RNG keys) global."""
+    import ctypes as C
+
+    import torch
+
+    ref, tgt, cfg, pair_index = make_case(seed)
+    r = np.random.default_rng(60000 + seed)
+    a, b = ref.render(), tgt.render()
+    full = run_device(a, b, cfg, pair_index=pair_index)
+    H, W = a.shape
+    pitch = W + int(r.choice([0, 1, 3, 8, 16, 29, 64]))
+    L = dic.lib()
+    L.dicb200_analyze_pair_device.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_abi.RunConfigC), C.c_uint64,
+                                              C.c_int32, C.c_int32, C.c_void_p, C.c_size_t,
+                                              C.POINTER(C.c_size_t), C.c_void_p]
+    ims, keep = [], []
+    for k, f in enumerate((a, b)):
+        host = np.full((H, pitch), 0xAB if f.dtype == np.uint8 else 0xABCD, f.dtype)  # junk in the pitch gap
+        host[:, :W] = f
+        t = torch.from_numpy(host.view(np.int16) if f.dtype == np.uint16 else host).cuda()
+        keep.append(t)
+        im = dic.GrayImage(f, k).as_c()
+        im.pitch = pitch
+        im.data = t.data_ptr()
+        ims.append(im)
+    xs = {x for x, _ in dic.grid_subsets(W, H, cfg.grid.half_width, cfg.grid.spacing, cfg.effective_margin())}
+    nx = len(xs)
+    ny = len(full) // max(nx, 1)
+    cuts = sorted({0, ny, *[int(v) for v in r.integers(0, ny + 1, size=int(r.integers(0, 4)))]})
+    parts = []
+    c = cfg.to_c()
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        out = torch.empty(max(1, (hi - lo) * nx) * C.sizeof(_abi.PoiRecordC), dtype=torch.uint8, device="cuda")
+        n = C.c_size_t(0)
+        st = L.dicb200_analyze_pair_device(C.byref(ims[0]), C.byref(ims[1]), C.byref(c), pair_index, lo, hi,
+                                           C.c_void_p(out.data_ptr()), (hi - lo) * nx, C.byref(n), None)
+        assert st == 0, (seed, st)
+        torch.cuda.synchronize()
+        assert n.value == (hi - lo) * nx
+        parts.append(np.frombuffer(out.cpu().numpy().tobytes(), dtype=_abi.record_dtype())[: n.value])
+    sharded = np.concatenate(parts) if parts else full[:0]
+    assert len(sharded) == len(full)
+    for f in full.dtype.names:
+        assert np.array_equal(sharded[f], full[f], equal_nan=True), (seed, pitch, cuts, f)
