@@ -269,3 +269,47 @@ def test_random_row_shards_and_pitches_on_device(gpu, seed):
     assert len(sharded) == len(full)
     for f in full.dtype.names:
         assert np.array_equal(sharded[f], full[f], equal_nan=True), (seed, pitch, cuts, f)
+
+
+N_LARGE = int(os.environ.get("FUZZ_LARGE_CASES", "3"))
+
+
+@pytest.mark.parametrize("seed", range(SEED0, SEED0 + N_LARGE))
+def test_random_large_frames_near_baseline_geometry(gpu, port, seed):
+    """Frames of 700-1700 px a side (not multiples of the kernels' tiles) around the C4 / C5 / C3
+    geometries - the block-sum search's tile remainders and dy slices, the fixed IC-GN strips' partial
+    last strips, the tensor-core surface's tile edges - with random bit depths, radii and fields."""
+    r = np.random.default_rng(80000 + seed)
+    W, H = int(r.integers(700, 1700)), int(r.integers(700, 1700))
+    kind = int(r.integers(0, 3))
+    if kind == 0:  # C5-like
+        bits, M, step, R, im, sp = int(r.choice([10, 12, 12, 14])), 20, 10, int(r.integers(6, 14)), dic.IntegerMethod.bfs, dic.SubpixelMethod.icgn
+    elif kind == 1:  # C4-like (fewer POIs than C4: step 5 on a smaller frame)
+        bits, M, step, R, im, sp = 12, 20, 5, int(r.integers(3, 8)), dic.IntegerMethod.bfs, dic.SubpixelMethod.icgn
+        W, H = min(W, 1100), min(H, 1100)
+    else:  # C3-like
+        bits, M, step, R, im, sp = 8, 15, 8, int(r.integers(10, 22)), dic.IntegerMethod.mpso, dic.SubpixelMethod.nr
+        W, H = min(W, 1100), min(H, 1100)
+    if bits == 8:
+        ref = configs.FrameSpec(W, H, _abi.U8, 255, 8000 + seed, W * H // 60, (2.0, 4.0), (60.0, 200.0))
+    else:
+        mx = (1 << bits) - 1
+        ref = configs.FrameSpec(W, H, _abi.U16, mx, 8000 + seed, W * H // 42, (1.5, 3.5), (0.23 * mx, 0.78 * mx))
+    lim = min(R - 0.6, 6.0)
+    a = (float(r.uniform(-lim, lim)), float(r.uniform(-0.002, 0.002)), float(r.uniform(-0.002, 0.002)),
+         float(r.uniform(-lim, lim)), float(r.uniform(-0.002, 0.002)), float(r.uniform(-0.002, 0.002)),
+         (W - 1) / 2.0, (H - 1) / 2.0)
+    tgt = configs.replace(ref, field=_abi.FIELD_AFFINE, a=a)
+    cfg = dic.RunConfig(
+        integer_method=im, subpixel_method=sp,
+        search=dic.SearchConfig(search_radius=R, bfs_domain=dic.BfsDomain.window, particle_count=20, max_generations=30,
+                                stop_threshold=0.995, c1=1.5, c2=1.5, rng_seed=int(r.integers(0, 1 << 40))),
+        refine=dic.RefineConfig(tol=1e-4, max_iter=30), grid=dic.GridParams(half_width=M, spacing=step, margin=-1))
+    fa, fb = ref.render(), tgt.render()
+    exp = port.analyze_pair(fa, fb, cfg, pair_index=seed)
+    got = run_device(fa, fb, cfg, pair_index=seed)
+    try:
+        worst, flips = check(got, exp, cfg.refine.max_iter, cfg.refine.tol)
+    except AssertionError as e:
+        raise AssertionError(f"seed {seed}: {W}x{H} {bits}-bit M{M} s{step} R{R} {im.name}/{sp.name} pois {len(exp)}: {e}") from None
+    print(f"seed {seed}: {W}x{H} {bits}-bit M{M} s{step} R{R} {im.name}/{sp.name} pois {len(exp)}: max|du,dv| {worst:.2e}")
