@@ -486,7 +486,9 @@ static dicb200_status enqueue_pair(const dicb200_image* ref, const dicb200_image
                                    dicb200_poi_record* out_dev, cudaStream_t st, TcRefCache* tcache = nullptr,
                                    long ref_key = -1, IcgnRefCache* icache = nullptr) {
   const bool integer_frames = ref->dtype == DICB200_U8 || ref->dtype == DICB200_U16;
-  if (!integer_frames || cfg->half_width >= kRefOrderBelowM || re <= rb)
+  // the A/B switches that force one of the exact-integer search kernels keep it (kernel-vs-kernel tests)
+  const bool forced = std::getenv("DICB200_BFS_LEGACY") || std::getenv("DICB200_BFS_TC") || std::getenv("DICB200_BFS_BS");
+  if (!integer_frames || cfg->half_width >= kRefOrderBelowM || re <= rb || forced)
     return enqueue_pair_impl(ref, tgt, cfg, pair_index, lat, rb, re, out_dev, st, tcache, ref_key, icache);
   double* buf[2] = {nullptr, nullptr};
   dicb200_image wide[2] = {*ref, *tgt};
