@@ -313,3 +313,40 @@ def test_random_large_frames_near_baseline_geometry(gpu, port, seed):
     except AssertionError as e:
         raise AssertionError(f"seed {seed}: {W}x{H} {bits}-bit M{M} s{step} R{R} {im.name}/{sp.name} pois {len(exp)}: {e}") from None
     print(f"seed {seed}: {W}x{H} {bits}-bit M{M} s{step} R{R} {im.name}/{sp.name} pois {len(exp)}: max|du,dv| {worst:.2e}")
+
+
+def test_concurrent_callers_match_serial(gpu):
+    """Several host threads inside dicb200_analyze_pair / _sequence at once (ctypes drops the GIL;
+    the library hands each caller its own pooled context): every caller's records equal the ones the
+    same call returns alone."""
+    import threading
+
+    cases = [make_case(s) for s in range(1000, 1012)]
+    frames = [(ref.render(), tgt.render()) for ref, tgt, _, _ in cases]
+    serial = [run_device(a, b, cfg, pair_index=pi) for (a, b), (_, _, cfg, pi) in zip(frames, cases)]
+    out, errs = {}, []
+
+    def worker(t):
+        try:
+            for rep in range(3):
+                for i in range(t, len(cases), 4):
+                    (a, b), (_, _, cfg, pi) = frames[i], cases[i]
+                    if (i + rep) % 3 == 0:  # through the sequence entry point (one pair, explicit index not kept)
+                        f = dic.analyze_sequence([dic.GrayImage(a, 0), dic.GrayImage(b, 1)], cfg)[0]
+                        if pi == 0:
+                            out[(i, rep)] = f.records
+                    else:
+                        out[(i, rep)] = run_device(a, b, cfg, pair_index=pi)
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    ts = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    assert len(out) >= 20
+    for (i, rep), got in out.items():
+        for k in got.dtype.names:
+            assert np.array_equal(got[k], serial[i][k], equal_nan=True), (i, rep, k)
