@@ -350,3 +350,52 @@ def test_concurrent_callers_match_serial(gpu):
     for (i, rep), got in out.items():
         for k in got.dtype.names:
             assert np.array_equal(got[k], serial[i][k], equal_nan=True), (i, rep, k)
+
+
+N_HOST = int(os.environ.get("FUZZ_HOST_CASES", "8"))
+
+
+@pytest.mark.parametrize("seed", range(SEED0, SEED0 + N_HOST))
+def test_random_host_pitches_and_pixel_types(gpu, seed):
+    """dicb200_analyze_pair on host images with a row pitch > width (junk in the gap), as stored
+    (u8 / u16) and as DICB200_F32 holding half-integer levels (widened exactly onto the fp64 path),
+    against the dense GrayImage calls."""
+    import ctypes as C
+
+    ref, tgt, cfg, pair_index = make_case(seed)
+    r = np.random.default_rng(65000 + seed)
+    a, b = ref.render(), tgt.render()
+    H, W = a.shape
+    L = dic.lib()
+
+    def call(fa, fb, dtype_code, bits):
+        pitch = W + int(r.integers(1, 40))
+        keep, ims = [], []
+        for k, f in enumerate((fa, fb)):
+            host = np.full((H, pitch), 7, f.dtype)
+            host[:, :W] = f
+            keep.append(host)
+            im = _abi.Image()
+            im.width, im.height, im.pitch, im.dtype, im.id, im.bits = W, H, pitch, dtype_code, k, bits
+            im.data = host.ctypes.data
+            ims.append(im)
+        c = cfg.to_c()
+        n = C.c_size_t(0)
+        assert L.dicb200_grid_size(W, H, C.byref(c), C.byref(n)) == 0
+        recs = np.zeros(n.value, dtype=_abi.record_dtype())
+        cnt = C.c_size_t(0)
+        st = L.dicb200_analyze_pair(C.byref(ims[0]), C.byref(ims[1]), C.byref(c), pair_index, recs.ctypes.data,
+                                    n.value, C.byref(cnt))
+        assert st == 0, st
+        return recs[: cnt.value]
+
+    dense = run_device(a, b, cfg, pair_index=pair_index)
+    code = _abi.U8 if a.dtype == np.uint8 else _abi.U16
+    got = call(a, b, code, max(1, int(max(a.max(), b.max())).bit_length()) if code == _abi.U16 else 0)
+    for k in dense.dtype.names:
+        assert np.array_equal(got[k], dense[k], equal_nan=True), (seed, "integer", k)
+    ha, hb = a.astype(np.float64) * 0.5, b.astype(np.float64) * 0.5  # exact in f32 for <= 16-bit levels
+    dense_fp = dic.analyze_pair(dic.GrayImage(ha), dic.GrayImage(hb, 1), cfg, pair_index).records
+    got_fp = call(ha.astype(np.float32), hb.astype(np.float32), _abi.F32, 0)
+    for k in dense_fp.dtype.names:
+        assert np.array_equal(got_fp[k], dense_fp[k], equal_nan=True), (seed, "f32", k)
