@@ -448,7 +448,7 @@ namespace {
 template <typename Pix, int J, bool kF64>
 cudaError_t launch_t(const BfsParams& p, dim3 grid, int threads, size_t smem, cudaStream_t st) {
   auto kern = bfs_tile_kernel<Pix, J, kF64>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_dyn_smem(kern, smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) return e;

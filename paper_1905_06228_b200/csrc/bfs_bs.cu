@@ -1238,7 +1238,7 @@ template <int S, int RR, int Q, int DXC, int NT, int MINB>
 cudaError_t launch_variant(const TcParams& p, const BsGeom& g, dim3 grid, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
   auto go = [&](auto k) {
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+    e = set_dyn_smem(k, g.smem);
     if (e == cudaSuccess) k<<<grid, NT, g.smem, st>>>(p, g);
   };
   if (p.planes == 1)
@@ -1444,7 +1444,7 @@ template <int S, int RR, int Q, int DXC, int NPW, int NCW, int PYM>
 cudaError_t launch_ws(const TcParams& p, const BsGeom& g, dim3 grid, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
   auto go = [&](auto k) {
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+    e = set_dyn_smem(k, g.smem);
     if (e == cudaSuccess) k<<<grid, 32 * (NPW + NCW), g.smem, st>>>(p, g);
   };
   if (g.PY > PYM) return cudaErrorInvalidValue;

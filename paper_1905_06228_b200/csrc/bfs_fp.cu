@@ -192,7 +192,7 @@ cudaError_t bfs_fp_launch(FpParams p, int rows, cudaStream_t st) {
   p.stage_window = !p.whole && smem + wbytes <= 160 * 1024;
   if (p.stage_window) smem += wbytes;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(bfs_fp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_dyn_smem(bfs_fp_kernel, smem);
   if (e != cudaSuccess) return e;
   const size_t npoi = (size_t)rows * p.lat.nx;
   if (npoi == 0) return cudaSuccess;

@@ -1069,7 +1069,7 @@ __global__ void __launch_bounds__(256) tc_surface_kernel(TcParams p) {
 
 template <typename K>
 cudaError_t set_smem(K kern, size_t bytes) {
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaError_t e = set_dyn_smem(kern, bytes);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
 }
@@ -1155,7 +1155,10 @@ bool tc_plan(TcParams& p) {
     p.rem = 0;
   p.stages = kGroups;
   p.smem = (size_t)p.stages * p.stage_bytes;
-  if (p.smem > 220 * 1024) return false;
+  // 227 KB per CTA on sm_100a, less the kernel's 9 KB of static shared memory (barriers, tile lists):
+  // the former 220 KB bound let a 220 KB ring through, which the launch rejected (found by the
+  // randomised sweep: side 25, R 9, step 4, two planes)
+  if (p.smem > (227 - 10) * 1024) return false;
   // cross-term buffer: one window per POI of the launch
   const size_t EW = 2 * (size_t)p.R + 1;
   if ((size_t)rows * p.lat.nx * EW * EW * 8 > ((size_t)3 << 30)) return false;
@@ -1280,6 +1283,7 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
   }
+  int failed_stage = e != cudaSuccess ? 1 : 0;  // first failing stage, named in the error trace below
   host_trace("tc stats");
   // (b) reference moments + strip images (skipped when cached; the block-sum
   //     kernel reads the reference directly and needs no strips)
@@ -1321,6 +1325,7 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
       cache->use_bs = use_bs;
     }
   }
+  if (e != cudaSuccess && !failed_stage) failed_stage = 2;
   host_trace("tc prep");
   // (c) tensor-core search
   if (e == cudaSuccess && use_bs) {
@@ -1365,6 +1370,7 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
       p.dbg_out = nullptr;
     }
   }
+  if (e != cudaSuccess && !failed_stage) failed_stage = 3;
   // (d) per POI: exact ZNCC -> argmax record, or the full surface for the swarm walk
   if (e == cudaSuccess && fused) {
     StageTimer tm(5, st);
@@ -1384,6 +1390,11 @@ cudaError_t tc_launch(TcParams& p, cudaStream_t st, TcRefCache* cache, long ref_
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
   }
+  if (e != cudaSuccess && !failed_stage) failed_stage = 4;
+  if (e != cudaSuccess)
+    fprintf(stderr, "[dicb200] tc_launch: stage %d (1 window sums, 2 reference prep, 3 search, 4 argmax / surface) failed: %s "
+            "(side %d R %d step %d planes %d SW %d SH %d tiles %d grid %d smem %zu)\n", failed_stage, cudaGetErrorString(e),
+            p.side, p.R, p.lat.step, p.planes, p.SW, p.SH, p.n_tiles, p.grid, p.smem);
   cleanup();
   return e;
 }

@@ -88,4 +88,14 @@ void set_error(const char* msg);
 // DICB200_HOST_TRACE=1: reports host-side gaps > 5 ms between consecutive
 // marks on this thread (enqueue stalls that would starve the GPU)
 void host_trace(const char* what, long i = 0);
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per-kernel (and per-device) state: concurrent host
+// callers that set it to what THEIR launch needs race - the one that set the larger value can find
+// it lowered before it launches (cudaErrorInvalidValue; seen with four threads in
+// dicb200_analyze_pair). The limit therefore only ever grows.
+cudaError_t set_dyn_smem(const void* kernel, size_t bytes);
+template <typename K>
+inline cudaError_t set_dyn_smem(K kernel, size_t bytes) {
+  return set_dyn_smem(reinterpret_cast<const void*>(kernel), bytes);
+}
+
 }  // namespace dicb200

@@ -464,7 +464,7 @@ dicb200_status pso_walk_launch(PsoParams& p, cudaStream_t st) {
   }
   cudaError_t e;
   auto go = [&](auto k) {
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = set_dyn_smem(k, smem);
     if (e == cudaSuccess) {
       k<<<(p.n_records + kWarpsPerCta - 1) / kWarpsPerCta, 32 * kWarpsPerCta, smem, st>>>(p);
       e = cudaGetLastError();

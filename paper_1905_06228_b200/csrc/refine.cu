@@ -1882,7 +1882,7 @@ cudaError_t refine_launch(const RefineParams& p0, int dtype, cudaStream_t st, Ic
     static const size_t smem_pad = std::getenv("DICB200_REFINE_SMEM_PAD") ? std::atoi(std::getenv("DICB200_REFINE_SMEM_PAD")) : 0;
     auto go = [&](auto k, size_t sm) {
       sm += smem_pad;
-      e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      e = set_dyn_smem(k, sm);
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
       if (e == cudaSuccess) k<<<grid, kNT, sm, st>>>(p, tm);
@@ -1901,7 +1901,7 @@ cudaError_t refine_launch(const RefineParams& p0, int dtype, cudaStream_t st, Ic
   }
   dim3 grid((p.lat.nx + p.spc - 1) / p.spc, rows);
   auto go = [&](auto k) {
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = set_dyn_smem(k, smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     if (e == cudaSuccess) k<<<grid, kNT, smem, st>>>(p, tm);
